@@ -1,0 +1,115 @@
+"""Adaptive cross approximation with partial pivoting -- TEST INFRASTRUCTURE ONLY.
+
+eq:aca: X ~ X(:,C) X(R,C)^-1 X(R,:) built one cross at a time,
+stored as U V^T; stop rule in the spirit of eq:erel with the
+Frobenius-norm estimate of DESIGN.md reading R5.  The pivot rules are unstated in the
+paper; this follows DESIGN.md reading R10 step by step:
+
+  (a) row residual r_j = X(i*,j) - sum_{l<k} U[i*,l] V[j,l]   (l ascending, no FMA)
+  (b) j* = argmax_{j unused} |r_j| (lowest j on ties), delta = r_{j*}
+  (c) delta == 0: mark i* used; stop if all rows used; else i* = smallest unused row
+  (d) v = r / delta
+  (e) column residual u_i = X(i,j*) - sum_{l<k} U[i,l] V[j*,l]
+  (f) nu2 = |u|^2, nv2 = |v|^2, X2 = sum_l (u.U_l)(v.V_l), S2' = S2 + nu2 nv2 + 2 X2
+  (g) nu2 nv2 <= eps^2 S2'  -> stop, discard this cross
+  (h) append (u, v), k += 1, S2 = S2', mark i*, j* used
+  (i) k == min(m, n) -> stop
+  (j) i* = argmax_{i unused} |u_i| (lowest i on ties)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class ACAResult:
+    U: np.ndarray          # (m, k)
+    V: np.ndarray          # (n, k)
+    margin: float          # min over stop decisions of |nu2 nv2 / (eps^2 S2') - 1|
+    rows: list = None      # pivot rows R = {i_1..i_k} (eq:aca)
+    cols: list = None      # pivot columns C = {j_1..j_k}
+
+    @property
+    def rank(self):
+        return self.U.shape[1]
+
+
+def aca_partial(row_fn, col_fn, m: int, n: int, eps: float) -> ACAResult:
+    Us: list = []
+    Vs: list = []
+    k = 0
+    S2 = 0.0
+    used_r = np.zeros(m, dtype=bool)
+    used_c = np.zeros(n, dtype=bool)
+    istar = 0
+    eps2 = eps * eps
+    margin = np.inf
+    prow: list = []
+    pcol: list = []
+    while True:
+        r = np.array(row_fn(istar), dtype=np.float64)                # (a)
+        for l in range(k):
+            r = r - Us[l][istar] * Vs[l]
+        ar = np.abs(r)
+        ar[used_c] = -1.0
+        jstar = int(np.argmax(ar))                                   # (b)
+        delta = r[jstar]
+        if delta == 0.0 or used_c[jstar]:                            # (c)
+            used_r[istar] = True
+            if used_r.all():
+                break
+            istar = int(np.argmin(used_r))
+            continue
+        v = r / delta                                                # (d)
+        u = np.array(col_fn(jstar), dtype=np.float64)                # (e)
+        for l in range(k):
+            u = u - Us[l] * Vs[l][jstar]
+        nu2 = float(np.sum(u * u))                                   # (f)
+        nv2 = float(np.sum(v * v))
+        X2 = 0.0
+        for l in range(k):
+            X2 += float(np.sum(u * Us[l])) * float(np.sum(v * Vs[l]))
+        S2n = (S2 + nu2 * nv2) + 2.0 * X2
+        lhs, rhs = nu2 * nv2, eps2 * S2n
+        if rhs > 0.0:
+            margin = min(margin, abs(lhs / rhs - 1.0))
+        if lhs <= rhs:                                               # (g)
+            break
+        Us.append(u)                                                 # (h)
+        Vs.append(v)
+        prow.append(istar)
+        pcol.append(jstar)
+        k += 1
+        S2 = S2n
+        used_r[istar] = True
+        used_c[jstar] = True
+        if k == min(m, n):                                           # (i)
+            break
+        if used_r.all():
+            break
+        au = np.abs(u)
+        au[used_r] = -1.0
+        istar = int(np.argmax(au))                                   # (j)
+    U = np.stack(Us, axis=1) if k else np.zeros((m, 0))
+    V = np.stack(Vs, axis=1) if k else np.zeros((n, 0))
+    return ACAResult(U, V, margin, prow, pcol)
+
+
+def aca_matrix(X: np.ndarray, eps: float) -> ACAResult:
+    """ACA of an explicit matrix (used by the textbook pins)."""
+    return aca_partial(lambda i: X[i, :], lambda j: X[:, j], X.shape[0], X.shape[1], eps)
+
+
+def svd_eps_rank(X: np.ndarray, eps: float) -> int:
+    """Smallest k with ||X - X_k||_F <= eps ||X||_F (truncated SVD, reading R5)."""
+    s = np.linalg.svd(X, compute_uv=False)
+    tot = float(np.sum(s * s))
+    if tot == 0.0:
+        return 0
+    tail = np.concatenate([np.cumsum((s * s)[::-1])[::-1], [0.0]])
+    for k in range(len(s) + 1):
+        if tail[k] <= eps * eps * tot:
+            return k
+    return len(s)

@@ -1,0 +1,265 @@
+"""Seeded synthetic inputs shared by the oracle and the CUDA path.
+
+This module only PRODUCES inputs (facet geometry, emissivities, temperatures,
+sampled row sets).  It holds none of the method's arithmetic (no view factors,
+no trees, no ACA, no LU): both `oracle/` and the product path consume its arrays
+bit-for-bit, which is what makes integer parity (partition, ACA ranks) possible.
+
+Geometry follows SURVEY.md §8(d) (BASELINE.json `configs`):
+  * closed unit-sphere icospheres (12-vertex icosahedron, 4-split with midpoints
+    projected to the sphere, shared-vertex cache, facet id parent-major);
+  * a closed capped cylinder R=1, L=4, n_theta x n_z wall quads split on one
+    diagonal plus two fan-triangulated caps (reading R17/B).
+Facets carry centroid, unit normal pointing INTO the cavity, and area; the
+paper's facet data (eq:Fdef_new_location) needs exactly these.
+
+Random numbers: SplitMix64 streams (reading R20), seeded with
+S ^ (k * 0x9E3779B97F4A7C15) where S = 2305068910 + cfg; u = (x >> 11) * 2^-53.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+MASK64 = (1 << 64) - 1
+SEED_BASE = 2305068910
+SIGMA_SB = 5.670374419e-8  # SI Stefan-Boltzmann constant (reading R2; PAPER.md:101 prints 10x too small)
+
+
+# ----------------------------------------------------------------------------- RNG
+def _mix64(z: np.ndarray) -> np.ndarray:
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def splitmix64(seed: int, count: int) -> np.ndarray:
+    """First `count` outputs of SplitMix64 started at state `seed` (uint64)."""
+    with np.errstate(over="ignore"):
+        k = np.arange(1, count + 1, dtype=np.uint64)
+        state = np.uint64(seed & MASK64) + k * GOLDEN
+        return _mix64(state)
+
+
+def stream_seed(cfg_seed: int, k: int) -> int:
+    return (cfg_seed ^ ((k * 0x9E3779B97F4A7C15) & MASK64)) & MASK64
+
+
+def uniform(seed: int, count: int) -> np.ndarray:
+    """u in [0,1): (x >> 11) * 2^-53."""
+    x = splitmix64(seed, count)
+    return (x >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
+def normal(seed: int, count: int) -> np.ndarray:
+    """Box-Muller standard normals from one uniform stream (pairs u1, u2)."""
+    m = (count + 1) // 2
+    u = uniform(seed, 2 * m)
+    u1 = 1.0 - u[0::2]          # (0, 1]
+    u2 = u[1::2]
+    r = np.sqrt(-2.0 * np.log(u1))
+    z = np.empty(2 * m)
+    z[0::2] = r * np.cos(2.0 * math.pi * u2)
+    z[1::2] = r * np.sin(2.0 * math.pi * u2)
+    return z[:count]
+
+
+def sample_rows(seed: int, n: int, count: int) -> np.ndarray:
+    """`count` distinct rows of range(n) by a partial Fisher-Yates shuffle."""
+    count = min(count, n)
+    perm = np.arange(n, dtype=np.int64)
+    x = splitmix64(seed, count)
+    for i in range(count):
+        j = i + int(x[i] % np.uint64(n - i))
+        perm[i], perm[j] = perm[j], perm[i]
+    return np.sort(perm[:count])
+
+
+# ----------------------------------------------------------------------------- meshes
+@dataclass
+class Facets:
+    """Facet set in EXTERNAL order.  Arrays are C-contiguous float64."""
+    centroid: np.ndarray      # (n,3) collocation point
+    normal: np.ndarray        # (n,3) unit normal into the cavity
+    area: np.ndarray          # (n,)
+    aabb: np.ndarray          # (n,6) lo_x lo_y lo_z hi_x hi_y hi_z of the triangle
+    tris: np.ndarray | None = None   # (n,3,3) vertices, kept for diagnostics
+    name: str = ""
+
+    @property
+    def n(self) -> int:
+        return int(self.area.shape[0])
+
+
+def _facets_from_tris(V: np.ndarray, T: np.ndarray, interior=(0.0, 0.0, 0.0), name="") -> Facets:
+    v0, v1, v2 = V[T[:, 0]], V[T[:, 1]], V[T[:, 2]]
+    cen = (v0 + v1 + v2) / 3.0
+    cr = np.cross(v1 - v0, v2 - v0)
+    ln = np.sqrt((cr * cr).sum(axis=1))
+    nrm = cr / ln[:, None]
+    # orient into the cavity: towards an interior point of the convex cavity
+    s = ((np.asarray(interior)[None, :] - cen) * nrm).sum(axis=1)
+    nrm = np.where(s[:, None] < 0, -nrm, nrm)
+    area = 0.5 * ln
+    tri = np.stack([v0, v1, v2], axis=1)
+    aabb = np.concatenate([tri.min(axis=1), tri.max(axis=1)], axis=1)
+    return Facets(np.ascontiguousarray(cen), np.ascontiguousarray(nrm), np.ascontiguousarray(area),
+                  np.ascontiguousarray(aabb), tri, name)
+
+
+def icosphere_mesh(sub: int):
+    """Vertices (on the unit sphere) and triangles, facet id parent-major."""
+    p = (1.0 + math.sqrt(5.0)) / 2.0
+    verts = [(-1, p, 0), (1, p, 0), (-1, -p, 0), (1, -p, 0),
+             (0, -1, p), (0, 1, p), (0, -1, -p), (0, 1, -p),
+             (p, 0, -1), (p, 0, 1), (-p, 0, -1), (-p, 0, 1)]
+    V = [np.array(v, dtype=np.float64) / math.sqrt(1.0 + p * p) for v in verts]
+    F = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11),
+         (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6), (7, 1, 8),
+         (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9),
+         (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(sub):
+        cache: dict = {}
+
+        def mid(a, b):
+            key = (a, b) if a < b else (b, a)
+            if key not in cache:
+                m = (V[a] + V[b]) * 0.5
+                V.append(m / math.sqrt(float(m @ m)))
+                cache[key] = len(V) - 1
+            return cache[key]
+
+        G = []
+        for (a, b, c) in F:
+            ab, bc, ca = mid(a, b), mid(b, c), mid(c, a)
+            G += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        F = G
+    return np.array(V), np.array(F, dtype=np.int64)
+
+
+def icosphere(sub: int, exact: bool = False) -> Facets:
+    """Closed unit-sphere cavity, 20*4^sub flat triangles.
+
+    exact=True is the 'sphere-exact' test mode: the
+    collocation point is c/|c| and the normal -c/|c| (radial, inward); areas stay flat.
+    """
+    V, T = icosphere_mesh(sub)
+    f = _facets_from_tris(V, T, name=f"icosphere{sub}{'-exact' if exact else ''}")
+    if exact:
+        r = np.sqrt((f.centroid * f.centroid).sum(axis=1))
+        f.centroid = np.ascontiguousarray(f.centroid / r[:, None])
+        f.normal = np.ascontiguousarray(-f.centroid)
+    return f
+
+
+def cylinder(n_theta: int = 1000, n_z: int = 40, R: float = 1.0, L: float = 4.0) -> Facets:
+    """Closed capped cylinder: wall quads (ring-major: z ring k, then theta m), each split
+    (v00,v10,v11),(v00,v11,v01); then the bottom fan, then the top fan."""
+    th = 2.0 * math.pi * np.arange(n_theta) / n_theta
+    z = -0.5 * L + L * np.arange(n_z + 1) / n_z
+    ring = np.stack([R * np.cos(th), R * np.sin(th)], axis=1)
+    V = np.zeros(((n_z + 1) * n_theta + 2, 3))
+    for k in range(n_z + 1):
+        V[k * n_theta:(k + 1) * n_theta, :2] = ring
+        V[k * n_theta:(k + 1) * n_theta, 2] = z[k]
+    cb, ct = (n_z + 1) * n_theta, (n_z + 1) * n_theta + 1
+    V[cb] = (0.0, 0.0, -0.5 * L)
+    V[ct] = (0.0, 0.0, 0.5 * L)
+    tris = []
+    for k in range(n_z):
+        for m in range(n_theta):
+            m1 = (m + 1) % n_theta
+            v00, v10 = k * n_theta + m, k * n_theta + m1
+            v01, v11 = (k + 1) * n_theta + m, (k + 1) * n_theta + m1
+            tris.append((v00, v10, v11))
+            tris.append((v00, v11, v01))
+    for m in range(n_theta):
+        tris.append((cb, m, (m + 1) % n_theta))
+    top = n_z * n_theta
+    for m in range(n_theta):
+        tris.append((ct, top + m, top + (m + 1) % n_theta))
+    return _facets_from_tris(V, np.array(tris, dtype=np.int64), name=f"cylinder{n_theta}x{n_z}")
+
+
+def line_facets(n: int) -> Facets:
+    """PAPER.md:368-370 Example 1: n equidistant facets on a straight line; facet i is the
+    interval [i-1/2, i+1/2] on the x axis (the facet-extent boxes that reproduce Fig. 1)."""
+    c = np.zeros((n, 3))
+    c[:, 0] = np.arange(n, dtype=np.float64)
+    nrm = np.zeros((n, 3))
+    nrm[:, 1] = 1.0
+    aabb = np.zeros((n, 6))
+    aabb[:, 0] = c[:, 0] - 0.5
+    aabb[:, 3] = c[:, 0] + 0.5
+    return Facets(c, nrm, np.ones(n), aabb, None, f"line{n}")
+
+
+# ----------------------------------------------------------------------------- configs
+@dataclass
+class Config:
+    cfg: int
+    name: str
+    facets: Facets
+    emissivity: np.ndarray
+    T: np.ndarray              # (n, nrhs) temperatures in K, external order
+    n_min: int
+    eta: float
+    eps_aca: float
+    seed: int
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def n(self):
+        return self.facets.n
+
+    def rhs(self) -> np.ndarray:
+        """x = sigma T^4 (eq:emission with eps=1)."""
+        return SIGMA_SB * self.T ** 4
+
+
+def temperatures(seed: int, n: int, nrhs: int) -> np.ndarray:
+    T = np.empty((n, nrhs))
+    for c in range(nrhs):
+        T[:, c] = 300.0 + 700.0 * uniform(stream_seed(seed, 1 + c), n)
+    return T
+
+
+def emissivities(seed: int, n: int, lo=0.3, hi=0.95) -> np.ndarray:
+    return lo + (hi - lo) * uniform(stream_seed(seed, 0), n)
+
+
+def make_config(cfg: int, *, exact: bool = False, geometry: Facets | None = None,
+                nrhs: int | None = None, cyl=(1000, 40)) -> Config:
+    """BASELINE.json configs[cfg-1].  `geometry` overrides the
+    mesh (used for small parity cases with the same recipe)."""
+    seed = SEED_BASE + cfg
+    if cfg == 1:
+        f = geometry or icosphere(3, exact)
+        n_min, eps_aca = 64, 1e-6
+    elif cfg == 2:
+        f = geometry or icosphere(5, exact)
+        n_min, eps_aca = 64, 1e-6
+    elif cfg == 3:
+        f = geometry or cylinder(*cyl)
+        n_min, eps_aca = 64, 1e-6
+    elif cfg == 4:
+        f = geometry or icosphere(7, exact)
+        n_min, eps_aca = 128, 1e-6
+    elif cfg == 5:
+        f = geometry or icosphere(8, exact)
+        n_min, eps_aca = 128, 1e-5
+    else:
+        raise ValueError(cfg)
+    n = f.n
+    eps = np.full(n, 0.8) if cfg == 1 else emissivities(seed, n)
+    r = nrhs if nrhs is not None else (64 if cfg == 5 else 1)
+    T = temperatures(seed, n, r)
+    return Config(cfg, f"C{cfg}:{f.name}", f, eps, T, n_min, 1.0, eps_aca, seed)
+
+
+def step_perturbation(cfg_seed: int, step: int, n: int) -> np.ndarray:
+    """Config 3 time-step emulation: T <- T + 5 N(0,1) per step (reading R18)."""
+    return 5.0 * normal(stream_seed(cfg_seed, 1000 + step), n)

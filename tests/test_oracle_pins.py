@@ -1,0 +1,367 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU needed).
+
+Each test names the passage it pins.  None of them retypes the oracle's formula:
+they compare against closed forms, library routines, invariants, brute force or
+values printed in the paper (tests/golden/).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import aca, hmatrix, tree
+from oracle import viewfactor as vf
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ generator invariants
+def test_splitmix64_reference_vector():
+    # SplitMix64 reference outputs for state 1234567 (public test vector of the generator).
+    assert list(synth.splitmix64(1234567, 3)) == [6457827717110365317, 3203168211198807973, 9817491932198370423]
+
+
+@pytest.mark.parametrize("sub", [0, 1, 2, 3])
+def test_icosphere_counts_closure_inward(sub):
+    f = synth.icosphere(sub)
+    assert f.n == 20 * 4 ** sub
+    # closed surface: sum A_i n_i = 0
+    assert np.abs((f.area[:, None] * f.normal).sum(0)).max() < 1e-13
+    assert (np.einsum("ij,ij->i", f.normal, f.centroid) < 0).all()        # into the cavity
+    assert np.allclose(np.linalg.norm(f.normal, axis=1), 1.0, atol=1e-15)
+
+
+def test_cylinder_counts_closure():
+    f = synth.cylinder(40, 8)
+    assert f.n == 2 * 40 * 8 + 2 * 40
+    assert np.abs((f.area[:, None] * f.normal).sum(0)).max() < 1e-13
+    wall_area = 2 * 40 * math.sin(math.pi / 40) * 4.0       # inscribed prism wall
+    assert abs(f.area[:640].sum() - wall_area) < 1e-12
+
+
+# ------------------------------------------------------------------ entry kernel
+@pytest.mark.parametrize("sub", [0, 1, 2, 3])
+def test_entry_sphere_exact_closed_form(sub):
+    """Two points on a sphere: cos(phi_i) = cos(phi_j) = r/2R, so eq:Fdef_new_location's
+    one-point rule gives F_ij = A_i A_j / (4 pi R^2) (BASELINE.json north_star closed form,
+    in the paper's unnormalised convention, reading R1)."""
+    f = synth.icosphere(sub, exact=True)
+    F = vf.dense_F(f.centroid, f.normal, f.area)
+    a = f.area
+    Fcl = (np.outer(a, a) - np.diag(a * a)) / (4.0 * math.pi)
+    assert np.abs(F - Fcl).max() <= 1e-13 * Fcl.max()
+
+
+def test_reciprocity_nonneg_zero_diagonal(cfg1):
+    """A_i F^std_ij = A_j F^std_ji: the paper's F is symmetric -- bitwise
+    with the canonical pair order; F_ii = 0; F >= 0."""
+    f = cfg1.facets
+    F = vf.dense_F(f.centroid, f.normal, f.area)
+    assert (F == F.T).all()
+    assert (np.diag(F) == 0).all()
+    assert (F >= 0).all()
+    # entry order independence: evaluating (j, i) gives the same bits as (i, j)
+    i = np.arange(0, f.n, 7)
+    j = (i * 13 + 5) % f.n
+    assert (vf.entry_pairs(f.centroid, f.normal, f.area, i, j) ==
+            vf.entry_pairs(f.centroid, f.normal, f.area, j, i)).all()
+
+
+def test_cylinder_coplanar_zero():
+    """Coplanar facets (cap-cap) see each other at cos = 0 exactly -> F_ij = 0."""
+    f = synth.cylinder(40, 8)
+    caps = np.arange(640, 720)
+    F = vf.dense_F(f.centroid, f.normal, f.area)
+    assert (F[np.ix_(caps[:40], caps[:40])] == 0).all()
+    assert (F[np.ix_(caps[40:], caps[40:])] == 0).all()
+    assert (F[np.ix_(caps[:40], caps[40:])] > 0).all()     # bottom sees top
+
+
+def test_degenerate_pair_raises():
+    f = synth.icosphere(0)
+    c = f.centroid.copy()
+    c[1] = c[0]
+    with pytest.raises(vf.DegenerateGeometry):
+        vf.entry_pairs(c, f.normal, f.area, np.array([0]), np.array([1]))
+
+
+def test_flat_convergence_order_h2():
+    """Flat one-point icospheres converge to the sphere closed form F_cl = (aa^T-diag a^2)/4pi
+    in the operator sense at O(h^2) (SURVEY.md §8(c) pins: ratio 4 per subdivision)."""
+    errs = []
+    for sub in (2, 3, 4):
+        f = synth.icosphere(sub)
+        F = vf.dense_F(f.centroid, f.normal, f.area)
+        a = f.area
+        x = synth.SIGMA_SB * (300.0 + 700.0 * synth.uniform(99, f.n)) ** 4
+        Fx = F @ x
+        Fcl = (a * (a @ x) - a * a * x) / (4.0 * math.pi)
+        errs.append(np.linalg.norm(Fx - Fcl) / np.linalg.norm(Fcl))
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert 3.3 < r1 < 4.7 and 3.3 < r2 < 4.7, errs
+
+
+def test_flat_row_sums_slightly_above_one(cfg1):
+    """eq:clamped_rowsum: flat one-point rows exceed 1 (reading R14) -> c = 1."""
+    f = cfg1.facets
+    F = vf.dense_F(f.centroid, f.normal, f.area)
+    s = vf.row_sums(F, f.area)
+    assert (s > 1.0).all() and (s < 1.01).all()
+    assert (vf.clamp_row_sums(s) == 1.0).all()
+    assert (vf.clamp_row_sums(np.array([-0.2, 0.4, 1.3])) == [0.0, 0.4, 1.0]).all()
+
+
+# ------------------------------------------------------------------ closed forms of F x and C^-1
+def _exact_setup(sub=3, seed=7):
+    f = synth.icosphere(sub, exact=True)
+    eps = synth.emissivities(seed, f.n)
+    a = f.area
+    k = 1.0 / (4.0 * math.pi)
+    cex = (a.sum() - a) * k           # s_i = (sum a - a_i) / 4pi < 1 -> c_i = s_i
+    return f, eps, a, k, cex
+
+
+def test_Fx_closed_form_sphere_exact_scaled():
+    f, eps, a, k, cex = _exact_setup()
+    F, C, cvec = vf.dense_operators(f, eps)
+    assert np.allclose(cvec, cex, rtol=1e-13, atol=0)
+    x = synth.uniform(3, f.n)
+    ycl = k * (a * (a @ x) - a * a * x) / cex
+    assert np.linalg.norm(F @ x - ycl) <= 1e-14 * np.linalg.norm(ycl)
+
+
+def test_Cinv_sherman_morrison_sphere_exact():
+    """C = M - k b a^T with M = diag(1 + k b_i a_i), b_i = (1-eps_i)/c_i: Sherman-Morrison
+    gives C^-1 x in O(n) (SURVEY.md §8(c) pins)."""
+    f, eps, a, k, cex = _exact_setup()
+    F, C, _ = vf.dense_operators(f, eps)
+    b = (1.0 - eps) / cex
+    Md = 1.0 + k * b * a
+    x = synth.uniform(5, f.n)
+    Mx = x / Md
+    Mb = b / Md
+    zcl = Mx + (k * (a @ Mx) / (1.0 - k * (a @ Mb))) * Mb
+    z = vf.solve(C, x)
+    assert np.linalg.norm(z - zcl) <= 1e-13 * np.linalg.norm(zcl)
+
+
+def test_own_lu_matches_lapack(cfg1):
+    """The oracle's textbook partial-pivot LU vs LAPACK gesv (library routine)."""
+    f = synth.icosphere(2)
+    eps = synth.emissivities(11, f.n)
+    F, C, _ = vf.dense_operators(f, eps)
+    b = synth.uniform(12, f.n)
+    LU, piv = vf.lu_partial_pivot(C)
+    z = vf.lu_solve(LU, piv, b)
+    zl = np.linalg.solve(C, b)
+    assert np.linalg.norm(z - zl) <= 1e-14 * np.linalg.norm(zl)
+    assert np.linalg.norm(C @ z - b) <= 1e-14 * np.linalg.norm(b)
+
+
+def test_blackbody_identity():
+    """eps = 1 -> Lambda = 0 -> C = I."""
+    f = synth.icosphere(1)
+    F, C, _ = vf.dense_operators(f, np.ones(f.n))
+    assert (C == np.eye(f.n)).all()
+    b = synth.uniform(4, f.n)
+    assert (vf.solve(C, b) == b).all()
+
+
+def test_reflection_diagonally_dominant(cfg1):
+    """DESIGN.md reading R12: no pivoting needed -- max_i (1-eps_i) s_i < 1."""
+    f = synth.icosphere(3)
+    eps = synth.emissivities(2305068912, f.n)
+    F, C, _ = vf.dense_operators(f, eps)
+    off = np.abs(C).sum(1) - np.abs(np.diag(C))
+    assert (off < np.abs(np.diag(C))).all()
+
+
+# ------------------------------------------------------------------ flux
+def test_flux_literal_equals_operator_form():
+    """eq:qi_new_location term by term == the operator form used on the hot path."""
+    f = synth.icosphere(0)
+    eps = synth.emissivities(3, f.n)
+    T = 300.0 + 700.0 * synth.uniform(4, f.n)
+    F, C, _ = vf.dense_operators(f, eps)
+    q1 = vf.flux_literal(F, C, f.area, eps, T)
+    q2 = vf.flux_from_dense(F, C, f.area, eps, T)[:, 0]
+    assert np.linalg.norm(q1 - q2) <= 1e-12 * np.linalg.norm(q1)
+
+
+def test_flux_energy_conservation_and_uniform_T(cfg1):
+    """Symmetric F => F C^-1 = F (I - Lambda F)^-1 symmetric => sum_i A_i q_i = 0 for any T
+    (eq:Rdef); uniform T => q = 0 (Rbar 1 = 0, eq:Rbardef)."""
+    f = cfg1.facets
+    eps = synth.emissivities(5, f.n)
+    F, C, _ = vf.dense_operators(f, eps)
+    T = cfg1.T[:, 0]
+    q = vf.flux_from_dense(F, C, f.area, eps, T)[:, 0]
+    assert abs(f.area @ q) <= 1e-13 * (f.area @ np.abs(q))
+    qu = vf.flux_from_dense(F, C, f.area, eps, np.full(f.n, 640.0))[:, 0]
+    assert np.abs(qu).max() <= 1e-12 * synth.SIGMA_SB * 640.0 ** 4
+
+
+# ------------------------------------------------------------------ trees (Alg. 1, Alg. 2)
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_fig1_block_structure(n):
+    """PAPER.md Fig. 1 (lines 371-589): 1-D line, n_min = 1, facet-extent boxes, eta = 1."""
+    f = synth.line_facets(n)
+    t = tree.build_cluster_tree(f.centroid, 1, f.aabb, adm_mode=1)
+    got = sorted((b.row.begin, b.row.end, b.col.begin, b.col.end, int(b.admissible))
+                 for b in tree.build_block_tree(t, 1.0))
+    exp = sorted(tuple(map(int, ln.split())) for ln in open(os.path.join(GOLDEN, f"fig1_n{n}.txt"))
+                 if not ln.startswith("#"))
+    assert got == exp
+
+
+def _check_partition(blocks, n):
+    cover = np.zeros((n, n), dtype=np.int32)
+    for b in blocks:
+        cover[b.row.begin:b.row.end, b.col.begin:b.col.end] += 1
+    assert (cover == 1).all()
+    assert sum(b.row.size * b.col.size for b in blocks) == n * n
+
+
+@pytest.mark.parametrize("geom", ["ico3", "cyl", "ico2-facetbox"])
+def test_partition_property(geom):
+    if geom == "cyl":
+        f, n_min, mode = synth.cylinder(40, 8), 64, 0
+    elif geom == "ico3":
+        f, n_min, mode = synth.icosphere(3), 64, 0
+    else:
+        f, n_min, mode = synth.icosphere(2), 16, 1
+    t = tree.build_cluster_tree(f.centroid, n_min, f.aabb, mode)
+    assert sorted(t.perm.tolist()) == list(range(f.n))
+    assert all(l.size <= n_min for l in t.leaves)
+    assert sum(l.size for l in t.leaves) == f.n
+    assert [l.begin for l in t.leaves] == sorted(l.begin for l in t.leaves)
+    for c in t.nodes:                       # every internal node has two children, ceil/floor split
+        if c.children:
+            assert len(c.children) == 2 and c.children[0].size == (c.size + 1) // 2
+    blocks = tree.build_block_tree(t, 1.0)
+    _check_partition(blocks, f.n)
+    for b in blocks:
+        assert b.row.level == b.col.level
+        if b.admissible:
+            assert tree.admissible(b.row, b.col, 1.0)
+        else:
+            assert b.row.is_leaf or b.col.is_leaf
+
+
+def test_split_is_median_on_longest_axis():
+    rng = np.random.default_rng(0)
+    c = rng.random((37, 3)) * np.array([1.0, 5.0, 2.0])
+    t = tree.build_cluster_tree(c, 4)
+    left, right = t.root.children
+    ys_l = c[t.perm[left.begin:left.end], 1]
+    ys_r = c[t.perm[right.begin:right.end], 1]
+    assert left.size == 19 and ys_l.max() <= ys_r.min()        # axis y is the longest
+
+
+def test_admissibility_arithmetic():
+    """SPEC.md:208-210 examples: unit-diameter clusters at distance 0.6 with c = 2 are
+    admissible (1 <= 1.2), at 0.4 not; identical clusters never; singletons at d > 0 always."""
+    C = tree.Cluster
+    s = C(0, 1, 0, (0.0, 0.0, 0.0), (1.0, 0.0, 0.0))
+    t06 = C(0, 1, 0, (1.6, 0.0, 0.0), (2.6, 0.0, 0.0))
+    t04 = C(0, 1, 0, (1.4, 0.0, 0.0), (2.4, 0.0, 0.0))
+    assert tree.admissible(s, t06, 2.0) and not tree.admissible(s, t04, 2.0)
+    assert not tree.admissible(s, s, 2.0)
+    p = C(0, 1, 0, (0.0, 0.0, 0.0), (0.0, 0.0, 0.0))
+    q = C(0, 1, 0, (0.0, 3.0, 0.0), (0.0, 3.0, 0.0))
+    assert tree.admissible(p, q, 1.0) and not tree.admissible(p, p, 1.0)
+
+
+def test_nmin_ge_n_single_dense_leaf():
+    """n_min >= n -> one dense leaf -> the H-apply is the dense product."""
+    f = synth.icosphere(1)
+    H = hmatrix.assemble(f, 1000, 1.0, 1e-6, closed=False)
+    assert len(H.blocks) == 1 and H.blocks[0].kind == hmatrix.KIND_DENSE
+    F = vf.dense_F(f.centroid, f.normal, f.area)
+    x = synth.uniform(1, f.n)
+    assert np.linalg.norm(H.apply(x) - F @ x) <= 1e-15 * np.linalg.norm(F @ x)
+
+
+# ------------------------------------------------------------------ ACA
+def test_aca_textbook_cases():
+    rng = np.random.default_rng(1)
+    u, v = rng.random(30), rng.random(20)
+    r = aca.aca_matrix(np.outer(u, v), 1e-10)
+    assert r.rank == 1
+    assert aca.aca_matrix(np.zeros((12, 9)), 1e-6).rank == 0
+    for rk in (2, 5, 8):
+        X = rng.standard_normal((50, rk)) @ rng.standard_normal((rk, 40))
+        r = aca.aca_matrix(X, 1e-12)
+        assert r.rank == rk
+        assert np.linalg.norm(X - r.U @ r.V.T) <= 1e-10 * np.linalg.norm(X)
+
+
+def test_aca_cross_interpolates_pivots():
+    """eq:aca: the approximant reproduces X exactly on the chosen rows and columns."""
+    rng = np.random.default_rng(2)
+    X = 1.0 / (1.0 + np.add.outer(rng.random(40) * 3 + 4, rng.random(30)))   # smooth kernel
+    r = aca.aca_matrix(X, 1e-8)
+    R = X - r.U @ r.V.T
+    assert r.rank >= 3
+    assert np.linalg.norm(R) <= 1e-6 * np.linalg.norm(X)
+    # cross interpolation: exact (to rounding) on the pivot rows and columns
+    assert np.abs(R[r.rows, :]).max() <= 1e-13 * np.abs(X).max()
+    assert np.abs(R[:, r.cols]).max() <= 1e-13 * np.abs(X).max()
+    # and equal to X(:,C) X(R,C)^-1 X(R,:) of eq:aca
+    Xcross = X[:, r.cols] @ np.linalg.solve(X[np.ix_(r.rows, r.cols)], X[r.rows, :])
+    assert np.linalg.norm(Xcross - r.U @ r.V.T) <= 1e-10 * np.linalg.norm(X)
+
+
+def test_aca_rank_vs_svd_rank_config1():
+    """SPEC.md:659 acceptance 4: ACA rank <= 2x SVD eps-rank on every admissible block (C1)."""
+    cfg = synth.make_config(1)
+    H = hmatrix.assemble(cfg.facets, cfg.n_min, cfg.eta, cfg.eps_aca, closed=False)
+    f = cfg.facets
+    c, nrm, A = f.centroid[H.perm], f.normal[H.perm], f.area[H.perm]
+    lr = [b for b in H.blocks if b.admissible]
+    assert len(lr) == 332
+    ratios = []
+    for b in lr[::4]:
+        I, J = np.meshgrid(np.arange(b.r0, b.r1), np.arange(b.c0, b.c1), indexing="ij")
+        X = vf.entry_pairs(c, nrm, A, I.ravel(), J.ravel()).reshape(I.shape)
+        ks = aca.svd_eps_rank(X, cfg.eps_aca)
+        assert b.rank <= 2 * ks
+        ratios.append(b.rank / ks)
+        assert np.linalg.norm(X - b.U @ b.V.T) <= 5 * cfg.eps_aca * np.linalg.norm(X)
+    assert 1.0 <= np.mean(ratios) < 1.6
+
+
+def test_aca_sphere_exact_all_rank_one():
+    """Admissible blocks of a sphere-exact icosphere are exactly A_s A_t^T / 4pi: rank 1."""
+    f = synth.icosphere(3, exact=True)
+    H = hmatrix.assemble(f, 64, 1.0, 1e-6)
+    P = H.partition()
+    assert set(P[P[:, 5] == 1, 7].tolist()) == {1}
+
+
+def test_hmatrix_apply_within_tolerance_config1(cfg1):
+    """H-apply vs dense oracle within 10 eps_ACA (BASELINE.json north_star)."""
+    f = cfg1.facets
+    H = hmatrix.assemble(f, cfg1.n_min, cfg1.eta, cfg1.eps_aca)
+    F, C, cvec = vf.dense_operators(f, cfg1.emissivity)
+    x = cfg1.rhs()[:, 0]
+    assert np.linalg.norm(H.apply(x) - F @ x) <= 10 * cfg1.eps_aca * np.linalg.norm(F @ x)
+    assert np.allclose(H.cvec, cvec)
+    # Table-2-style F error: relative Frobenius error well below eps
+    Fi = vf.dense_F(f.centroid[H.perm], f.normal[H.perm], f.area[H.perm])
+    err = np.linalg.norm(H.to_dense_internal() - Fi) / np.linalg.norm(Fi)
+    assert err < cfg1.eps_aca
+
+
+def test_sampled_rows_match_dense(cfg1):
+    f = cfg1.facets
+    F, C, _ = vf.dense_operators(f, cfg1.emissivity)
+    rows = synth.sample_rows(synth.stream_seed(cfg1.seed, 999), f.n, 50)
+    X = cfg1.rhs()
+    Y = vf.sampled_apply(f.centroid, f.normal, f.area, rows, X)
+    assert np.allclose(Y, (F @ X)[rows], rtol=1e-13, atol=0)
+    Z = vf.solve(C, X)
+    r = vf.sampled_residual(f.centroid, f.normal, f.area, cfg1.emissivity, rows, Z, X)
+    assert np.abs(r).max() <= 1e-12 * np.abs(X).max()
