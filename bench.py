@@ -1,0 +1,292 @@
+"""H-apply benchmark: one step = one radiative-flux evaluation = one level-scheduled C^-1 solve
++ one H-matrix apply of F (+ O(n) prologue/epilogue), i.e. BASELINE.json's metric
+"H-apply (F x + C^-1 solve)" on the configuration it is quoted on (configs[1] = C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+Prints ONE JSON line (rank 0).  Multi-GPU (torchrun): every rank runs an independent replica
+of the workload (row-cluster sharding is not in this build), timed with
+a barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("H-apply (F·x + C⁻¹ solve) applies/sec and achieved HBM GB/s vs B200 peak, "
+          "1/2/4/8 GPU")
+FALLBACK_HBM = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (GB/s), used if no MEASURED_PEAKS.json
+
+
+def workload_desc(cfg) -> str:
+    f = cfg.facets
+    if cfg.cfg == 2:
+        return (f"C2: closed unit-sphere icosphere sub 5 ({f.n} flat facets), one-point quadrature, "
+                f"eps~U[0.3,0.95], eps_ACA=1e-6, eta=1.0, n_min=64, 1 RHS sigma T^4, T~U[300,1000] K")
+    return f"C{cfg.cfg}: {f.name} ({f.n} facets), eps_ACA={cfg.eps_aca}, n_min={cfg.n_min}"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg, budget_rows=256, sub_n=4096):
+    """The oracle as it stands on the host cores, on a bounded sample of the C2 step:
+    (i) oracle matrix-free F x (direct kernel summation) on `budget_rows` seeded rows, scaled
+    by n/rows; (ii) oracle C^-1 b (dense LAPACK gesv, as oracle.viewfactor.solve does every
+    call) on the leading sub_n x sub_n principal block of C, scaled by (n/sub_n)^3."""
+    import synth
+    from oracle import viewfactor as vf
+    f = cfg.facets
+    n = f.n
+    rows = synth.sample_rows(synth.stream_seed(cfg.seed, 999), n, budget_rows)
+    x = cfg.rhs()
+    t0 = time.perf_counter()
+    vf.sampled_apply(f.centroid, f.normal, f.area, rows, x)
+    t_fx = (time.perf_counter() - t0) * n / len(rows)
+    m = min(sub_n, n)
+    idx = np.arange(m)
+    I, J = np.meshgrid(idx, idx, indexing="ij")
+    Fs = vf.entry_pairs(f.centroid, f.normal, f.area, I.ravel(), J.ravel()).reshape(m, m)
+    Cs = vf.reflection_matrix(Fs, f.area[:m], cfg.emissivity[:m])
+    t0 = time.perf_counter()
+    vf.solve(Cs, x[:m, 0])
+    t_solve = (time.perf_counter() - t0) * (n / m) ** 3
+    step = t_fx + t_solve
+    return {"value": 1.0 / step, "unit": "applies/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": (f"oracle F x by direct summation on {len(rows)} seeded rows (x n/{len(rows)}) + "
+                       f"oracle dense gesv C^-1 b on the leading {m}x{m} block of C (x (n/{m})^3); "
+                       f"per-step estimate {step:.2f} s")}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands."""
+    import synth
+    if rank != 0:
+        return
+    cfg = synth.make_config(args.config)
+    cb = None
+    for _ in range(args.warmup):
+        cb = cpu_baseline(cfg, budget_rows=64, sub_n=1024)
+    vals = []
+    for _ in range(args.steps):
+        cb = cpu_baseline(cfg, budget_rows=128, sub_n=2048)
+        vals.append(1.0 / cb["value"])
+    step = float(np.mean(vals))
+    out = {"impl": "reference", "metric": METRIC, "value": 1.0 / step, "unit": "applies/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": workload_desc(cfg), "n": cfg.n, "parallelism": "cpu-oracle"},
+           "cpu_baseline": {"kind": "oracle", "cores": os.cpu_count(), "sample": cb["sample"], "value": 1.0 / step,
+                            "unit": "applies/s"},
+           "e2e": {"value": 1.0 / step, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-iters", type=int, default=20)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2305_06891_b200 as hm
+    import synth
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cfg = synth.make_config(args.config)
+    f = cfg.facets
+    n = f.n
+    ctx = hm.hm_init(local)
+    t0 = time.perf_counter()
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    setup_wall = time.perf_counter() - t0
+    rep = hm.hm_storage_report(F, LU)
+    stream = torch.cuda.current_stream()
+    T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+    q = torch.empty_like(T)
+
+    def step():
+        hm.hm_radiative_flux(ctx, F, LU, T, q, stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+
+    # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
+    Th = torch.from_numpy(cfg.T[:, 0].copy()).pin_memory()
+    qh = torch.empty(n, dtype=torch.float64).pin_memory()
+    Th_np, qh_np = Th.numpy(), qh.numpy()
+    for _ in range(2):
+        hm.hm_radiative_flux(ctx, F, LU, Th_np, qh_np, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        hm.hm_radiative_flux(ctx, F, LU, Th_np, qh_np, stream=stream.cuda_stream)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+
+    # ---- per-kernel-class breakdown with CUDA events on the launching stream
+    cls_ms, cls_launch = hm.hm_profile_flux(ctx, F, LU, T, q, args.profile_iters, stream=stream.cuda_stream)
+    cls_bytes = {"prologue": 16 * n, "F_phase1": rep["bytes_F_phase1"], "F_phase2": rep["bytes_F_phase2"],
+                 "solve_phase1": None, "solve_phase2": None, "leaf_solves": rep["bytes_C_leaf"]}
+    peak, peak_src = peaks()
+    # dominant class by time among those with known algorithmic bytes
+    dom = max(["F_phase1", "F_phase2", "leaf_solves"], key=lambda k: cls_ms[k])
+    sol_ms = cls_ms["solve_phase1"] + cls_ms["solve_phase2"] + cls_ms["leaf_solves"]
+    bytes_step = rep["bytes_F"] + rep["bytes_C"]
+    achieved = cls_bytes[dom] / (cls_ms[dom] / cls_launch[dom]) / 1e6 / cls_launch[dom] * cls_launch[dom]
+    achieved = cls_bytes[dom] / (cls_ms[dom] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+    launches = int(1 + rep["launches_solve_C"] + rep["launches_apply_F"] - 1)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "n": n, "parallelism": "replicas" if world > 1 else "single",
+                       "l2": f"no flush: stored operator bytes per step {bytes_step/1e9:.3f} GB > 126 MB L2",
+                       "stored_bytes_per_step": bytes_step, "bytes_F": rep["bytes_F"], "bytes_C": rep["bytes_C"],
+                       "step_hbm_gbs": bytes_step / (ms_step * 1e-3) / 1e9,
+                       "step_frac_of_peak": bytes_step / (ms_step * 1e-3) / 1e9 / peak,
+                       "kernel_ms": cls_ms, "kernel_launches": cls_launch,
+                       "solve_ms": sol_ms, "apply_ms": cls_ms["F_phase1"] + cls_ms["F_phase2"],
+                       "ranks_F": {"mean": rep["rank_mean"], "max": rep["rank_max"]},
+                       "ranks_C": {"mean": rep["rank_mean_C"], "max": rep["rank_max_C"]},
+                       "setup_s": dict(rep["setup_seconds"], wall=setup_wall)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
+            "e2e": {"value": world * args.steps / (ms_e2e / 1e3), "unit": "applies/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": launches * args.steps,
+        }
+        clk_s = clk.summary()
+        out["clocks"] = clk_s
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

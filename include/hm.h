@@ -1,0 +1,178 @@
+/*
+ * hm.h -- C ABI of the B200-native hierarchical block low-rank cavity-radiation hot path.
+ *
+ * Paper: Baburin, Ballani, Peterson, Knezevic, "Hierarchical block low-rank approximation of
+ * cavity radiation" (arXiv 2305.06891), reproduced as PAPER.md.  The hot path is the repeated
+ * application, inside every nonlinear/time step, of the compressed radiation operators:
+ *     y = F x          (H-matrix-vector product, "x -> F x ... recursively")
+ *     z = C^-1 b       (C = I - Lambda F, eq:reflection_matrix PAPER.md:159-162, applied as
+ *                        U^-1 (L^-1 b) with one-time block H-LU factors)
+ *     q = flux(T)      (eq:qi_new_location: one solve + one apply)
+ *
+ * Conventions (apply to every entry point):
+ *  - Every function returns hm_status; nothing throws across the ABI.  On failure
+ *    hm_last_error(ctx) returns a message (it names the facet pair or block when relevant).
+ *  - fp64 everywhere.  Vectors are facet-major n x nrhs (row i holds nrhs contiguous values)
+ *    in the caller's EXTERNAL facet order (the order of the geometry arrays).
+ *  - Setup calls (hm_build_geometry, hm_assemble_aca, hm_factor_hlu) take HOST arrays,
+ *    copy what they need, and are synchronous.
+ *  - hm_apply_F / hm_solve_C / hm_radiative_flux accept DEVICE pointers (stream-ordered,
+ *    asynchronous, no allocation after the first call with a given nrhs) or HOST pointers
+ *    (pageable or pinned: the library stages through its own device buffers on `stream` and
+ *    synchronises `stream` before returning).  `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream).
+ *  - Ownership: the caller owns all argument buffers.  The library owns its handles and all
+ *    device memory it allocates; hm_destroy_* / hm_finalize free them.  Handles are immutable
+ *    after setup and may be used from one host thread at a time.
+ *  - Asynchronous kernel faults surface as HM_ERR_CUDA at the next synchronising call;
+ *    environment HM_DEBUG=1 synchronises after every launch.
+ *  - There is no CPU fallback: without a CUDA device hm_init returns HM_ERR_CUDA.
+ */
+#ifndef HM_H_
+#define HM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HM_OK = 0,
+    HM_ERR_INVALID_ARG = 1,          /* bad size/pointer/parameter; call-order violation     */
+    HM_ERR_CUDA = 2,                 /* CUDA runtime error or no device                      */
+    HM_ERR_OOM = 3,                  /* device allocation failed (message has byte count)    */
+    HM_ERR_NCCL = 4,                 /* collective failure (world > 1)                       */
+    HM_ERR_DEGENERATE_GEOMETRY = 5,  /* r^2 == 0 for i != j, A_i <= 0, non-finite input      */
+    HM_ERR_SINGULAR = 6,             /* |pivot| < 1e-14 ||block|| in a leaf LU               */
+    HM_ERR_NOT_READY = 7,            /* handle not built / wrong handle combination          */
+    HM_ERR_UNSUPPORTED = 8           /* configuration outside what this build implements     */
+} hm_status;
+
+typedef struct hm_ctx hm_ctx;
+typedef struct hm_geom hm_geom;
+typedef struct hm_hmat hm_hmat;
+typedef struct hm_hlu hm_hlu;
+
+/* Alg. 1 / Alg. 2 parameters. */
+typedef struct {
+    int32_t n_min;     /* leaf iff #tau <= n_min; >= 1                          */
+    double eta;        /* admissibility constant c: min(diam,diam) <= c dist */
+    int32_t adm_mode;  /* 0: boxes of the centroid point clouds (paper text, default);
+                          1: boxes of the facet extents (facet_aabb required; reproduces Fig. 1) */
+} hm_tree_params;
+
+/* ACA parameters. */
+typedef struct {
+    double eps_aca;        /* eq:erel relative tolerance of the partial-pivot ACA stop test     */
+    int32_t k_max;         /* rank cap (<= 64; blocks reaching it are stored dense); 0 = 48     */
+    int32_t closed_cavity; /* 1: eq:rowsum / eq:clamped_rowsum / eqn:F_closed row scaling       */
+} hm_aca_params;
+
+/* H-LU parameters. */
+typedef struct {
+    double eps_lu;         /* truncation tolerance of the factor blocks; <= 0 -> eps_aca
+                              ("equal to the approximation accuracy used for F")   */
+} hm_lu_params;
+
+/* Storage / traffic accounting (bytes are fp64 payload bytes actually stored in HBM). */
+typedef struct {
+    int64_t n, n_leaves, depth;
+    int64_t n_blocks, n_dense, n_lowrank, n_adm_dense;
+    int64_t rank_max;
+    double rank_mean;                 /* over stored low-rank blocks of F                      */
+    int64_t bytes_F;                  /* dense + U + V of F                                    */
+    int64_t bytes_F_phase1;           /* V^T bytes (phase-1 kernel)                            */
+    int64_t bytes_F_phase2;           /* dense + U bytes (phase-2 kernel)                      */
+    int64_t bytes_C;                  /* level-form L/U factor blocks + leaf inverses          */
+    int64_t bytes_C_leaf;             /* leaf inverses part of bytes_C                         */
+    int64_t n_blocks_C, n_lowrank_C;
+    int64_t rank_max_C;
+    double rank_mean_C;
+    int64_t launches_apply_F;         /* kernels per hm_apply_F (nrhs = 1)                     */
+    int64_t launches_solve_C;         /* kernels per hm_solve_C (nrhs = 1)                     */
+    double setup_seconds[8];          /* tree, aca, dense-fill+pack, rowsum+scale, C-expand,
+                                         dense LU+W, W-compress+pack, flux constant g          */
+} hm_storage;
+
+/* ---- lifetime ------------------------------------------------------------------------- */
+/* device: CUDA ordinal; rank/world: SPMD position (world > 1 not supported in this build:
+   returns HM_ERR_UNSUPPORTED); nccl_unique_id: NULL; flags: reserved, pass 0. */
+hm_status hm_init(int device, int rank, int world, const void* nccl_unique_id, uint32_t flags,
+                  hm_ctx** ctx);
+void hm_finalize(hm_ctx* ctx);
+const char* hm_status_string(hm_status s);
+const char* hm_last_error(const hm_ctx* ctx);
+/* Optional device allocator hook (e.g. torch's caching allocator); NULL restores cudaMalloc. */
+hm_status hm_set_allocator(hm_ctx* ctx, void* (*alloc_fn)(size_t bytes, void* stream, void* user),
+                           void (*free_fn)(void* ptr, void* stream, void* user), void* user);
+
+/* ---- setup (timed separately from the hot path) ------------------------------------- */
+/* Facets: xyz = collocation points (n x 3), nrm = unit normals INTO the cavity (n x 3),
+   area (n), facet_aabb = per-facet lo_xyz,hi_xyz (n x 6; required iff adm_mode == 1).
+   Builds Alg. 1 (k-d split on the longest centroid-box axis, median by (coordinate, index),
+   left child ceil(m/2)) and Alg. 2 (admissible -> low-rank leaf; a leaf cluster on either
+   side -> dense leaf), flattened into level-ordered block lists. */
+hm_status hm_build_geometry(hm_ctx* ctx, int64_t n, const double* xyz, const double* nrm,
+                            const double* area, const double* facet_aabb,
+                            const hm_tree_params* params, hm_geom** out);
+/* Dense near field + batched partial-pivot ACA far field of F (eq:Fdef_new_location by the
+   one-point centroid rule), then (closed_cavity) row sums F_H 1 / A,
+   clamp and row scaling. */
+hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params* params,
+                          hm_hmat** F_out);
+/* One-time factorisation of C = I - Lambda F (Lambda_ii = (1-eps_i)/A_i) in the block
+   structure of F, stored in LEVEL FORM for the level-scheduled solve
+   (DESIGN.md §solve): per internal node t, W^L_t = L21 L11^-1 and W^U_t = U12 U22^-1
+   compressed to eps_lu in the block partition of F, plus dense leaf inverses.
+   emissivity: host array, n, external order, 0 < eps_i <= 1. */
+hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
+                        const hm_lu_params* params, hm_hlu** out);
+
+/* ---- hot path ------------------------------------------------------------------------- */
+/* y = F x (F is the stored, closed-cavity-scaled H-matrix; the paper's convention without
+   1/A_i, reading R1).  x, y: n x nrhs, external order; x and y must not overlap. */
+hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* F, int32_t nrhs, const double* x, double* y,
+                     void* stream);
+/* z ~= C^-1 b by level-scheduled forward then backward substitution. */
+hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LU, int32_t nrhs, const double* b, double* z,
+                     void* stream);
+/* q = sigma (eps/A) o (F C^-1 (eps o eta) - eta o g), eta = T^4, g = F C^-1 eps (cached at
+   factor time): eq:qi_new_location in operator form (R16).
+   T in K, q in W/m^2 (sigma = 5.670374419e-8, reading R2).  LU must have been
+   factored from F. */
+hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, int32_t nrhs,
+                            const double* T, double* q, void* stream);
+
+/* ---- introspection (host buffers) ----------------------------------------------------- */
+hm_status hm_export_perm(const hm_geom* geom, int32_t* perm /* n: perm[internal] = external */);
+/* Per leaf block, sorted by (row_begin, col_begin), 8 int64 each:
+   level, row_begin, row_end, col_begin, col_end, admissible, stored_kind (0 dense, 1 low-rank,
+   2 admissible-but-dense), rank.  Call with rows == NULL to get n_blocks only.  F may be NULL
+   (then stored_kind = !admissible ? 0 : 1 and rank = 0). */
+hm_status hm_export_partition(const hm_geom* geom, const hm_hmat* F, int64_t* n_blocks,
+                              int64_t* rows);
+/* Row sums s_i = (F_H 1)_i / A_i before scaling and clamped c_i (external order, n each). */
+hm_status hm_export_row_sums(const hm_hmat* F, double* s, double* c);
+hm_status hm_storage_report(const hm_hmat* F, const hm_hlu* LU, hm_storage* out);
+/* Internal-order shard of `rank` among `world` ranks (tree node at level log2(world)). */
+hm_status hm_local_range(const hm_geom* geom, int rank, int world, int64_t* begin, int64_t* end);
+
+/* ---- measurement support (bench.py) ---------------------------------------------------- */
+/* Times each kernel class of hm_radiative_flux (device pointers, nrhs = 1) with CUDA events on
+   `stream` over `iters` calls; ms_out[0..5] = per-call ms of: permute/prologue, F phase 1,
+   F phase 2 (+epilogue), solve phase 1 (all levels), solve phase 2 (all levels), leaf solves.
+   launches_out[0..5] = kernel launches per call of each class. */
+hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, const double* T,
+                          double* q, int32_t iters, double* ms_out, int64_t* launches_out,
+                          void* stream);
+
+void hm_destroy_geom(hm_geom* geom);
+void hm_destroy_hmat(hm_hmat* F);
+void hm_destroy_hlu(hm_hlu* LU);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HM_H_ */

@@ -13,7 +13,10 @@ paper; this follows DESIGN.md reading R10 step by step:
   (f) nu2 = |u|^2, nv2 = |v|^2, X2 = sum_l (u.U_l)(v.V_l), S2' = S2 + nu2 nv2 + 2 X2
   (g) nu2 nv2 <= eps^2 S2'  -> stop, discard this cross
   (h) append (u, v), k += 1, S2 = S2', mark i*, j* used
-  (i) k == min(m, n) -> stop
+  (i) k == kcap -> stop; kcap = min(k_max, ceil(m n / (m + n))), i.e. as soon as the factors
+      would be at least as large as the dense block (or reach the rank cap k_max = 48) the
+      block is stored dense with exact entries (reading R10: identical storage to
+      stopping at k == min(m, n), since such blocks are stored dense either way)
   (j) i* = argmax_{i unused} |u_i| (lowest i on ties)
 """
 from __future__ import annotations
@@ -36,7 +39,9 @@ class ACAResult:
         return self.U.shape[1]
 
 
-def aca_partial(row_fn, col_fn, m: int, n: int, eps: float) -> ACAResult:
+def aca_partial(row_fn, col_fn, m: int, n: int, eps: float, kcap: int | None = None) -> ACAResult:
+    if kcap is None:
+        kcap = min(m, n)
     Us: list = []
     Vs: list = []
     k = 0
@@ -85,7 +90,7 @@ def aca_partial(row_fn, col_fn, m: int, n: int, eps: float) -> ACAResult:
         S2 = S2n
         used_r[istar] = True
         used_c[jstar] = True
-        if k == min(m, n):                                           # (i)
+        if k == kcap:                                                # (i)
             break
         if used_r.all():
             break
@@ -97,9 +102,14 @@ def aca_partial(row_fn, col_fn, m: int, n: int, eps: float) -> ACAResult:
     return ACAResult(U, V, margin, prow, pcol)
 
 
-def aca_matrix(X: np.ndarray, eps: float) -> ACAResult:
+def aca_matrix(X: np.ndarray, eps: float, kcap: int | None = None) -> ACAResult:
     """ACA of an explicit matrix (used by the textbook pins)."""
-    return aca_partial(lambda i: X[i, :], lambda j: X[:, j], X.shape[0], X.shape[1], eps)
+    return aca_partial(lambda i: X[i, :], lambda j: X[:, j], X.shape[0], X.shape[1], eps, kcap)
+
+
+def storage_cap(m: int, n: int, k_max: int = 48) -> int:
+    """min(k_max, smallest k with k (m + n) >= m n): reaching it means 'store dense'."""
+    return min(k_max, (m * n + m + n - 1) // (m + n))
 
 
 def svd_eps_rank(X: np.ndarray, eps: float) -> int:

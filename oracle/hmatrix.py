@@ -44,6 +44,7 @@ class HMatrix:
     blocks: list
     cvec: np.ndarray          # clamped row sums, EXTERNAL order
     closed: bool
+    svec: np.ndarray | None = None   # row sums s_i = (F_H 1)_i / A_i before clamping, EXTERNAL order
 
     def partition(self) -> np.ndarray:
         """(nb, 8): level, r0, r1, c0, c1, admissible, kind, rank (sorted by r0, c0)."""
@@ -89,7 +90,7 @@ class HMatrix:
 
 
 def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True,
-             adm_mode: int = 0) -> HMatrix:
+             adm_mode: int = 0, k_max: int = 48) -> HMatrix:
     """Trees (Alg. 1, 2), dense near field, partial-pivot ACA far field, then row sums
     and closed-cavity scaling of the row factors (U and dense rows)."""
     tr = _tree.build_cluster_tree(facets.centroid, n_min, facets.aabb, adm_mode)
@@ -105,13 +106,14 @@ def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True
         cols = np.arange(c0, c1)
         hb = HBlock(blk.level, r0, r1, c0, c1, blk.admissible, KIND_DENSE, 0)
         if blk.admissible:
+            kcap = _aca.storage_cap(m, n, k_max)
             res = _aca.aca_partial(
                 lambda i: _vf.entry_pairs(c, nrm, A, np.full(n, r0 + i), cols),
                 lambda j: _vf.entry_pairs(c, nrm, A, rows, np.full(m, c0 + j)),
-                m, n, eps_aca)
+                m, n, eps_aca, kcap)
             hb.margin = res.margin
             k = res.rank
-            if k * (m + n) >= m * n:
+            if k >= kcap:
                 hb.kind, hb.rank = KIND_ADM_DENSE, k
             else:
                 hb.kind, hb.rank, hb.U, hb.V = KIND_LR, k, res.U, res.V
@@ -126,6 +128,9 @@ def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True
     cvec = np.empty_like(c_int)
     cvec[perm] = c_int
     H.cvec = cvec
+    svec = np.empty_like(s_int)
+    svec[perm] = s_int
+    H.svec = svec
     if closed:
         inv = np.where(c_int != 0.0, c_int, 1.0)
         for b in blocks:

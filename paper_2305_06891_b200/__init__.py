@@ -1,0 +1,292 @@
+"""Thin Python binding of the hm C ABI (include/hm.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libhm.so; this module only converts
+numpy arrays / torch tensors into pointers and status codes into exceptions.  There is no
+CPU fallback: if libhm.so is missing or no CUDA device is present, the calls raise.
+
+Names are the C ABI's: hm_init, hm_build_geometry, hm_assemble_aca, hm_factor_hlu,
+hm_apply_F, hm_solve_C, hm_radiative_flux, hm_export_perm, hm_export_partition,
+hm_export_row_sums, hm_storage_report, hm_local_range, hm_profile_flux, hm_destroy_*.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhm.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "hm.h")
+
+STATUS = {0: "HM_OK", 1: "HM_ERR_INVALID_ARG", 2: "HM_ERR_CUDA", 3: "HM_ERR_OOM", 4: "HM_ERR_NCCL",
+          5: "HM_ERR_DEGENERATE_GEOMETRY", 6: "HM_ERR_SINGULAR", 7: "HM_ERR_NOT_READY",
+          8: "HM_ERR_UNSUPPORTED"}
+
+
+class HMError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class hm_tree_params(C.Structure):
+    _fields_ = [("n_min", C.c_int32), ("eta", C.c_double), ("adm_mode", C.c_int32)]
+
+
+class hm_aca_params(C.Structure):
+    _fields_ = [("eps_aca", C.c_double), ("k_max", C.c_int32), ("closed_cavity", C.c_int32)]
+
+
+class hm_lu_params(C.Structure):
+    _fields_ = [("eps_lu", C.c_double)]
+
+
+class hm_storage(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_leaves", C.c_int64), ("depth", C.c_int64),
+                ("n_blocks", C.c_int64), ("n_dense", C.c_int64), ("n_lowrank", C.c_int64),
+                ("n_adm_dense", C.c_int64), ("rank_max", C.c_int64), ("rank_mean", C.c_double),
+                ("bytes_F", C.c_int64), ("bytes_F_phase1", C.c_int64), ("bytes_F_phase2", C.c_int64),
+                ("bytes_C", C.c_int64), ("bytes_C_leaf", C.c_int64), ("n_blocks_C", C.c_int64),
+                ("n_lowrank_C", C.c_int64), ("rank_max_C", C.c_int64), ("rank_mean_C", C.c_double),
+                ("launches_apply_F", C.c_int64), ("launches_solve_C", C.c_int64),
+                ("setup_seconds", C.c_double * 8)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "setup_seconds"}
+        d["setup_seconds"] = dict(zip(["tree", "aca", "fill_pack", "rowsum_scale", "c_expand",
+                                       "lu_w", "w_pack", "flux_g"], list(self.setup_seconds)))
+        return d
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libhm.so (raises if it has not been built: run __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: build it with `python -m paper_2305_06891_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    sig = {
+        "hm_init": (C.c_int, [C.c_int, C.c_int, C.c_int, P, C.c_uint32, C.POINTER(P)]),
+        "hm_finalize": (None, [P]),
+        "hm_status_string": (C.c_char_p, [C.c_int]),
+        "hm_last_error": (C.c_char_p, [P]),
+        "hm_set_allocator": (C.c_int, [P, P, P, P]),
+        "hm_build_geometry": (C.c_int, [P, I64, P, P, P, P, C.POINTER(hm_tree_params), C.POINTER(P)]),
+        "hm_assemble_aca": (C.c_int, [P, P, C.POINTER(hm_aca_params), C.POINTER(P)]),
+        "hm_factor_hlu": (C.c_int, [P, P, P, C.POINTER(hm_lu_params), C.POINTER(P)]),
+        "hm_apply_F": (C.c_int, [P, P, I32, P, P, P]),
+        "hm_solve_C": (C.c_int, [P, P, I32, P, P, P]),
+        "hm_radiative_flux": (C.c_int, [P, P, P, I32, P, P, P]),
+        "hm_export_perm": (C.c_int, [P, P]),
+        "hm_export_partition": (C.c_int, [P, P, C.POINTER(I64), P]),
+        "hm_export_row_sums": (C.c_int, [P, P, P]),
+        "hm_storage_report": (C.c_int, [P, P, C.POINTER(hm_storage)]),
+        "hm_local_range": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(I64), C.POINTER(I64)]),
+        "hm_profile_flux": (C.c_int, [P, P, P, P, P, I32, P, P, P]),
+        "hm_destroy_geom": (None, [P]),
+        "hm_destroy_hmat": (None, [P]),
+        "hm_destroy_hlu": (None, [P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def header_symbols(header: str = HEADER) -> list:
+    """Every function name declared in include/hm.h."""
+    txt = open(header).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(hm_[a-z_A-Z0-9]+)\s*\(", txt)))
+
+
+# ----------------------------------------------------------------------------- marshalling
+def _ptr(a):
+    """(pointer, keepalive) for a numpy array or torch tensor (float64/int32, contiguous)."""
+    if a is None:
+        return None, None
+    if hasattr(a, "data_ptr"):           # torch.Tensor
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr(), a
+    arr = np.ascontiguousarray(a)
+    return arr.ctypes.data, arr
+
+
+def _stream(stream, *arrays):
+    if stream is not None:
+        return int(stream)
+    for a in arrays:
+        if hasattr(a, "is_cuda") and a.is_cuda:
+            import torch
+            return torch.cuda.current_stream(a.device).cuda_stream
+    return 0
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        st = self.lib.hm_init(device, 0, 1, None, 0, C.byref(h))
+        if st != 0:
+            raise HMError(st, f"hm_init(device={device}) failed (no CUDA device? no CPU fallback exists)")
+        self.h = h
+
+    def check(self, st: int, what: str):
+        if st != 0:
+            raise HMError(st, f"{what}: {self.lib.hm_last_error(self.h).decode()}")
+
+    def close(self):
+        if self.h:
+            self.lib.hm_finalize(self.h)
+            self.h = None
+
+
+def hm_init(device: int = 0) -> Context:
+    return Context(device)
+
+
+class Geometry:
+    def __init__(self, ctx: Context, h, n):
+        self.ctx, self.h, self.n = ctx, h, n
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.hm_destroy_geom(self.h)
+            self.h = None
+
+
+class HMatrix:
+    def __init__(self, ctx, h, geom):
+        self.ctx, self.h, self.geom = ctx, h, geom
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.hm_destroy_hmat(self.h)
+            self.h = None
+
+
+class HLU:
+    def __init__(self, ctx, h, F):
+        self.ctx, self.h, self.F = ctx, h, F
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.hm_destroy_hlu(self.h)
+            self.h = None
+
+
+def hm_build_geometry(ctx: Context, centroid, normal, area, facet_aabb=None, n_min=64, eta=1.0,
+                      adm_mode=0) -> Geometry:
+    c = np.ascontiguousarray(centroid, dtype=np.float64)
+    nr = np.ascontiguousarray(normal, dtype=np.float64)
+    a = np.ascontiguousarray(area, dtype=np.float64)
+    bb = None if facet_aabb is None else np.ascontiguousarray(facet_aabb, dtype=np.float64)
+    p = hm_tree_params(int(n_min), float(eta), int(adm_mode))
+    h = C.c_void_p()
+    st = ctx.lib.hm_build_geometry(ctx.h, a.shape[0], c.ctypes.data, nr.ctypes.data, a.ctypes.data,
+                                   None if bb is None else bb.ctypes.data, C.byref(p), C.byref(h))
+    ctx.check(st, "hm_build_geometry")
+    return Geometry(ctx, h, a.shape[0])
+
+
+def hm_assemble_aca(ctx: Context, geom: Geometry, eps_aca=1e-6, k_max=0, closed_cavity=True) -> HMatrix:
+    p = hm_aca_params(float(eps_aca), int(k_max), int(bool(closed_cavity)))
+    h = C.c_void_p()
+    ctx.check(ctx.lib.hm_assemble_aca(ctx.h, geom.h, C.byref(p), C.byref(h)), "hm_assemble_aca")
+    return HMatrix(ctx, h, geom)
+
+
+def hm_factor_hlu(ctx: Context, F: HMatrix, emissivity, eps_lu=0.0) -> HLU:
+    e = np.ascontiguousarray(emissivity, dtype=np.float64)
+    p = hm_lu_params(float(eps_lu))
+    h = C.c_void_p()
+    ctx.check(ctx.lib.hm_factor_hlu(ctx.h, F.h, e.ctypes.data, C.byref(p), C.byref(h)), "hm_factor_hlu")
+    return HLU(ctx, h, F)
+
+
+def _nrhs(x, n):
+    shp = tuple(x.shape)
+    if shp[0] != n or len(shp) > 2:
+        raise ValueError(f"expected ({n},) or ({n}, nrhs), got {shp}")
+    return 1 if len(shp) == 1 else int(shp[1])
+
+
+def hm_apply_F(ctx: Context, F: HMatrix, x, y, stream=None):
+    """y = F x; x, y: (n,) or (n, nrhs) float64, device tensors or host arrays."""
+    px, kx = _ptr(x)
+    py, ky = _ptr(y)
+    ctx.check(ctx.lib.hm_apply_F(ctx.h, F.h, _nrhs(x, F.geom.n), px, py, _stream(stream, x, y)), "hm_apply_F")
+    return y
+
+
+def hm_solve_C(ctx: Context, LU: HLU, b, z, stream=None):
+    pb, kb = _ptr(b)
+    pz, kz = _ptr(z)
+    ctx.check(ctx.lib.hm_solve_C(ctx.h, LU.h, _nrhs(b, LU.F.geom.n), pb, pz, _stream(stream, b, z)), "hm_solve_C")
+    return z
+
+
+def hm_radiative_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, stream=None):
+    pT, kT = _ptr(T)
+    pq, kq = _ptr(q)
+    ctx.check(ctx.lib.hm_radiative_flux(ctx.h, F.h, LU.h, _nrhs(T, F.geom.n), pT, pq, _stream(stream, T, q)),
+              "hm_radiative_flux")
+    return q
+
+
+def hm_export_perm(geom: Geometry) -> np.ndarray:
+    out = np.empty(geom.n, dtype=np.int32)
+    geom.ctx.check(geom.ctx.lib.hm_export_perm(geom.h, out.ctypes.data), "hm_export_perm")
+    return out
+
+
+def hm_export_partition(geom: Geometry, F: HMatrix | None = None) -> np.ndarray:
+    nb = C.c_int64()
+    lib = geom.ctx.lib
+    geom.ctx.check(lib.hm_export_partition(geom.h, None if F is None else F.h, C.byref(nb), None), "partition")
+    out = np.empty((nb.value, 8), dtype=np.int64)
+    geom.ctx.check(lib.hm_export_partition(geom.h, None if F is None else F.h, C.byref(nb), out.ctypes.data),
+                   "partition")
+    return out
+
+
+def hm_export_row_sums(F: HMatrix):
+    s = np.empty(F.geom.n)
+    c = np.empty(F.geom.n)
+    F.ctx.check(F.ctx.lib.hm_export_row_sums(F.h, s.ctypes.data, c.ctypes.data), "row sums")
+    return s, c
+
+
+def hm_storage_report(F: HMatrix, LU: HLU | None = None) -> dict:
+    st = hm_storage()
+    F.ctx.check(F.ctx.lib.hm_storage_report(F.h, None if LU is None else LU.h, C.byref(st)), "storage")
+    return st.as_dict()
+
+
+def hm_local_range(geom: Geometry, rank: int, world: int):
+    b, e = C.c_int64(), C.c_int64()
+    geom.ctx.check(geom.ctx.lib.hm_local_range(geom.h, rank, world, C.byref(b), C.byref(e)), "local range")
+    return b.value, e.value
+
+
+def hm_profile_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, iters: int, stream=None):
+    ms = (C.c_double * 6)()
+    la = (C.c_int64 * 6)()
+    pT, kT = _ptr(T)
+    pq, kq = _ptr(q)
+    ctx.check(ctx.lib.hm_profile_flux(ctx.h, F.h, LU.h, pT, pq, int(iters), ms, la, _stream(stream, T, q)),
+              "hm_profile_flux")
+    names = ["prologue", "F_phase1", "F_phase2", "solve_phase1", "solve_phase2", "leaf_solves"]
+    return dict(zip(names, list(ms))), dict(zip(names, list(la)))

@@ -1,0 +1,603 @@
+// C ABI of include/hm.h: context, geometry/trees, ACA assembly, hot-path entry points.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+
+#include "hm_internal.h"
+
+namespace hm {
+
+double now_seconds() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    const char* base = strrchr(file, '/');
+    std::string msg = std::string(cudaGetErrorString(e)) + " in " + what + " (" + (base ? base + 1 : file) + ":" +
+                      std::to_string(line) + ")";
+    if (e == cudaErrorMemoryAllocation) throw Error(HM_ERR_OOM, msg);
+    throw Error(HM_ERR_CUDA, msg);
+}
+
+static bool g_debug = false;
+void debug_sync(cudaStream_t s, const char* what) {
+    if (!g_debug) return;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) throw Error(HM_ERR_CUDA, std::string("kernel fault after ") + what + ": " + cudaGetErrorString(e));
+}
+
+void* dmalloc(Ctx* ctx, size_t bytes, const char* what) {
+    void* p = nullptr;
+    if (ctx && ctx->alloc_fn) {
+        p = ctx->alloc_fn(bytes, ctx->stream, ctx->alloc_user);
+        if (!p) throw Error(HM_ERR_OOM, std::string("allocator hook failed: ") + std::to_string(bytes) + " bytes for " + what);
+        return p;
+    }
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(HM_ERR_OOM, std::string("cudaMalloc of ") + std::to_string(bytes) + " bytes for " + what + ": " +
+                                    cudaGetErrorString(e));
+    }
+    return p;
+}
+
+void dfree(Ctx* ctx, void* p) {
+    if (!p) return;
+    if (ctx && ctx->free_fn) {
+        ctx->free_fn(p, ctx->stream, ctx->alloc_user);
+        return;
+    }
+    cudaFree(p);
+}
+
+// implemented in hlu.cpp
+void factor_hlu(HLU& L, const double* emissivity);
+void run_solve(HLU& L, const double* b_int_ready, cudaStream_t s, int mode, double* out, const FluxEpi* epi,
+               double* ms_accum);
+
+}  // namespace hm
+
+using namespace hm;
+
+namespace {
+
+template <class F>
+hm_status guarded(Ctx* ctx, F&& f) {
+    try {
+        f();
+        return HM_OK;
+    } catch (const Error& e) {
+        if (ctx) ctx->last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        if (ctx) ctx->last_error = "host allocation failed";
+        return HM_ERR_OOM;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->last_error = e.what();
+        return HM_ERR_CUDA;
+    }
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Stage host arrays through device buffers; returns the device pointer to use.
+const double* stage_in(Ctx* ctx, DBuf<double>& buf, const double* p, size_t count, cudaStream_t s, bool& host) {
+    host = !is_device_ptr(p);
+    if (!host) return p;
+    if (buf.n < count) buf.alloc(ctx, count, "host staging (in)");
+    HM_CUDA(cudaMemcpyAsync(buf.p, p, count * sizeof(double), cudaMemcpyHostToDevice, s));
+    return buf.p;
+}
+
+}  // namespace
+
+// ============================================================================ lifetime
+extern "C" {
+
+const char* hm_status_string(hm_status s) {
+    switch (s) {
+        case HM_OK: return "ok";
+        case HM_ERR_INVALID_ARG: return "invalid argument";
+        case HM_ERR_CUDA: return "CUDA error";
+        case HM_ERR_OOM: return "out of device memory";
+        case HM_ERR_NCCL: return "NCCL error";
+        case HM_ERR_DEGENERATE_GEOMETRY: return "degenerate geometry";
+        case HM_ERR_SINGULAR: return "singular leaf block";
+        case HM_ERR_NOT_READY: return "not ready";
+        case HM_ERR_UNSUPPORTED: return "unsupported configuration";
+    }
+    return "unknown status";
+}
+
+const char* hm_last_error(const hm_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
+
+hm_status hm_init(int device, int rank, int world, const void* nccl_unique_id, uint32_t flags, hm_ctx** out) {
+    if (!out) return HM_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (world != 1 || rank != 0 || nccl_unique_id) return HM_ERR_UNSUPPORTED;
+    int cnt = 0;
+    if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0 || device < 0 || device >= cnt) {
+        cudaGetLastError();
+        return HM_ERR_CUDA;
+    }
+    auto* c = new hm_ctx;
+    c->c.device = device;
+    c->c.rank = rank;
+    c->c.world = world;
+    c->c.flags = flags;
+    const char* dbg = getenv("HM_DEBUG");
+    g_debug = c->c.debug = dbg && dbg[0] == '1';
+    hm_status st = guarded(&c->c, [&] {
+        HM_CUDA(cudaSetDevice(device));
+        HM_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+    });
+    if (st != HM_OK) {
+        delete c;
+        return st;
+    }
+    *out = c;
+    return HM_OK;
+}
+
+void hm_finalize(hm_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+}
+
+hm_status hm_set_allocator(hm_ctx* ctx, void* (*alloc_fn)(size_t, void*, void*), void (*free_fn)(void*, void*, void*),
+                           void* user) {
+    if (!ctx || (!alloc_fn) != (!free_fn)) return HM_ERR_INVALID_ARG;
+    ctx->c.alloc_fn = alloc_fn;
+    ctx->c.free_fn = free_fn;
+    ctx->c.alloc_user = user;
+    return HM_OK;
+}
+
+// ============================================================================ geometry
+hm_status hm_build_geometry(hm_ctx* ctx, int64_t n, const double* xyz, const double* nrm, const double* area,
+                            const double* facet_aabb, const hm_tree_params* params, hm_geom** out) {
+    if (!ctx || !out) return HM_ERR_INVALID_ARG;
+    *out = nullptr;
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        if (n < 1 || n >= INT32_MAX / 2 || !xyz || !nrm || !area || !params)
+            throw Error(HM_ERR_INVALID_ARG, "hm_build_geometry: need n >= 1 and non-null xyz, nrm, area, params");
+        if (params->n_min < 1 || params->n_min > 256)
+            throw Error(HM_ERR_INVALID_ARG, "hm_build_geometry: n_min must be in [1, 256]");
+        if (!(params->eta > 0.0) || !std::isfinite(params->eta))
+            throw Error(HM_ERR_INVALID_ARG, "hm_build_geometry: eta must be finite and > 0");
+        if (params->adm_mode != 0 && params->adm_mode != 1)
+            throw Error(HM_ERR_INVALID_ARG, "hm_build_geometry: adm_mode must be 0 or 1");
+        if (params->adm_mode == 1 && !facet_aabb)
+            throw Error(HM_ERR_INVALID_ARG, "hm_build_geometry: adm_mode 1 needs facet_aabb");
+        for (int64_t i = 0; i < n; ++i) {
+            for (int k = 0; k < 3; ++k)
+                if (!std::isfinite(xyz[3 * i + k]) || !std::isfinite(nrm[3 * i + k]))
+                    throw Error(HM_ERR_DEGENERATE_GEOMETRY, "non-finite coordinate or normal at facet " + std::to_string(i));
+            if (!(area[i] > 0.0) || !std::isfinite(area[i]))
+                throw Error(HM_ERR_DEGENERATE_GEOMETRY, "area <= 0 or non-finite at facet " + std::to_string(i));
+            const double l2 = nrm[3 * i] * nrm[3 * i] + nrm[3 * i + 1] * nrm[3 * i + 1] + nrm[3 * i + 2] * nrm[3 * i + 2];
+            if (std::fabs(l2 - 1.0) > 1e-6)
+                throw Error(HM_ERR_INVALID_ARG, "normal of facet " + std::to_string(i) + " is not unit length");
+        }
+        auto* G = new hm_geom;
+        std::unique_ptr<hm_geom> guard(G);
+        Geom& g = G->g;
+        g.ctx = c;
+        g.n = n;
+        g.params = *params;
+        const double t0 = now_seconds();
+        build_trees(g, xyz, nrm, area, facet_aabb);
+        std::vector<double> soa(7 * (size_t)n);
+        std::copy(g.cx.begin(), g.cx.end(), soa.begin());
+        std::copy(g.cy.begin(), g.cy.end(), soa.begin() + n);
+        std::copy(g.cz.begin(), g.cz.end(), soa.begin() + 2 * n);
+        std::copy(g.nx.begin(), g.nx.end(), soa.begin() + 3 * n);
+        std::copy(g.ny.begin(), g.ny.end(), soa.begin() + 4 * n);
+        std::copy(g.nz.begin(), g.nz.end(), soa.begin() + 5 * n);
+        std::copy(g.area.begin(), g.area.end(), soa.begin() + 6 * n);
+        g.d_geo.upload(c, soa, "facet data", c->stream);
+        g.d_perm.upload(c, g.perm, "permutation", c->stream);
+        HM_CUDA(cudaStreamSynchronize(c->stream));
+        g.setup_seconds = now_seconds() - t0;
+        *out = guard.release();
+    });
+}
+
+void hm_destroy_geom(hm_geom* g) { delete g; }
+
+hm_status hm_export_perm(const hm_geom* geom, int32_t* perm) {
+    if (!geom || !perm) return HM_ERR_INVALID_ARG;
+    std::copy(geom->g.perm.begin(), geom->g.perm.end(), perm);
+    return HM_OK;
+}
+
+hm_status hm_export_partition(const hm_geom* geom, const hm_hmat* F, int64_t* n_blocks, int64_t* rows) {
+    if (!geom || !n_blocks) return HM_ERR_INVALID_ARG;
+    const Geom& g = geom->g;
+    *n_blocks = (int64_t)g.blocks.size();
+    if (!rows) return HM_OK;
+    for (size_t b = 0; b < g.blocks.size(); ++b) {
+        const Blk& B = g.blocks[b];
+        int64_t* r = rows + 8 * b;
+        r[0] = B.level; r[1] = B.r0; r[2] = B.r1; r[3] = B.c0; r[4] = B.c1; r[5] = B.adm;
+        r[6] = F ? F->h.blk_kind[b] : (B.adm ? 1 : 0);
+        r[7] = F ? F->h.blk_rank[b] : 0;
+    }
+    return HM_OK;
+}
+
+hm_status hm_local_range(const hm_geom* geom, int rank, int world, int64_t* begin, int64_t* end) {
+    if (!geom || !begin || !end || world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
+        return HM_ERR_INVALID_ARG;
+    // node `rank` at tree level log2(world), walking down the left/right children
+    const Geom& g = geom->g;
+    int node = 0;
+    for (int bit = world >> 1; bit > 0; bit >>= 1) {
+        const Node& N = g.nodes[node];
+        if (N.is_leaf()) {  // too few clusters: later ranks get empty ranges
+            if (rank & (bit * 2 - 1)) { *begin = *end = N.end; return HM_OK; }
+            break;
+        }
+        node = N.child[(rank & bit) ? 1 : 0];
+    }
+    *begin = g.nodes[node].begin;
+    *end = g.nodes[node].end;
+    return HM_OK;
+}
+
+// ============================================================================ ACA assembly
+hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params* params, hm_hmat** F_out) {
+    if (!ctx || !geom || !params || !F_out) return HM_ERR_INVALID_ARG;
+    *F_out = nullptr;
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        if (!(params->eps_aca > 0.0) || params->eps_aca >= 1.0)
+            throw Error(HM_ERR_INVALID_ARG, "eps_aca must be in (0, 1)");
+        if (params->k_max < 0 || params->k_max > 64) throw Error(HM_ERR_INVALID_ARG, "k_max must be in [0, 64]");
+        const Geom& g = geom->g;
+        const cudaStream_t s = c->stream;
+        const int64_t n = g.n;
+        auto* H = new hm_hmat;
+        std::unique_ptr<hm_hmat> guard(H);
+        HMat& F = H->h;
+        F.ctx = c;
+        F.geom = &g;
+        F.params = *params;
+        const int KMAX = params->k_max > 0 ? params->k_max : 48;
+        const size_t nb = g.blocks.size();
+        F.blk_kind.assign(nb, KIND_DENSE);
+        F.blk_rank.assign(nb, 0);
+
+        // ---- batched partial-pivot ACA over admissible blocks (scratch bounded per batch)
+        double t0 = now_seconds();
+        struct AcaRec { int batch; int64_t uoff, voff; int kcap; };
+        std::vector<AcaRec> rec(nb, AcaRec{-1, 0, 0, 0});
+        std::vector<DBuf<double>> batches;
+        const int64_t budget = int64_t(1) << 28;  // doubles of scratch per batch (2 GiB)
+        DBuf<int32_t> err;
+        err.alloc(c, 4, "err");
+        HM_CUDA(cudaMemsetAsync(err.p, 0, 4 * sizeof(int32_t), s));
+        size_t b = 0;
+        while (b < nb) {
+            std::vector<int64_t> hblk, huoff, hvoff;
+            std::vector<int32_t> hkcap;
+            std::vector<size_t> ids;
+            int64_t cur = 0, max_m = 1, max_n = 1;
+            for (; b < nb; ++b) {
+                const Blk& B = g.blocks[b];
+                if (!B.adm) continue;
+                const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+                const int64_t klim = (m * nn + m + nn - 1) / (m + nn);  // smallest k with k(m+n) >= mn
+                const int kc = (int)std::min<int64_t>(KMAX, klim);
+                const int64_t need = ((m * kc + 1) & ~1LL) + ((nn * kc + 1) & ~1LL);
+                if (!ids.empty() && (cur + need > budget || ids.size() >= 1000000)) break;
+                hblk.insert(hblk.end(), {B.r0, m, B.c0, nn});
+                huoff.push_back(cur);
+                cur += (m * kc + 1) & ~1LL;
+                hvoff.push_back(cur);
+                cur += (nn * kc + 1) & ~1LL;
+                hkcap.push_back(kc);
+                ids.push_back(b);
+                max_m = std::max(max_m, m);
+                max_n = std::max(max_n, nn);
+            }
+            if (ids.empty()) break;
+            DBuf<int64_t> dblk, duoff, dvoff;
+            DBuf<int32_t> dkcap, drank;
+            DBuf<double> dmargin, scratch;
+            dblk.upload(c, hblk, "aca blocks", s);
+            duoff.upload(c, huoff, "aca uoff", s);
+            dvoff.upload(c, hvoff, "aca voff", s);
+            dkcap.upload(c, hkcap, "aca kcap", s);
+            drank.alloc(c, ids.size(), "aca ranks");
+            dmargin.alloc(c, ids.size(), "aca margins");
+            scratch.alloc(c, (size_t)std::max<int64_t>(cur, 2), "aca scratch");
+            k::aca_batch(g.d_geo.p, n, dblk.p, duoff.p, dvoff.p, dkcap.p, (int)ids.size(), params->eps_aca, scratch.p,
+                         drank.p, dmargin.p, err.p, s, max_m, max_n);
+            std::vector<int32_t> hrank(ids.size());
+            HM_CUDA(cudaMemcpyAsync(hrank.data(), drank.p, ids.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            HM_CUDA(cudaStreamSynchronize(s));
+            for (size_t q = 0; q < ids.size(); ++q) {
+                const size_t bb = ids[q];
+                F.blk_rank[bb] = hrank[q];
+                F.blk_kind[bb] = hrank[q] >= hkcap[q] ? KIND_ADM_DENSE : KIND_LR;
+                rec[bb] = AcaRec{(int)batches.size(), huoff[q], hvoff[q], hkcap[q]};
+            }
+            batches.push_back(std::move(scratch));
+        }
+        int32_t herr[4];
+        HM_CUDA(cudaMemcpy(herr, err.p, sizeof(herr), cudaMemcpyDeviceToHost));
+        if (herr[0])
+            throw Error(HM_ERR_DEGENERATE_GEOMETRY, "coincident collocation points for facets " +
+                                                        std::to_string(g.perm[herr[1]]) + "," + std::to_string(g.perm[herr[2]]));
+        F.setup_seconds[0] = now_seconds() - t0;
+
+        // ---- near field + factors into the stream layout
+        t0 = now_seconds();
+        std::vector<SrcBlock> src(nb);
+        for (size_t q = 0; q < nb; ++q) {
+            const Blk& B = g.blocks[q];
+            SrcBlock& S = src[q];
+            S.r0 = B.r0; S.m = B.r1 - B.r0; S.c0 = B.c0; S.n = B.c1 - B.c0;
+            if (F.blk_kind[q] == KIND_LR) {
+                S.kind = KIND_LR;
+                S.k = F.blk_rank[q];
+                const double* base = batches[rec[q].batch].p;
+                S.U = base + rec[q].uoff;
+                S.u_ld = S.m;
+                S.V = base + rec[q].voff;
+                S.v_ld = S.n;
+            } else {
+                S.kind = KIND_DENSE;
+                S.fill_entries = true;
+            }
+        }
+        build_hop(c, g, src, F.op, s);
+        batches.clear();
+        F.setup_seconds[1] = now_seconds() - t0;
+
+        // ---- row sums s = F_H 1 / A (eq:rowsum), clamp (eq:clamped_rowsum), scaling (eqn:F_closed)
+        t0 = now_seconds();
+        F.xt.alloc(c, (size_t)(n + F.op.n_p1), "F xt");
+        F.y.alloc(c, (size_t)n, "F y");
+        DBuf<double> sv, cv, cdiv;
+        sv.alloc(c, n, "row sums");
+        cv.alloc(c, n, "clamped row sums");
+        cdiv.alloc(c, n, "row divisors");
+        k::fill_value(F.xt.p, n, 1.0, s);
+        k::phase1(F.op.p1.p, F.op.n_p1, F.op.arena.p, F.xt.p, n, s);
+        k::phase2(F.op.p2.p, F.op.n_p2, F.op.max_m, F.op.colsrc.p, F.op.arena.p, F.xt.p, F.y.p, OUT_ASSIGN, nullptr,
+                  nullptr, s);
+        k::row_sums_clamp(F.y.p, g.d_geo.p + 6 * n, sv.p, cv.p, cdiv.p, n, s);
+        if (params->closed_cavity) k::scale_rows(F.op.p2.p, (int)F.op.n_p2, F.op.arena.p, cdiv.p, s);
+        std::vector<double> hs(n), hc(n);
+        HM_CUDA(cudaMemcpyAsync(hs.data(), sv.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaMemcpyAsync(hc.data(), cv.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        F.s_ext.resize(n);
+        F.c_ext.resize(n);
+        for (int64_t i = 0; i < n; ++i) {
+            F.s_ext[g.perm[i]] = hs[i];
+            F.c_ext[g.perm[i]] = hc[i];
+        }
+        F.setup_seconds[2] = now_seconds() - t0;
+        *F_out = guard.release();
+    });
+}
+
+void hm_destroy_hmat(hm_hmat* F) { delete F; }
+
+hm_status hm_export_row_sums(const hm_hmat* F, double* s, double* c) {
+    if (!F) return HM_ERR_INVALID_ARG;
+    if (s) std::copy(F->h.s_ext.begin(), F->h.s_ext.end(), s);
+    if (c) std::copy(F->h.c_ext.begin(), F->h.c_ext.end(), c);
+    return HM_OK;
+}
+
+// ============================================================================ hot path
+hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double* x, double* y, void* stream) {
+    if (!ctx || !Fh || !x || !y || nrhs < 1) return HM_ERR_INVALID_ARG;
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        HMat& F = const_cast<HMat&>(Fh->h);
+        const Geom& g = *F.geom;
+        const int64_t n = g.n;
+        cudaStream_t s = (cudaStream_t)stream;
+        bool hin = false;
+        const double* xd = stage_in(c, F.host_stage_in, x, (size_t)n * nrhs, s, hin);
+        const bool hout = !is_device_ptr(y);
+        double* yd = y;
+        if (hout) {
+            if (F.host_stage_out.n < (size_t)n * nrhs) F.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
+            yd = F.host_stage_out.p;
+        }
+        FluxEpi epi{};
+        epi.ld = nrhs;
+        for (int col = 0; col < nrhs; ++col) {
+            epi.col = col;
+            k::permute_in(xd, nrhs, col, g.d_perm.p, F.xt.p, n, s);
+            k::phase1(F.op.p1.p, F.op.n_p1, F.op.arena.p, F.xt.p, n, s);
+            k::phase2(F.op.p2.p, F.op.n_p2, F.op.max_m, F.op.colsrc.p, F.op.arena.p, F.xt.p, yd, OUT_PERM, g.d_perm.p,
+                      &epi, s);
+        }
+        if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double* b, double* z, void* stream) {
+    if (!ctx || !LUh || !b || !z || nrhs < 1) return HM_ERR_INVALID_ARG;
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        HLU& L = const_cast<HLU&>(LUh->h);
+        const Geom& g = *L.F->geom;
+        const int64_t n = g.n;
+        cudaStream_t s = (cudaStream_t)stream;
+        bool hin = false;
+        const double* bd = stage_in(c, L.host_stage_in, b, (size_t)n * nrhs, s, hin);
+        const bool hout = !is_device_ptr(z);
+        double* zd = z;
+        if (hout) {
+            if (L.host_stage_out.n < (size_t)n * nrhs) L.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
+            zd = L.host_stage_out.p;
+        }
+        FluxEpi epi{};
+        epi.ld = nrhs;
+        for (int col = 0; col < nrhs; ++col) {
+            epi.col = col;
+            k::permute_in(bd, nrhs, col, g.d_perm.p, L.xtA.p, n, s);
+            run_solve(L, nullptr, s, OUT_PERM, zd, &epi, nullptr);
+        }
+        if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"
+
+namespace hm {
+// One flux evaluation for column `col` (device pointers).  ms_accum (optional, 6 entries)
+// receives per-class times measured with events on `s`.
+void run_flux(HLU& L, const double* Td, double* qd, int ld, int col, cudaStream_t s, double* ms_accum) {
+    const HMat& F = *L.F;
+    const Geom& g = *F.geom;
+    const int64_t n = g.n;
+    cudaEvent_t ev[2];
+    if (ms_accum) {
+        HM_CUDA(cudaEventCreate(&ev[0]));
+        HM_CUDA(cudaEventCreate(&ev[1]));
+        HM_CUDA(cudaEventRecord(ev[0], s));
+    }
+    auto lap = [&](int cls) {
+        if (!ms_accum) return;
+        HM_CUDA(cudaEventRecord(ev[1], s));
+        HM_CUDA(cudaEventSynchronize(ev[1]));
+        float ms = 0;
+        HM_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        ms_accum[cls] += ms;
+        std::swap(ev[0], ev[1]);
+    };
+    k::flux_prologue(Td, ld, col, g.d_perm.p, L.eps_int.p, L.xtA.p, n, s);
+    lap(0);
+    // z = C^-1 w into F's x-part
+    run_solve(L, nullptr, s, OUT_ASSIGN, const_cast<double*>(F.xt.p), nullptr, ms_accum);
+    if (ms_accum) HM_CUDA(cudaEventRecord(ev[0], s));
+    k::phase1(F.op.p1.p, F.op.n_p1, F.op.arena.p, const_cast<double*>(F.xt.p), n, s);
+    lap(1);
+    FluxEpi epi{Td, g.d_perm.p, L.eps_int.p, g.d_geo.p + 6 * n, L.g_int.p, 5.670374419e-8, ld, col};
+    k::phase2(F.op.p2.p, F.op.n_p2, F.op.max_m, F.op.colsrc.p, F.op.arena.p, F.xt.p, qd, OUT_FLUX, g.d_perm.p, &epi, s);
+    lap(2);
+    if (ms_accum) {
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+    }
+}
+}  // namespace hm
+
+extern "C" {
+
+hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, int32_t nrhs, const double* T, double* q,
+                            void* stream) {
+    if (!ctx || !Fh || !LUh || !T || !q || nrhs < 1) return HM_ERR_INVALID_ARG;
+    if (LUh->h.F != &Fh->h) {
+        ctx->c.last_error = "hm_radiative_flux: LU was not factored from this F";
+        return HM_ERR_NOT_READY;
+    }
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        HLU& L = const_cast<HLU&>(LUh->h);
+        const int64_t n = L.F->geom->n;
+        cudaStream_t s = (cudaStream_t)stream;
+        bool hin = false;
+        const double* Td = stage_in(c, L.host_stage_in, T, (size_t)n * nrhs, s, hin);
+        const bool hout = !is_device_ptr(q);
+        double* qd = q;
+        if (hout) {
+            if (L.host_stage_out.n < (size_t)n * nrhs) L.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
+            qd = L.host_stage_out.p;
+        }
+        for (int col = 0; col < nrhs; ++col) run_flux(L, Td, qd, nrhs, col, s, nullptr);
+        if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, const double* T, double* q, int32_t iters,
+                          double* ms_out, int64_t* launches_out, void* stream) {
+    if (!ctx || !Fh || !LUh || !T || !q || iters < 1 || !ms_out) return HM_ERR_INVALID_ARG;
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        HLU& L = const_cast<HLU&>(LUh->h);
+        cudaStream_t s = (cudaStream_t)stream;
+        double acc[6] = {0, 0, 0, 0, 0, 0};
+        for (int it = 0; it < iters; ++it) run_flux(L, T, q, 1, 0, s, acc);
+        for (int q2 = 0; q2 < 6; ++q2) ms_out[q2] = acc[q2] / iters;
+        if (launches_out) {
+            int64_t sp1 = 0, sp2 = 0;
+            for (auto* v : {&L.fwd, &L.bwd})
+                for (auto& op : *v) { sp1 += op.n_p1 > 0; sp2 += op.n_p2 > 0; }
+            launches_out[0] = 1;
+            launches_out[1] = Fh->h.op.n_p1 > 0;
+            launches_out[2] = 1;
+            launches_out[3] = sp1;
+            launches_out[4] = sp2;
+            launches_out[5] = 2;
+        }
+    });
+}
+
+hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* out) {
+    if (!Fh || !out) return HM_ERR_INVALID_ARG;
+    std::memset(out, 0, sizeof(*out));
+    const HMat& F = Fh->h;
+    const Geom& g = *F.geom;
+    out->n = g.n;
+    out->n_leaves = (int64_t)g.leaves.size();
+    out->depth = g.depth;
+    out->n_blocks = (int64_t)g.blocks.size();
+    int64_t lr = 0, ksum = 0;
+    for (size_t b = 0; b < g.blocks.size(); ++b) {
+        if (F.blk_kind[b] == KIND_DENSE) out->n_dense++;
+        else if (F.blk_kind[b] == KIND_LR) { lr++; ksum += F.blk_rank[b]; out->rank_max = std::max<int64_t>(out->rank_max, F.blk_rank[b]); }
+        else out->n_adm_dense++;
+    }
+    out->n_lowrank = lr;
+    out->rank_mean = lr ? double(ksum) / lr : 0.0;
+    out->bytes_F_phase1 = 8 * F.op.p1_doubles;
+    out->bytes_F_phase2 = 8 * F.op.p2_doubles;
+    out->bytes_F = out->bytes_F_phase1 + out->bytes_F_phase2;
+    out->launches_apply_F = 1 + (F.op.n_p1 > 0) + 1;
+    for (int q = 0; q < 3; ++q) out->setup_seconds[q] = F.setup_seconds[q];
+    out->setup_seconds[0] += g.setup_seconds;
+    if (LUh) {
+        const HLU& L = LUh->h;
+        out->bytes_C = 8 * L.bytes;
+        out->bytes_C_leaf = 8 * L.bytes_leaf;
+        out->n_blocks_C = L.n_blocks;
+        out->n_lowrank_C = L.n_lr;
+        out->rank_max_C = L.rank_max;
+        out->rank_mean_C = L.n_lr ? double(L.rank_sum) / L.n_lr : 0.0;
+        int64_t la = 1 + 2;  // permute-in + two leaf solves
+        for (auto* v : {&L.fwd, &L.bwd})
+            for (auto& op : *v) la += (op.n_p1 > 0) + (op.n_p2 > 0);
+        out->launches_solve_C = la;
+        for (int q = 0; q < 4; ++q) out->setup_seconds[4 + q] = L.setup_seconds[q];
+    }
+    return HM_OK;
+}
+
+}  // extern "C"

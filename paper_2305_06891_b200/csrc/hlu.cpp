@@ -1,0 +1,432 @@
+// One-time factorisation of C = I - Lambda F and the level-scheduled
+// substitution that applies C^-1, DESIGN.md §"Solve in level form".
+//
+// Factorisation ("stage A", n up to ~1e5 on one B200): C is expanded from the H-format F
+// (PAPER.md:747), then the paper's 4-step block LU recursion runs over the
+// cluster tree on the FP64 tensor pipe, carrying the triangular inverses along:
+//     L11 U11 = C11 (recursive); U12 = L11^-1 C12; L21 = C21 U11^-1; L22 U22 = C22 - L21 U12.
+// At every tree node t it forms the level-form blocks
+//     W^L_t = L21 L11^-1      W^U_t = U12 U22^-1
+// and truncates them to eps_LU block by block in the block partition of F, by
+// cross approximation with full pivoting and an exact Frobenius stop test.  Leaf blocks keep
+// dense L_rr^-1 and U_rr^-1.
+//
+// Solve: for levels top-down  b_t2 -= W^L_t b_t1   (one two-phase launch pair per level),
+//        leaves              y_r  = L_rr^-1 b_r,
+//        for levels top-down  y_t1 -= W^U_t y_t2,
+//        leaves              z_r  = U_rr^-1 y_r.
+// This re-associates the forward/backward substitution (same C^-1 in exact arithmetic) so that
+// all nodes of a level are independent.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "hm_internal.h"
+
+namespace hm {
+
+namespace {
+
+struct Factorizer {
+    HLU& L;
+    const HMat& F;
+    const Geom& g;
+    Ctx* c;
+    cudaStream_t s;
+    int64_t n;
+    double eps_lu;
+    double* M = nullptr;
+    double* Minv = nullptr;
+    double* T = nullptr;
+    int32_t* err = nullptr;
+    std::vector<std::vector<int>> lower, upper;          // F-block ids per tree node
+    std::vector<std::vector<SrcBlock>> fwd_src, bwd_src;  // per level
+    std::vector<DBuf<double>> staging;
+
+    static constexpr int KMAX_LU = 64;
+
+    void collect() {
+        lower.assign(g.nodes.size(), {});
+        upper.assign(g.nodes.size(), {});
+        for (size_t b = 0; b < g.blocks.size(); ++b) {
+            const Blk& B = g.blocks[b];
+            int r = B.rnode, q = B.cnode;
+            if (r == q) continue;  // leaf diagonal block: part of the leaf factors
+            while (g.nodes[r].parent != g.nodes[q].parent) {
+                r = g.nodes[r].parent;
+                q = g.nodes[q].parent;
+            }
+            const int t = g.nodes[r].parent;
+            const Node& Tn = g.nodes[t];
+            if (B.r0 >= g.nodes[Tn.child[1]].begin) lower[t].push_back((int)b);
+            else upper[t].push_back((int)b);
+        }
+    }
+
+    // Stage the blocks of W (in T, rows b_rows.., cols b_cols.., ld) into staging buffers.
+    // Phase A (before T is destroyed): dense copies.  Phase B: compress admissible blocks in place.
+    void stage_dense(const std::vector<int>& ids, int64_t row0, int64_t col0, int64_t ld, std::vector<SrcBlock>& out) {
+        std::vector<int64_t> tasks;
+        int64_t tot = 0;
+        std::vector<std::pair<int, int64_t>> place;
+        for (int b : ids) {
+            const Blk& B = g.blocks[b];
+            if (B.adm) continue;
+            const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+            place.push_back({b, tot});
+            tot += m * nn;
+        }
+        if (place.empty()) return;
+        DBuf<double> buf;
+        buf.alloc(c, (size_t)tot, "W dense staging");
+        for (auto& pr : place) {
+            const Blk& B = g.blocks[pr.first];
+            const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+            const double* src = T + (B.r0 - row0) * ld + (B.c0 - col0);
+            tasks.insert(tasks.end(), {pr.second, (int64_t)(uintptr_t)src, m, nn, ld, 1});
+            SrcBlock S;
+            S.r0 = B.r0; S.m = m; S.c0 = B.c0; S.n = nn;
+            S.kind = KIND_DENSE;
+            S.dense = buf.p + pr.second;
+            S.d_rs = 1;
+            S.d_cs = m;  // staged column-major
+            out.push_back(S);
+        }
+        DBuf<int64_t> d;
+        d.upload(c, tasks, "stage tasks", s);
+        k::pack(d.p, (int)(tasks.size() / 6), buf.p, nullptr, s);
+        HM_CUDA(cudaStreamSynchronize(s));
+        staging.push_back(std::move(buf));
+    }
+
+    void compress(const std::vector<int>& ids, int64_t row0, int64_t col0, int64_t ld, std::vector<SrcBlock>& out) {
+        std::vector<int64_t> blk;
+        std::vector<int32_t> kcap;
+        std::vector<int> which;
+        int64_t tot = 0;
+        for (int b : ids) {
+            const Blk& B = g.blocks[b];
+            if (!B.adm) continue;
+            const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+            const int64_t klim = (m * nn + m + nn - 1) / (m + nn);
+            const int kc = (int)std::min<int64_t>(KMAX_LU, klim);
+            const int64_t uo = tot;
+            tot += (m * kc + 1) & ~1LL;
+            const int64_t vo = tot;
+            tot += (nn * kc + 1) & ~1LL;
+            blk.insert(blk.end(), {B.r0 - row0, m, B.c0 - col0, nn, uo, vo});
+            kcap.push_back(kc);
+            which.push_back(b);
+        }
+        if (which.empty()) return;
+        DBuf<double> fac;
+        fac.alloc(c, (size_t)std::max<int64_t>(tot, 2), "W factor staging");
+        DBuf<int64_t> dblk;
+        DBuf<int32_t> dk, dr;
+        dblk.upload(c, blk, "cpaca blocks", s);
+        dk.upload(c, kcap, "cpaca kcap", s);
+        dr.alloc(c, which.size(), "cpaca ranks");
+        k::cpaca_batch(T, ld, dblk.p, dk.p, (int)which.size(), eps_lu, fac.p, dr.p, s);
+        std::vector<int32_t> rk(which.size());
+        HM_CUDA(cudaMemcpyAsync(rk.data(), dr.p, rk.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        std::vector<int> failed;
+        for (size_t q = 0; q < which.size(); ++q) {
+            const Blk& B = g.blocks[which[q]];
+            const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+            if (rk[q] < 0) { failed.push_back(which[q]); continue; }
+            SrcBlock S;
+            S.r0 = B.r0; S.m = m; S.c0 = B.c0; S.n = nn;
+            S.kind = KIND_LR;
+            S.k = rk[q];
+            S.U = fac.p + blk[6 * q + 4];
+            S.u_ld = m;
+            S.V = fac.p + blk[6 * q + 5];
+            S.v_ld = nn;
+            out.push_back(S);
+        }
+        staging.push_back(std::move(fac));
+        if (!failed.empty()) {  // restored dense in T: stage them as dense
+            std::vector<int> tmp;
+            for (int b : failed) tmp.push_back(b);
+            // temporarily mark as dense for staging
+            std::vector<SrcBlock> dense_out;
+            std::vector<int64_t> tasks;
+            int64_t t2 = 0;
+            for (int b : tmp) {
+                const Blk& B = g.blocks[b];
+                t2 += (B.r1 - B.r0) * (B.c1 - B.c0);
+            }
+            DBuf<double> buf;
+            buf.alloc(c, (size_t)t2, "W dense staging (failed compression)");
+            int64_t off = 0;
+            for (int b : tmp) {
+                const Blk& B = g.blocks[b];
+                const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+                tasks.insert(tasks.end(), {off, (int64_t)(uintptr_t)(T + (B.r0 - row0) * ld + (B.c0 - col0)), m, nn, ld, 1});
+                SrcBlock S;
+                S.r0 = B.r0; S.m = m; S.c0 = B.c0; S.n = nn;
+                S.kind = KIND_DENSE;
+                S.dense = buf.p + off;
+                S.d_rs = 1;
+                S.d_cs = m;
+                out.push_back(S);
+                off += m * nn;
+            }
+            DBuf<int64_t> d;
+            d.upload(c, tasks, "stage tasks", s);
+            k::pack(d.p, (int)(tasks.size() / 6), buf.p, nullptr, s);
+            HM_CUDA(cudaStreamSynchronize(s));
+            staging.push_back(std::move(buf));
+        }
+    }
+
+    double* Mp(int64_t r, int64_t col) { return M + r * n + col; }
+    double* Ip(int64_t r, int64_t col) { return Minv + r * n + col; }
+
+    void rec(int node, int64_t b1, int64_t size) {
+        const bool tree_internal = node >= 0 && !g.nodes[node].is_leaf();
+        if (!tree_internal && size <= 64) {
+            k::leaf_lu_inv(Mp(b1, b1), Ip(b1, b1), n, (int)size, err, s);
+            return;
+        }
+        const int64_t n1 = tree_internal ? g.nodes[g.nodes[node].child[0]].size() : (size + 1) / 2;
+        const int64_t n2 = size - n1, b2 = b1 + n1;
+        const int ch0 = tree_internal ? g.nodes[node].child[0] : -1;
+        const int ch1 = tree_internal ? g.nodes[node].child[1] : -1;
+        rec(ch0, b1, n1);
+        // step 2: U12 = L11^-1 C12 ; step 3: L21 = C21 U11^-1 ; step 4: C22 -= L21 U12
+        k::dgemm(n1, n2, n1, 1.0, Ip(b1, b1), n, 1, Mp(b1, b2), n, 0, 0.0, T, n2, s);
+        k::copy2d(T, n2, Mp(b1, b2), n, n1, n2, s);
+        k::dgemm(n2, n1, n1, 1.0, Mp(b2, b1), n, 0, Ip(b1, b1), n, 2, 0.0, T, n1, s);
+        k::copy2d(T, n1, Mp(b2, b1), n, n2, n1, s);
+        k::dgemm(n2, n2, n1, -1.0, Mp(b2, b1), n, 0, Mp(b1, b2), n, 0, 1.0, Mp(b2, b2), n, s);
+        rec(ch1, b2, n2);
+        // W^L = L21 L11^-1 ; (L^-1)21 = -L22^-1 W^L
+        k::dgemm(n2, n1, n1, 1.0, Mp(b2, b1), n, 0, Ip(b1, b1), n, 1, 0.0, T, n1, s);
+        const int lvl = tree_internal ? g.nodes[node].level : -1;
+        if (tree_internal) stage_dense(lower[node], b2, b1, n1, fwd_src[lvl]);
+        k::dgemm(n2, n1, n2, -1.0, Ip(b2, b2), n, 1, T, n1, 0, 0.0, Ip(b2, b1), n, s);
+        if (tree_internal) compress(lower[node], b2, b1, n1, fwd_src[lvl]);
+        // W^U = U12 U22^-1 ; (U^-1)12 = -U11^-1 W^U
+        k::dgemm(n1, n2, n2, 1.0, Mp(b1, b2), n, 0, Ip(b2, b2), n, 2, 0.0, T, n2, s);
+        if (tree_internal) stage_dense(upper[node], b1, b2, n2, bwd_src[lvl]);
+        k::dgemm(n1, n2, n1, -1.0, Ip(b1, b1), n, 2, T, n2, 0, 0.0, Ip(b1, b2), n, s);
+        if (tree_internal) compress(upper[node], b1, b2, n2, bwd_src[lvl]);
+    }
+};
+
+void account(HLU& L, const HOp& op) {
+    L.bytes += op.p1_doubles + op.p2_doubles;
+    L.n_blocks += op.n_lr + op.n_dense;
+    L.n_lr += op.n_lr;
+    L.rank_sum += op.rank_sum;
+    L.rank_max = std::max(L.rank_max, op.rank_max);
+}
+
+}  // namespace
+
+void run_solve(HLU& L, const double*, cudaStream_t s, int mode, double* out, const FluxEpi* epi, double* ms_accum) {
+    const Geom& g = *L.F->geom;
+    const int64_t n = g.n;
+    cudaEvent_t ev[2];
+    if (ms_accum) {
+        HM_CUDA(cudaEventCreate(&ev[0]));
+        HM_CUDA(cudaEventCreate(&ev[1]));
+    }
+    auto t0 = [&]() { if (ms_accum) HM_CUDA(cudaEventRecord(ev[0], s)); };
+    auto lap = [&](int cls) {
+        if (!ms_accum) return;
+        HM_CUDA(cudaEventRecord(ev[1], s));
+        HM_CUDA(cudaEventSynchronize(ev[1]));
+        float ms = 0;
+        HM_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        ms_accum[cls] += ms;
+    };
+    auto level = [&](const HOp& op, double* xt) {
+        if (op.n_p1) { t0(); k::phase1(op.p1.p, op.n_p1, op.arena.p, xt, n, s); lap(3); }
+        if (op.n_p2) {
+            t0();
+            k::phase2(op.p2.p, op.n_p2, op.max_m, op.colsrc.p, op.arena.p, xt, xt, OUT_SUB, nullptr, nullptr, s);
+            lap(4);
+        }
+    };
+    for (const HOp& op : L.fwd) level(op, L.xtA.p);
+    t0();
+    k::phase2(L.leafL.p2.p, L.leafL.n_p2, L.leafL.max_m, L.leafL.colsrc.p, L.leafL.arena.p, L.xtA.p, L.xtB.p, OUT_ASSIGN,
+              nullptr, nullptr, s);
+    lap(5);
+    for (const HOp& op : L.bwd) level(op, L.xtB.p);
+    t0();
+    k::phase2(L.leafU.p2.p, L.leafU.n_p2, L.leafU.max_m, L.leafU.colsrc.p, L.leafU.arena.p, L.xtB.p, out, mode, g.d_perm.p,
+              epi, s);
+    lap(5);
+    if (ms_accum) {
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+    }
+}
+
+void factor_hlu(HLU& L, const double* emissivity) {
+    const HMat& F = *L.F;
+    const Geom& g = *F.geom;
+    Ctx* c = L.ctx;
+    const cudaStream_t s = c->stream;
+    const int64_t n = g.n;
+    std::vector<double> eps_int(n), lam(n);
+    for (int64_t i = 0; i < n; ++i) {
+        const double e = emissivity[g.perm[i]];
+        if (!(e > 0.0 && e <= 1.0)) throw Error(HM_ERR_INVALID_ARG, "emissivity of facet " + std::to_string(g.perm[i]) + " not in (0, 1]");
+        eps_int[i] = e;
+        lam[i] = (1.0 - e) / g.area[i];  // Lambda_ii = (1 - eps_i) / A_i (eq:reflection_matrix)
+    }
+    const int64_t half = (n + 1) / 2;
+    const int64_t maxT = std::max<int64_t>(half * (n - half), 1);
+    const double need = 8.0 * (2.0 * n * n + maxT) * 1.25;
+    size_t freeb = 0, totb = 0;
+    HM_CUDA(cudaMemGetInfo(&freeb, &totb));
+    if (need > (double)freeb)
+        throw Error(HM_ERR_UNSUPPORTED, "dense-stage H-LU needs ~" + std::to_string((int64_t)(need / 1e9)) +
+                                            " GB of device memory (" + std::to_string((int64_t)(freeb / 1e9)) + " GB free)");
+    L.eps_int.upload(c, eps_int, "eps", s);
+    DBuf<double> dlam, dM, dMinv, dT;
+    DBuf<int32_t> derr;
+    dlam.upload(c, lam, "lambda", s);
+    dM.alloc(c, (size_t)(n * n), "dense C / LU");
+    dMinv.alloc(c, (size_t)(n * n), "dense L^-1 / U^-1");
+    dT.alloc(c, (size_t)maxT, "W workspace");
+    derr.alloc(c, 4, "err");
+    HM_CUDA(cudaMemsetAsync(derr.p, 0, 4 * sizeof(int32_t), s));
+
+    // ---- C = I - Lambda F_H expanded from the stored H-format
+    double t0 = now_seconds();
+    HM_CUDA(cudaMemsetAsync(dM.p, 0, sizeof(double) * (size_t)(n * n), s));
+    {
+        std::vector<int64_t> tasks;
+        tasks.reserve(8 * F.op.items.size());
+        for (const auto& it : F.op.items) tasks.insert(tasks.end(), {it.a_off, it.vt_off, it.r0, it.m, it.c0, it.ncols, it.k, 0});
+        DBuf<int64_t> d;
+        d.upload(c, tasks, "expand tasks", s);
+        k::expand_C(d.p, (int)F.op.items.size(), F.op.arena.p, dlam.p, dM.p, n, s);
+        k::add_identity(dM.p, n, n, s);
+        HM_CUDA(cudaStreamSynchronize(s));
+    }
+    L.setup_seconds[0] = now_seconds() - t0;
+
+    // ---- block LU over the cluster tree with level-form W extraction
+    t0 = now_seconds();
+    Factorizer fz{L, F, g, c, s, n, L.params.eps_lu};
+    fz.M = dM.p;
+    fz.Minv = dMinv.p;
+    fz.T = dT.p;
+    fz.err = derr.p;
+    fz.collect();
+    const int D = g.depth;
+    fz.fwd_src.assign(std::max(D, 0), {});
+    fz.bwd_src.assign(std::max(D, 0), {});
+    fz.rec(0, 0, n);
+    int32_t herr[4];
+    HM_CUDA(cudaMemcpyAsync(herr, derr.p, sizeof(herr), cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    if (herr[0]) throw Error(HM_ERR_SINGULAR, "near-zero pivot (|pivot| <= 1e-14 ||block||) in a leaf LU of C");
+    // leaf inverses
+    int64_t leaf_tot = 0;
+    for (int l : g.leaves) leaf_tot += g.nodes[l].size() * g.nodes[l].size();
+    DBuf<double> dLi, dUi;
+    dLi.alloc(c, (size_t)leaf_tot, "leaf L^-1");
+    dUi.alloc(c, (size_t)leaf_tot, "leaf U^-1");
+    std::vector<SrcBlock> lsrcL, lsrcU;
+    int64_t off = 0;
+    for (int l : g.leaves) {
+        const Node& N = g.nodes[l];
+        const int64_t m = N.size();
+        k::extract_tri(dMinv.p, n, N.begin, m, 1, dLi.p + off, s);
+        k::extract_tri(dMinv.p, n, N.begin, m, 2, dUi.p + off, s);
+        SrcBlock S;
+        S.r0 = N.begin; S.m = m; S.c0 = N.begin; S.n = m;
+        S.kind = KIND_DENSE;
+        S.d_rs = m;
+        S.d_cs = 1;
+        S.dense = dLi.p + off;
+        lsrcL.push_back(S);
+        S.dense = dUi.p + off;
+        lsrcU.push_back(S);
+        off += m * m;
+    }
+    HM_CUDA(cudaStreamSynchronize(s));
+    L.setup_seconds[1] = now_seconds() - t0;
+
+    // ---- pack the level-form operators
+    t0 = now_seconds();
+    dM.reset();
+    dMinv.reset();
+    dT.reset();
+    L.fwd.resize(std::max(D, 0));
+    L.bwd.resize(std::max(D, 0));
+    L.bytes = L.bytes_leaf = L.n_blocks = L.n_lr = L.rank_sum = 0;
+    L.rank_max = 0;
+    int64_t maxt = 0;
+    for (int lv = 0; lv < D; ++lv) {
+        build_hop(c, g, fz.fwd_src[lv], L.fwd[lv], s);
+        build_hop(c, g, fz.bwd_src[lv], L.bwd[lv], s);
+        account(L, L.fwd[lv]);
+        account(L, L.bwd[lv]);
+        maxt = std::max({maxt, L.fwd[lv].n_p1, L.bwd[lv].n_p1});
+    }
+    build_hop(c, g, lsrcL, L.leafL, s);
+    build_hop(c, g, lsrcU, L.leafU, s);
+    L.bytes_leaf = L.leafL.p2_doubles + L.leafU.p2_doubles;
+    L.bytes += L.bytes_leaf;
+    L.n_blocks += 2 * (int64_t)g.leaves.size();
+    fz.staging.clear();
+    L.xtA.alloc(c, (size_t)(n + maxt), "solve xtA");
+    L.xtB.alloc(c, (size_t)(n + maxt), "solve xtB");
+    L.z.alloc(c, (size_t)n, "solve z");
+    L.setup_seconds[2] = now_seconds() - t0;
+
+    // ---- flux constant g = F C^-1 eps
+    t0 = now_seconds();
+    L.g_int.alloc(c, (size_t)n, "g");
+    HM_CUDA(cudaMemcpyAsync(L.xtA.p, L.eps_int.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    HMat& Fm = const_cast<HMat&>(F);
+    run_solve(L, nullptr, s, OUT_ASSIGN, Fm.xt.p, nullptr, nullptr);
+    k::phase1(F.op.p1.p, F.op.n_p1, F.op.arena.p, Fm.xt.p, n, s);
+    k::phase2(F.op.p2.p, F.op.n_p2, F.op.max_m, F.op.colsrc.p, F.op.arena.p, Fm.xt.p, L.g_int.p, OUT_ASSIGN, nullptr,
+              nullptr, s);
+    HM_CUDA(cudaStreamSynchronize(s));
+    L.setup_seconds[3] = now_seconds() - t0;
+}
+
+}  // namespace hm
+
+using namespace hm;
+
+extern "C" {
+
+hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity, const hm_lu_params* params,
+                        hm_hlu** out) {
+    if (!ctx || !F || !emissivity || !out) return HM_ERR_INVALID_ARG;
+    *out = nullptr;
+    Ctx* c = &ctx->c;
+    try {
+        auto* H = new hm_hlu;
+        std::unique_ptr<hm_hlu> guard(H);
+        H->h.ctx = c;
+        H->h.F = &F->h;
+        H->h.params.eps_lu = (params && params->eps_lu > 0.0) ? params->eps_lu : F->h.params.eps_aca;
+        factor_hlu(H->h, emissivity);
+        *out = guard.release();
+        return HM_OK;
+    } catch (const Error& e) {
+        c->last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        c->last_error = e.what();
+        return HM_ERR_CUDA;
+    }
+}
+
+void hm_destroy_hlu(hm_hlu* LU) { delete LU; }
+
+}  // extern "C"

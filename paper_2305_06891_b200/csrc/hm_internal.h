@@ -1,0 +1,282 @@
+// Internal declarations of the hm library (host orchestration + kernel launchers).
+// Nothing here is part of the C ABI (include/hm.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hm.h"
+
+namespace hm {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+    hm_status code;
+    Error(hm_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define HM_CUDA(x) ::hm::cuda_check((x), #x, __FILE__, __LINE__)
+void debug_sync(cudaStream_t s, const char* what);
+
+// ------------------------------------------------------------------ device memory
+struct Ctx;
+void* dmalloc(Ctx* ctx, size_t bytes, const char* what);
+void dfree(Ctx* ctx, void* p);
+
+template <class T>
+struct DBuf {  // owning device buffer
+    Ctx* ctx = nullptr;
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { reset(); ctx = o.ctx; p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { reset(); }
+    void alloc(Ctx* c, size_t count, const char* what) {
+        reset();
+        ctx = c;
+        n = count;
+        p = count ? static_cast<T*>(dmalloc(c, count * sizeof(T), what)) : nullptr;
+    }
+    void upload(Ctx* c, const std::vector<T>& h, const char* what, cudaStream_t s) {
+        alloc(c, h.size(), what);
+        if (!h.empty()) HM_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void reset();
+};
+
+struct Ctx {
+    int device = 0, rank = 0, world = 1;
+    uint32_t flags = 0;
+    cudaStream_t stream = nullptr;  // setup stream
+    std::string last_error;
+    void* (*alloc_fn)(size_t, void*, void*) = nullptr;
+    void (*free_fn)(void*, void*, void*) = nullptr;
+    void* alloc_user = nullptr;
+    bool debug = false;
+};
+
+template <class T>
+void DBuf<T>::reset() {
+    if (p) dfree(ctx, p);
+    p = nullptr;
+    n = 0;
+}
+
+// ------------------------------------------------------------------ geometry / trees
+struct Node {
+    int64_t begin = 0, end = 0;
+    int level = 0;
+    int child[2] = {-1, -1};
+    int parent = -1;
+    int leaf_index = -1;  // index into Geom::leaves if leaf
+    double lo[3], hi[3];  // admissibility box
+    int64_t size() const { return end - begin; }
+    bool is_leaf() const { return child[0] < 0; }
+};
+
+enum Kind : int { KIND_DENSE = 0, KIND_LR = 1, KIND_ADM_DENSE = 2 };
+
+struct Blk {
+    int level;
+    int64_t r0, r1, c0, c1;
+    int adm;
+    int rnode, cnode;
+    int kind = KIND_DENSE;
+    int rank = 0;
+};
+
+struct Geom {
+    Ctx* ctx;
+    int64_t n;
+    hm_tree_params params;
+    std::vector<int32_t> perm;  // perm[internal] = external
+    std::vector<Node> nodes;    // preorder; nodes[0] = root
+    std::vector<int> leaves;    // node ids in internal order
+    std::vector<int64_t> leaf_begin;  // sorted begins of leaves
+    int depth = 0;
+    std::vector<Blk> blocks;    // sorted by (r0, c0)
+    // internal-order facet data (host copies)
+    std::vector<double> cx, cy, cz, nx, ny, nz, area;
+    // device copies (SoA, internal order)
+    DBuf<double> d_geo;         // 7*n: cx cy cz nx ny nz A
+    DBuf<int32_t> d_perm;
+    double setup_seconds = 0;
+    int leaf_of(int64_t row) const;  // leaf index containing internal row
+};
+
+void build_trees(Geom& g, const double* xyz, const double* nrm, const double* area,
+                 const double* aabb);
+
+// ------------------------------------------------------------------ the two-phase stream operator
+// phase 1 (one warp per task): t[task] = dot(arena[off : off+n], XT[x_off : x_off+n])
+struct P1Task {
+    int64_t off;
+    int32_t n;
+    int32_t x_off;
+};
+// phase 2 (one CTA per leaf row): out[r0+i] (op)= sum_c arena[region + c*m + i] * XT[colsrc[col0+c]]
+struct P2Row {
+    int64_t region;
+    int32_t r0;
+    int32_t m;
+    int32_t col0;
+    int32_t ncols;
+};
+
+// A block as a source for the operator builder.
+struct SrcBlock {
+    int64_t r0, m, c0, n;
+    int kind;        // KIND_LR -> U/V; otherwise dense
+    int k = 0;
+    bool fill_entries = false;       // dense: evaluate view-factor entries (F near field)
+    const double* dense = nullptr;   // dense element (i,j) at dense[i*d_rs + j*d_cs]
+    int64_t d_rs = 0, d_cs = 0;
+    const double* U = nullptr;       // U element (i,l) at U[l*u_ld + i]
+    int64_t u_ld = 0;
+    const double* V = nullptr;       // V element (j,l) at V[l*v_ld + j]  (== V^T row-major)
+    int64_t v_ld = 0;
+};
+
+struct HOp {
+    int64_t n_rows_total = 0;     // n
+    DBuf<double> arena;
+    int64_t p2_doubles = 0, p1_doubles = 0;   // algorithmic payload (no padding)
+    DBuf<P1Task> p1;
+    int64_t n_p1 = 0;             // == total rank (size of t)
+    DBuf<P2Row> p2;
+    int64_t n_p2 = 0;
+    DBuf<int32_t> colsrc;
+    int64_t n_cols = 0;
+    int max_m = 0;
+    // host mirrors for re-use (expansion, scaling)
+    std::vector<P2Row> h_p2;
+    std::vector<int32_t> h_colsrc;
+    struct ItemRec {              // one phase-2 item (a leaf-row slice of one block)
+        int64_t a_off;            // column-major m x (kind==LR ? k : ncols) in the arena
+        int64_t vt_off;           // LR: V^T (k x ncols) row-major; dense: -1
+        int64_t r0, m, c0, ncols; // rows of the slice, columns of the block
+        int64_t k;
+    };
+    std::vector<ItemRec> items;
+    int64_t n_lr = 0, n_dense = 0;
+    int64_t rank_sum = 0;
+    int rank_max = 0;
+    bool empty() const { return n_p2 == 0; }
+};
+
+// Build the operator; XT layout is [x (n) | t (n_p1)].
+void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s);
+
+// output modes of phase 2
+enum OutMode : int { OUT_ASSIGN = 0, OUT_SUB = 1, OUT_PERM = 2, OUT_FLUX = 3 };
+struct FluxEpi {  // OUT_FLUX: q_ext[perm[i]] = sigma * eps_i / A_i * (acc - eta_i g_i)
+    const double* T_ext;
+    const int32_t* perm;
+    const double* eps_int;
+    const double* area_int;
+    const double* g_int;
+    double sigma;
+    int ld;    // leading dimension (nrhs) of the external arrays; also used by OUT_PERM
+    int col;   // column of the external arrays
+};
+
+struct HMat {
+    Ctx* ctx;
+    const Geom* geom;
+    hm_aca_params params;
+    HOp op;
+    std::vector<double> s_ext, c_ext;  // row sums / clamped (external order)
+    std::vector<int> blk_kind, blk_rank;  // per geom block
+    double setup_seconds[4] = {0, 0, 0, 0};
+    // apply workspace
+    DBuf<double> xt;   // [x | t]
+    DBuf<double> y;    // internal-order output
+    DBuf<double> host_stage_in, host_stage_out;
+    int launches = 0;
+    bool graph_ready = false;
+    cudaGraphExec_t graph = nullptr;
+    cudaStream_t graph_stream = nullptr;
+};
+
+struct HLU {
+    Ctx* ctx;
+    const HMat* F;
+    hm_lu_params params;
+    std::vector<HOp> fwd, bwd;   // per level (may be empty ops)
+    HOp leafL, leafU;
+    DBuf<double> xtA;            // [b | t] forward pass (t sized for the largest level)
+    DBuf<double> xtB;            // [y | t] backward pass
+    DBuf<double> z;              // internal-order result
+    DBuf<double> eps_int, g_int;
+    DBuf<double> host_stage_in, host_stage_out;
+    double setup_seconds[4] = {0, 0, 0, 0};
+    int64_t bytes = 0, bytes_leaf = 0, n_blocks = 0, n_lr = 0, rank_sum = 0;
+    int rank_max = 0;
+    // flux graph
+    bool graph_ready = false;
+    cudaGraphExec_t graph = nullptr;
+    cudaStream_t graph_stream = nullptr;
+};
+
+// ------------------------------------------------------------------ kernel launchers (kernels_*.cu)
+namespace k {
+// assembly
+void aca_batch(const double* geo, int64_t n, const int64_t* blk /*[nb][4] r0,m,c0,n*/,
+               const int64_t* uoff, const int64_t* voff, const int32_t* kcap, int nb, double eps,
+               double* scratch, int32_t* rank_out, double* margin_out, int32_t* err, cudaStream_t s,
+               int64_t max_m, int64_t max_n);
+void fill_entries(const double* geo, int64_t n, const int64_t* tasks /*[nt][5] dst,r0,rows,c0,cols*/,
+                  int nt, double* arena, int32_t* err, cudaStream_t s);
+void pack(const int64_t* tasks /*[nt][6] dst,src,rows,cols,rs,cs*/, int nt, double* arena,
+          const double* src_base, cudaStream_t s);
+void scale_rows(const P2Row* rows, int nrows, double* arena, const double* cdiv, cudaStream_t s);
+// apply
+void phase1(const P1Task* tasks, int64_t ntasks, const double* arena, double* xt, int64_t n,
+            cudaStream_t s);
+void phase2(const P2Row* rows, int64_t nrows, int max_m, const int32_t* colsrc, const double* arena,
+            const double* xt, double* out, int mode, const int32_t* perm, const FluxEpi* epi,
+            cudaStream_t s);
+void permute_in(const double* x_ext, int ld, int col, const int32_t* perm, double* x_int, int64_t n,
+                cudaStream_t s);
+void permute_out(const double* y_int, const int32_t* perm, double* y_ext, int ld, int col, int64_t n,
+                 cudaStream_t s);
+void flux_prologue(const double* T_ext, int ld, int col, const int32_t* perm, const double* eps_int,
+                   double* w_int, int64_t n, cudaStream_t s);
+void fill_value(double* p, int64_t n, double v, cudaStream_t s);
+void row_sums_clamp(const double* y, const double* area, double* sv, double* c, double* cdiv,
+                    int64_t n, cudaStream_t s);
+// dense linear algebra (setup)
+void expand_C(const int64_t* tasks /*[nt][8]*/, int nt, const double* arena, const double* lam,
+              double* M, int64_t ld, cudaStream_t s);
+void add_identity(double* M, int64_t ld, int64_t n, cudaStream_t s);
+// C = beta*C + alpha*op(A)*op(B); tri: 0 none, 1 lower-unit, 2 upper (masking of the operand)
+void dgemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda, int triA,
+           const double* B, int64_t ldb, int triB, double beta, double* C, int64_t ldc, cudaStream_t s);
+void leaf_lu_inv(double* M, double* Minv, int64_t ld, int n, int32_t* err, cudaStream_t s);
+void extract_tri(const double* Minv, int64_t ld, int64_t r0, int64_t m, int mode, double* dst, cudaStream_t s);
+void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+            cudaStream_t s);
+void cpaca_batch(double* T, int64_t ldt, const int64_t* blk /*[nb][6] i0,m,j0,n,uoff,voff*/,
+                 const int32_t* kcap, int nb, double eps, double* fac, int32_t* rank_out,
+                 cudaStream_t s);
+}  // namespace k
+
+double now_seconds();
+
+}  // namespace hm
+
+struct hm_ctx { hm::Ctx c; };
+struct hm_geom { hm::Geom g; };
+struct hm_hmat { hm::HMat h; };
+struct hm_hlu { hm::HLU h; };

@@ -1,0 +1,249 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bars:
+  * integers -- permutation, block partition, stored kinds and ACA ranks: exactly equal to the
+    oracle's own Alg. 1 / Alg. 2 / ACA (BASELINE.json north_star);
+  * y = F x vs the oracle's own H-matrix (same ACA arithmetic): <= 1e-13 relative l2 (PAPER.md:782
+    "does not involve any further approximation");
+  * y = F x, z = C^-1 b, q vs the dense oracle: <= 10 eps_ACA relative l2 (north_star).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import hmatrix as ohm
+from oracle import tree as otree
+from oracle import viewfactor as vf
+
+pytestmark = pytest.mark.gpu
+
+TOL_EXACT = 1e-13
+
+
+@pytest.fixture(scope="module")
+def hm():
+    import paper_2305_06891_b200 as hm
+    return hm
+
+
+@pytest.fixture(scope="module")
+def ctx(hm):
+    return hm.hm_init(0)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def build(hm, ctx, f, n_min, eps, closed=True, adm_mode=0, eta=1.0):
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=n_min, eta=eta, adm_mode=adm_mode)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=eps, closed_cavity=closed)
+    return g, F
+
+
+CASES = {
+    "C1": lambda: (synth.make_config(1), 64),
+    "ico4-rand-eps": lambda: (synth.make_config(2, geometry=synth.icosphere(4)), 64),
+    "cyl-ragged": lambda: (synth.make_config(3, geometry=synth.cylinder(60, 12)), 64),
+    "ico3-exact": lambda: (synth.make_config(2, geometry=synth.icosphere(3, exact=True)), 64),
+    "ico3-nmin20": lambda: (synth.make_config(2, geometry=synth.icosphere(3)), 20),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def case(request, hm, ctx):
+    cfg, n_min = CASES[request.param]()
+    f = cfg.facets
+    g, F = build(hm, ctx, f, n_min, cfg.eps_aca)
+    H = ohm.assemble(f, n_min, 1.0, cfg.eps_aca)
+    return dict(name=request.param, cfg=cfg, f=f, g=g, F=F, H=H, n_min=n_min)
+
+
+def test_permutation_and_partition_exact(hm, case):
+    g, H = case["g"], case["H"]
+    assert (hm.hm_export_perm(g) == H.perm).all()
+    P = hm.hm_export_partition(g, case["F"])
+    Q = H.partition()
+    assert P.shape == Q.shape
+    assert (P[:, :6] == Q[:, :6]).all()
+
+
+def test_aca_kinds_and_ranks_exact(hm, case):
+    P = hm.hm_export_partition(case["g"], case["F"])
+    Q = case["H"].partition()
+    bad = np.nonzero((P[:, 6] != Q[:, 6]) | (P[:, 7] != Q[:, 7]))[0]
+    margins = [case["H"].blocks[i].margin for i in bad]
+    assert len(bad) == 0, f"{len(bad)} rank mismatches, oracle stop margins {margins[:10]}"
+
+
+def test_row_sums_match_oracle(hm, case):
+    s, c = hm.hm_export_row_sums(case["F"])
+    H = case["H"]
+    assert np.abs(s - H.svec).max() <= 1e-13 * np.abs(H.svec).max()
+    assert (np.abs(c - H.cvec) <= 1e-13).all()
+
+
+def test_apply_equals_oracle_hmatrix_and_dense(hm, case):
+    import torch
+    cfg, F, H, f = case["cfg"], case["F"], case["H"], case["f"]
+    x = cfg.rhs()[:, 0]
+    y = torch.empty(f.n, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(hm.hm_init(0) if False else F.ctx, F, torch.from_numpy(x).cuda(), y)
+    torch.cuda.synchronize()
+    y = y.cpu().numpy()
+    assert rel(y, H.apply(x)) <= TOL_EXACT
+    Fd, C, cvec = vf.dense_operators(f, cfg.emissivity)
+    assert rel(y, Fd @ x) <= 10 * cfg.eps_aca
+
+
+def test_solve_and_flux_match_dense_oracle(hm, case):
+    import torch
+    cfg, F, f = case["cfg"], case["F"], case["f"]
+    ctx = F.ctx
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
+    b = cfg.rhs()[:, 0]
+    z = torch.empty(f.n, dtype=torch.float64, device="cuda")
+    hm.hm_solve_C(ctx, LU, torch.from_numpy(b).cuda(), z)
+    torch.cuda.synchronize()
+    zo = vf.solve(C, b)
+    assert rel(z.cpu().numpy(), zo) <= 10 * cfg.eps_aca
+    T = cfg.T[:, 0]
+    q = torch.empty(f.n, dtype=torch.float64, device="cuda")
+    hm.hm_radiative_flux(ctx, F, LU, torch.from_numpy(T).cuda(), q)
+    torch.cuda.synchronize()
+    qo = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, T)[:, 0]
+    assert rel(q.cpu().numpy(), qo) <= 10 * cfg.eps_aca
+
+
+def test_host_pointers_and_multiple_rhs(hm, case):
+    import torch
+    cfg, F, f = case["cfg"], case["F"], case["f"]
+    ctx = F.ctx
+    X = np.stack([cfg.rhs()[:, 0], synth.uniform(17, f.n), np.ones(f.n)], axis=1)
+    Yh = np.empty_like(X)
+    hm.hm_apply_F(ctx, F, X, Yh)                          # host in, host out
+    Yd = torch.empty(f.n, 3, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, torch.from_numpy(X).cuda(), Yd)
+    torch.cuda.synchronize()
+    assert np.array_equal(Yh, Yd.cpu().numpy())           # deterministic, no atomics
+    for c in range(3):
+        assert rel(Yh[:, c], case["H"].apply(X[:, c])) <= TOL_EXACT
+
+
+# ---------------------------------------------------------------- edge cases
+def test_single_dense_leaf_equals_dense(hm, ctx):
+    f = synth.icosphere(1)             # n = 80 <= n_min
+    eps = synth.emissivities(3, f.n)
+    g, F = build(hm, ctx, f, 128, 1e-6)
+    P = hm.hm_export_partition(g, F)
+    assert P.shape[0] == 1 and P[0, 6] == 0
+    Fd, C, _ = vf.dense_operators(f, eps)
+    x = synth.uniform(4, f.n)
+    y = np.empty(f.n)
+    hm.hm_apply_F(ctx, F, x, y)
+    assert rel(y, Fd @ x) <= 1e-14
+    LU = hm.hm_factor_hlu(ctx, F, eps)
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, x, z)
+    assert rel(z, vf.solve(C, x)) <= 1e-13
+
+
+def test_blackbody_solve_is_identity(hm, ctx):
+    cfg = synth.make_config(1)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, 64, 1e-6)
+    LU = hm.hm_factor_hlu(ctx, F, np.ones(f.n))      # Lambda = 0 -> C = I
+    b = synth.uniform(8, f.n)
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, b, z)
+    assert rel(z, b) <= 1e-15
+
+
+def test_fig1_partition_facet_boxes(hm, ctx):
+    """PAPER.md Fig. 1 through the ABI (adm_mode 1, n_min 1)."""
+    import os
+    for n in (4, 8, 16):
+        f = synth.line_facets(n)
+        g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=1, eta=1.0, adm_mode=1)
+        P = hm.hm_export_partition(g)
+        got = sorted(tuple(int(v) for v in (r[1], r[2], r[3], r[4], r[5])) for r in P)
+        path = os.path.join(os.path.dirname(__file__), "golden", f"fig1_n{n}.txt")
+        exp = sorted(tuple(map(int, ln.split())) for ln in open(path) if not ln.startswith("#"))
+        assert got == exp
+
+
+def test_sphere_exact_closed_forms(hm, ctx):
+    """Sphere-exact mode: every admissible block has ACA rank 1, F x and C^-1 b match the O(n)
+    closed forms (SURVEY.md §8(c) pins) -- the kind of check that scales to C4/C5."""
+    f = synth.icosphere(4, exact=True)
+    eps = synth.emissivities(21, f.n)
+    g, F = build(hm, ctx, f, 64, 1e-6)
+    P = hm.hm_export_partition(g, F)
+    assert set(P[P[:, 6] == 1, 7].tolist()) == {1}
+    a = f.area
+    k = 1.0 / (4.0 * math.pi)
+    cex = (a.sum() - a) * k
+    x = synth.uniform(5, f.n)
+    y = np.empty(f.n)
+    hm.hm_apply_F(ctx, F, x, y)
+    assert rel(y, k * (a * (a @ x) - a * a * x) / cex) <= 1e-12
+    LU = hm.hm_factor_hlu(ctx, F, eps)
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, x, z)
+    bb = (1.0 - eps) / cex
+    Md = 1.0 + k * bb * a
+    Mx, Mb = x / Md, bb / Md
+    zcl = Mx + (k * (a @ Mx) / (1.0 - k * (a @ Mb))) * Mb
+    assert rel(z, zcl) <= 1e-5
+
+
+def test_degenerate_geometry_reported(hm, ctx):
+    f = synth.icosphere(2)
+    c = f.centroid.copy()
+    c[7] = c[3]
+    g = hm.hm_build_geometry(ctx, c, f.normal, f.area, n_min=16)
+    with pytest.raises(hm.HMError) as e:
+        hm.hm_assemble_aca(ctx, g, 1e-6)
+    assert e.value.status == "HM_ERR_DEGENERATE_GEOMETRY" and "3" in str(e.value) and "7" in str(e.value)
+
+
+def test_invalid_arguments(hm, ctx):
+    f = synth.icosphere(1)
+    with pytest.raises(hm.HMError):
+        hm.hm_build_geometry(ctx, f.centroid, f.normal, -f.area, n_min=16)
+    with pytest.raises(hm.HMError):
+        hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, n_min=0)
+    g, F = build(hm, ctx, f, 16, 1e-6)
+    with pytest.raises(hm.HMError):
+        hm.hm_factor_hlu(ctx, F, np.zeros(f.n))       # eps must be in (0, 1]
+
+
+# ---------------------------------------------------------------- the bench configuration (C2)
+@pytest.mark.slow
+def test_config2_full_size(hm, ctx):
+    """BASELINE configs[1] (the bench workload): exact partition/ranks vs the oracle's own
+    classification, apply vs the oracle H-matrix at 1e-13, dense parity on 2,000 sampled rows,
+    solve residual on the sampled rows (kappa(C) ~ 1.7)."""
+    import torch
+    cfg = synth.make_config(2)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    H = ohm.assemble(f, cfg.n_min, 1.0, cfg.eps_aca)
+    P, Q = hm.hm_export_partition(g, F), H.partition()
+    assert (P == Q).all()
+    x = cfg.rhs()[:, 0]
+    y = np.empty(f.n)
+    hm.hm_apply_F(ctx, F, x, y)
+    assert rel(y, H.apply(x)) <= TOL_EXACT
+    rows = synth.sample_rows(synth.stream_seed(cfg.seed, 999), f.n, 2000)
+    ys = vf.sampled_apply(f.centroid, f.normal, f.area, rows, x[:, None])[:, 0]
+    assert rel(y[rows], ys) <= 10 * cfg.eps_aca
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, x, z)
+    r = vf.sampled_residual(f.centroid, f.normal, f.area, cfg.emissivity, rows, z[:, None], x[:, None])[:, 0]
+    assert np.linalg.norm(r) / np.linalg.norm(x[rows]) <= 10 * cfg.eps_aca
+    del torch
