@@ -372,18 +372,24 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
 
         // ---- row sums s = F_H 1 / A (eq:rowsum), clamp (eq:clamped_rowsum), scaling (eqn:F_closed)
         t0 = now_seconds();
-        F.xt.alloc(c, (size_t)(n + F.op.n_p1), "F xt");
+        F.xt.alloc(c, (size_t)(n + F.op.n_t), "F xt");
         F.y.alloc(c, (size_t)n, "F y");
         DBuf<double> sv, cv, cdiv;
         sv.alloc(c, n, "row sums");
         cv.alloc(c, n, "clamped row sums");
         cdiv.alloc(c, n, "row divisors");
         k::fill_value(F.xt.p, n, 1.0, s);
-        k::phase1(F.op.p1.p, F.op.n_p1, F.op.arena.p, F.xt.p, n, s);
-        k::phase2(F.op.p2.p, F.op.n_p2, F.op.max_m, F.op.colsrc.p, F.op.arena.p, F.xt.p, F.y.p, OUT_ASSIGN, nullptr,
-                  nullptr, s);
+        k::stream_pass(F.op.p1, F.op.colsrc.p, F.op.arena.p, F.xt.p, F.xt.p, OUT_ASSIGN, nullptr, nullptr, s);
+        k::stream_pass(F.op.p2, F.op.colsrc.p, F.op.arena.p, F.xt.p, F.y.p, OUT_ASSIGN, nullptr, nullptr, s);
         k::row_sums_clamp(F.y.p, g.d_geo.p + 6 * n, sv.p, cv.p, cdiv.p, n, s);
-        if (params->closed_cavity) k::scale_rows(F.op.p2.p, (int)F.op.n_p2, F.op.arena.p, cdiv.p, s);
+        if (params->closed_cavity) {
+            std::vector<int64_t> tasks;
+            for (const Panel& pn : F.op.p2.panels) tasks.insert(tasks.end(), {pn.a_off, pn.ld, pn.nrows, pn.ncols, pn.out0});
+            DBuf<int64_t> dt;
+            dt.upload(c, tasks, "scale tasks", s);
+            k::scale_rows(dt.p, (int)F.op.p2.panels.size(), F.op.arena.p, cdiv.p, s);
+            HM_CUDA(cudaStreamSynchronize(s));
+        }
         std::vector<double> hs(n), hc(n);
         HM_CUDA(cudaMemcpyAsync(hs.data(), sv.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaMemcpyAsync(hc.data(), cv.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -430,9 +436,8 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
         for (int col = 0; col < nrhs; ++col) {
             epi.col = col;
             k::permute_in(xd, nrhs, col, g.d_perm.p, F.xt.p, n, s);
-            k::phase1(F.op.p1.p, F.op.n_p1, F.op.arena.p, F.xt.p, n, s);
-            k::phase2(F.op.p2.p, F.op.n_p2, F.op.max_m, F.op.colsrc.p, F.op.arena.p, F.xt.p, yd, OUT_PERM, g.d_perm.p,
-                      &epi, s);
+            k::stream_pass(F.op.p1, F.op.colsrc.p, F.op.arena.p, F.xt.p, F.xt.p, OUT_ASSIGN, nullptr, nullptr, s);
+            k::stream_pass(F.op.p2, F.op.colsrc.p, F.op.arena.p, F.xt.p, yd, OUT_PERM, g.d_perm.p, &epi, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
@@ -496,10 +501,11 @@ void run_flux(HLU& L, const double* Td, double* qd, int ld, int col, cudaStream_
     // z = C^-1 w into F's x-part
     run_solve(L, nullptr, s, OUT_ASSIGN, const_cast<double*>(F.xt.p), nullptr, ms_accum);
     if (ms_accum) HM_CUDA(cudaEventRecord(ev[0], s));
-    k::phase1(F.op.p1.p, F.op.n_p1, F.op.arena.p, const_cast<double*>(F.xt.p), n, s);
+    double* fxt = const_cast<double*>(F.xt.p);
+    k::stream_pass(F.op.p1, F.op.colsrc.p, F.op.arena.p, fxt, fxt, OUT_ASSIGN, nullptr, nullptr, s);
     lap(1);
     FluxEpi epi{Td, g.d_perm.p, L.eps_int.p, g.d_geo.p + 6 * n, L.g_int.p, 5.670374419e-8, ld, col};
-    k::phase2(F.op.p2.p, F.op.n_p2, F.op.max_m, F.op.colsrc.p, F.op.arena.p, F.xt.p, qd, OUT_FLUX, g.d_perm.p, &epi, s);
+    k::stream_pass(F.op.p2, F.op.colsrc.p, F.op.arena.p, fxt, qd, OUT_FLUX, g.d_perm.p, &epi, s);
     lap(2);
     if (ms_accum) {
         cudaEventDestroy(ev[0]);
@@ -549,9 +555,9 @@ hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, con
         if (launches_out) {
             int64_t sp1 = 0, sp2 = 0;
             for (auto* v : {&L.fwd, &L.bwd})
-                for (auto& op : *v) { sp1 += op.n_p1 > 0; sp2 += op.n_p2 > 0; }
+                for (auto& op : *v) { sp1 += !op.p1.empty(); sp2 += !op.p2.empty(); }
             launches_out[0] = 1;
-            launches_out[1] = Fh->h.op.n_p1 > 0;
+            launches_out[1] = !Fh->h.op.p1.empty();
             launches_out[2] = 1;
             launches_out[3] = sp1;
             launches_out[4] = sp2;
@@ -577,10 +583,10 @@ hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* ou
     }
     out->n_lowrank = lr;
     out->rank_mean = lr ? double(ksum) / lr : 0.0;
-    out->bytes_F_phase1 = 8 * F.op.p1_doubles;
-    out->bytes_F_phase2 = 8 * F.op.p2_doubles;
+    out->bytes_F_phase1 = 8 * F.op.p1_doubles();
+    out->bytes_F_phase2 = 8 * F.op.p2_doubles();
     out->bytes_F = out->bytes_F_phase1 + out->bytes_F_phase2;
-    out->launches_apply_F = 1 + (F.op.n_p1 > 0) + 1;
+    out->launches_apply_F = 1 + !F.op.p1.empty() + 1;
     for (int q = 0; q < 3; ++q) out->setup_seconds[q] = F.setup_seconds[q];
     out->setup_seconds[0] += g.setup_seconds;
     if (LUh) {
@@ -593,7 +599,7 @@ hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* ou
         out->rank_mean_C = L.n_lr ? double(L.rank_sum) / L.n_lr : 0.0;
         int64_t la = 1 + 2;  // permute-in + two leaf solves
         for (auto* v : {&L.fwd, &L.bwd})
-            for (auto& op : *v) la += (op.n_p1 > 0) + (op.n_p2 > 0);
+            for (auto& op : *v) la += !op.p1.empty() + !op.p2.empty();
         out->launches_solve_C = la;
         for (int q = 0; q < 4; ++q) out->setup_seconds[4 + q] = L.setup_seconds[q];
     }

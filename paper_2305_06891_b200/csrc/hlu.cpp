@@ -84,7 +84,7 @@ struct Factorizer {
             const Blk& B = g.blocks[pr.first];
             const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
             const double* src = T + (B.r0 - row0) * ld + (B.c0 - col0);
-            tasks.insert(tasks.end(), {pr.second, (int64_t)(uintptr_t)src, m, nn, ld, 1});
+            tasks.insert(tasks.end(), {pr.second, (int64_t)(uintptr_t)src, m, nn, ld, 1, m});
             SrcBlock S;
             S.r0 = B.r0; S.m = m; S.c0 = B.c0; S.n = nn;
             S.kind = KIND_DENSE;
@@ -95,7 +95,7 @@ struct Factorizer {
         }
         DBuf<int64_t> d;
         d.upload(c, tasks, "stage tasks", s);
-        k::pack(d.p, (int)(tasks.size() / 6), buf.p, nullptr, s);
+        k::pack(d.p, (int)(tasks.size() / 7), buf.p, s);
         HM_CUDA(cudaStreamSynchronize(s));
         staging.push_back(std::move(buf));
     }
@@ -164,7 +164,7 @@ struct Factorizer {
             for (int b : tmp) {
                 const Blk& B = g.blocks[b];
                 const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
-                tasks.insert(tasks.end(), {off, (int64_t)(uintptr_t)(T + (B.r0 - row0) * ld + (B.c0 - col0)), m, nn, ld, 1});
+                tasks.insert(tasks.end(), {off, (int64_t)(uintptr_t)(T + (B.r0 - row0) * ld + (B.c0 - col0)), m, nn, ld, 1, m});
                 SrcBlock S;
                 S.r0 = B.r0; S.m = m; S.c0 = B.c0; S.n = nn;
                 S.kind = KIND_DENSE;
@@ -176,7 +176,7 @@ struct Factorizer {
             }
             DBuf<int64_t> d;
             d.upload(c, tasks, "stage tasks", s);
-            k::pack(d.p, (int)(tasks.size() / 6), buf.p, nullptr, s);
+            k::pack(d.p, (int)(tasks.size() / 7), buf.p, s);
             HM_CUDA(cudaStreamSynchronize(s));
             staging.push_back(std::move(buf));
         }
@@ -218,7 +218,7 @@ struct Factorizer {
 };
 
 void account(HLU& L, const HOp& op) {
-    L.bytes += op.p1_doubles + op.p2_doubles;
+    L.bytes += op.p1_doubles() + op.p2_doubles();
     L.n_blocks += op.n_lr + op.n_dense;
     L.n_lr += op.n_lr;
     L.rank_sum += op.rank_sum;
@@ -245,22 +245,24 @@ void run_solve(HLU& L, const double*, cudaStream_t s, int mode, double* out, con
         ms_accum[cls] += ms;
     };
     auto level = [&](const HOp& op, double* xt) {
-        if (op.n_p1) { t0(); k::phase1(op.p1.p, op.n_p1, op.arena.p, xt, n, s); lap(3); }
-        if (op.n_p2) {
+        if (!op.p1.empty()) {
             t0();
-            k::phase2(op.p2.p, op.n_p2, op.max_m, op.colsrc.p, op.arena.p, xt, xt, OUT_SUB, nullptr, nullptr, s);
+            k::stream_pass(op.p1, op.colsrc.p, op.arena.p, xt, xt, OUT_ASSIGN, nullptr, nullptr, s);
+            lap(3);
+        }
+        if (!op.p2.empty()) {
+            t0();
+            k::stream_pass(op.p2, op.colsrc.p, op.arena.p, xt, xt, OUT_SUB, nullptr, nullptr, s);
             lap(4);
         }
     };
     for (const HOp& op : L.fwd) level(op, L.xtA.p);
     t0();
-    k::phase2(L.leafL.p2.p, L.leafL.n_p2, L.leafL.max_m, L.leafL.colsrc.p, L.leafL.arena.p, L.xtA.p, L.xtB.p, OUT_ASSIGN,
-              nullptr, nullptr, s);
+    k::stream_pass(L.leafL.p2, L.leafL.colsrc.p, L.leafL.arena.p, L.xtA.p, L.xtB.p, OUT_ASSIGN, nullptr, nullptr, s);
     lap(5);
     for (const HOp& op : L.bwd) level(op, L.xtB.p);
     t0();
-    k::phase2(L.leafU.p2.p, L.leafU.n_p2, L.leafU.max_m, L.leafU.colsrc.p, L.leafU.arena.p, L.xtB.p, out, mode, g.d_perm.p,
-              epi, s);
+    k::stream_pass(L.leafU.p2, L.leafU.colsrc.p, L.leafU.arena.p, L.xtB.p, out, mode, g.d_perm.p, epi, s);
     lap(5);
     if (ms_accum) {
         cudaEventDestroy(ev[0]);
@@ -304,8 +306,9 @@ void factor_hlu(HLU& L, const double* emissivity) {
     HM_CUDA(cudaMemsetAsync(dM.p, 0, sizeof(double) * (size_t)(n * n), s));
     {
         std::vector<int64_t> tasks;
-        tasks.reserve(8 * F.op.items.size());
-        for (const auto& it : F.op.items) tasks.insert(tasks.end(), {it.a_off, it.vt_off, it.r0, it.m, it.c0, it.ncols, it.k, 0});
+        tasks.reserve(10 * F.op.items.size());
+        for (const auto& it : F.op.items)
+            tasks.insert(tasks.end(), {it.a_off, it.a_ld, it.v_off, it.v_ld, it.r0, it.m, it.c0, it.ncols, it.k, 0});
         DBuf<int64_t> d;
         d.upload(c, tasks, "expand tasks", s);
         k::expand_C(d.p, (int)F.op.items.size(), F.op.arena.p, dlam.p, dM.p, n, s);
@@ -372,11 +375,11 @@ void factor_hlu(HLU& L, const double* emissivity) {
         build_hop(c, g, fz.bwd_src[lv], L.bwd[lv], s);
         account(L, L.fwd[lv]);
         account(L, L.bwd[lv]);
-        maxt = std::max({maxt, L.fwd[lv].n_p1, L.bwd[lv].n_p1});
+        maxt = std::max({maxt, L.fwd[lv].n_t, L.bwd[lv].n_t});
     }
     build_hop(c, g, lsrcL, L.leafL, s);
     build_hop(c, g, lsrcU, L.leafU, s);
-    L.bytes_leaf = L.leafL.p2_doubles + L.leafU.p2_doubles;
+    L.bytes_leaf = L.leafL.p2_doubles() + L.leafU.p2_doubles();
     L.bytes += L.bytes_leaf;
     L.n_blocks += 2 * (int64_t)g.leaves.size();
     fz.staging.clear();
@@ -391,9 +394,8 @@ void factor_hlu(HLU& L, const double* emissivity) {
     HM_CUDA(cudaMemcpyAsync(L.xtA.p, L.eps_int.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     HMat& Fm = const_cast<HMat&>(F);
     run_solve(L, nullptr, s, OUT_ASSIGN, Fm.xt.p, nullptr, nullptr);
-    k::phase1(F.op.p1.p, F.op.n_p1, F.op.arena.p, Fm.xt.p, n, s);
-    k::phase2(F.op.p2.p, F.op.n_p2, F.op.max_m, F.op.colsrc.p, F.op.arena.p, Fm.xt.p, L.g_int.p, OUT_ASSIGN, nullptr,
-              nullptr, s);
+    k::stream_pass(F.op.p1, F.op.colsrc.p, F.op.arena.p, Fm.xt.p, Fm.xt.p, OUT_ASSIGN, nullptr, nullptr, s);
+    k::stream_pass(F.op.p2, F.op.colsrc.p, F.op.arena.p, Fm.xt.p, L.g_int.p, OUT_ASSIGN, nullptr, nullptr, s);
     HM_CUDA(cudaStreamSynchronize(s));
     L.setup_seconds[3] = now_seconds() - t0;
 }

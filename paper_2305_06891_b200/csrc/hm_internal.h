@@ -119,19 +119,43 @@ void build_trees(Geom& g, const double* xyz, const double* nrm, const double* ar
                  const double* aabb);
 
 // ------------------------------------------------------------------ the two-phase stream operator
-// phase 1 (one warp per task): t[task] = dot(arena[off : off+n], XT[x_off : x_off+n])
-struct P1Task {
-    int64_t off;
-    int32_t n;
-    int32_t x_off;
+// Both phases are "column-stream panels": a column-major matrix (column stride ld, even) whose
+// column c multiplies the gathered input XT[colsrc[cs_off + c]].
+//   phase 1: one panel per column cluster tau: the V^T of every low-rank block (sigma, tau)
+//            stacked (K_tau = sum k rows); output rows are t entries (XT[n + ...]).
+//   phase 2: one panel per leaf row r: the leaf-row slices of the dense blocks and U factors
+//            covering r; output rows are the leaf's facets.
+// A panel is cut into work units (row tile <= 128 rows x column chunk of ~48 KB).  Units of the
+// same row tile ("group") write partial sums; the last-arriving unit adds them in segment order
+// (deterministic, no floating-point atomics).
+struct Unit {
+    int64_t a_off;     // arena offset of (tile row 0, panel column 0)
+    int64_t out0;      // output index of tile row 0
+    int64_t part_off;  // partial-sum scratch offset of this unit (nseg > 1)
+    int32_t ld;        // column stride of the panel (even)
+    int32_t nrows;     // rows in this tile (<= 128)
+    int32_t c0;        // first column of the chunk (relative to the panel)
+    int32_t ncols;     // columns in the chunk
+    int32_t cs_off;    // colsrc index of panel column 0
+    int32_t grp;       // combine group (-1: single unit writes directly)
+    int32_t nseg;      // units in the group
+    int32_t seg;       // index of this unit in its group (units of a group are consecutive)
 };
-// phase 2 (one CTA per leaf row): out[r0+i] (op)= sum_c arena[region + c*m + i] * XT[colsrc[col0+c]]
-struct P2Row {
-    int64_t region;
-    int32_t r0;
-    int32_t m;
-    int32_t col0;
-    int32_t ncols;
+
+struct Panel {         // host description of a panel
+    int64_t a_off;     // arena offset of row 0, column 0
+    int64_t out0;      // output index of row 0
+    int32_t ld, nrows, ncols, cs_off;
+};
+
+struct StreamPass {    // one launch worth of units
+    DBuf<Unit> units;
+    int64_t n_units = 0;
+    DBuf<double> part;
+    DBuf<int32_t> counters;
+    std::vector<Panel> panels;
+    int64_t doubles = 0;   // algorithmic payload read by this pass
+    bool empty() const { return n_units == 0; }
 };
 
 // A block as a source for the operator builder.
@@ -144,27 +168,21 @@ struct SrcBlock {
     int64_t d_rs = 0, d_cs = 0;
     const double* U = nullptr;       // U element (i,l) at U[l*u_ld + i]
     int64_t u_ld = 0;
-    const double* V = nullptr;       // V element (j,l) at V[l*v_ld + j]  (== V^T row-major)
+    const double* V = nullptr;       // V element (j,l) at V[l*v_ld + j]
     int64_t v_ld = 0;
 };
 
 struct HOp {
     int64_t n_rows_total = 0;     // n
     DBuf<double> arena;
-    int64_t p2_doubles = 0, p1_doubles = 0;   // algorithmic payload (no padding)
-    DBuf<P1Task> p1;
-    int64_t n_p1 = 0;             // == total rank (size of t)
-    DBuf<P2Row> p2;
-    int64_t n_p2 = 0;
+    StreamPass p1, p2;
     DBuf<int32_t> colsrc;
-    int64_t n_cols = 0;
-    int max_m = 0;
-    // host mirrors for re-use (expansion, scaling)
-    std::vector<P2Row> h_p2;
-    std::vector<int32_t> h_colsrc;
+    int64_t n_t = 0;              // total rank (size of t)
     struct ItemRec {              // one phase-2 item (a leaf-row slice of one block)
-        int64_t a_off;            // column-major m x (kind==LR ? k : ncols) in the arena
-        int64_t vt_off;           // LR: V^T (k x ncols) row-major; dense: -1
+        int64_t a_off;            // U slice / dense slice, column-major with stride a_ld
+        int64_t a_ld;
+        int64_t v_off;            // LR: V_b[j,l] at v_off + j*v_ld + l ; dense: -1
+        int64_t v_ld;
         int64_t r0, m, c0, ncols; // rows of the slice, columns of the block
         int64_t k;
     };
@@ -172,7 +190,9 @@ struct HOp {
     int64_t n_lr = 0, n_dense = 0;
     int64_t rank_sum = 0;
     int rank_max = 0;
-    bool empty() const { return n_p2 == 0; }
+    int64_t p1_doubles() const { return p1.doubles; }
+    int64_t p2_doubles() const { return p2.doubles; }
+    bool empty() const { return p1.empty() && p2.empty(); }
 };
 
 // Build the operator; XT layout is [x (n) | t (n_p1)].
@@ -236,17 +256,15 @@ void aca_batch(const double* geo, int64_t n, const int64_t* blk /*[nb][4] r0,m,c
                const int64_t* uoff, const int64_t* voff, const int32_t* kcap, int nb, double eps,
                double* scratch, int32_t* rank_out, double* margin_out, int32_t* err, cudaStream_t s,
                int64_t max_m, int64_t max_n);
-void fill_entries(const double* geo, int64_t n, const int64_t* tasks /*[nt][5] dst,r0,rows,c0,cols*/,
+void fill_entries(const double* geo, int64_t n, const int64_t* tasks /*[nt][6] dst,r0,rows,c0,cols,dld*/,
                   int nt, double* arena, int32_t* err, cudaStream_t s);
-void pack(const int64_t* tasks /*[nt][6] dst,src,rows,cols,rs,cs*/, int nt, double* arena,
-          const double* src_base, cudaStream_t s);
-void scale_rows(const P2Row* rows, int nrows, double* arena, const double* cdiv, cudaStream_t s);
-// apply
-void phase1(const P1Task* tasks, int64_t ntasks, const double* arena, double* xt, int64_t n,
-            cudaStream_t s);
-void phase2(const P2Row* rows, int64_t nrows, int max_m, const int32_t* colsrc, const double* arena,
-            const double* xt, double* out, int mode, const int32_t* perm, const FluxEpi* epi,
-            cudaStream_t s);
+// dst element (i,j) at arena[dst + j*dld + i] = src[i*rs + j*cs] (src absolute address)
+void pack(const int64_t* tasks /*[nt][7] dst,src,rows,cols,rs,cs,dld*/, int nt, double* arena, cudaStream_t s);
+void scale_rows(const int64_t* tasks /*[nt][5] a_off,ld,m,ncols,r0*/, int nt, double* arena, const double* cdiv,
+                cudaStream_t s);
+// apply: one stream pass (phase 1 -> out = xt, mode OUT_ASSIGN; phase 2 -> any mode)
+void stream_pass(const StreamPass& p, const int32_t* colsrc, const double* arena, const double* xt, double* out,
+                 int mode, const int32_t* perm, const FluxEpi* epi, cudaStream_t s);
 void permute_in(const double* x_ext, int ld, int col, const int32_t* perm, double* x_int, int64_t n,
                 cudaStream_t s);
 void permute_out(const double* y_int, const int32_t* perm, double* y_ext, int ld, int col, int64_t n,
@@ -257,7 +275,7 @@ void fill_value(double* p, int64_t n, double v, cudaStream_t s);
 void row_sums_clamp(const double* y, const double* area, double* sv, double* c, double* cdiv,
                     int64_t n, cudaStream_t s);
 // dense linear algebra (setup)
-void expand_C(const int64_t* tasks /*[nt][8]*/, int nt, const double* arena, const double* lam,
+void expand_C(const int64_t* tasks /*[nt][10]*/, int nt, const double* arena, const double* lam,
               double* M, int64_t ld, cudaStream_t s);
 void add_identity(double* M, int64_t ld, int64_t n, cudaStream_t s);
 // C = beta*C + alpha*op(A)*op(B); tri: 0 none, 1 lower-unit, 2 upper (masking of the operand)

@@ -1,13 +1,15 @@
 // Hot-path kernels: the two-phase streaming H-apply.
 //
-//   phase 1 (K6): t_b = V_b^T x_tau for every low-rank block b -- one warp per row of V_b^T,
-//                 coalesced loads along the row, warp-shuffle reduction, no atomics.
-//   phase 2 (K7): per leaf row r: out_r (op)= sum of the leaf row's column stream
-//                 (dense near-field slices and U slices, contiguous in HBM, column-major) times
-//                 the gathered inputs XT[colsrc[c]] (x for dense columns, t for U columns).
-//                 One CTA per leaf row owns its outputs (deterministic, no atomics).
-// The same two kernels run the F apply ("x -> F x ... recursively") and every
-// level of the level-scheduled substitution (W^L / W^U updates, leaf inverses).
+//   phase 1 (K6): t_b = V_b^T x_tau for every low-rank block b.  All blocks sharing a column
+//                 cluster tau are stacked into one column-major panel (K_tau x n_tau), so the
+//                 pass is a stream of contiguous columns times x_tau.
+//   phase 2 (K7): per leaf row r: out_r (op)= the leaf row's column stream (dense near-field
+//                 slices and U slices, contiguous in HBM, column-major) times the gathered
+//                 inputs XT[colsrc[c]] (x for dense columns, t for U columns).
+// Both run through ONE kernel over ~48 KB work units with 16-byte loads; split-K partials of a
+// row tile are added by its last-arriving unit in fixed order (deterministic, no FP atomics).
+// The same kernel runs the F apply ("x -> F x ... recursively") and every level
+// of the level-scheduled substitution (W^L / W^U updates, leaf inverses).
 #include <cstdint>
 
 #include "hm_internal.h"
@@ -15,86 +17,129 @@
 namespace hm {
 namespace {
 
-constexpr int kP1Threads = 256;
-constexpr int kP2Threads = 256;
-
-__global__ void __launch_bounds__(kP1Threads)
-phase1_kernel(const P1Task* __restrict__ tasks, int64_t ntasks, const double* __restrict__ arena,
-              double* __restrict__ xt, int64_t n) {
-    const int64_t w = ((int64_t)blockIdx.x * kP1Threads + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= ntasks) return;
-    const P1Task t = tasks[w];
-    const double* a = arena + t.off;
-    const double* x = xt + t.x_off;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int c = lane;
-    for (; c + 96 < t.n; c += 128) {
-        const double a0 = __ldg(a + c), a1 = __ldg(a + c + 32), a2 = __ldg(a + c + 64), a3 = __ldg(a + c + 96);
-        s0 = fma(a0, x[c], s0);
-        s1 = fma(a1, x[c + 32], s1);
-        s2 = fma(a2, x[c + 64], s2);
-        s3 = fma(a3, x[c + 96], s3);
-    }
-    for (; c < t.n; c += 32) s0 = fma(__ldg(a + c), x[c], s0);
-    double s = (s0 + s1) + (s2 + s3);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) xt[n + w] = s;
-}
+constexpr int kThreads = 256;
+constexpr int kQ = 12;          // columns per thread per work unit (row tile <= 128 rows)
 
 __device__ __forceinline__ double pow4(double T) {
     const double t2 = T * T;
     return t2 * t2;
 }
 
-__global__ void __launch_bounds__(kP2Threads)
-phase2_kernel(const P2Row* __restrict__ rows, const int32_t* __restrict__ colsrc,
-              const double* __restrict__ arena, const double* __restrict__ xt, double* __restrict__ out,
-              int mode, const int32_t* __restrict__ perm, FluxEpi epi) {
-    extern __shared__ double red[];
-    const P2Row r = rows[blockIdx.x];
-    const int m = r.m;
-    const int G = kP2Threads / m;
-    const int g = threadIdx.x / m;
-    const int i = threadIdx.x - g * m;
-    double acc = 0.0;
-    if (g < G) {
-        const double* a = arena + r.region + i;
-        const int32_t* cs = colsrc + r.col0;
-        double acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-        int c = g;
-        for (; c + 3 * G < r.ncols; c += 4 * G) {
-            const int32_t s0 = cs[c], s1 = cs[c + G], s2 = cs[c + 2 * G], s3 = cs[c + 3 * G];
-            const double a0 = __ldg(a + (int64_t)c * m);
-            const double a1 = __ldg(a + (int64_t)(c + G) * m);
-            const double a2 = __ldg(a + (int64_t)(c + 2 * G) * m);
-            const double a3 = __ldg(a + (int64_t)(c + 3 * G) * m);
-            acc = fma(a0, xt[s0], acc);
-            acc1 = fma(a1, xt[s1], acc1);
-            acc2 = fma(a2, xt[s2], acc2);
-            acc3 = fma(a3, xt[s3], acc3);
+__device__ __forceinline__ void emit(double* __restrict__ out, int64_t row, double s, int mode,
+                                     const int32_t* __restrict__ perm, const FluxEpi& epi) {
+    switch (mode) {
+        case OUT_ASSIGN: out[row] = s; break;
+        case OUT_SUB: out[row] -= s; break;
+        case OUT_PERM: out[(int64_t)perm[row] * epi.ld + epi.col] = s; break;
+        default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g), eq:qi_new_location operator form
+            const int64_t e = perm[row];
+            const double eta = pow4(epi.T_ext[e * epi.ld + epi.col]);
+            out[e * epi.ld + epi.col] = epi.sigma * (epi.eps_int[row] / epi.area_int[row]) * (s - eta * epi.g_int[row]);
         }
-        for (; c < r.ncols; c += G) acc = fma(__ldg(a + (int64_t)c * m), xt[cs[c]], acc);
-        acc = (acc + acc1) + (acc2 + acc3);
-        red[g * m + i] = acc;
+    }
+}
+
+// One CTA per work unit.  Rows are processed in pairs (16-byte loads); the chunk's columns are
+// split over G = 256 / pairs thread groups so that every thread owns at most kQ columns.  Each
+// thread issues all of its payload loads first (streaming hint: the factors are read once, the
+// vectors stay in L2), the gathered inputs of the chunk are staged once in shared memory, then
+// the FMAs run; partial sums are reduced through shared memory in fixed order.
+__global__ void __launch_bounds__(kThreads, 3)
+stream_kernel(const Unit* __restrict__ units, const int32_t* __restrict__ colsrc, const double* __restrict__ arena,
+              const double* __restrict__ xt, double* __restrict__ out, int mode, const int32_t* __restrict__ perm,
+              FluxEpi epi, double* __restrict__ part, int32_t* __restrict__ counters) {
+    __shared__ double2 red[kThreads];
+    __shared__ double xs[kThreads * kQ];
+    __shared__ int s_last;
+    // PDL: the next pass may start streaming its (constant) factor payload while this one drains
+    asm volatile("griddepcontrol.launch_dependents;");
+    const Unit u = units[blockIdx.x];
+    const int P = (u.nrows + 1) >> 1;
+    const int G = kThreads / P;
+    const int g = threadIdx.x / P;
+    const int p = threadIdx.x - g * P;
+    const bool active = g < G;
+    double2 av[kQ];
+    {
+        const double2* a = reinterpret_cast<const double2*>(arena + u.a_off + (int64_t)u.c0 * u.ld) + p;
+        const int64_t ld2 = u.ld >> 1;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            const int c = g + q * G;
+            av[q] = (active && c < u.ncols) ? __ldcs(a + (int64_t)c * ld2) : make_double2(0.0, 0.0);
+        }
+    }
+    // everything above reads only constant operator data; vectors are produced by the previous pass
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    {
+        const int32_t* cs = colsrc + u.cs_off + u.c0;
+        for (int c = threadIdx.x; c < u.ncols; c += kThreads) xs[c] = xt[__ldg(cs + c)];
     }
     __syncthreads();
-    if (g == 0) {
-        double s = red[i];
-        for (int q = 1; q < G; ++q) s += red[q * m + i];
-        const int64_t row = (int64_t)r.r0 + i;
-        switch (mode) {
-            case OUT_ASSIGN: out[row] = s; break;
-            case OUT_SUB: out[row] -= s; break;
-            case OUT_PERM: out[(int64_t)perm[row] * epi.ld + epi.col] = s; break;
-            default: {  // OUT_FLUX
-                const int64_t e = perm[row];
-                const double eta = pow4(epi.T_ext[e * epi.ld + epi.col]);
-                out[e * epi.ld + epi.col] =
-                    epi.sigma * (epi.eps_int[row] / epi.area_int[row]) * (s - eta * epi.g_int[row]);
+    double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+    if (active) {
+#pragma unroll
+        for (int q = 0; q < kQ; q += 2) {
+            const int c = g + q * G;
+            if (c < u.ncols) {
+                const double x = xs[c];
+                acc.x = fma(av[q].x, x, acc.x);
+                acc.y = fma(av[q].y, x, acc.y);
+            }
+            if (q + 1 < kQ && c + G < u.ncols) {
+                const double x = xs[c + G];
+                acc2.x = fma(av[q + 1].x, x, acc2.x);
+                acc2.y = fma(av[q + 1].y, x, acc2.y);
             }
         }
+        acc.x += acc2.x;
+        acc.y += acc2.y;
+        red[g * P + p] = acc;
     }
+    __syncthreads();
+    double2 s = make_double2(0.0, 0.0);
+    const bool owner = threadIdx.x < P;
+    if (owner) {
+        s = red[p];
+        for (int q = 1; q < G; ++q) {
+            const double2 v = red[q * P + p];
+            s.x += v.x;
+            s.y += v.y;
+        }
+    }
+    if (u.grp < 0) {
+        if (owner) {
+            const int r = 2 * p;
+            emit(out, u.out0 + r, s.x, mode, perm, epi);
+            if (r + 1 < u.nrows) emit(out, u.out0 + r + 1, s.y, mode, perm, epi);
+        }
+        return;
+    }
+    // split-K: publish the partial, the last unit of the group adds all partials in order
+    if (owner) reinterpret_cast<double2*>(part + u.part_off)[p] = s;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(counters + u.grp, 1);
+        s_last = (prev == u.nseg - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (owner) {
+        const int first = (int)blockIdx.x - u.seg;   // units of a group are consecutive
+        double2 t = make_double2(0.0, 0.0);
+        for (int q = 0; q < u.nseg; ++q) {
+            const Unit& uq = units[first + q];
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(part + uq.part_off) + p);
+            t.x += v.x;
+            t.y += v.y;
+        }
+        const int r = 2 * p;
+        emit(out, u.out0 + r, t.x, mode, perm, epi);
+        if (r + 1 < u.nrows) emit(out, u.out0 + r + 1, t.y, mode, perm, epi);
+    }
+    if (threadIdx.x == 0) counters[u.grp] = 0;   // re-arm for the next launch (graph-replay safe)
 }
 
 __global__ void permute_in_kernel(const double* __restrict__ x_ext, int ld, int col, const int32_t* __restrict__ perm,
@@ -135,24 +180,25 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 namespace k {
 
-void phase1(const P1Task* tasks, int64_t ntasks, const double* arena, double* xt, int64_t n, cudaStream_t s) {
-    if (ntasks == 0) return;
-    phase1_kernel<<<nblk(ntasks * 32, kP1Threads), kP1Threads, 0, s>>>(tasks, ntasks, arena, xt, n);
-    HM_CUDA(cudaGetLastError());
-    debug_sync(s, "phase1");
-}
-
-void phase2(const P2Row* rows, int64_t nrows, int max_m, const int32_t* colsrc, const double* arena,
-            const double* xt, double* out, int mode, const int32_t* perm, const FluxEpi* epi, cudaStream_t s) {
-    if (nrows == 0) return;
+void stream_pass(const StreamPass& p, const int32_t* colsrc, const double* arena, const double* xt, double* out,
+                 int mode, const int32_t* perm, const FluxEpi* epi, cudaStream_t s) {
+    if (p.n_units == 0) return;
     FluxEpi e{};
     if (epi) e = *epi;
     if (e.ld == 0) e.ld = 1;
-    phase2_kernel<<<(unsigned)nrows, kP2Threads, kP2Threads * sizeof(double), s>>>(rows, colsrc, arena, xt, out,
-                                                                                    mode, perm, e);
-    HM_CUDA(cudaGetLastError());
-    debug_sync(s, "phase2");
-    (void)max_m;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)p.n_units);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HM_CUDA(cudaLaunchKernelEx(&cfg, stream_kernel, p.units.p, colsrc, arena, xt, out, mode, perm, e, p.part.p,
+                               p.counters.p));
+    debug_sync(s, "stream_kernel");
 }
 
 void permute_in(const double* x_ext, int ld, int col, const int32_t* perm, double* x_int, int64_t n, cudaStream_t s) {

@@ -215,33 +215,33 @@ aca_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restri
 
 __global__ void fill_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restrict__ tasks,
                             double* __restrict__ arena, int32_t* err) {
-    const int64_t* t = tasks + 5 * blockIdx.x;
-    const int64_t dst = t[0], r0 = t[1], rows = t[2], c0 = t[3], cols = t[4];
+    const int64_t* t = tasks + 6 * blockIdx.x;
+    const int64_t dst = t[0], r0 = t[1], rows = t[2], c0 = t[3], cols = t[4], dld = t[5];
     const GeoView g(geo, ntot);
     for (int64_t e = threadIdx.x; e < rows * cols; e += blockDim.x) {
         const int64_t i = e % rows, j = e / rows;  // column-major slice
-        arena[dst + e] = vf_entry(g, r0 + i, c0 + j, err);
+        arena[dst + j * dld + i] = vf_entry(g, r0 + i, c0 + j, err);
     }
 }
 
 __global__ void pack_kernel(const int64_t* __restrict__ tasks, double* __restrict__ arena) {
-    const int64_t* t = tasks + 6 * blockIdx.x;
+    const int64_t* t = tasks + 7 * blockIdx.x;
     const int64_t dst = t[0];
     const double* src = reinterpret_cast<const double*>(t[1]);
-    const int64_t rows = t[2], cols = t[3], rs = t[4], cs = t[5];
+    const int64_t rows = t[2], cols = t[3], rs = t[4], cs = t[5], dld = t[6];
     for (int64_t e = threadIdx.x; e < rows * cols; e += blockDim.x) {
         const int64_t i = e % rows, j = e / rows;
-        arena[dst + e] = src[i * rs + j * cs];
+        arena[dst + j * dld + i] = src[i * rs + j * cs];
     }
 }
 
-__global__ void scale_rows_kernel(const P2Row* __restrict__ rows, double* __restrict__ arena,
+__global__ void scale_rows_kernel(const int64_t* __restrict__ tasks, double* __restrict__ arena,
                                   const double* __restrict__ cdiv) {
-    const P2Row r = rows[blockIdx.x];
-    const int64_t tot = (int64_t)r.m * r.ncols;
-    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int i = (int)(e % r.m);
-        arena[r.region + e] = arena[r.region + e] / cdiv[r.r0 + i];
+    const int64_t* t = tasks + 5 * blockIdx.x;
+    const int64_t a_off = t[0], ld = t[1], m = t[2], ncols = t[3], r0 = t[4];
+    for (int64_t e = threadIdx.x; e < m * ncols; e += blockDim.x) {
+        const int64_t i = e % m, j = e / m;
+        arena[a_off + j * ld + i] = arena[a_off + j * ld + i] / cdiv[r0 + i];
     }
 }
 
@@ -270,16 +270,16 @@ void fill_entries(const double* geo, int64_t n, const int64_t* tasks, int nt, do
     debug_sync(s, "fill_kernel");
 }
 
-void pack(const int64_t* tasks, int nt, double* arena, const double*, cudaStream_t s) {
+void pack(const int64_t* tasks, int nt, double* arena, cudaStream_t s) {
     if (nt == 0) return;
     pack_kernel<<<nt, 256, 0, s>>>(tasks, arena);
     HM_CUDA(cudaGetLastError());
     debug_sync(s, "pack_kernel");
 }
 
-void scale_rows(const P2Row* rows, int nrows, double* arena, const double* cdiv, cudaStream_t s) {
-    if (nrows == 0) return;
-    scale_rows_kernel<<<nrows, 256, 0, s>>>(rows, arena, cdiv);
+void scale_rows(const int64_t* tasks, int nt, double* arena, const double* cdiv, cudaStream_t s) {
+    if (nt == 0) return;
+    scale_rows_kernel<<<nt, 256, 0, s>>>(tasks, arena, cdiv);
     HM_CUDA(cudaGetLastError());
     debug_sync(s, "scale_rows");
 }

@@ -201,16 +201,17 @@ __global__ void extract_tri_kernel(const double* __restrict__ Minv, int64_t ld, 
 
 __global__ void expand_kernel(const int64_t* __restrict__ tasks, const double* __restrict__ arena,
                               const double* __restrict__ lam, double* __restrict__ M, int64_t ld) {
-    const int64_t* t = tasks + 8 * blockIdx.x;
-    const int64_t a_off = t[0], vt_off = t[1], r0 = t[2], m = t[3], c0 = t[4], nc = t[5], k = t[6];
+    const int64_t* t = tasks + 10 * blockIdx.x;
+    const int64_t a_off = t[0], a_ld = t[1], v_off = t[2], v_ld = t[3], r0 = t[4], m = t[5], c0 = t[6], nc = t[7],
+                  k = t[8];
     for (int64_t e = threadIdx.x; e < m * nc; e += blockDim.x) {
         const int64_t i = e / nc, j = e % nc;
         double v;
-        if (vt_off < 0) {
-            v = arena[a_off + j * m + i];
+        if (v_off < 0) {
+            v = arena[a_off + j * a_ld + i];
         } else {
             v = 0.0;
-            for (int64_t l = 0; l < k; ++l) v += arena[a_off + l * m + i] * arena[vt_off + l * nc + j];
+            for (int64_t l = 0; l < k; ++l) v += arena[a_off + l * a_ld + i] * arena[v_off + j * v_ld + l];
         }
         M[(r0 + i) * ld + c0 + j] = -lam[r0 + i] * v;
     }
