@@ -74,6 +74,11 @@ typedef struct {
 typedef struct {
     double eps_lu;         /* truncation tolerance of the factor blocks; <= 0 -> eps_aca
                               ("equal to the approximation accuracy used for F")   */
+    int32_t cut_level;     /* level-scheduled substitution: W-form updates for
+                              tree levels < cut_level, then ONE block-diagonal solve with the
+                              inverse factors of the cut_level diagonal blocks (H-format).
+                              cut_level = depth: leaf inverses only (pure level form);
+                              0: C^-1 b = U^-1 (L^-1 b) as two H-applies; < 0: depth          */
 } hm_lu_params;
 
 /* Storage / traffic accounting (bytes are fp64 payload bytes actually stored in HBM). */
@@ -90,8 +95,8 @@ typedef struct {
     int64_t n_blocks_C, n_lowrank_C;
     int64_t rank_max_C;
     double rank_mean_C;
-    int64_t launches_apply_F;         /* kernels per hm_apply_F (nrhs = 1)                     */
-    int64_t launches_solve_C;         /* kernels per hm_solve_C (nrhs = 1)                     */
+    int64_t launches_apply_F;         /* kernel launches per hm_apply_F column (engine: 1)      */
+    int64_t launches_solve_C;         /* kernel launches per hm_solve_C column (engine: 1)      */
     double setup_seconds[8];          /* tree, aca, dense-fill+pack, rowsum+scale, C-expand,
                                          dense LU+W, W-compress+pack, flux constant g          */
 } hm_storage;
@@ -160,13 +165,22 @@ hm_status hm_storage_report(const hm_hmat* F, const hm_hlu* LU, hm_storage* out)
 hm_status hm_local_range(const hm_geom* geom, int rank, int world, int64_t* begin, int64_t* end);
 
 /* ---- measurement support (bench.py) ---------------------------------------------------- */
-/* Times each kernel class of hm_radiative_flux (device pointers, nrhs = 1) with CUDA events on
-   `stream` over `iters` calls; ms_out[0..5] = per-call ms of: permute/prologue, F phase 1,
-   F phase 2 (+epilogue), solve phase 1 (all levels), solve phase 2 (all levels), leaf solves.
-   launches_out[0..5] = kernel launches per call of each class. */
+/* Times the hot-path programs with CUDA events on `stream` (device pointers T, q; nrhs = 1) over
+   `iters` calls each: ms_out[0] = hm_radiative_flux, ms_out[1] = hm_apply_F, ms_out[2] =
+   hm_solve_C (per call; each call is ONE launch of the persistent stream engine); ms_out[3..5]
+   = 0.  launches_out[0..2] = kernel launches per call (1); launches_out[3] = passes of the flux
+   program, [4] = its work units, [5] = its grid size. */
 hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, const double* T,
                           double* q, int32_t iters, double* ms_out, int64_t* launches_out,
                           void* stream);
+
+/* Per-pass timeline of one hm_radiative_flux call (device pointers, nrhs = 1), from %globaltimer
+   stamps inside the engine: t_begin_us[p] = first input gather of pass p, t_end_us[p] = last task
+   retirement, both relative to the earliest pass start; pass_bytes[p] = factor payload bytes of
+   pass p.  Arrays have max_passes entries; *n_passes receives the program's pass count. */
+hm_status hm_trace_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, const double* T, double* q,
+                        int32_t max_passes, int32_t* n_passes, double* t_begin_us, double* t_end_us,
+                        int64_t* pass_bytes, void* stream);
 
 void hm_destroy_geom(hm_geom* geom);
 void hm_destroy_hmat(hm_hmat* F);

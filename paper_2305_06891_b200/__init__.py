@@ -41,7 +41,7 @@ class hm_aca_params(C.Structure):
 
 
 class hm_lu_params(C.Structure):
-    _fields_ = [("eps_lu", C.c_double)]
+    _fields_ = [("eps_lu", C.c_double), ("cut_level", C.c_int32)]
 
 
 class hm_storage(C.Structure):
@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH):
         "hm_storage_report": (C.c_int, [P, P, C.POINTER(hm_storage)]),
         "hm_local_range": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(I64), C.POINTER(I64)]),
         "hm_profile_flux": (C.c_int, [P, P, P, P, P, I32, P, P, P]),
+        "hm_trace_flux": (C.c_int, [P, P, P, P, P, I32, C.POINTER(I32), P, P, P, P]),
         "hm_destroy_geom": (None, [P]),
         "hm_destroy_hmat": (None, [P]),
         "hm_destroy_hlu": (None, [P]),
@@ -208,9 +209,9 @@ def hm_assemble_aca(ctx: Context, geom: Geometry, eps_aca=1e-6, k_max=0, closed_
     return HMatrix(ctx, h, geom)
 
 
-def hm_factor_hlu(ctx: Context, F: HMatrix, emissivity, eps_lu=0.0) -> HLU:
+def hm_factor_hlu(ctx: Context, F: HMatrix, emissivity, eps_lu=0.0, cut_level=-1) -> HLU:
     e = np.ascontiguousarray(emissivity, dtype=np.float64)
-    p = hm_lu_params(float(eps_lu))
+    p = hm_lu_params(float(eps_lu), int(cut_level))
     h = C.c_void_p()
     ctx.check(ctx.lib.hm_factor_hlu(ctx.h, F.h, e.ctypes.data, C.byref(p), C.byref(h)), "hm_factor_hlu")
     return HLU(ctx, h, F)
@@ -288,5 +289,20 @@ def hm_profile_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, iters: int, stream=
     pq, kq = _ptr(q)
     ctx.check(ctx.lib.hm_profile_flux(ctx.h, F.h, LU.h, pT, pq, int(iters), ms, la, _stream(stream, T, q)),
               "hm_profile_flux")
-    names = ["prologue", "F_phase1", "F_phase2", "solve_phase1", "solve_phase2", "leaf_solves"]
-    return dict(zip(names, list(ms))), dict(zip(names, list(la)))
+    ms_d = {"flux": ms[0], "apply_F": ms[1], "solve_C": ms[2]}
+    info = {"launches_per_call": int(la[0]), "passes": int(la[3]), "units": int(la[4]), "grid": int(la[5])}
+    return ms_d, info
+
+
+def hm_trace_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, max_passes: int = 256, stream=None):
+    """Per-pass timeline of one flux call: list of (pass, begin_us, end_us, bytes)."""
+    npass = C.c_int32()
+    b = np.zeros(max_passes)
+    e = np.zeros(max_passes)
+    by = np.zeros(max_passes, dtype=np.int64)
+    pT, kT = _ptr(T)
+    pq, kq = _ptr(q)
+    ctx.check(ctx.lib.hm_trace_flux(ctx.h, F.h, LU.h, pT, pq, max_passes, C.byref(npass), b.ctypes.data,
+                                    e.ctypes.data, by.ctypes.data, _stream(stream, T, q)), "hm_trace_flux")
+    m = min(npass.value, max_passes)
+    return [(i, float(b[i]), float(e[i]), int(by[i])) for i in range(m)]

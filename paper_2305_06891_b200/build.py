@@ -18,8 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", CSRC,
           "-I", os.path.join(os.path.dirname(HERE), "include")]
-SOURCES = ["tree.cpp", "hop.cpp", "api.cpp", "hlu.cpp",
-           "kernels_assembly.cu", "kernels_apply.cu", "kernels_dense.cu"]
+SOURCES = ["tree.cpp", "hop.cpp", "api.cpp", "hlu.cpp", "engine.cpp",
+           "kernels_assembly.cu", "kernels_apply.cu", "kernels_dense.cu", "kernels_engine.cu"]
 
 
 def _digest() -> str:

@@ -57,8 +57,6 @@ void dfree(Ctx* ctx, void* p) {
 
 // implemented in hlu.cpp
 void factor_hlu(HLU& L, const double* emissivity);
-void run_solve(HLU& L, const double* b_int_ready, cudaStream_t s, int mode, double* out, const FluxEpi* epi,
-               double* ms_accum);
 
 }  // namespace hm
 
@@ -378,9 +376,15 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         sv.alloc(c, n, "row sums");
         cv.alloc(c, n, "clamped row sums");
         cdiv.alloc(c, n, "row divisors");
-        k::fill_value(F.xt.p, n, 1.0, s);
-        k::stream_pass(F.op.p1, F.op.colsrc.p, F.op.arena.p, F.xt.p, F.xt.p, OUT_ASSIGN, nullptr, nullptr, s);
-        k::stream_pass(F.op.p2, F.op.colsrc.p, F.op.arena.p, F.xt.p, F.y.p, OUT_ASSIGN, nullptr, nullptr, s);
+        {   // F_H 1 with the engine (setup program, internal order)
+            Program rs;
+            rs.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN);
+            rs.add_stream(F.op.p2, F.op, F.xt.p, F.y.p, OUT_ASSIGN);
+            rs.finalize(c, s);
+            k::fill_value(F.xt.p, n, 1.0, s);
+            rs.launch(ProgArgs{}, s);
+            HM_CUDA(cudaStreamSynchronize(s));
+        }
         k::row_sums_clamp(F.y.p, g.d_geo.p + 6 * n, sv.p, cv.p, cdiv.p, n, s);
         if (params->closed_cavity) {
             std::vector<int64_t> tasks;
@@ -400,6 +404,12 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             F.s_ext[g.perm[i]] = hs[i];
             F.c_ext[g.perm[i]] = hc[i];
         }
+        // hot-path program: permute-in -> phase 1 -> phase 2 with permute-out fused
+        F.prog_apply.add_elementwise(UNIT_PERMUTE, n, F.xt.p);
+        F.prog_apply.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN);
+        F.prog_apply.add_stream(F.op.p2, F.op, F.xt.p, nullptr, OUT_PERM);
+        F.prog_apply.finalize(c, s);
+        HM_CUDA(cudaStreamSynchronize(s));
         F.setup_seconds[2] = now_seconds() - t0;
         *F_out = guard.release();
     });
@@ -431,13 +441,14 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
             if (F.host_stage_out.n < (size_t)n * nrhs) F.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
             yd = F.host_stage_out.p;
         }
-        FluxEpi epi{};
-        epi.ld = nrhs;
         for (int col = 0; col < nrhs; ++col) {
-            epi.col = col;
-            k::permute_in(xd, nrhs, col, g.d_perm.p, F.xt.p, n, s);
-            k::stream_pass(F.op.p1, F.op.colsrc.p, F.op.arena.p, F.xt.p, F.xt.p, OUT_ASSIGN, nullptr, nullptr, s);
-            k::stream_pass(F.op.p2, F.op.colsrc.p, F.op.arena.p, F.xt.p, yd, OUT_PERM, g.d_perm.p, &epi, s);
+            ProgArgs a{};
+            a.perm = g.d_perm.p;
+            a.user_in = xd;
+            a.user_out = yd;
+            a.ld = nrhs;
+            a.col = col;
+            F.prog_apply.launch(a, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
@@ -460,12 +471,14 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
             if (L.host_stage_out.n < (size_t)n * nrhs) L.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
             zd = L.host_stage_out.p;
         }
-        FluxEpi epi{};
-        epi.ld = nrhs;
         for (int col = 0; col < nrhs; ++col) {
-            epi.col = col;
-            k::permute_in(bd, nrhs, col, g.d_perm.p, L.xtA.p, n, s);
-            run_solve(L, nullptr, s, OUT_PERM, zd, &epi, nullptr);
+            ProgArgs a{};
+            a.perm = g.d_perm.p;
+            a.user_in = bd;
+            a.user_out = zd;
+            a.ld = nrhs;
+            a.col = col;
+            L.prog_solve.launch(a, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
@@ -475,43 +488,22 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
 }  // extern "C"
 
 namespace hm {
-// One flux evaluation for column `col` (device pointers).  ms_accum (optional, 6 entries)
-// receives per-class times measured with events on `s`.
-void run_flux(HLU& L, const double* Td, double* qd, int ld, int col, cudaStream_t s, double* ms_accum) {
-    const HMat& F = *L.F;
-    const Geom& g = *F.geom;
-    const int64_t n = g.n;
-    cudaEvent_t ev[2];
-    if (ms_accum) {
-        HM_CUDA(cudaEventCreate(&ev[0]));
-        HM_CUDA(cudaEventCreate(&ev[1]));
-        HM_CUDA(cudaEventRecord(ev[0], s));
-    }
-    auto lap = [&](int cls) {
-        if (!ms_accum) return;
-        HM_CUDA(cudaEventRecord(ev[1], s));
-        HM_CUDA(cudaEventSynchronize(ev[1]));
-        float ms = 0;
-        HM_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-        ms_accum[cls] += ms;
-        std::swap(ev[0], ev[1]);
-    };
-    k::flux_prologue(Td, ld, col, g.d_perm.p, L.eps_int.p, L.xtA.p, n, s);
-    lap(0);
-    // z = C^-1 w into F's x-part
-    run_solve(L, nullptr, s, OUT_ASSIGN, const_cast<double*>(F.xt.p), nullptr, ms_accum);
-    if (ms_accum) HM_CUDA(cudaEventRecord(ev[0], s));
-    double* fxt = const_cast<double*>(F.xt.p);
-    k::stream_pass(F.op.p1, F.op.colsrc.p, F.op.arena.p, fxt, fxt, OUT_ASSIGN, nullptr, nullptr, s);
-    lap(1);
-    FluxEpi epi{Td, g.d_perm.p, L.eps_int.p, g.d_geo.p + 6 * n, L.g_int.p, 5.670374419e-8, ld, col};
-    k::stream_pass(F.op.p2, F.op.colsrc.p, F.op.arena.p, fxt, qd, OUT_FLUX, g.d_perm.p, &epi, s);
-    lap(2);
-    if (ms_accum) {
-        cudaEventDestroy(ev[0]);
-        cudaEventDestroy(ev[1]);
-    }
+// One flux evaluation (engine program, one launch) for column `col` (device pointers).
+void launch_flux(HLU& L, const double* Td, double* qd, int ld, int col, cudaStream_t s) {
+    const Geom& g = *L.F->geom;
+    ProgArgs a{};
+    a.perm = g.d_perm.p;
+    a.user_in = Td;
+    a.user_out = qd;
+    a.ld = ld;
+    a.col = col;
+    a.eps_int = L.eps_int.p;
+    a.area_int = g.d_geo.p + 6 * g.n;
+    a.g_int = L.g_int.p;
+    a.sigma = 5.670374419e-8;  // DESIGN.md reading R2
+    L.prog_flux.launch(a, s);
 }
+
 }  // namespace hm
 
 extern "C" {
@@ -536,7 +528,7 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
             if (L.host_stage_out.n < (size_t)n * nrhs) L.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
             qd = L.host_stage_out.p;
         }
-        for (int col = 0; col < nrhs; ++col) run_flux(L, Td, qd, nrhs, col, s, nullptr);
+        for (int col = 0; col < nrhs; ++col) launch_flux(L, Td, qd, nrhs, col, s);
         if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
     });
@@ -548,20 +540,80 @@ hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, con
     Ctx* c = &ctx->c;
     return guarded(c, [&] {
         HLU& L = const_cast<HLU&>(LUh->h);
+        HMat& F = const_cast<HMat&>(Fh->h);
+        const Geom& g = *F.geom;
         cudaStream_t s = (cudaStream_t)stream;
-        double acc[6] = {0, 0, 0, 0, 0, 0};
-        for (int it = 0; it < iters; ++it) run_flux(L, T, q, 1, 0, s, acc);
-        for (int q2 = 0; q2 < 6; ++q2) ms_out[q2] = acc[q2] / iters;
+        cudaEvent_t e0, e1;
+        HM_CUDA(cudaEventCreate(&e0));
+        HM_CUDA(cudaEventCreate(&e1));
+        auto timeit = [&](auto&& fn) {
+            fn();
+            HM_CUDA(cudaEventRecord(e0, s));
+            for (int it = 0; it < iters; ++it) fn();
+            HM_CUDA(cudaEventRecord(e1, s));
+            HM_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            HM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            return (double)ms / iters;
+        };
+        ProgArgs a{};
+        a.perm = g.d_perm.p;
+        a.user_in = T;
+        a.user_out = q;
+        a.ld = 1;
+        ms_out[0] = timeit([&] { launch_flux(L, T, q, 1, 0, s); });
+        ms_out[1] = timeit([&] { F.prog_apply.launch(a, s); });
+        ms_out[2] = timeit([&] { L.prog_solve.launch(a, s); });
+        for (int i = 3; i < 6; ++i) ms_out[i] = 0.0;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
         if (launches_out) {
-            int64_t sp1 = 0, sp2 = 0;
-            for (auto* v : {&L.fwd, &L.bwd})
-                for (auto& op : *v) { sp1 += !op.p1.empty(); sp2 += !op.p2.empty(); }
-            launches_out[0] = 1;
-            launches_out[1] = !Fh->h.op.p1.empty();
-            launches_out[2] = 1;
-            launches_out[3] = sp1;
-            launches_out[4] = sp2;
-            launches_out[5] = 2;
+            launches_out[0] = launches_out[1] = launches_out[2] = 1;
+            launches_out[3] = (int64_t)L.prog_flux.h_passes.size();
+            launches_out[4] = (int64_t)L.prog_flux.h_units.size();
+            launches_out[5] = L.prog_flux.grid;
+        }
+    });
+}
+
+hm_status hm_trace_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, const double* T, double* q,
+                        int32_t max_passes, int32_t* n_passes, double* t_begin_us, double* t_end_us,
+                        int64_t* pass_bytes, void* stream) {
+    if (!ctx || !Fh || !LUh || !T || !q || !n_passes) return HM_ERR_INVALID_ARG;
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        HLU& L = const_cast<HLU&>(LUh->h);
+        Program& P = L.prog_flux;
+        cudaStream_t s = (cudaStream_t)stream;
+        const size_t np = P.h_passes.size();
+        *n_passes = (int32_t)np;
+        std::vector<unsigned long long> init(2 * np);
+        for (size_t i = 0; i < np; ++i) { init[2 * i] = ~0ull; init[2 * i + 1] = 0ull; }
+        if (P.trace.n < 2 * np) P.trace.alloc(c, 2 * np, "engine trace");
+        HM_CUDA(cudaMemcpyAsync(P.trace.p, init.data(), 2 * np * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+        const Geom& g = *L.F->geom;
+        ProgArgs a{};
+        a.perm = g.d_perm.p;
+        a.user_in = T;
+        a.user_out = q;
+        a.ld = 1;
+        a.eps_int = L.eps_int.p;
+        a.area_int = g.d_geo.p + 6 * g.n;
+        a.g_int = L.g_int.p;
+        a.sigma = 5.670374419e-8;
+        a.trace = P.trace.p;
+        P.launch(a, s);
+        std::vector<unsigned long long> tr(2 * np);
+        HM_CUDA(cudaMemcpyAsync(tr.data(), P.trace.p, 2 * np * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        unsigned long long t0 = ~0ull;
+        for (size_t i = 0; i < np; ++i) t0 = std::min(t0, tr[2 * i]);
+        std::vector<int64_t> bytes(np, 0);
+        for (const Unit& u : P.h_units) bytes[u.pass] += u.type == UNIT_STREAM ? 8LL * u.ncols * u.ld : 0;
+        for (size_t i = 0; i < np && (int32_t)i < max_passes; ++i) {
+            if (t_begin_us) t_begin_us[i] = (tr[2 * i] == ~0ull) ? -1.0 : (double)(tr[2 * i] - t0) * 1e-3;
+            if (t_end_us) t_end_us[i] = (double)(tr[2 * i + 1] - t0) * 1e-3;
+            if (pass_bytes) pass_bytes[i] = bytes[i];
         }
     });
 }
@@ -586,7 +638,7 @@ hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* ou
     out->bytes_F_phase1 = 8 * F.op.p1_doubles();
     out->bytes_F_phase2 = 8 * F.op.p2_doubles();
     out->bytes_F = out->bytes_F_phase1 + out->bytes_F_phase2;
-    out->launches_apply_F = 1 + !F.op.p1.empty() + 1;
+    out->launches_apply_F = 1;  // one persistent engine launch
     for (int q = 0; q < 3; ++q) out->setup_seconds[q] = F.setup_seconds[q];
     out->setup_seconds[0] += g.setup_seconds;
     if (LUh) {
@@ -597,10 +649,7 @@ hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* ou
         out->n_lowrank_C = L.n_lr;
         out->rank_max_C = L.rank_max;
         out->rank_mean_C = L.n_lr ? double(L.rank_sum) / L.n_lr : 0.0;
-        int64_t la = 1 + 2;  // permute-in + two leaf solves
-        for (auto* v : {&L.fwd, &L.bwd})
-            for (auto& op : *v) la += !op.p1.empty() + !op.p2.empty();
-        out->launches_solve_C = la;
+        out->launches_solve_C = 1;  // one persistent engine launch
         for (int q = 0; q < 4; ++q) out->setup_seconds[4 + q] = L.setup_seconds[q];
     }
     return HM_OK;

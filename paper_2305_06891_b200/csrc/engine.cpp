@@ -1,0 +1,174 @@
+// Host side of the persistent stream engine: assemble passes, chunks and tasks into a program and
+// derive each task's dependency waits.
+//
+// Level-form sweeps (DESIGN.md §"Solve in level form"): the update of node t reads b[t1] and
+// writes b[t2]; every ancestor's update writes rows of t (RAW) or reads rows t writes (WAR), and
+// every descendant's update touches rows t reads or writes.  So the sweep's dependency graph is
+// the cluster tree itself: a node's tasks wait for its nearest ancestor with work to have retired
+// (which transitively covers all ancestors), and a node's phase-2 tasks also wait for its own
+// phase-1 tasks (the t = V^T b values).  Independent subtrees never wait for each other; only the
+// sweep boundaries (forward -> backward -> F apply) are barriers.
+#include "engine.h"
+
+namespace hm {
+
+int add_stream_impl(Program& P, const StreamPass& sp, const HOp& op, const double* in, double* out, int mode, int kind,
+                    const std::vector<int32_t>* panel_node) {
+    if (sp.h_units.empty()) return -1;
+    Pass p{};
+    p.type = UNIT_STREAM;
+    p.dep = (int32_t)P.h_passes.size() - 1;
+    p.mode = mode;
+    p.first_unit = (int64_t)P.h_units.size();
+    p.n_units = (int64_t)sp.h_units.size();
+    p.arena = op.arena.p;
+    p.colsrc = op.colsrc.p;
+    p.in = in;
+    p.out = out;
+    p.part = sp.part.p;
+    p.counters = sp.counters.p;
+    const int32_t idx = (int32_t)P.h_passes.size();
+    const int64_t base = (int64_t)P.h_units.size();
+    for (size_t q = 0; q < sp.h_units.size(); ++q) {
+        Unit u = sp.h_units[q];
+        u.pass = idx;
+        u.type = UNIT_STREAM;
+        u.first_chunk += base;
+        if (u.chunk == 0) {
+            Task t{};
+            t.first_unit = (int64_t)P.h_units.size();
+            t.n_units = u.nchunks;
+            t.pass = idx;
+            t.wait_id[0] = t.wait_id[1] = t.inc_id[0] = t.inc_id[1] = -1;
+            P.h_tasks.push_back(t);
+            P.task_kind.push_back(kind);
+            P.task_node.push_back(panel_node ? (*panel_node)[sp.unit_panel[q]] : -1);
+            ++p.n_tasks;
+        }
+        P.h_units.push_back(u);
+    }
+    P.h_passes.push_back(p);
+    return idx;
+}
+
+void Program::add_stream(const StreamPass& sp, const HOp& op, const double* in, double* out, int mode, int kind,
+                         const std::vector<int32_t>* panel_node) {
+    add_stream_impl(*this, sp, op, in, out, mode, kind, panel_node);
+}
+
+void Program::add_elementwise(int type, int64_t n, double* out) {
+    Pass p{};
+    p.type = type;
+    p.dep = (int32_t)h_passes.size() - 1;
+    p.mode = OUT_ASSIGN;
+    p.first_unit = (int64_t)h_units.size();
+    p.out = out;
+    const int32_t idx = (int32_t)h_passes.size();
+    for (int64_t r = 0; r < n; r += 160) {   // one row per consumer thread
+        Unit u{};
+        u.out0 = r;
+        u.nrows = (int32_t)std::min<int64_t>(160, n - r);
+        u.grp = -1;
+        u.nseg = 1;
+        u.pass = idx;
+        u.type = type;
+        u.chunk = 0;
+        u.nchunks = 1;
+        u.first_chunk = (int64_t)h_units.size();
+        Task t{};
+        t.first_unit = (int64_t)h_units.size();
+        t.n_units = 1;
+        t.pass = idx;
+        t.wait_id[0] = t.wait_id[1] = t.inc_id[0] = t.inc_id[1] = -1;
+        h_tasks.push_back(t);
+        task_kind.push_back(DEP_BARRIER);
+        task_node.push_back(-1);
+        h_units.push_back(u);
+    }
+    p.n_units = (int64_t)h_units.size() - p.first_unit;
+    p.n_tasks = p.n_units;
+    h_passes.push_back(p);
+}
+
+void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
+    for (const Unit& u : h_units)
+        if (u.type == UNIT_STREAM && (u.ncols > kUnitMaxCols || u.ld > 128 || (int64_t)u.ncols * u.ld > kUnitPayloadDoubles))
+            throw Error(HM_ERR_UNSUPPORTED, "work unit exceeds the engine stage size");
+    const int64_t P = (int64_t)h_passes.size();
+    const int64_t nn = g ? (int64_t)g->nodes.size() : 0;
+    n_counters = P + 4 * nn;
+    auto c_p1 = [&](int sw, int node) { return (int32_t)(P + sw * 2 * nn + node); };
+    auto c_all = [&](int sw, int node) { return (int32_t)(P + sw * 2 * nn + nn + node); };
+    std::vector<int64_t> cnt(n_counters, 0);  // tasks that increment each counter
+    auto sweep_of = [](int kind) { return kind >= DEP_BWD_P1 ? 1 : 0; };
+    for (size_t i = 0; i < h_tasks.size(); ++i) {
+        Task& t = h_tasks[i];
+        const int kind = task_kind[i], node = task_node[i];
+        cnt[t.pass]++;
+        if (kind == DEP_FWD_P1 || kind == DEP_BWD_P1) {
+            t.inc_id[0] = c_p1(sweep_of(kind), node);
+            t.inc_id[1] = c_all(sweep_of(kind), node);
+        } else if (kind == DEP_FWD_P2 || kind == DEP_BWD_P2) {
+            t.inc_id[0] = c_all(sweep_of(kind), node);
+        }
+        for (int q = 0; q < 2; ++q)
+            if (t.inc_id[q] >= 0) cnt[t.inc_id[q]]++;
+    }
+    for (size_t i = 0; i < h_tasks.size(); ++i) {
+        Task& t = h_tasks[i];
+        const int kind = task_kind[i], node = task_node[i];
+        int nw = 0;
+        auto wait = [&](int32_t id) {
+            if (id >= 0 && cnt[id] > 0 && nw < 2) {
+                t.wait_id[nw] = id;
+                t.wait_cnt[nw] = (int32_t)cnt[id];
+                ++nw;
+            }
+        };
+        if (kind == DEP_BARRIER) {
+            wait(t.pass - 1);
+            continue;
+        }
+        if (!g || node < 0) throw Error(HM_ERR_INVALID_ARG, "tree-dependency pass without tree nodes");
+        const int sw = sweep_of(kind);
+        int par = g->nodes[node].parent;
+        while (par >= 0 && cnt[c_all(sw, par)] == 0) par = g->nodes[par].parent;
+        if (par >= 0) wait(c_all(sw, par));
+        else wait(sweep_dep[sw]);
+        if (kind == DEP_FWD_P2 || kind == DEP_BWD_P2) wait(c_p1(sw, node));
+    }
+    passes.upload(ctx, h_passes, "engine passes", s);
+    units.upload(ctx, h_units, "engine units", s);
+    tasks.upload(ctx, h_tasks, "engine tasks", s);
+    done.alloc(ctx, (size_t)std::max<int64_t>(n_counters, 1), "engine dependency counters");
+    HM_CUDA(cudaMemsetAsync(done.p, 0, sizeof(unsigned long long) * std::max<int64_t>(n_counters, 1), s));
+    queue.alloc(ctx, 1, "engine task queue");
+    HM_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(unsigned long long), s));
+    pf.alloc(ctx, 1, "engine prefetch counter");
+    HM_CUDA(cudaMemsetAsync(pf.p, 0, sizeof(unsigned long long), s));
+    grid = engine_grid();
+    epoch = 0;
+    ready = true;
+}
+
+void Program::launch(ProgArgs a, cudaStream_t s) {
+    if (h_tasks.empty()) return;
+    a.passes = passes.p;
+    a.units = units.p;
+    a.tasks = tasks.p;
+    a.n_tasks = (int64_t)h_tasks.size();
+    a.queue = queue.p;
+    // every CTA's producer takes exactly one index past the end: the counter advances by
+    // n_tasks + grid per launch
+    a.queue_base = epoch * (unsigned long long)(h_tasks.size() + grid);
+    // the prefetch warp's 32 lanes each take one index past the end per CTA
+    a.pf_counter = pf.p;
+    a.pf_base = epoch * (unsigned long long)(h_units.size() + 32ull * grid);
+    a.n_units = (int64_t)h_units.size();
+    a.done = done.p;
+    a.epoch = ++epoch;
+    if (a.ld == 0) a.ld = 1;
+    engine_launch(a, grid, s);
+}
+
+}  // namespace hm

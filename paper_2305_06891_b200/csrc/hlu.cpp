@@ -45,6 +45,7 @@ struct Factorizer {
     std::vector<DBuf<double>> staging;
 
     static constexpr int KMAX_LU = 64;
+    int cut = 0;  // W blocks are formed only for tree nodes above the cut level
 
     void collect() {
         lower.assign(g.nodes.size(), {});
@@ -206,14 +207,15 @@ struct Factorizer {
         // W^L = L21 L11^-1 ; (L^-1)21 = -L22^-1 W^L
         k::dgemm(n2, n1, n1, 1.0, Mp(b2, b1), n, 0, Ip(b1, b1), n, 1, 0.0, T, n1, s);
         const int lvl = tree_internal ? g.nodes[node].level : -1;
-        if (tree_internal) stage_dense(lower[node], b2, b1, n1, fwd_src[lvl]);
+        const bool wform = tree_internal && lvl < cut;
+        if (wform) stage_dense(lower[node], b2, b1, n1, fwd_src[lvl]);
         k::dgemm(n2, n1, n2, -1.0, Ip(b2, b2), n, 1, T, n1, 0, 0.0, Ip(b2, b1), n, s);
-        if (tree_internal) compress(lower[node], b2, b1, n1, fwd_src[lvl]);
+        if (wform) compress(lower[node], b2, b1, n1, fwd_src[lvl]);
         // W^U = U12 U22^-1 ; (U^-1)12 = -U11^-1 W^U
         k::dgemm(n1, n2, n2, 1.0, Mp(b1, b2), n, 0, Ip(b2, b2), n, 2, 0.0, T, n2, s);
-        if (tree_internal) stage_dense(upper[node], b1, b2, n2, bwd_src[lvl]);
+        if (wform) stage_dense(upper[node], b1, b2, n2, bwd_src[lvl]);
         k::dgemm(n1, n2, n1, -1.0, Ip(b1, b1), n, 2, T, n2, 0, 0.0, Ip(b1, b2), n, s);
-        if (tree_internal) compress(upper[node], b1, b2, n2, bwd_src[lvl]);
+        if (wform) compress(upper[node], b1, b2, n2, bwd_src[lvl]);
     }
 };
 
@@ -226,49 +228,6 @@ void account(HLU& L, const HOp& op) {
 }
 
 }  // namespace
-
-void run_solve(HLU& L, const double*, cudaStream_t s, int mode, double* out, const FluxEpi* epi, double* ms_accum) {
-    const Geom& g = *L.F->geom;
-    const int64_t n = g.n;
-    cudaEvent_t ev[2];
-    if (ms_accum) {
-        HM_CUDA(cudaEventCreate(&ev[0]));
-        HM_CUDA(cudaEventCreate(&ev[1]));
-    }
-    auto t0 = [&]() { if (ms_accum) HM_CUDA(cudaEventRecord(ev[0], s)); };
-    auto lap = [&](int cls) {
-        if (!ms_accum) return;
-        HM_CUDA(cudaEventRecord(ev[1], s));
-        HM_CUDA(cudaEventSynchronize(ev[1]));
-        float ms = 0;
-        HM_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-        ms_accum[cls] += ms;
-    };
-    auto level = [&](const HOp& op, double* xt) {
-        if (!op.p1.empty()) {
-            t0();
-            k::stream_pass(op.p1, op.colsrc.p, op.arena.p, xt, xt, OUT_ASSIGN, nullptr, nullptr, s);
-            lap(3);
-        }
-        if (!op.p2.empty()) {
-            t0();
-            k::stream_pass(op.p2, op.colsrc.p, op.arena.p, xt, xt, OUT_SUB, nullptr, nullptr, s);
-            lap(4);
-        }
-    };
-    for (const HOp& op : L.fwd) level(op, L.xtA.p);
-    t0();
-    k::stream_pass(L.leafL.p2, L.leafL.colsrc.p, L.leafL.arena.p, L.xtA.p, L.xtB.p, OUT_ASSIGN, nullptr, nullptr, s);
-    lap(5);
-    for (const HOp& op : L.bwd) level(op, L.xtB.p);
-    t0();
-    k::stream_pass(L.leafU.p2, L.leafU.colsrc.p, L.leafU.arena.p, L.xtB.p, out, mode, g.d_perm.p, epi, s);
-    lap(5);
-    if (ms_accum) {
-        cudaEventDestroy(ev[0]);
-        cudaEventDestroy(ev[1]);
-    }
-}
 
 void factor_hlu(HLU& L, const double* emissivity) {
     const HMat& F = *L.F;
@@ -326,20 +285,38 @@ void factor_hlu(HLU& L, const double* emissivity) {
     fz.err = derr.p;
     fz.collect();
     const int D = g.depth;
-    fz.fwd_src.assign(std::max(D, 0), {});
-    fz.bwd_src.assign(std::max(D, 0), {});
+    // cut level: W-form updates for levels < Lc, then block-diagonal solves with the inverse
+    // factors of the level-Lc diagonal blocks (Lc = depth: leaf inverses only)
+    const int Lc = (L.params.cut_level < 0 || L.params.cut_level > D) ? D : L.params.cut_level;
+    L.cut_level = Lc;
+    fz.cut = Lc;
+    fz.fwd_src.assign(std::max(Lc, 0), {});
+    fz.bwd_src.assign(std::max(Lc, 0), {});
     fz.rec(0, 0, n);
     int32_t herr[4];
     HM_CUDA(cudaMemcpyAsync(herr, derr.p, sizeof(herr), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
     if (herr[0]) throw Error(HM_ERR_SINGULAR, "near-zero pivot (|pivot| <= 1e-14 ||block||) in a leaf LU of C");
-    // leaf inverses
+    // cut nodes: level == Lc, or leaves shallower than Lc
+    std::vector<int> cut_nodes;
+    {
+        std::vector<int> st{0};
+        while (!st.empty()) {
+            const int t = st.back();
+            st.pop_back();
+            const Node& N = g.nodes[t];
+            if (N.level == Lc || N.is_leaf()) { cut_nodes.push_back(t); continue; }
+            st.push_back(N.child[1]);
+            st.push_back(N.child[0]);
+        }
+    }
+    // leaf diagonal inverses (masked unit-lower / upper)
     int64_t leaf_tot = 0;
     for (int l : g.leaves) leaf_tot += g.nodes[l].size() * g.nodes[l].size();
     DBuf<double> dLi, dUi;
     dLi.alloc(c, (size_t)leaf_tot, "leaf L^-1");
     dUi.alloc(c, (size_t)leaf_tot, "leaf U^-1");
-    std::vector<SrcBlock> lsrcL, lsrcU;
+    std::vector<SrcBlock> srcL, srcU;
     int64_t off = 0;
     for (int l : g.leaves) {
         const Node& N = g.nodes[l];
@@ -352,10 +329,29 @@ void factor_hlu(HLU& L, const double* emissivity) {
         S.d_rs = m;
         S.d_cs = 1;
         S.dense = dLi.p + off;
-        lsrcL.push_back(S);
+        srcL.push_back(S);
         S.dense = dUi.p + off;
-        lsrcU.push_back(S);
+        srcU.push_back(S);
         off += m * m;
+    }
+    HM_CUDA(cudaStreamSynchronize(s));
+    // off-diagonal blocks of the cut diagonal blocks' inverse factors, compressed in F's partition
+    // straight out of L^-1 / U^-1 (dense blocks staged first, admissible blocks truncated in place)
+    fz.T = dMinv.p;
+    for (int t0n : cut_nodes) {
+        std::vector<int> st{t0n};
+        while (!st.empty()) {
+            const int t = st.back();
+            st.pop_back();
+            const Node& N = g.nodes[t];
+            if (N.is_leaf()) continue;
+            fz.stage_dense(fz.lower[t], 0, 0, n, srcL);
+            fz.stage_dense(fz.upper[t], 0, 0, n, srcU);
+            fz.compress(fz.lower[t], 0, 0, n, srcL);
+            fz.compress(fz.upper[t], 0, 0, n, srcU);
+            st.push_back(N.child[0]);
+            st.push_back(N.child[1]);
+        }
     }
     HM_CUDA(cudaStreamSynchronize(s));
     L.setup_seconds[1] = now_seconds() - t0;
@@ -365,38 +361,97 @@ void factor_hlu(HLU& L, const double* emissivity) {
     dM.reset();
     dMinv.reset();
     dT.reset();
-    L.fwd.resize(std::max(D, 0));
-    L.bwd.resize(std::max(D, 0));
+    L.fwd.resize(std::max(Lc, 0));
+    L.bwd.resize(std::max(Lc, 0));
     L.bytes = L.bytes_leaf = L.n_blocks = L.n_lr = L.rank_sum = 0;
     L.rank_max = 0;
     int64_t maxt = 0;
-    for (int lv = 0; lv < D; ++lv) {
+    for (int lv = 0; lv < Lc; ++lv) {
         build_hop(c, g, fz.fwd_src[lv], L.fwd[lv], s);
         build_hop(c, g, fz.bwd_src[lv], L.bwd[lv], s);
         account(L, L.fwd[lv]);
         account(L, L.bwd[lv]);
         maxt = std::max({maxt, L.fwd[lv].n_t, L.bwd[lv].n_t});
     }
-    build_hop(c, g, lsrcL, L.leafL, s);
-    build_hop(c, g, lsrcU, L.leafU, s);
-    L.bytes_leaf = L.leafL.p2_doubles() + L.leafU.p2_doubles();
-    L.bytes += L.bytes_leaf;
-    L.n_blocks += 2 * (int64_t)g.leaves.size();
+    build_hop(c, g, srcL, L.leafL, s);
+    build_hop(c, g, srcU, L.leafU, s);
+    account(L, L.leafL);
+    account(L, L.leafU);
+    maxt = std::max({maxt, L.leafL.n_t, L.leafU.n_t});
+    L.bytes_leaf = L.leafL.p1_doubles() + L.leafL.p2_doubles() + L.leafU.p1_doubles() + L.leafU.p2_doubles();
     fz.staging.clear();
     L.xtA.alloc(c, (size_t)(n + maxt), "solve xtA");
     L.xtB.alloc(c, (size_t)(n + maxt), "solve xtB");
     L.z.alloc(c, (size_t)n, "solve z");
     L.setup_seconds[2] = now_seconds() - t0;
 
-    // ---- flux constant g = F C^-1 eps
+    // ---- hot-path programs for the persistent engine (tree dependencies within each sweep)
+    HMat& Fm = const_cast<HMat&>(F);
+    auto node_at_level = [&](int64_t row, int level) {   // deepest node on the row's path with level <= level
+        int node = 0;
+        while (g.nodes[node].level < level && !g.nodes[node].is_leaf()) {
+            const Node& N = g.nodes[node];
+            node = row < g.nodes[N.child[1]].begin ? N.child[0] : N.child[1];
+        }
+        return node;
+    };
+    auto node_map = [&](const StreamPass& sp, int level) {
+        std::vector<int32_t> m;
+        for (const Panel& pn : sp.panels) m.push_back(node_at_level(pn.key, level));
+        return m;
+    };
+    const auto mL1 = node_map(L.leafL.p1, Lc), mL2 = node_map(L.leafL.p2, Lc);
+    const auto mU1 = node_map(L.leafU.p1, Lc), mU2 = node_map(L.leafU.p2, Lc);
+    // forward sweep, block-diagonal L^-1 at the cut, backward sweep (U^-1 at the cut left to the caller)
+    auto solve_passes = [&](Program& P) {
+        P.sweep_dep[0] = (int32_t)P.h_passes.size() - 1;  // the prologue / permute pass
+        for (int lv = 0; lv < Lc; ++lv) {
+            HOp& op = L.fwd[lv];
+            const auto m1 = node_map(op.p1, lv), m2 = node_map(op.p2, lv);
+            P.add_stream(op.p1, op, L.xtA.p, L.xtA.p, OUT_ASSIGN, DEP_FWD_P1, &m1);
+            P.add_stream(op.p2, op, L.xtA.p, L.xtA.p, OUT_SUB, DEP_FWD_P2, &m2);
+        }
+        P.add_stream(L.leafL.p1, L.leafL, L.xtA.p, L.xtA.p, OUT_ASSIGN, DEP_FWD_P1, &mL1);
+        P.sweep_dep[1] = (int32_t)P.h_passes.size();  // the cut L^-1 phase-2 pass
+        P.add_stream(L.leafL.p2, L.leafL, L.xtA.p, L.xtB.p, OUT_ASSIGN, DEP_FWD_P2, &mL2);
+        for (int lv = 0; lv < Lc; ++lv) {
+            HOp& op = L.bwd[lv];
+            const auto m1 = node_map(op.p1, lv), m2 = node_map(op.p2, lv);
+            P.add_stream(op.p1, op, L.xtB.p, L.xtB.p, OUT_ASSIGN, DEP_BWD_P1, &m1);
+            P.add_stream(op.p2, op, L.xtB.p, L.xtB.p, OUT_SUB, DEP_BWD_P2, &m2);
+        }
+        P.add_stream(L.leafU.p1, L.leafU, L.xtB.p, L.xtB.p, OUT_ASSIGN, DEP_BWD_P1, &mU1);
+    };
+    L.prog_solve.add_elementwise(UNIT_PERMUTE, n, L.xtA.p);
+    solve_passes(L.prog_solve);
+    L.prog_solve.add_stream(L.leafU.p2, L.leafU, L.xtB.p, nullptr, OUT_PERM, DEP_BWD_P2, &mU2);
+    L.prog_solve.finalize(c, s, &g);
+    L.prog_flux.add_elementwise(UNIT_PROLOGUE, n, L.xtA.p);
+    solve_passes(L.prog_flux);
+    L.prog_flux.add_stream(L.leafU.p2, L.leafU, L.xtB.p, Fm.xt.p, OUT_ASSIGN, DEP_BWD_P2, &mU2);
+    L.prog_flux.add_stream(F.op.p1, F.op, Fm.xt.p, Fm.xt.p, OUT_ASSIGN);
+    L.prog_flux.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX);
+    L.prog_flux.finalize(c, s, &g);
+
+    // ---- flux constant g = F C^-1 eps, with a setup program
     t0 = now_seconds();
     L.g_int.alloc(c, (size_t)n, "g");
-    HM_CUDA(cudaMemcpyAsync(L.xtA.p, L.eps_int.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    HMat& Fm = const_cast<HMat&>(F);
-    run_solve(L, nullptr, s, OUT_ASSIGN, Fm.xt.p, nullptr, nullptr);
-    k::stream_pass(F.op.p1, F.op.colsrc.p, F.op.arena.p, Fm.xt.p, Fm.xt.p, OUT_ASSIGN, nullptr, nullptr, s);
-    k::stream_pass(F.op.p2, F.op.colsrc.p, F.op.arena.p, Fm.xt.p, L.g_int.p, OUT_ASSIGN, nullptr, nullptr, s);
-    HM_CUDA(cudaStreamSynchronize(s));
+    {
+        Program pg;
+        pg.add_elementwise(UNIT_PERMUTE, n, L.xtA.p);
+        solve_passes(pg);
+        pg.add_stream(L.leafU.p2, L.leafU, L.xtB.p, Fm.xt.p, OUT_ASSIGN, DEP_BWD_P2, &mU2);
+        pg.add_stream(F.op.p1, F.op, Fm.xt.p, Fm.xt.p, OUT_ASSIGN);
+        pg.add_stream(F.op.p2, F.op, Fm.xt.p, L.g_int.p, OUT_ASSIGN);
+        pg.finalize(c, s, &g);
+        DBuf<double> eps_ext;
+        eps_ext.upload(c, std::vector<double>(emissivity, emissivity + n), "eps (external)", s);
+        ProgArgs a{};
+        a.perm = g.d_perm.p;
+        a.user_in = eps_ext.p;
+        pg.launch(a, s);
+        HM_CUDA(cudaStreamSynchronize(s));
+    }
     L.setup_seconds[3] = now_seconds() - t0;
 }
 
@@ -417,6 +472,7 @@ hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
         H->h.ctx = c;
         H->h.F = &F->h;
         H->h.params.eps_lu = (params && params->eps_lu > 0.0) ? params->eps_lu : F->h.params.eps_aca;
+        H->h.params.cut_level = params ? params->cut_level : -1;
         factor_hlu(H->h, emissivity);
         *out = guard.release();
         return HM_OK;

@@ -128,28 +128,55 @@ void build_trees(Geom& g, const double* xyz, const double* nrm, const double* ar
 // A panel is cut into work units (row tile <= 128 rows x column chunk of ~48 KB).  Units of the
 // same row tile ("group") write partial sums; the last-arriving unit adds them in segment order
 // (deterministic, no floating-point atomics).
+// A chunk: <= 32 KB of contiguous payload (ncols * ld doubles) + its column-source list; the unit
+// of TMA transfer.  A task = consecutive chunks of one panel piece, processed by one CTA that
+// accumulates in registers and emits once.  Pieces of the same panel (only panels > 512 KB are
+// split) combine deterministically: the last-finishing piece adds the partials in piece order.
 struct Unit {
-    int64_t a_off;     // arena offset of (tile row 0, panel column 0)
-    int64_t out0;      // output index of tile row 0
-    int64_t part_off;  // partial-sum scratch offset of this unit (nseg > 1)
-    int32_t ld;        // column stride of the panel (even)
-    int32_t nrows;     // rows in this tile (<= 128)
-    int32_t c0;        // first column of the chunk (relative to the panel)
-    int32_t ncols;     // columns in the chunk
-    int32_t cs_off;    // colsrc index of panel column 0
-    int32_t grp;       // combine group (-1: single unit writes directly)
-    int32_t nseg;      // units in the group
-    int32_t seg;       // index of this unit in its group (units of a group are consecutive)
+    int64_t a_off;     // arena offset of the chunk payload
+    int64_t out0;      // output index of row 0 of the panel
+    int64_t part_off;  // partial-sum scratch offset of this piece (nseg > 1)
+    int64_t cs_off;    // colsrc offset of the chunk's first column (multiple of 4: 16-byte aligned)
+    int32_t ld;        // column stride (even, <= 128)
+    int32_t nrows;     // rows (<= 128)
+    int32_t ncols;     // columns of this chunk (<= 512)
+    int32_t grp;       // combine group of the panel (-1: single piece writes directly)
+    int32_t nseg;      // pieces in the group
+    int32_t seg;       // piece index
+    int32_t pass;      // program pass index (engine)
+    int32_t type;      // UNIT_STREAM / UNIT_PROLOGUE / UNIT_PERMUTE
+    int32_t chunk;     // chunk index within the piece
+    int32_t nchunks;   // chunks in the piece
+    int64_t first_chunk;  // index (in the unit list) of the piece's first chunk
 };
+enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2 };
+constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage
+constexpr int kUnitMaxCols = 512;
+constexpr int64_t kPieceDoubles = 65536;    // panels above 512 KB are split into pieces
+
+// A task waits until counter[wait_id[i]] >= epoch * wait_cnt[i] (i < 2, id -1 = none) before its
+// first input gather, and on retirement increments counter[pass] and counter[inc_id[i]].
+struct Task {
+    int64_t first_unit;
+    int32_t n_units;
+    int32_t pass;
+    int32_t wait_id[2];
+    int32_t wait_cnt[2];
+    int32_t inc_id[2];
+};
+// dependency kinds of a pass (engine programs)
+enum DepKind : int { DEP_BARRIER = 0, DEP_FWD_P1, DEP_FWD_P2, DEP_FWD_LEAF, DEP_BWD_P1, DEP_BWD_P2, DEP_BWD_LEAF };
 
 struct Panel {         // host description of a panel
     int64_t a_off;     // arena offset of row 0, column 0
     int64_t out0;      // output index of row 0
     int32_t ld, nrows, ncols, cs_off;
+    int64_t key;       // phase 1: first column of the cluster tau; phase 2: first row of the leaf
 };
 
-struct StreamPass {    // one launch worth of units
-    DBuf<Unit> units;
+struct StreamPass {    // one pass worth of chunks (host copy; programs upload them)
+    std::vector<Unit> h_units;
+    std::vector<int32_t> unit_panel;   // panel index of each chunk
     int64_t n_units = 0;
     DBuf<double> part;
     DBuf<int32_t> counters;
@@ -176,7 +203,7 @@ struct HOp {
     int64_t n_rows_total = 0;     // n
     DBuf<double> arena;
     StreamPass p1, p2;
-    DBuf<int32_t> colsrc;
+    DBuf<int32_t> colsrc;          // per-unit, 16-byte aligned column-source segments
     int64_t n_t = 0;              // total rank (size of t)
     struct ItemRec {              // one phase-2 item (a leaf-row slice of one block)
         int64_t a_off;            // U slice / dense slice, column-major with stride a_ld
@@ -197,6 +224,75 @@ struct HOp {
 
 // Build the operator; XT layout is [x (n) | t (n_p1)].
 void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s);
+
+// ------------------------------------------------------------------ persistent stream engine
+struct Pass {
+    int32_t type;        // UnitType of its units
+    int32_t dep;         // pass whose completion this pass waits for (-1: none)
+    int32_t mode;        // OutMode
+    int32_t pad;
+    int64_t first_unit, n_units;
+    int64_t n_tasks;
+    const double* arena;
+    const int32_t* colsrc;
+    const double* in;    // input vector (nullptr: the call's user_in)
+    double* out;         // output vector (OUT_ASSIGN / OUT_SUB; element-wise units)
+    double* part;        // split-K partials
+    int32_t* counters;   // split-K group counters
+};
+
+struct ProgArgs {
+    const Pass* passes;
+    const Unit* units;
+    const Task* tasks;
+    int64_t n_tasks;
+    unsigned long long* queue;  // monotone task counter
+    unsigned long long queue_base;  // counter value at the start of this launch
+    unsigned long long* pf_counter; // monotone L2-prefetch chunk counter
+    unsigned long long pf_base;
+    int64_t n_units;
+    unsigned long long* done;   // dependency counters (passes, then per-node), monotone over launches
+    unsigned long long* trace;  // optional: per pass [first gather, last retire] (%globaltimer ns)
+    unsigned long long epoch;   // launch number of this program (1-based)
+    const int32_t* perm;
+    const double* user_in;      // x / b / T (external order, ld x ncol)
+    double* user_out;           // y / z / q (external order)
+    int ld, col;
+    const double* eps_int;
+    const double* area_int;
+    const double* g_int;
+    double sigma;
+};
+
+// A program = passes in topological order; executes in one cooperative launch.
+struct Program {
+    std::vector<Pass> h_passes;
+    std::vector<Unit> h_units;
+    std::vector<Task> h_tasks;
+    DBuf<Pass> passes;
+    DBuf<Unit> units;
+    DBuf<Task> tasks;
+    DBuf<unsigned long long> queue;   // monotone task counter (epoch * n_tasks at the end of a launch)
+    DBuf<unsigned long long> pf;      // monotone L2-prefetch counter
+    DBuf<unsigned long long> done;
+    unsigned long long epoch = 0;
+    int grid = 0;
+    bool ready = false;
+    std::vector<int32_t> task_kind, task_node;   // dependency kind / tree node of each task
+    int32_t sweep_dep[2] = {-1, -1};             // pass the root of the fwd / bwd sweep waits for
+    int64_t n_counters = 0;
+    DBuf<unsigned long long> trace;
+    // builder: panel_node (optional) maps each panel of `sp` to its tree node (tree kinds)
+    void add_stream(const StreamPass& sp, const HOp& op, const double* in, double* out, int mode,
+                    int kind = DEP_BARRIER, const std::vector<int32_t>* panel_node = nullptr);
+    void add_elementwise(int type, int64_t n, double* out);
+    void finalize(Ctx* ctx, cudaStream_t s, const Geom* g = nullptr);
+    void launch(ProgArgs a, cudaStream_t s);
+};
+
+size_t engine_smem_bytes();
+int engine_grid();
+void engine_launch(const ProgArgs& A, int grid, cudaStream_t s);
 
 // output modes of phase 2
 enum OutMode : int { OUT_ASSIGN = 0, OUT_SUB = 1, OUT_PERM = 2, OUT_FLUX = 3 };
@@ -223,18 +319,16 @@ struct HMat {
     DBuf<double> xt;   // [x | t]
     DBuf<double> y;    // internal-order output
     DBuf<double> host_stage_in, host_stage_out;
-    int launches = 0;
-    bool graph_ready = false;
-    cudaGraphExec_t graph = nullptr;
-    cudaStream_t graph_stream = nullptr;
+    Program prog_apply;   // permute-in -> F phase 1 -> F phase 2 (+ permute-out)
 };
 
 struct HLU {
     Ctx* ctx;
     const HMat* F;
     hm_lu_params params;
-    std::vector<HOp> fwd, bwd;   // per level (may be empty ops)
-    HOp leafL, leafU;
+    std::vector<HOp> fwd, bwd;   // per level above the cut (may be empty ops)
+    HOp leafL, leafU;            // block-diagonal inverse factors of the cut-level diagonal blocks
+    int cut_level = 0;
     DBuf<double> xtA;            // [b | t] forward pass (t sized for the largest level)
     DBuf<double> xtB;            // [y | t] backward pass
     DBuf<double> z;              // internal-order result
@@ -243,10 +337,8 @@ struct HLU {
     double setup_seconds[4] = {0, 0, 0, 0};
     int64_t bytes = 0, bytes_leaf = 0, n_blocks = 0, n_lr = 0, rank_sum = 0;
     int rank_max = 0;
-    // flux graph
-    bool graph_ready = false;
-    cudaGraphExec_t graph = nullptr;
-    cudaStream_t graph_stream = nullptr;
+    Program prog_solve;   // permute-in -> forward levels -> leaf L^-1 -> backward levels -> leaf U^-1
+    Program prog_flux;    // prologue -> solve passes -> F phase 1 -> F phase 2 + flux epilogue
 };
 
 // ------------------------------------------------------------------ kernel launchers (kernels_*.cu)
@@ -262,9 +354,6 @@ void fill_entries(const double* geo, int64_t n, const int64_t* tasks /*[nt][6] d
 void pack(const int64_t* tasks /*[nt][7] dst,src,rows,cols,rs,cs,dld*/, int nt, double* arena, cudaStream_t s);
 void scale_rows(const int64_t* tasks /*[nt][5] a_off,ld,m,ncols,r0*/, int nt, double* arena, const double* cdiv,
                 cudaStream_t s);
-// apply: one stream pass (phase 1 -> out = xt, mode OUT_ASSIGN; phase 2 -> any mode)
-void stream_pass(const StreamPass& p, const int32_t* colsrc, const double* arena, const double* xt, double* out,
-                 int mode, const int32_t* perm, const FluxEpi* epi, cudaStream_t s);
 void permute_in(const double* x_ext, int ld, int col, const int32_t* perm, double* x_int, int64_t n,
                 cudaStream_t s);
 void permute_out(const double* y_int, const int32_t* perm, double* y_ext, int ld, int col, int64_t n,

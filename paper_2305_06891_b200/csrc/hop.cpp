@@ -6,7 +6,7 @@
 //           [ phase-2 panels: per leaf row r, the leaf-row slices of every dense block and U
 //             factor covering r: column-major, ld = m_r (even), in block order              ]
 //   colsrc[c] = index into XT = [x (n) | t (sum k)] of the input multiplying column c.
-// Panels are cut into ~48 KB work units (row tile <= 128 rows x column chunk).
+// Panels have <= 128 rows and are cut into work units of <= 32 KB contiguous payload.
 #include <algorithm>
 #include <map>
 
@@ -16,41 +16,62 @@ namespace hm {
 
 static inline int64_t align2(int64_t x) { return (x + 1) & ~int64_t(1); }
 
-static void make_units(Ctx* ctx, StreamPass& P, cudaStream_t s) {
-    std::vector<Unit> units;
+// Cut panels into pieces (only panels above 512 KB are split, for load balance) and pieces into
+// chunks of <= 32 KB contiguous payload (<= 512 columns), each chunk with its own 16-byte
+// aligned column-source segment (so the engine can TMA both).
+static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs, std::vector<int32_t>& ucs,
+                       cudaStream_t s) {
+    std::vector<Unit>& units = P.h_units;
+    units.clear();
+    P.unit_panel.clear();
     int64_t part = 0;
     int32_t grp = 0;
-    constexpr int kThreads = 256, kQ = 12;  // must match kernels_apply.cu: <= kQ columns per thread
-    for (const Panel& pn : P.panels) {
+    // piece size adapted to the pass: ~4 tasks per SM (small passes still spread over the chip),
+    // between one chunk and kPieceDoubles
+    int64_t pass_doubles = 0;
+    for (const Panel& pn : P.panels) pass_doubles += (int64_t)pn.ncols * pn.ld;
+    const int64_t piece = std::max<int64_t>(4 * kUnitPayloadDoubles,
+                                            std::min<int64_t>(kPieceDoubles, pass_doubles / (2 * 148)));
+    for (size_t pi = 0; pi < P.panels.size(); ++pi) {
+        const Panel& pn = P.panels[pi];
         if (pn.ncols == 0) continue;
-        for (int32_t tr0 = 0; tr0 < pn.nrows; tr0 += 128) {
-            const int32_t tn = std::min<int32_t>(128, pn.nrows - tr0);
-            const int32_t tn_pad = (tn + 1) & ~1;
-            const int64_t G = kThreads / (tn_pad / 2);
-            int64_t C = kQ * G;  // ~ 12 * 256 * 2 doubles = 48 KB of payload per work unit
-            const int32_t nseg = (int32_t)((pn.ncols + C - 1) / C);
-            C = (pn.ncols + nseg - 1) / nseg;
-            const int32_t g = nseg > 1 ? grp++ : -1;
-            for (int32_t sg = 0; sg < nseg; ++sg) {
+        const int64_t total = (int64_t)pn.ncols * pn.ld;
+        const int32_t npieces = (int32_t)std::min<int64_t>(pn.ncols, (total + piece - 1) / piece);
+        const int64_t Cp = (pn.ncols + npieces - 1) / npieces;
+        const int32_t g = npieces > 1 ? grp++ : -1;
+        for (int32_t pc = 0; pc < npieces; ++pc) {
+            const int64_t p0 = pc * Cp, p1 = std::min<int64_t>(pn.ncols, p0 + Cp);
+            int64_t C = std::min<int64_t>(kUnitMaxCols, kUnitPayloadDoubles / pn.ld);
+            const int32_t nch = (int32_t)((p1 - p0 + C - 1) / C);
+            C = (p1 - p0 + nch - 1) / nch;
+            const int64_t first = (int64_t)units.size();
+            for (int32_t ch = 0; ch < nch; ++ch) {
                 Unit u{};
-                u.a_off = pn.a_off + tr0;
-                u.out0 = pn.out0 + tr0;
-                u.part_off = nseg > 1 ? part : 0;
+                const int64_t c0 = p0 + ch * C;
+                u.ncols = (int32_t)std::min<int64_t>(C, p1 - c0);
+                u.a_off = pn.a_off + c0 * pn.ld;
+                u.out0 = pn.out0;
+                u.part_off = npieces > 1 ? part : 0;
+                u.cs_off = (int64_t)ucs.size();
+                for (int32_t c = 0; c < u.ncols; ++c) ucs.push_back(pcs[pn.cs_off + c0 + c]);
+                while (ucs.size() % 4) ucs.push_back(0);
                 u.ld = pn.ld;
-                u.nrows = tn;
-                u.c0 = (int32_t)(sg * C);
-                u.ncols = (int32_t)std::min<int64_t>(C, pn.ncols - sg * C);
-                u.cs_off = pn.cs_off;
+                u.nrows = pn.nrows;
                 u.grp = g;
-                u.nseg = nseg;
-                u.seg = sg;
+                u.nseg = npieces;
+                u.seg = pc;
+                u.pass = 0;
+                u.type = UNIT_STREAM;
+                u.chunk = ch;
+                u.nchunks = nch;
+                u.first_chunk = first;
                 units.push_back(u);
-                if (nseg > 1) part += tn_pad;
+                P.unit_panel.push_back((int32_t)pi);
             }
+            if (npieces > 1) part += pn.ld;
         }
     }
     P.n_units = (int64_t)units.size();
-    P.units.upload(ctx, units, "work units", s);
     P.part.alloc(ctx, (size_t)std::max<int64_t>(part, 2), "split-K partials");
     P.counters.alloc(ctx, (size_t)std::max<int32_t>(grp, 1), "split-K counters");
     HM_CUDA(cudaMemsetAsync(P.counters.p, 0, sizeof(int32_t) * std::max<int32_t>(grp, 1), s));
@@ -92,26 +113,32 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
         }
     }
     for (const auto& members : taus) {
-        const SrcBlock& B0 = blocks[members[0]];
-        int64_t K = 0;
-        for (int b : members) K += blocks[b].k;
-        const int64_t ld = align2(K);
-        Panel pn{off, n + tcount, (int32_t)ld, (int32_t)K, (int32_t)B0.n, (int32_t)colsrc.size()};
-        for (int64_t j = 0; j < B0.n; ++j) colsrc.push_back((int32_t)(B0.c0 + j));
-        int64_t local = 0;
-        for (int b : members) {
-            const SrcBlock& B = blocks[b];
-            tbase[b] = tcount + local;
-            voff[b] = off + local;
-            vld[b] = ld;
-            // V_b[j, l] -> panel row local+l, column j
-            pack.insert(pack.end(), {off + local, (int64_t)(uintptr_t)B.V, (int64_t)B.k, B.n, B.v_ld, 1, ld});
-            local += B.k;
+        size_t q0 = 0;
+        while (q0 < members.size()) {           // sub-panels of <= 128 rows, whole blocks each
+            size_t q1 = q0;
+            int64_t K = 0;
+            while (q1 < members.size() && K + blocks[members[q1]].k <= 128) K += blocks[members[q1++]].k;
+            const SrcBlock& B0 = blocks[members[q0]];
+            const int64_t ld = align2(K);
+            Panel pn{off, n + tcount, (int32_t)ld, (int32_t)K, (int32_t)B0.n, (int32_t)colsrc.size(), B0.c0};
+            for (int64_t j = 0; j < B0.n; ++j) colsrc.push_back((int32_t)(B0.c0 + j));
+            int64_t local = 0;
+            for (size_t q = q0; q < q1; ++q) {
+                const int b = members[q];
+                const SrcBlock& B = blocks[b];
+                tbase[b] = tcount + local;
+                voff[b] = off + local;
+                vld[b] = ld;
+                // V_b[j, l] -> panel row local+l, column j
+                pack.insert(pack.end(), {off + local, (int64_t)(uintptr_t)B.V, (int64_t)B.k, B.n, B.v_ld, 1, ld});
+                local += B.k;
+            }
+            op.p1.panels.push_back(pn);
+            op.p1.doubles += K * B0.n;
+            off += ld * B0.n;
+            tcount += K;
+            q0 = q1;
         }
-        op.p1.panels.push_back(pn);
-        op.p1.doubles += K * B0.n;
-        off += ld * B0.n;
-        tcount += K;
     }
     op.n_t = tcount;
 
@@ -126,40 +153,43 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     for (int l = 0; l < nleaves; ++l) {
         if (items[l].empty()) continue;
         const Node& L = g.nodes[g.leaves[l]];
-        const int64_t lr0 = L.begin, lm = L.size(), ld = align2(lm);
-        Panel pn{off, lr0, (int32_t)ld, (int32_t)lm, 0, (int32_t)colsrc.size()};
-        for (int b : items[l]) {
-            const SrcBlock& B = blocks[b];
-            const int64_t ro = lr0 - B.r0;
-            if (B.kind != KIND_LR) {
-                if (B.fill_entries)
-                    fill.insert(fill.end(), {off, lr0, lm, B.c0, B.n, ld});
-                else
-                    pack.insert(pack.end(), {off, (int64_t)(uintptr_t)(B.dense + ro * B.d_rs), lm, B.n, B.d_rs, B.d_cs, ld});
-                for (int64_t j = 0; j < B.n; ++j) colsrc.push_back((int32_t)(B.c0 + j));
-                op.items.push_back(HOp::ItemRec{off, ld, -1, 0, lr0, lm, B.c0, B.n, 0});
-                off += ld * B.n;
-                pn.ncols += (int32_t)B.n;
-                op.p2.doubles += lm * B.n;
-            } else {
-                pack.insert(pack.end(), {off, (int64_t)(uintptr_t)(B.U + ro), lm, (int64_t)B.k, 1, B.u_ld, ld});
-                for (int q = 0; q < B.k; ++q) colsrc.push_back((int32_t)(n + tbase[b] + q));
-                op.items.push_back(HOp::ItemRec{off, ld, voff[b], vld[b], lr0, lm, B.c0, B.n, B.k});
-                off += ld * B.k;
-                pn.ncols += B.k;
-                op.p2.doubles += lm * B.k;
+        for (int64_t rc = L.begin; rc < L.end; rc += 128) {   // row chunks of <= 128
+            const int64_t lr0 = rc, lm = std::min<int64_t>(128, L.end - rc), ld = align2(lm);
+            Panel pn{off, lr0, (int32_t)ld, (int32_t)lm, 0, (int32_t)colsrc.size(), lr0};
+            for (int b : items[l]) {
+                const SrcBlock& B = blocks[b];
+                const int64_t ro = lr0 - B.r0;
+                if (B.kind != KIND_LR) {
+                    if (B.fill_entries)
+                        fill.insert(fill.end(), {off, lr0, lm, B.c0, B.n, ld});
+                    else
+                        pack.insert(pack.end(), {off, (int64_t)(uintptr_t)(B.dense + ro * B.d_rs), lm, B.n, B.d_rs, B.d_cs, ld});
+                    for (int64_t j = 0; j < B.n; ++j) colsrc.push_back((int32_t)(B.c0 + j));
+                    op.items.push_back(HOp::ItemRec{off, ld, -1, 0, lr0, lm, B.c0, B.n, 0});
+                    off += ld * B.n;
+                    pn.ncols += (int32_t)B.n;
+                    op.p2.doubles += lm * B.n;
+                } else {
+                    pack.insert(pack.end(), {off, (int64_t)(uintptr_t)(B.U + ro), lm, (int64_t)B.k, 1, B.u_ld, ld});
+                    for (int q = 0; q < B.k; ++q) colsrc.push_back((int32_t)(n + tbase[b] + q));
+                    op.items.push_back(HOp::ItemRec{off, ld, voff[b], vld[b], lr0, lm, B.c0, B.n, B.k});
+                    off += ld * B.k;
+                    pn.ncols += B.k;
+                    op.p2.doubles += lm * B.k;
+                }
             }
+            op.p2.panels.push_back(pn);
         }
-        op.p2.panels.push_back(pn);
     }
     if ((int64_t)n + tcount >= INT32_MAX || (int64_t)colsrc.size() >= INT32_MAX)
         throw Error(HM_ERR_UNSUPPORTED, "index space exceeds int32");
 
     op.arena.alloc(ctx, (size_t)std::max<int64_t>(off, 2), "operator arena");
     HM_CUDA(cudaMemsetAsync(op.arena.p, 0, sizeof(double) * (size_t)std::max<int64_t>(off, 2), s));
-    op.colsrc.upload(ctx, colsrc, "colsrc", s);
-    make_units(ctx, op.p1, s);
-    make_units(ctx, op.p2, s);
+    std::vector<int32_t> ucs;
+    make_units(ctx, op.p1, colsrc, ucs, s);
+    make_units(ctx, op.p2, colsrc, ucs, s);
+    op.colsrc.upload(ctx, ucs, "colsrc", s);
     DBuf<int64_t> d_pack, d_fill;
     d_pack.upload(ctx, pack, "pack tasks", s);
     d_fill.upload(ctx, fill, "fill tasks", s);

@@ -98,11 +98,13 @@ def test_apply_equals_oracle_hmatrix_and_dense(hm, case):
     assert rel(y, Fd @ x) <= 10 * cfg.eps_aca
 
 
-def test_solve_and_flux_match_dense_oracle(hm, case):
+@pytest.mark.parametrize("cut", [-1, 0, 2])
+def test_solve_and_flux_match_dense_oracle(hm, case, cut):
+    """cut -1: pure level form (leaf inverses); 0: U^-1 (L^-1 b) as two H-applies; 2: mixed."""
     import torch
     cfg, F, f = case["cfg"], case["F"], case["f"]
     ctx = F.ctx
-    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=cut)
     Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
     b = cfg.rhs()[:, 0]
     z = torch.empty(f.n, dtype=torch.float64, device="cuda")
