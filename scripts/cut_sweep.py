@@ -23,7 +23,8 @@ def main(cfg_id=2):
     q = torch.empty_like(T)
     rows = synth.sample_rows(synth.stream_seed(cfg.seed, 999), f.n, 300)
     x = cfg.rhs()
-    for Lc in list(range(0, D + 1)):
+    cuts = [int(c) for c in os.environ.get('CUTS', '').split(',') if c] or list(range(0, D + 1))
+    for Lc in cuts:
         LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=Lc)
         r = hm.hm_storage_report(F, LU)
         ms, info = hm.hm_profile_flux(ctx, F, LU, T, q, 20)
