@@ -379,7 +379,7 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         {   // F_H 1 with the engine (setup program, internal order)
             Program rs;
             rs.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN);
-            rs.add_stream(F.op.p2, F.op, F.xt.p, F.y.p, OUT_ASSIGN);
+            rs.add_stream(F.op.p2, F.op, F.xt.p, F.y.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, -1);
             rs.finalize(c, s);
             k::fill_value(F.xt.p, n, 1.0, s);
             rs.launch(ProgArgs{}, s);
@@ -404,10 +404,11 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             F.s_ext[g.perm[i]] = hs[i];
             F.c_ext[g.perm[i]] = hc[i];
         }
-        // hot-path program: permute-in -> phase 1 -> phase 2 with permute-out fused
-        F.prog_apply.add_elementwise(UNIT_PERMUTE, n, F.xt.p);
-        F.prog_apply.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN);
-        F.prog_apply.add_stream(F.op.p2, F.op, F.xt.p, nullptr, OUT_PERM);
+        // hot-path program: phase 1 -> phase 2, permute-in fused into the gathers, permute-out into
+        // the emit
+        F.prog_apply.n_x = n;
+        F.prog_apply.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PERM);
+        F.prog_apply.add_stream(F.op.p2, F.op, F.xt.p, nullptr, OUT_PERM, DEP_BARRIER, nullptr, IN_PERM, -1);
         F.prog_apply.finalize(c, s);
         HM_CUDA(cudaStreamSynchronize(s));
         F.setup_seconds[2] = now_seconds() - t0;
@@ -498,6 +499,7 @@ void launch_flux(HLU& L, const double* Td, double* qd, int ld, int col, cudaStre
     a.ld = ld;
     a.col = col;
     a.eps_int = L.eps_int.p;
+    a.eps_ext = L.eps_ext.p;
     a.area_int = g.d_geo.p + 6 * g.n;
     a.g_int = L.g_int.p;
     a.sigma = 5.670374419e-8;  // DESIGN.md reading R2
@@ -598,6 +600,8 @@ hm_status hm_trace_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, const
         a.user_out = q;
         a.ld = 1;
         a.eps_int = L.eps_int.p;
+        a.eps_ext = L.eps_ext.p;
+    a.eps_ext = L.eps_ext.p;
         a.area_int = g.d_geo.p + 6 * g.n;
         a.g_int = L.g_int.p;
         a.sigma = 5.670374419e-8;

@@ -10,19 +10,23 @@
 // sweep boundaries (forward -> backward -> F apply) are barriers.
 #include "engine.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace hm {
 
 int add_stream_impl(Program& P, const StreamPass& sp, const HOp& op, const double* in, double* out, int mode, int kind,
-                    const std::vector<int32_t>* panel_node) {
+                    const std::vector<int32_t>* panel_node, int in_mode, int xdep) {
     if (sp.h_units.empty()) return -1;
     Pass p{};
     p.type = UNIT_STREAM;
     p.dep = (int32_t)P.h_passes.size() - 1;
     p.mode = mode;
+    p.in_mode = in_mode;
     p.first_unit = (int64_t)P.h_units.size();
     p.n_units = (int64_t)sp.h_units.size();
     p.arena = op.arena.p;
-    p.colsrc = op.colsrc.p;
+    p.colsrc = in_mode == IN_PLAIN ? op.colsrc.p : op.colsrc_ext.p;
     p.in = in;
     p.out = out;
     p.part = sp.part.p;
@@ -43,17 +47,19 @@ int add_stream_impl(Program& P, const StreamPass& sp, const HOp& op, const doubl
             P.h_tasks.push_back(t);
             P.task_kind.push_back(kind);
             P.task_node.push_back(panel_node ? (*panel_node)[sp.unit_panel[q]] : -1);
+            P.task_xonly.push_back(sp.unit_xonly[q]);
             ++p.n_tasks;
         }
         P.h_units.push_back(u);
     }
     P.h_passes.push_back(p);
+    P.pass_xdep.push_back(xdep);
     return idx;
 }
 
 void Program::add_stream(const StreamPass& sp, const HOp& op, const double* in, double* out, int mode, int kind,
-                         const std::vector<int32_t>* panel_node) {
-    add_stream_impl(*this, sp, op, in, out, mode, kind, panel_node);
+                         const std::vector<int32_t>* panel_node, int in_mode, int xdep) {
+    add_stream_impl(*this, sp, op, in, out, mode, kind, panel_node, in_mode, xdep);
 }
 
 void Program::add_elementwise(int type, int64_t n, double* out) {
@@ -64,10 +70,10 @@ void Program::add_elementwise(int type, int64_t n, double* out) {
     p.first_unit = (int64_t)h_units.size();
     p.out = out;
     const int32_t idx = (int32_t)h_passes.size();
-    for (int64_t r = 0; r < n; r += 160) {   // one row per consumer thread
+    for (int64_t r = 0; r < n; r += 1024) {   // four rows per consumer thread
         Unit u{};
         u.out0 = r;
-        u.nrows = (int32_t)std::min<int64_t>(160, n - r);
+        u.nrows = (int32_t)std::min<int64_t>(1024, n - r);
         u.grp = -1;
         u.nseg = 1;
         u.pass = idx;
@@ -83,11 +89,13 @@ void Program::add_elementwise(int type, int64_t n, double* out) {
         h_tasks.push_back(t);
         task_kind.push_back(DEP_BARRIER);
         task_node.push_back(-1);
+        task_xonly.push_back(0);
         h_units.push_back(u);
     }
     p.n_units = (int64_t)h_units.size() - p.first_unit;
     p.n_tasks = p.n_units;
     h_passes.push_back(p);
+    pass_xdep.push_back(-2);
 }
 
 void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
@@ -95,6 +103,11 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
         if (u.type == UNIT_STREAM && (u.ncols > kUnitMaxCols || u.ld > 128 || (int64_t)u.ncols * u.ld > kUnitPayloadDoubles))
             throw Error(HM_ERR_UNSUPPORTED, "work unit exceeds the engine stage size");
     const int64_t P = (int64_t)h_passes.size();
+    if (P > engine_max_passes()) throw Error(HM_ERR_UNSUPPORTED, "program has more passes than the engine's pass table");
+    {
+        const char* e = getenv("HM_PREFETCH");
+        prefetch = e && e[0] == '1';   // default off: measured slower on C2 (extra DRAM reads)
+    }
     const int64_t nn = g ? (int64_t)g->nodes.size() : 0;
     n_counters = P + 4 * nn;
     auto c_p1 = [&](int sw, int node) { return (int32_t)(P + sw * 2 * nn + node); };
@@ -125,8 +138,10 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
                 ++nw;
             }
         };
+        const bool xonly = task_xonly[i] != 0;
         if (kind == DEP_BARRIER) {
-            wait(t.pass - 1);
+            const int xd = pass_xdep[t.pass];
+            wait(xonly && xd != -2 ? xd : t.pass - 1);
             continue;
         }
         if (!g || node < 0) throw Error(HM_ERR_INVALID_ARG, "tree-dependency pass without tree nodes");
@@ -135,7 +150,7 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
         while (par >= 0 && cnt[c_all(sw, par)] == 0) par = g->nodes[par].parent;
         if (par >= 0) wait(c_all(sw, par));
         else wait(sweep_dep[sw]);
-        if (kind == DEP_FWD_P2 || kind == DEP_BWD_P2) wait(c_p1(sw, node));
+        if ((kind == DEP_FWD_P2 || kind == DEP_BWD_P2) && !xonly) wait(c_p1(sw, node));
     }
     passes.upload(ctx, h_passes, "engine passes", s);
     units.upload(ctx, h_units, "engine units", s);
@@ -154,6 +169,9 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
 void Program::launch(ProgArgs a, cudaStream_t s) {
     if (h_tasks.empty()) return;
     a.passes = passes.p;
+    a.n_passes = (int32_t)h_passes.size();
+    a.n_x = n_x;
+    a.prefetch = prefetch ? 1 : 0;
     a.units = units.p;
     a.tasks = tasks.p;
     a.n_tasks = (int64_t)h_tasks.size();
@@ -168,7 +186,25 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
     a.done = done.p;
     a.epoch = ++epoch;
     if (a.ld == 0) a.ld = 1;
+    static const bool want_stats = [] { const char* e = getenv("HM_ENGINE_STATS"); return e && e[0] == '1'; }();
+    if (want_stats) {
+        if (!stats.p) stats.alloc(nullptr, 16, "engine stats");
+        HM_CUDA(cudaMemsetAsync(stats.p, 0, 16 * sizeof(unsigned long long), s));
+        a.stats = stats.p;
+    }
     engine_launch(a, grid, s);
+    if (want_stats) {
+        unsigned long long h[16];
+        HM_CUDA(cudaMemcpyAsync(h, stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        const double G = (double)grid;
+        fprintf(stderr,
+                "[engine stats] passes %zu units %zu grid %d | per CTA (kcycles): producer wait-empty %.1f meta %.1f "
+                "chunks %.0f | gatherer(sum of warps) wait-full %.1f dep %.1f gather %.1f | consumer wait %.1f "
+                "compute %.1f task-end %.1f | retire wait %.1f work %.1f | TMA issue->land %.0f cycles (n %.0f, landed before gather done %.0f)\n",
+                h_passes.size(), h_units.size(), grid, h[0] / G / 1e3, h[1] / G / 1e3, h[2] / G, h[3] / G / 1e3,
+                h[4] / G / 1e3, h[5] / G / 1e3, h[6] / G / 1e3, h[7] / G / 1e3, h[8] / G / 1e3, h[9] / G / 1e3, h[10] / G / 1e3, h[12] ? (double)h[11] / h[12] : 0.0, (double)h[12], (double)h[13]);
+    }
 }
 
 }  // namespace hm

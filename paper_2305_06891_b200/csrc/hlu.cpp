@@ -251,6 +251,7 @@ void factor_hlu(HLU& L, const double* emissivity) {
         throw Error(HM_ERR_UNSUPPORTED, "dense-stage H-LU needs ~" + std::to_string((int64_t)(need / 1e9)) +
                                             " GB of device memory (" + std::to_string((int64_t)(freeb / 1e9)) + " GB free)");
     L.eps_int.upload(c, eps_int, "eps", s);
+    L.eps_ext.upload(c, std::vector<double>(emissivity, emissivity + n), "eps (external)", s);
     DBuf<double> dlam, dM, dMinv, dT;
     DBuf<int32_t> derr;
     dlam.upload(c, lam, "lambda", s);
@@ -402,18 +403,26 @@ void factor_hlu(HLU& L, const double* emissivity) {
     };
     const auto mL1 = node_map(L.leafL.p1, Lc), mL2 = node_map(L.leafL.p2, Lc);
     const auto mU1 = node_map(L.leafU.p1, Lc), mU2 = node_map(L.leafU.p2, Lc);
-    // forward sweep, block-diagonal L^-1 at the cut, backward sweep (U^-1 at the cut left to the caller)
-    auto solve_passes = [&](Program& P) {
-        P.sweep_dep[0] = (int32_t)P.h_passes.size() - 1;  // the prologue / permute pass
+    // forward sweep, block-diagonal L^-1 at the cut, backward sweep (U^-1 at the cut left to the caller).
+    // With Lc == 0 nothing updates b in place, so the prologue (permute-in, or eta = T^4 and
+    // w = eps eta for the flux) is fused into the gathers of the first operator's passes (in_mode);
+    // otherwise an element-wise pass materialises b first.
+    auto solve_passes = [&](Program& P, int in_mode) {
+        P.n_x = n;
+        if (Lc > 0) {
+            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA.p);
+            in_mode = IN_PLAIN;
+        }
+        P.sweep_dep[0] = (int32_t)P.h_passes.size() - 1;  // the prologue / permute pass (-1: fused)
         for (int lv = 0; lv < Lc; ++lv) {
             HOp& op = L.fwd[lv];
             const auto m1 = node_map(op.p1, lv), m2 = node_map(op.p2, lv);
             P.add_stream(op.p1, op, L.xtA.p, L.xtA.p, OUT_ASSIGN, DEP_FWD_P1, &m1);
             P.add_stream(op.p2, op, L.xtA.p, L.xtA.p, OUT_SUB, DEP_FWD_P2, &m2);
         }
-        P.add_stream(L.leafL.p1, L.leafL, L.xtA.p, L.xtA.p, OUT_ASSIGN, DEP_FWD_P1, &mL1);
+        P.add_stream(L.leafL.p1, L.leafL, L.xtA.p, L.xtA.p, OUT_ASSIGN, DEP_FWD_P1, &mL1, in_mode);
         P.sweep_dep[1] = (int32_t)P.h_passes.size();  // the cut L^-1 phase-2 pass
-        P.add_stream(L.leafL.p2, L.leafL, L.xtA.p, L.xtB.p, OUT_ASSIGN, DEP_FWD_P2, &mL2);
+        P.add_stream(L.leafL.p2, L.leafL, L.xtA.p, L.xtB.p, OUT_ASSIGN, DEP_FWD_P2, &mL2, in_mode);
         for (int lv = 0; lv < Lc; ++lv) {
             HOp& op = L.bwd[lv];
             const auto m1 = node_map(op.p1, lv), m2 = node_map(op.p2, lv);
@@ -422,15 +431,15 @@ void factor_hlu(HLU& L, const double* emissivity) {
         }
         P.add_stream(L.leafU.p1, L.leafU, L.xtB.p, L.xtB.p, OUT_ASSIGN, DEP_BWD_P1, &mU1);
     };
-    L.prog_solve.add_elementwise(UNIT_PERMUTE, n, L.xtA.p);
-    solve_passes(L.prog_solve);
+    solve_passes(L.prog_solve, IN_PERM);
     L.prog_solve.add_stream(L.leafU.p2, L.leafU, L.xtB.p, nullptr, OUT_PERM, DEP_BWD_P2, &mU2);
     L.prog_solve.finalize(c, s, &g);
-    L.prog_flux.add_elementwise(UNIT_PROLOGUE, n, L.xtA.p);
-    solve_passes(L.prog_flux);
+    solve_passes(L.prog_flux, IN_FLUX);
     L.prog_flux.add_stream(L.leafU.p2, L.leafU, L.xtB.p, Fm.xt.p, OUT_ASSIGN, DEP_BWD_P2, &mU2);
     L.prog_flux.add_stream(F.op.p1, F.op, Fm.xt.p, Fm.xt.p, OUT_ASSIGN);
-    L.prog_flux.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX);
+    // x-only (near-field) tasks of phase 2 wait for z, not for phase 1
+    L.prog_flux.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN,
+                           (int)L.prog_flux.h_passes.size() - 2);
     L.prog_flux.finalize(c, s, &g);
 
     // ---- flux constant g = F C^-1 eps, with a setup program
@@ -438,11 +447,11 @@ void factor_hlu(HLU& L, const double* emissivity) {
     L.g_int.alloc(c, (size_t)n, "g");
     {
         Program pg;
-        pg.add_elementwise(UNIT_PERMUTE, n, L.xtA.p);
-        solve_passes(pg);
+        solve_passes(pg, IN_PERM);
         pg.add_stream(L.leafU.p2, L.leafU, L.xtB.p, Fm.xt.p, OUT_ASSIGN, DEP_BWD_P2, &mU2);
         pg.add_stream(F.op.p1, F.op, Fm.xt.p, Fm.xt.p, OUT_ASSIGN);
-        pg.add_stream(F.op.p2, F.op, Fm.xt.p, L.g_int.p, OUT_ASSIGN);
+        pg.add_stream(F.op.p2, F.op, Fm.xt.p, L.g_int.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
+                      (int)pg.h_passes.size() - 2);
         pg.finalize(c, s, &g);
         DBuf<double> eps_ext;
         eps_ext.upload(c, std::vector<double>(emissivity, emissivity + n), "eps (external)", s);

@@ -132,6 +132,7 @@ void build_trees(Geom& g, const double* xyz, const double* nrm, const double* ar
 // of TMA transfer.  A task = consecutive chunks of one panel piece, processed by one CTA that
 // accumulates in registers and emits once.  Pieces of the same panel (only panels > 512 KB are
 // split) combine deterministically: the last-finishing piece adds the partials in piece order.
+constexpr int kMaxRuns = 16;
 struct Unit {
     int64_t a_off;     // arena offset of the chunk payload
     int64_t out0;      // output index of row 0 of the panel
@@ -148,6 +149,11 @@ struct Unit {
     int32_t chunk;     // chunk index within the piece
     int32_t nchunks;   // chunks in the piece
     int64_t first_chunk;  // index (in the unit list) of the piece's first chunk
+    // column sources as runs of consecutive input indices (nruns = 0: too many runs, use colsrc):
+    // the gather can start as soon as the descriptor is known, without a round trip for colsrc
+    int32_t nruns;
+    int32_t run_src[kMaxRuns];
+    uint16_t run_len[kMaxRuns];
 };
 enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2 };
 constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage
@@ -172,11 +178,13 @@ struct Panel {         // host description of a panel
     int64_t out0;      // output index of row 0
     int32_t ld, nrows, ncols, cs_off;
     int64_t key;       // phase 1: first column of the cluster tau; phase 2: first row of the leaf
+    int32_t ndense;    // leading columns that read only the x region (phase 2: dense blocks first)
 };
 
 struct StreamPass {    // one pass worth of chunks (host copy; programs upload them)
     std::vector<Unit> h_units;
     std::vector<int32_t> unit_panel;   // panel index of each chunk
+    std::vector<uint8_t> unit_xonly;   // 1: the chunk's piece reads only the x region (no t)
     int64_t n_units = 0;
     DBuf<double> part;
     DBuf<int32_t> counters;
@@ -204,6 +212,7 @@ struct HOp {
     DBuf<double> arena;
     StreamPass p1, p2;
     DBuf<int32_t> colsrc;          // per-unit, 16-byte aligned column-source segments
+    DBuf<int32_t> colsrc_ext;      // same, x-region entries as -(external index + 1) (fused prologue)
     int64_t n_t = 0;              // total rank (size of t)
     struct ItemRec {              // one phase-2 item (a leaf-row slice of one block)
         int64_t a_off;            // U slice / dense slice, column-major with stride a_ld
@@ -230,7 +239,7 @@ struct Pass {
     int32_t type;        // UnitType of its units
     int32_t dep;         // pass whose completion this pass waits for (-1: none)
     int32_t mode;        // OutMode
-    int32_t pad;
+    int32_t in_mode;     // InMode: how x-region inputs (index < n_x) are gathered
     int64_t first_unit, n_units;
     int64_t n_tasks;
     const double* arena;
@@ -243,6 +252,8 @@ struct Pass {
 
 struct ProgArgs {
     const Pass* passes;
+    int32_t n_passes;
+    int32_t prefetch;           // 1: the L2 prefetch warp runs ahead of the task queue
     const Unit* units;
     const Task* tasks;
     int64_t n_tasks;
@@ -253,16 +264,22 @@ struct ProgArgs {
     int64_t n_units;
     unsigned long long* done;   // dependency counters (passes, then per-node), monotone over launches
     unsigned long long* trace;  // optional: per pass [first gather, last retire] (%globaltimer ns)
+    unsigned long long* stats;  // optional: per-role SM cycle counters (diagnostics, HM_ENGINE_STATS=1)
     unsigned long long epoch;   // launch number of this program (1-based)
     const int32_t* perm;
     const double* user_in;      // x / b / T (external order, ld x ncol)
+    int64_t n_x;                // size of the x region of XT (IN_PERM / IN_FLUX apply below it)
     double* user_out;           // y / z / q (external order)
     int ld, col;
     const double* eps_int;
+    const double* eps_ext;      // emissivity in external order (IN_FLUX gathers)
     const double* area_int;
     const double* g_int;
     double sigma;
 };
+
+// input modes of a stream pass: the prologue / permute-in fused into the gather
+enum InMode : int { IN_PLAIN = 0, IN_PERM = 1, IN_FLUX = 2 };
 
 // A program = passes in topological order; executes in one cooperative launch.
 struct Program {
@@ -278,19 +295,28 @@ struct Program {
     unsigned long long epoch = 0;
     int grid = 0;
     bool ready = false;
+    bool prefetch = true;
+    int64_t n_x = 0;     // x-region size of the programs' XT buffers (fused-prologue gathers)
     std::vector<int32_t> task_kind, task_node;   // dependency kind / tree node of each task
+    std::vector<uint8_t> task_xonly;             // task reads only the x region of its input
+    std::vector<int32_t> pass_xdep;              // per pass: see add_stream
     int32_t sweep_dep[2] = {-1, -1};             // pass the root of the fwd / bwd sweep waits for
     int64_t n_counters = 0;
     DBuf<unsigned long long> trace;
+    DBuf<unsigned long long> stats;
     // builder: panel_node (optional) maps each panel of `sp` to its tree node (tree kinds)
+    // xdep (DEP_BARRIER passes): the pass whose completion x-only tasks wait for instead of the
+    // previous pass (-2: no distinction, -1: no wait)
     void add_stream(const StreamPass& sp, const HOp& op, const double* in, double* out, int mode,
-                    int kind = DEP_BARRIER, const std::vector<int32_t>* panel_node = nullptr);
+                    int kind = DEP_BARRIER, const std::vector<int32_t>* panel_node = nullptr, int in_mode = IN_PLAIN,
+                    int xdep = -2);
     void add_elementwise(int type, int64_t n, double* out);
     void finalize(Ctx* ctx, cudaStream_t s, const Geom* g = nullptr);
     void launch(ProgArgs a, cudaStream_t s);
 };
 
 size_t engine_smem_bytes();
+int engine_max_passes();
 int engine_grid();
 void engine_launch(const ProgArgs& A, int grid, cudaStream_t s);
 
@@ -300,6 +326,7 @@ struct FluxEpi {  // OUT_FLUX: q_ext[perm[i]] = sigma * eps_i / A_i * (acc - eta
     const double* T_ext;
     const int32_t* perm;
     const double* eps_int;
+    const double* eps_ext;      // emissivity in external order (IN_FLUX gathers)
     const double* area_int;
     const double* g_int;
     double sigma;
@@ -332,7 +359,7 @@ struct HLU {
     DBuf<double> xtA;            // [b | t] forward pass (t sized for the largest level)
     DBuf<double> xtB;            // [y | t] backward pass
     DBuf<double> z;              // internal-order result
-    DBuf<double> eps_int, g_int;
+    DBuf<double> eps_int, eps_ext, g_int;
     DBuf<double> host_stage_in, host_stage_out;
     double setup_seconds[4] = {0, 0, 0, 0};
     int64_t bytes = 0, bytes_leaf = 0, n_blocks = 0, n_lr = 0, rank_sum = 0;

@@ -9,6 +9,7 @@
 // Panels have <= 128 rows and are cut into work units of <= 32 KB contiguous payload.
 #include <algorithm>
 #include <map>
+#include <algorithm>
 
 #include "hm_internal.h"
 
@@ -24,51 +25,109 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
     std::vector<Unit>& units = P.h_units;
     units.clear();
     P.unit_panel.clear();
+    P.unit_xonly.clear();
     int64_t part = 0;
     int32_t grp = 0;
     // piece size adapted to the pass: ~4 tasks per SM (small passes still spread over the chip),
-    // between one chunk and kPieceDoubles
+    // between four chunks and kPieceDoubles, so the tail of a pass (the dependency barrier of the
+    // next one) is short
     int64_t pass_doubles = 0;
     for (const Panel& pn : P.panels) pass_doubles += (int64_t)pn.ncols * pn.ld;
     const int64_t piece = std::max<int64_t>(4 * kUnitPayloadDoubles,
-                                            std::min<int64_t>(kPieceDoubles, pass_doubles / (2 * 148)));
+                                            std::min<int64_t>(kPieceDoubles, pass_doubles / (4 * 148)));
+    struct Piece { std::vector<Unit> u; std::vector<int32_t> cs; int32_t panel; int64_t doubles; uint8_t xonly; };
+    std::vector<Piece> pieces;
     for (size_t pi = 0; pi < P.panels.size(); ++pi) {
         const Panel& pn = P.panels[pi];
         if (pn.ncols == 0) continue;
-        const int64_t total = (int64_t)pn.ncols * pn.ld;
-        const int32_t npieces = (int32_t)std::min<int64_t>(pn.ncols, (total + piece - 1) / piece);
-        const int64_t Cp = (pn.ncols + npieces - 1) / npieces;
+        // two column segments: [0, ndense) reads only x (may run before the t values exist),
+        // [ndense, ncols) reads t; each is cut into pieces, all pieces of the panel combine
+        struct Seg { int64_t c0, c1; int32_t np; };
+        Seg segs[2] = {{0, pn.ndense, 0}, {pn.ndense, pn.ncols, 0}};
+        int32_t npieces = 0;
+        for (Seg& sg : segs) {
+            const int64_t w = sg.c1 - sg.c0;
+            if (w <= 0) continue;
+            sg.np = (int32_t)std::min<int64_t>(w, (w * pn.ld + piece - 1) / piece);
+            npieces += sg.np;
+        }
         const int32_t g = npieces > 1 ? grp++ : -1;
-        for (int32_t pc = 0; pc < npieces; ++pc) {
-            const int64_t p0 = pc * Cp, p1 = std::min<int64_t>(pn.ncols, p0 + Cp);
-            int64_t C = std::min<int64_t>(kUnitMaxCols, kUnitPayloadDoubles / pn.ld);
-            const int32_t nch = (int32_t)((p1 - p0 + C - 1) / C);
-            C = (p1 - p0 + nch - 1) / nch;
-            const int64_t first = (int64_t)units.size();
-            for (int32_t ch = 0; ch < nch; ++ch) {
-                Unit u{};
-                const int64_t c0 = p0 + ch * C;
-                u.ncols = (int32_t)std::min<int64_t>(C, p1 - c0);
-                u.a_off = pn.a_off + c0 * pn.ld;
-                u.out0 = pn.out0;
-                u.part_off = npieces > 1 ? part : 0;
-                u.cs_off = (int64_t)ucs.size();
-                for (int32_t c = 0; c < u.ncols; ++c) ucs.push_back(pcs[pn.cs_off + c0 + c]);
-                while (ucs.size() % 4) ucs.push_back(0);
-                u.ld = pn.ld;
-                u.nrows = pn.nrows;
-                u.grp = g;
-                u.nseg = npieces;
-                u.seg = pc;
-                u.pass = 0;
-                u.type = UNIT_STREAM;
-                u.chunk = ch;
-                u.nchunks = nch;
-                u.first_chunk = first;
-                units.push_back(u);
-                P.unit_panel.push_back((int32_t)pi);
+        int32_t pc = 0;
+        for (int sgi = 0; sgi < 2; ++sgi) {
+            const Seg& sg = segs[sgi];
+            if (sg.np == 0) continue;
+            const int64_t Cp = (sg.c1 - sg.c0 + sg.np - 1) / sg.np;
+            for (int32_t q = 0; q < sg.np; ++q, ++pc) {
+                const int64_t p0 = sg.c0 + q * Cp, p1 = std::min<int64_t>(sg.c1, p0 + Cp);
+                if (p1 <= p0) { --pc; continue; }
+                int64_t C = std::min<int64_t>(kUnitMaxCols, kUnitPayloadDoubles / pn.ld);
+                const int32_t nch = (int32_t)((p1 - p0 + C - 1) / C);
+                C = (p1 - p0 + nch - 1) / nch;
+                Piece PC;
+                PC.panel = (int32_t)pi;
+                PC.doubles = (p1 - p0) * pn.ld;
+                PC.xonly = sgi == 0 ? 1 : 0;
+                for (int32_t ch = 0; ch < nch; ++ch) {
+                    Unit u{};
+                    const int64_t c0 = p0 + ch * C;
+                    u.ncols = (int32_t)std::min<int64_t>(C, p1 - c0);
+                    u.a_off = pn.a_off + c0 * pn.ld;
+                    u.out0 = pn.out0;
+                    u.part_off = part + (npieces > 1 ? (int64_t)pc * pn.ld : 0);
+                    u.cs_off = (int64_t)PC.cs.size();   // relative; rebased below
+                    for (int32_t c = 0; c < u.ncols; ++c) PC.cs.push_back(pcs[pn.cs_off + c0 + c]);
+                    {   // run-length form of the column sources
+                        const int32_t* src = &pcs[pn.cs_off + c0];
+                        int nr = 0;
+                        bool ok = true;
+                        for (int32_t c = 0; c < u.ncols && ok; ++c) {
+                            if (c > 0 && src[c] == src[c - 1] + 1 && u.run_len[nr - 1] < 65535) {
+                                ++u.run_len[nr - 1];
+                            } else if (nr < kMaxRuns) {
+                                u.run_src[nr] = src[c];
+                                u.run_len[nr] = 1;
+                                ++nr;
+                            } else {
+                                ok = false;
+                            }
+                        }
+                        u.nruns = ok ? nr : 0;
+                    }
+                    while (PC.cs.size() % 4) PC.cs.push_back(0);
+                    u.ld = pn.ld;
+                    u.nrows = pn.nrows;
+                    u.grp = g;
+                    u.seg = pc;
+                    u.pass = 0;
+                    u.type = UNIT_STREAM;
+                    u.chunk = ch;
+                    u.nchunks = nch;
+                    PC.u.push_back(u);
+                }
+                pieces.push_back(std::move(PC));
             }
-            if (npieces > 1) part += pn.ld;
+        }
+        for (size_t q = pieces.size() - pc; q < pieces.size(); ++q)
+            for (Unit& u : pieces[q].u) u.nseg = pc;
+        if (pc > 1) part += (int64_t)pc * pn.ld;
+        else for (size_t q = pieces.size() - pc; q < pieces.size(); ++q) for (Unit& u : pieces[q].u) { u.grp = -1; u.part_off = 0; }
+    }
+    // x-only pieces first, then largest first (tasks are taken in order: a pass starts with work that
+    // needs no t values and ends on small tasks)
+    std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& a, const Piece& b) {
+        if (a.xonly != b.xonly) return a.xonly > b.xonly;
+        return a.doubles > b.doubles;
+    });
+    for (Piece& PC : pieces) {
+        const int64_t first = (int64_t)units.size();
+        const int64_t cs0 = (int64_t)ucs.size();
+        ucs.insert(ucs.end(), PC.cs.begin(), PC.cs.end());
+        for (Unit& u : PC.u) {
+            u.cs_off += cs0;
+            u.first_chunk = first;
+            units.push_back(u);
+            P.unit_panel.push_back(PC.panel);
+            P.unit_xonly.push_back(PC.xonly);
         }
     }
     P.n_units = (int64_t)units.size();
@@ -120,7 +179,8 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
             while (q1 < members.size() && K + blocks[members[q1]].k <= 128) K += blocks[members[q1++]].k;
             const SrcBlock& B0 = blocks[members[q0]];
             const int64_t ld = align2(K);
-            Panel pn{off, n + tcount, (int32_t)ld, (int32_t)K, (int32_t)B0.n, (int32_t)colsrc.size(), B0.c0};
+            Panel pn{off, n + tcount, (int32_t)ld, (int32_t)K, (int32_t)B0.n, (int32_t)colsrc.size(), B0.c0,
+                     (int32_t)B0.n};
             for (int64_t j = 0; j < B0.n; ++j) colsrc.push_back((int32_t)(B0.c0 + j));
             int64_t local = 0;
             for (size_t q = q0; q < q1; ++q) {
@@ -155,8 +215,14 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
         const Node& L = g.nodes[g.leaves[l]];
         for (int64_t rc = L.begin; rc < L.end; rc += 128) {   // row chunks of <= 128
             const int64_t lr0 = rc, lm = std::min<int64_t>(128, L.end - rc), ld = align2(lm);
-            Panel pn{off, lr0, (int32_t)ld, (int32_t)lm, 0, (int32_t)colsrc.size(), lr0};
-            for (int b : items[l]) {
+            Panel pn{off, lr0, (int32_t)ld, (int32_t)lm, 0, (int32_t)colsrc.size(), lr0, 0};
+            // dense blocks first (they read only x), then the U factors (they read t)
+            std::vector<int> order;
+            for (int b : items[l]) if (blocks[b].kind != KIND_LR) order.push_back(b);
+            pn.ndense = 0;
+            for (int b : order) pn.ndense += (int32_t)blocks[b].n;
+            for (int b : items[l]) if (blocks[b].kind == KIND_LR) order.push_back(b);
+            for (int b : order) {
                 const SrcBlock& B = blocks[b];
                 const int64_t ro = lr0 - B.r0;
                 if (B.kind != KIND_LR) {
@@ -190,6 +256,11 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     make_units(ctx, op.p1, colsrc, ucs, s);
     make_units(ctx, op.p2, colsrc, ucs, s);
     op.colsrc.upload(ctx, ucs, "colsrc", s);
+    // the same column sources for passes that gather straight from the caller's external-order
+    // vector (fused prologue): x-region index j becomes -(perm[j] + 1)
+    for (int32_t& j : ucs)
+        if (j < n) j = -(g.perm[j] + 1);
+    op.colsrc_ext.upload(ctx, ucs, "colsrc (external)", s);
     DBuf<int64_t> d_pack, d_fill;
     d_pack.upload(ctx, pack, "pack tasks", s);
     d_fill.upload(ctx, fill, "fill tasks", s);

@@ -28,15 +28,20 @@
 namespace hm {
 namespace {
 
-constexpr int kThreads = 288;      // warp 0 producer, warps 1-2 gatherers, warps 3..7 consumers, warp 8 L2 prefetcher
-constexpr int kPrefetchWarp = 8;
-constexpr int64_t kPrefetchWindow = 1536;   // chunks (~48 MB) ahead of the task-queue frontier
-constexpr int kGatherers = 2;
-constexpr int kConsumers = 160;
-constexpr int kConsumerWarps = kConsumers / 32;
+// warp roles
+constexpr int kGatherers = 5;                       // warps 1..5 (gatherer w owns stage w-1)
+constexpr int kConsumerWarps = 8;                   // warps 6..13
+constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kConsumer0 = 32 * (1 + kGatherers);
-constexpr int kStages = 4;         // multiple of kGatherers
+constexpr int kRetireWarp = 1 + kGatherers + kConsumerWarps;   // warps 14..15
+constexpr int kRetireWarps = 2;
+constexpr int kPrefetchWarp = kRetireWarp + kRetireWarps;     // warp 16
+constexpr int kThreads = 32 * (kPrefetchWarp + 1);            // 544
+constexpr int64_t kPrefetchWindow = 1536;   // chunks (~48 MB) ahead of the task-queue frontier
+constexpr int kStages = 5;         // multiple of kGatherers
+constexpr int kRetireSlots = 4;    // task-end handoff buffers (consumers -> retire warps)
 constexpr int kMaxCols = 512;      // per chunk; payload <= 32 KB
+constexpr int kMaxPasses = 96;     // pass table held in shared memory
 static_assert(kStages % kGatherers == 0, "stage ownership");
 
 struct __align__(16) Stage {
@@ -45,13 +50,35 @@ struct __align__(16) Stage {
     int32_t cs[kMaxCols];
 };
 
+// Per-stage header written by the producer: everything the gatherers and consumers need about the
+// chunk in flight, so that no role issues a dependent global-memory load per chunk.
+struct StageHdr {
+    Unit u;            // the chunk's descriptor (u.type < 0: end-of-work marker)
+    int64_t task;      // task index
+    int32_t wait_id[2], wait_cnt[2], inc_id[2];
+    int32_t pad[2];
+    long long t_issue;  // stats only: clock64 at TMA issue
+};
+
+// Task-end handoff: the consumers deposit their per-thread partial sums and the task's descriptor,
+// the retire warp reduces, emits, publishes (fence + counters) off the consumers' critical path.
+struct TaskEnd {       // what the retire warps need of a task's last chunk
+    int32_t type, pass, nrows, ld, grp, nseg, seg, pad;
+    int64_t out0, part_off;
+};
+struct RetireSlot {
+    double2 red[kConsumers];
+    TaskEnd u;         // u.type < 0: end of work
+    int32_t inc_id[2];
+};
+
 struct EngineSmem {
     Stage st[kStages];
-    int64_t hdr[kStages];      // chunk index in flight in each stage (-1: end of work)
-    int64_t hdr_task[kStages]; // its task
-    double2 red[kConsumers];
-    unsigned long long full[kStages], gathered[kStages], empty[kStages];
-    int last;
+    StageHdr hdr[kStages];
+    Pass passes[kMaxPasses];   // the program's pass table, copied once per launch
+    RetireSlot rs[kRetireSlots];
+    unsigned long long csfull[kStages], full[kStages], gathered[kStages], empty[kStages];
+    unsigned long long rfull[kRetireSlots], rempty[kRetireSlots];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -76,6 +103,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ bool mbar_test(unsigned long long* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, unsigned long long* b) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
@@ -85,7 +119,17 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
+// split-K arrival: release this thread's (and, cumulatively, its warp's) partial-sum writes,
+// acquire the other pieces' when last
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+// task publication: outputs visible GPU-wide before the counter moves (pairs with ld.acquire.gpu)
+__device__ __forceinline__ void red_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -130,50 +174,99 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
     const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
+            mbar_init(&S.csfull[s], 1);
             mbar_init(&S.full[s], 1);
             mbar_init(&S.gathered[s], 1);
             mbar_init(&S.empty[s], kConsumerWarps);
         }
+        for (int r = 0; r < kRetireSlots; ++r) {
+            mbar_init(&S.rfull[r], kConsumerWarps);
+            mbar_init(&S.rempty[r], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int i = tid; i < A.n_passes; i += kThreads) S.passes[i] = A.passes[i];
     __syncthreads();
 
     if (warp == 0) {
-        // ------------------------------------------------ producer: grab tasks, TMA their chunks
-        if (lane == 0) {
-            int64_t k = 0;
-            while (true) {
-                const unsigned long long t = atomicAdd(A.queue, 1ull) - A.queue_base;
-                const bool end = t >= (unsigned long long)A.n_tasks;
-                const Task task = end ? Task{} : A.tasks[t];
-                // end of work: one marker per gatherer warp (each owns its own stages)
-                const int nch = end ? kGatherers : task.n_units;
-                for (int c = 0; c < nch; ++c, ++k) {
-                    const int s = (int)(k % kStages);
-                    if (k >= kStages) mbar_wait(&S.empty[s], (uint32_t)(((k / kStages) - 1) & 1));
-                    if (end) {
-                        S.hdr[s] = -1;
-                        mbar_arrive(&S.full[s]);
-                        continue;
-                    }
-                    const int64_t ui = task.first_unit + c;
-                    S.hdr[s] = ui;
-                    S.hdr_task[s] = (int64_t)t;
-                    const Unit& u = A.units[ui];
-                    if (u.type != UNIT_STREAM) {
-                        mbar_arrive(&S.full[s]);
-                        continue;
-                    }
-                    const Pass& P = A.passes[u.pass];
-                    const uint32_t pb = (uint32_t)u.ncols * (uint32_t)u.ld * 8u;
-                    const uint32_t cb = (((uint32_t)u.ncols + 3u) & ~3u) * 4u;
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_expect_tx(&S.full[s], pb + cb);
-                    tma_load_1d(S.st[s].payload, P.arena + u.a_off, pb, &S.full[s]);
-                    tma_load_1d(S.st[s].cs, P.colsrc + u.cs_off, cb, &S.full[s]);
-                }
-                if (end) break;
+        // ------------------------------------------------ producer warp: grab tasks, TMA their chunks.
+        // The next task index is requested while the current task streams, and the unit descriptors
+        // of a task are loaded 32 at a time (one per lane), so the TMA issue loop never waits on a
+        // dependent global load.
+        unsigned long long nxt = 0, st_empty = 0, st_meta = 0, st_chunks = 0;
+        if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - A.queue_base;
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        int64_t k = 0;
+        while (true) {
+            const unsigned long long t = nxt;
+            const bool end = t >= (unsigned long long)A.n_tasks;
+            Task task{};
+            long long c0 = clock64();
+            if (!end) {
+                task = A.tasks[t];
+                if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - A.queue_base;
             }
+            // end of work: one marker per gatherer warp (each owns its own stages)
+            const int nch = end ? kGatherers : task.n_units;
+            for (int base = 0; base < nch; base += 32) {
+                Unit mine{};
+                if (!end && base + lane < nch) mine = A.units[task.first_unit + base + lane];
+                __syncwarp();
+                st_meta += clock64() - c0;
+                const int cnt = min(32, nch - base);
+                for (int c = 0; c < cnt; ++c, ++k) {
+                    const int s = (int)(k % kStages);
+                    c0 = clock64();
+                    if (k >= kStages && lane == 0) mbar_wait(&S.empty[s], (uint32_t)(((k / kStages) - 1) & 1));
+                    __syncwarp();
+                    st_empty += clock64() - c0;
+                    ++st_chunks;
+                    StageHdr& H = S.hdr[s];
+                    if (lane == c) {
+                        if (end) {
+                            H.u.type = -1;
+                        } else {
+                            H.u = mine;
+                            H.task = (int64_t)t;
+                            H.wait_id[0] = task.wait_id[0]; H.wait_id[1] = task.wait_id[1];
+                            H.wait_cnt[0] = task.wait_cnt[0]; H.wait_cnt[1] = task.wait_cnt[1];
+                            H.inc_id[0] = task.inc_id[0]; H.inc_id[1] = task.inc_id[1];
+                            if (mine.type == UNIT_STREAM) {
+                                const Pass& P = S.passes[mine.pass];
+                                const uint32_t pb = (uint32_t)mine.ncols * (uint32_t)mine.ld * 8u;
+                                const uint32_t cb = (((uint32_t)mine.ncols + 3u) & ~3u) * 4u;
+                                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                                // column sources first, on their own barrier: the gather overlaps the
+                                // payload's flight (run-encoded chunks need no column-source copy)
+                                if (mine.nruns > 0 && P.in_mode == IN_PLAIN) {
+                                    mbar_arrive(&S.csfull[s]);
+                                } else {
+                                    mbar_expect_tx(&S.csfull[s], cb);
+                                    tma_load_1d(S.st[s].cs, P.colsrc + mine.cs_off, cb, &S.csfull[s]);
+                                }
+                                if (A.stats) H.t_issue = clock64();
+                                mbar_expect_tx(&S.full[s], pb);
+                                tma_load_1d(S.st[s].payload, P.arena + mine.a_off, pb, &S.full[s]);
+                            } else {
+                                mbar_arrive(&S.csfull[s]);
+                                mbar_arrive(&S.full[s]);
+                            }
+                        }
+                        if (end) {
+                            mbar_arrive(&S.csfull[s]);
+                            mbar_arrive(&S.full[s]);
+                        }
+                    }
+                }
+                nxt = __shfl_sync(0xffffffffu, nxt, 0);
+                c0 = clock64();
+            }
+            if (end) break;
+        }
+        if (A.stats && lane == 0) {
+            atomicAdd(A.stats + 0, st_empty);
+            atomicAdd(A.stats + 1, st_meta);
+            atomicAdd(A.stats + 2, st_chunks);
         }
         return;
     }
@@ -181,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
         // ------------------------------------------------ L2 prefetcher: stream the program's chunks into
         // L2 in program order, at most kPrefetchWindow chunks ahead of the task-queue frontier, so HBM
         // stays busy while tasks wait on their dependencies
+        if (!A.prefetch) return;
         while (true) {
             const unsigned long long p = atomicAdd(A.pf_counter, 1ull) - A.pf_base;
             if (p >= (unsigned long long)A.n_units) break;
@@ -196,69 +290,239 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             }
             const Unit& u = A.units[p];
             if (u.type == UNIT_STREAM) {
-                const Pass& P = A.passes[u.pass];
+                const Pass& P = S.passes[u.pass];
                 prefetch_l2(P.arena + u.a_off, (uint32_t)u.ncols * (uint32_t)u.ld * 8u);
             }
         }
         return;
     }
-    if (warp <= kGatherers) {
-        // ------------------------------------------------ gatherers: warp w owns stages s = w-1 (mod 2)
+    if (warp >= 1 && warp <= kGatherers) {
+        // ------------------------------------------------ gatherers: warp w owns stages s = w-1 (mod kGatherers)
         int64_t verified = -1;  // last task whose waits this warp has checked
+        unsigned long long st_full = 0, st_dep = 0, st_gather = 0, st_lat = 0, st_nlat = 0, st_early = 0;
         for (int64_t k = warp - 1;; k += kGatherers) {
             const int s = (int)(k % kStages);
-            mbar_wait(&S.full[s], (uint32_t)((k / kStages) & 1));
-            const int64_t ui = S.hdr[s];
-            if (ui >= 0) {
-                const Unit& u = A.units[ui];
-                const Pass& P = A.passes[u.pass];
-                const int64_t ti = S.hdr_task[s];
+            long long c0 = clock64();
+            mbar_wait(&S.csfull[s], (uint32_t)((k / kStages) & 1));
+            long long c1 = clock64();
+            st_full += c1 - c0;
+            const StageHdr& H = S.hdr[s];
+            const int type = H.u.type;
+            if (type >= 0) {
+                const int64_t ti = H.task;
                 if (ti != verified) {
-                    const Task& t = A.tasks[ti];
                     if (lane == 0) {
-                        if (t.wait_id[0] >= 0) wait_counter(A, t.wait_id[0], t.wait_cnt[0]);
-                        if (t.wait_id[1] >= 0) wait_counter(A, t.wait_id[1], t.wait_cnt[1]);
-                        if (A.trace && u.chunk == 0) atomicMin(A.trace + 2 * u.pass, gtimer());
+                        if (H.wait_id[0] >= 0) wait_counter(A, H.wait_id[0], H.wait_cnt[0]);
+                        if (H.wait_id[1] >= 0) wait_counter(A, H.wait_id[1], H.wait_cnt[1]);
+                        if (A.trace && H.u.chunk == 0) atomicMin(A.trace + 2 * H.u.pass, gtimer());
                     }
                     __syncwarp();
                     __threadfence();
                     verified = ti;
                 }
-                if (u.type == UNIT_STREAM) {
+                c0 = clock64();
+                st_dep += c0 - c1;
+                if (type == UNIT_STREAM) {
+                    const Pass& P = S.passes[H.u.pass];
                     const double* in = P.in ? P.in : A.user_in;
                     const int32_t* cs = S.st[s].cs;
+                    const int ncols = H.u.ncols;
+                    const int im = P.in_mode;
                     constexpr int kPer = kMaxCols / 32;
                     double v[kPer];
+                    if (im == IN_PLAIN && H.u.nruns > 0) {
+                        // run-encoded column sources: lane's columns c = lane + 32 q are increasing
+                        const int nr = H.u.nruns;
+                        int r = 0, rs = 0;
+                        int32_t idx[kPer];
 #pragma unroll
-                    for (int q = 0; q < kPer; ++q) {
-                        const int c = lane + 32 * q;
-                        v[q] = c < u.ncols ? __ldcg(in + cs[c]) : 0.0;
+                        for (int q = 0; q < kPer; ++q) {
+                            const int c = lane + 32 * q;
+                            while (r < nr - 1 && c >= rs + (int)H.u.run_len[r]) { rs += H.u.run_len[r]; ++r; }
+                            idx[q] = c < ncols ? H.u.run_src[r] + (c - rs) : -1;
+                        }
+#pragma unroll
+                        for (int q = 0; q < kPer; ++q) v[q] = idx[q] >= 0 ? __ldcg(in + idx[q]) : 0.0;
+                    } else if (im == IN_PLAIN) {
+#pragma unroll
+                        for (int q = 0; q < kPer; ++q) {
+                            const int c = lane + 32 * q;
+                            v[q] = c < ncols ? __ldcg(in + cs[c]) : 0.0;
+                        }
+                    } else {
+                        // fused prologue: x-region inputs come straight from the caller's external-order
+                        // vector (colsrc_ext holds -(external index + 1)); IN_FLUX: w = eps * T^4
+                        // (eq:qi_new_location)
+#pragma unroll
+                        for (int q = 0; q < kPer; ++q) {
+                            const int c = lane + 32 * q;
+                            const int32_t j = c < ncols ? cs[c] : 0;
+                            if (c >= ncols) {
+                                v[q] = 0.0;
+                            } else if (j >= 0) {
+                                v[q] = __ldcg(in + j);
+                            } else {
+                                const int64_t e = -(int64_t)j - 1;
+                                const double t = __ldg(A.user_in + e * A.ld + A.col);
+                                v[q] = im == IN_PERM ? t : __ldg(A.eps_ext + e) * pow4(t);
+                            }
+                        }
                     }
 #pragma unroll
                     for (int q = 0; q < kPer; ++q) {
                         const int c = lane + 32 * q;
-                        if (c < u.ncols) S.st[s].xs[c] = v[q];
+                        if (c < ncols) S.st[s].xs[c] = v[q];
                     }
                 }
             }
             __syncwarp();
+            if (type >= 0) st_gather += clock64() - c0;
+            if (A.stats && type == UNIT_STREAM) {   // landing probe: issue -> payload complete
+                const long long ti = H.t_issue;
+                const bool pending = !mbar_test(&S.full[s], (uint32_t)((k / kStages) & 1));
+                mbar_wait(&S.full[s], (uint32_t)((k / kStages) & 1));
+                if (pending) { st_lat += clock64() - ti; ++st_nlat; }
+                else ++st_early;
+            }
             if (lane == 0) mbar_arrive(&S.gathered[s]);
-            if (ui < 0) break;
+            if (type < 0) break;
+        }
+        if (A.stats && lane == 0) {
+            atomicAdd(A.stats + 3, st_full);
+            atomicAdd(A.stats + 4, st_dep);
+            atomicAdd(A.stats + 5, st_gather);
+            atomicAdd(A.stats + 11, st_lat);
+            atomicAdd(A.stats + 12, st_nlat);
+            atomicAdd(A.stats + 13, st_early);
+        }
+        return;
+    }
+    if (warp >= kRetireWarp && warp < kRetireWarp + kRetireWarps) {
+        // ------------------------------------------------ retire warp: per task, reduce the consumers'
+        // partial sums in fixed order, emit (split panels: publish the partial, the last-finishing piece
+        // adds all partials in piece order), then publish the task (release fence, dependency counters)
+        unsigned long long st_rwait = 0, st_rwork = 0;
+        for (int64_t k = warp - kRetireWarp;; k += kRetireWarps) {   // retire warp w: slots k = w (mod 2)
+            const int r = (int)(k % kRetireSlots);
+            long long c0 = clock64();
+            mbar_wait(&S.rfull[r], (uint32_t)((k / kRetireSlots) & 1));
+            long long c1 = clock64();
+            st_rwait += c1 - c0;
+            const RetireSlot& R = S.rs[r];
+            struct { int32_t type, pass, nrows, ld, grp, nseg, seg; int64_t out0, part_off; } u;
+            u.type = R.u.type; u.pass = R.u.pass; u.nrows = R.u.nrows; u.ld = R.u.ld; u.grp = R.u.grp;
+            u.nseg = R.u.nseg; u.seg = R.u.seg; u.out0 = R.u.out0; u.part_off = R.u.part_off;
+            if (u.type < 0) break;
+            const int32_t inc0 = R.inc_id[0], inc1 = R.inc_id[1];
+            const Pass& P = S.passes[u.pass];
+            const int Pp = (u.nrows + 1) >> 1;
+            const int G = kConsumers / Pp;
+            double2 sum[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+            if (u.type == UNIT_STREAM) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int pp = lane + 32 * h;
+                    if (pp < Pp) {
+                        double2 t = R.red[pp];
+                        for (int q = 1; q < G; ++q) {
+                            const double2 v = R.red[q * Pp + pp];
+                            t.x += v.x;
+                            t.y += v.y;
+                        }
+                        sum[h] = t;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.rempty[r]);   // slot free: the consumers may deposit the next task
+            if (u.type == UNIT_STREAM) {
+                if (u.grp < 0) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int pp = lane + 32 * h;
+                        if (pp < Pp) {
+                            emit(A, P, u.out0 + 2 * pp, sum[h].x);
+                            if (2 * pp + 1 < u.nrows) emit(A, P, u.out0 + 2 * pp + 1, sum[h].y);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int pp = lane + 32 * h;
+                        if (pp < Pp) reinterpret_cast<double2*>(P.part + u.part_off)[pp] = sum[h];
+                    }
+                    __syncwarp();
+                    int last = 0;
+                    if (lane == 0) last = (atom_add_acq_rel(P.counters + u.grp, 1) == u.nseg - 1);
+                    last = __shfl_sync(0xffffffffu, last, 0);
+                    if (last) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int pp = lane + 32 * h;
+                            if (pp < Pp) {
+                                double2 t = make_double2(0.0, 0.0);
+                                for (int q = 0; q < u.nseg; ++q) {  // piece q's partial sits (q - seg) * ld doubles away
+                                    const double2 v = __ldcg(reinterpret_cast<const double2*>(P.part + u.part_off) +
+                                                             (int64_t)(q - u.seg) * (u.ld >> 1) + pp);
+                                    t.x += v.x;
+                                    t.y += v.y;
+                                }
+                                emit(A, P, u.out0 + 2 * pp, t.x);
+                                if (2 * pp + 1 < u.nrows) emit(A, P, u.out0 + 2 * pp + 1, t.y);
+                            }
+                        }
+                        if (lane == 0) P.counters[u.grp] = 0;
+                    }
+                }
+            }
+            // ---- publish: outputs (this warp's, and the element-wise ones the consumers wrote before
+            // their mbarrier release) visible GPU-wide before the counters move
+            __syncwarp();
+            if (lane == 0) {
+                if (u.type != UNIT_STREAM) __threadfence();   // element-wise outputs were written by the consumers
+                red_release(A.done + u.pass, 1ull);
+                if (inc0 >= 0) red_release(A.done + inc0, 1ull);
+                if (inc1 >= 0) red_release(A.done + inc1, 1ull);
+                if (A.trace) atomicMax(A.trace + 2 * u.pass + 1, gtimer());
+            }
+            st_rwork += clock64() - c1;
+        }
+        if (A.stats && lane == 0) {
+            atomicAdd(A.stats + 9, st_rwait);
+            atomicAdd(A.stats + 10, st_rwork);
         }
         return;
     }
     // ---------------------------------------------------- consumers: accumulate a task's chunks in
-    // registers, reduce and emit once per task
+    // registers; at the task's last chunk hand the per-thread partials to the retire warp
     const int ct = tid - kConsumer0;
     double2 acc = make_double2(0.0, 0.0), acc2 = acc;
+    unsigned long long st_wait = 0, st_comp = 0, st_task = 0;
+    int64_t ntask = 0;
+    long long c0 = clock64();
     for (int64_t k = 0;; ++k) {
         const int s = (int)(k % kStages);
         mbar_wait(&S.gathered[s], (uint32_t)((k / kStages) & 1));
-        const int64_t ui = S.hdr[s];
-        if (ui < 0) break;
-        const int64_t ti = S.hdr_task[s];
-        const Unit u = A.units[ui];
-        const Pass P = A.passes[u.pass];
+        mbar_wait(&S.full[s], (uint32_t)((k / kStages) & 1));
+        long long c1 = clock64();
+        st_wait += c1 - c0;
+        const StageHdr& H = S.hdr[s];
+        struct { int32_t type, pass, nrows, ld, ncols, chunk, nchunks, grp, nseg, seg; int64_t out0, part_off; } u;
+        u.type = H.u.type; u.pass = H.u.pass; u.nrows = H.u.nrows; u.ld = H.u.ld; u.ncols = H.u.ncols;
+        u.chunk = H.u.chunk; u.nchunks = H.u.nchunks; u.out0 = H.u.out0;
+        u.grp = H.u.grp; u.nseg = H.u.nseg; u.seg = H.u.seg; u.part_off = H.u.part_off;
+        const int32_t inc0 = H.inc_id[0], inc1 = H.inc_id[1];
+        if (u.type < 0) {   // end of work: one marker per retire warp
+            for (int w = 0; w < kRetireWarps; ++w, ++ntask) {
+                const int r = (int)(ntask % kRetireSlots);
+                if (ntask >= kRetireSlots) mbar_wait(&S.rempty[r], (uint32_t)(((ntask / kRetireSlots) - 1) & 1));
+                if (ct == 0) S.rs[r].u.type = -1;
+                asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");   // slot reuse across markers
+                if (lane == 0) mbar_arrive(&S.rfull[r]);
+            }
+            break;
+        }
+        const Pass& P = S.passes[u.pass];
         const int Pp = (u.nrows + 1) >> 1;
         const int G = kConsumers / Pp;
         const int g = ct / Pp;
@@ -269,16 +533,22 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                 const double2* a = reinterpret_cast<const double2*>(S.st[s].payload) + p;
                 const double* xs = S.st[s].xs;
                 const int ld2 = u.ld >> 1;
+                const int nc = u.ncols;
                 int c = g;
-                for (; c + G < u.ncols; c += 2 * G) {
+                for (; c + 3 * G < nc; c += 4 * G) {
                     const double2 a0 = a[c * ld2], a1 = a[(c + G) * ld2];
-                    const double x0 = xs[c], x1 = xs[c + G];
+                    const double2 a2 = a[(c + 2 * G) * ld2], a3 = a[(c + 3 * G) * ld2];
+                    const double x0 = xs[c], x1 = xs[c + G], x2 = xs[c + 2 * G], x3 = xs[c + 3 * G];
                     acc.x = fma(a0.x, x0, acc.x);
                     acc.y = fma(a0.y, x0, acc.y);
                     acc2.x = fma(a1.x, x1, acc2.x);
                     acc2.y = fma(a1.y, x1, acc2.y);
+                    acc.x = fma(a2.x, x2, acc.x);
+                    acc.y = fma(a2.y, x2, acc.y);
+                    acc2.x = fma(a3.x, x3, acc2.x);
+                    acc2.y = fma(a3.y, x3, acc2.y);
                 }
-                if (c < u.ncols) {
+                for (; c < nc; c += G) {
                     const double2 a0 = a[c * ld2];
                     const double x0 = xs[c];
                     acc.x = fma(a0.x, x0, acc.x);
@@ -295,67 +565,37 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
         // stage consumed: release it to the producer (per warp, no CTA-wide barrier)
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[s]);
+        c0 = clock64();
+        st_comp += c0 - c1;
         if (u.chunk != u.nchunks - 1) continue;
-        // ---- last chunk of the task
-        if (u.type == UNIT_STREAM) {
-            if (g < G) S.red[g * Pp + p] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
-            consumers_sync();
-            const bool owner = ct < Pp;
-            double2 sum = make_double2(0.0, 0.0);
-            if (owner) {
-                sum = S.red[ct];
-                for (int q = 1; q < G; ++q) {
-                    const double2 v = S.red[q * Pp + ct];
-                    sum.x += v.x;
-                    sum.y += v.y;
-                }
-            }
-            if (u.grp < 0) {
-                if (owner) {
-                    emit(A, P, u.out0 + 2 * ct, sum.x);
-                    if (2 * ct + 1 < u.nrows) emit(A, P, u.out0 + 2 * ct + 1, sum.y);
-                }
-            } else {  // panel split into pieces: the last-finishing piece adds the partials in order
-                if (owner) reinterpret_cast<double2*>(P.part + u.part_off)[ct] = sum;
-                consumers_sync();
-                if (ct == 0) {
-                    __threadfence();
-                    S.last = (atomicAdd(P.counters + u.grp, 1) == u.nseg - 1);
-                    if (S.last) __threadfence();
-                }
-                consumers_sync();
-                if (S.last) {
-                    if (owner) {
-                        double2 t = make_double2(0.0, 0.0);
-                        for (int q = 0; q < u.nseg; ++q) {  // piece q's partial sits (q - seg) * ld doubles away
-                            const double2 v = __ldcg(reinterpret_cast<const double2*>(P.part + u.part_off) +
-                                                     (int64_t)(q - u.seg) * (u.ld >> 1) + ct);
-                            t.x += v.x;
-                            t.y += v.y;
-                        }
-                        emit(A, P, u.out0 + 2 * ct, t.x);
-                        if (2 * ct + 1 < u.nrows) emit(A, P, u.out0 + 2 * ct + 1, t.y);
-                    }
-                    if (ct == 0) P.counters[u.grp] = 0;
-                }
-            }
-        }
-        // ---- retire the task: outputs visible to other SMs (cumulative fence after the barrier)
-        consumers_sync();
+        // ---- last chunk of the task: deposit partials + descriptor, hand off to the retire warp
+        const int r = (int)(ntask % kRetireSlots);
+        if (ntask >= kRetireSlots) mbar_wait(&S.rempty[r], (uint32_t)(((ntask / kRetireSlots) - 1) & 1));
+        ++ntask;
+        RetireSlot& R = S.rs[r];
+        if (u.type == UNIT_STREAM && g < G) R.red[g * Pp + p] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
         if (ct == 0) {
-            const Task& t = A.tasks[ti];
-            __threadfence();
-            atomicAdd(A.done + u.pass, 1ull);
-            if (t.inc_id[0] >= 0) atomicAdd(A.done + t.inc_id[0], 1ull);
-            if (t.inc_id[1] >= 0) atomicAdd(A.done + t.inc_id[1], 1ull);
-            if (A.trace) atomicMax(A.trace + 2 * u.pass + 1, gtimer());
+            R.u = TaskEnd{u.type, u.pass, u.nrows, u.ld, u.grp, u.nseg, u.seg, 0, u.out0, u.part_off};
+            R.inc_id[0] = inc0;
+            R.inc_id[1] = inc1;
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.rfull[r]);
+        const long long c2 = clock64();
+        st_task += c2 - c0;
+        c0 = c2;
+    }
+    if (A.stats && ct == 0) {
+        atomicAdd(A.stats + 6, st_wait);
+        atomicAdd(A.stats + 7, st_comp);
+        atomicAdd(A.stats + 8, st_task);
     }
 }
 
 }  // namespace
 
 size_t engine_smem_bytes() { return sizeof(EngineSmem) + 128; }
+int engine_max_passes() { return kMaxPasses; }
 
 static void set_attr() {
     static bool attr = false;

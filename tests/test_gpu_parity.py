@@ -248,4 +248,22 @@ def test_config2_full_size(hm, ctx):
     hm.hm_solve_C(ctx, LU, x, z)
     r = vf.sampled_residual(f.centroid, f.normal, f.area, cfg.emissivity, rows, z[:, None], x[:, None])[:, 0]
     assert np.linalg.norm(r) / np.linalg.norm(x[rows]) <= 10 * cfg.eps_aca
-    del torch
+    # the flux exactly as bench.py times it (device pointers, one engine launch per call):
+    # properties that hold at any size (SURVEY.md §8(c) pins), and run-to-run
+    # bitwise equality (no floating-point atomics: a race detector)
+    T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+    q = torch.empty_like(T)
+    hm.hm_radiative_flux(ctx, F, LU, T, q)
+    torch.cuda.synchronize()
+    q0 = q.cpu().numpy().copy()
+    for _ in range(20):
+        hm.hm_radiative_flux(ctx, F, LU, T, q)
+    torch.cuda.synchronize()
+    assert np.array_equal(q.cpu().numpy(), q0)
+    Aq = f.area * q0
+    assert abs(Aq.sum()) <= 10 * cfg.eps_aca * np.abs(Aq).sum()       # energy conservation
+    Tu = torch.full_like(T, 700.0)
+    hm.hm_radiative_flux(ctx, F, LU, Tu, q)                            # uniform T -> q = 0
+    torch.cuda.synchronize()
+    sig = vf.SIGMA_SB * 700.0 ** 4
+    assert np.abs(q.cpu().numpy()).max() <= 10 * cfg.eps_aca * sig
