@@ -4,9 +4,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
-Prints ONE JSON line (rank 0).  Multi-GPU (torchrun): every rank runs an independent replica
-of the workload (row-cluster sharding is not in this build), timed with
-a barrier + synchronize on both sides, max over ranks.
+Prints ONE JSON line (rank 0).  Multi-GPU (torchrun, N = 2/4/8): ONE apply is sharded by row
+cluster over the N ranks: rank r owns the rows of tree node r at level log2 N, the
+library allgathers the vector between its engine programs over NCCL; timed with a barrier +
+synchronize on both sides, max over ranks; scaling "strong" (total work fixed).
 """
 from __future__ import annotations
 
@@ -172,6 +173,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=20)
+    ap.add_argument("--no-level-form", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -197,7 +199,12 @@ def main():
     cfg = synth.make_config(args.config)
     f = cfg.facets
     n = f.n
-    ctx = hm.hm_init(local)
+    if world > 1:
+        obj = [hm.hm_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = hm.hm_init(local, rank, world, obj[0])
+    else:
+        ctx = hm.hm_init(local)
     t0 = time.perf_counter()
     g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
     F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
@@ -205,7 +212,14 @@ def main():
     setup_wall = time.perf_counter() - t0
     rep = hm.hm_storage_report(F, LU)
     stream = torch.cuda.current_stream()
-    T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+    if world > 1:   # this rank's slice of T in internal order
+        perm = hm.hm_export_perm(g)
+        b0, e0 = hm.hm_local_range(g, rank, world)
+        T_host = np.ascontiguousarray(cfg.T[perm[b0:e0], 0])
+    else:
+        T_host = np.ascontiguousarray(cfg.T[:, 0])
+    n_loc = T_host.shape[0]
+    T = torch.from_numpy(T_host.copy()).cuda()
     q = torch.empty_like(T)
 
     def step():
@@ -235,11 +249,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * args.steps / (ms / 1e3)
+    value = args.steps / (ms / 1e3)   # one (sharded) apply per step for the whole job
 
     # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
-    Th = torch.from_numpy(cfg.T[:, 0].copy()).pin_memory()
-    qh = torch.empty(n, dtype=torch.float64).pin_memory()
+    Th = torch.from_numpy(T_host.copy()).pin_memory()
+    qh = torch.empty(n_loc, dtype=torch.float64).pin_memory()
     Th_np, qh_np = Th.numpy(), qh.numpy()
     for _ in range(2):
         hm.hm_radiative_flux(ctx, F, LU, Th_np, qh_np, stream=stream.cuda_stream)
@@ -260,21 +274,36 @@ def main():
     # ---- the dominant (and only) kernel of a step: one persistent engine launch per call;
     # timed live with CUDA events on the launching stream, alongside F-only and solve-only calls
     eng_ms, eng_info = hm.hm_profile_flux(ctx, F, LU, T, q, args.profile_iters, stream=stream.cuda_stream)
+    # the pure level-form substitution (cut level = depth) on the same operators,
+    # reported beside the default inverse-factor form (reading R27)
+    level_form = None
+    if not args.no_level_form and world == 1:
+        LU_lf = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=99)
+        rep_lf = hm.hm_storage_report(F, LU_lf)
+        lf_ms, lf_info = hm.hm_profile_flux(ctx, F, LU_lf, T, q, args.profile_iters, stream=stream.cuda_stream)
+        level_form = {"flux_ms": lf_ms["flux"], "solve_ms": lf_ms["solve_C"], "passes": lf_info["passes"],
+                      "bytes_C": rep_lf["bytes_C"],
+                      "solve_hbm_gbs": rep_lf["bytes_C"] / (lf_ms["solve_C"] * 1e-3) / 1e9}
+        del LU_lf
     peak, peak_src = peaks()
     bytes_step = rep["bytes_F"] + rep["bytes_C"]
-    achieved = bytes_step / (eng_ms["flux"] * 1e-3) / 1e9
+    bytes_local = rep["bytes_F_local"] + rep["bytes_C_local"]    # this rank's stored bytes (= bytes_step at N=1)
+    achieved = bytes_local / (eng_ms["flux"] * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and world == 1 and args.config == 2:
         traffic = json.load(open(tp)).get("engine_kernel_flux_c2")
     launches = eng_info["launches_per_call"]
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "n": n, "parallelism": "replicas" if world > 1 else "single",
+            "config": {"workload": workload_desc(cfg), "n": n,
+                       "parallelism": f"row-cluster sharded x{world} (NCCL allgather)" if world > 1 else "single",
+                       "bytes_local_rank0": bytes_local,
                        "l2": f"no flush: stored operator bytes per step {bytes_step/1e9:.3f} GB > 126 MB L2",
                        "stored_bytes_per_step": bytes_step, "bytes_F": rep["bytes_F"], "bytes_C": rep["bytes_C"],
                        "step_hbm_gbs": bytes_step / (ms_step * 1e-3) / 1e9,
@@ -284,17 +313,20 @@ def main():
                        "solve_C_hbm_gbs": rep["bytes_C"] / (eng_ms["solve_C"] * 1e-3) / 1e9,
                        "ranks_F": {"mean": rep["rank_mean"], "max": rep["rank_max"]},
                        "ranks_C": {"mean": rep["rank_mean_C"], "max": rep["rank_max_C"]},
-                       "setup_s": dict(rep["setup_seconds"], wall=setup_wall)},
-            "roofline": {"bound": "hbm", "kernel": "engine_kernel (flux program)", "achieved": achieved,
+                       "setup_s": dict(rep["setup_seconds"], wall=setup_wall),
+                       "solve_form": "inverse factors (cut level 0, DESIGN.md R27)",
+                       "level_form": level_form},
+            "roofline": {"bound": "hbm", "kernel": "engine_kernel (flux program)" + (" + NCCL allgathers, rank 0" if world > 1 else ""),
+                         "achieved": achieved,
                          "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
-            "e2e": {"value": world * args.steps / (ms_e2e / 1e3), "unit": "applies/s",
-                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
-            "gpu_launches": launches * args.steps,
+            "e2e": {"value": args.steps / (ms_e2e / 1e3), "unit": "applies/s",
+                    "h2d_bytes_per_step": 8 * n_loc, "d2h_bytes_per_step": 8 * n_loc},
+            "gpu_launches": launches * args.steps,   # engine launches by this rank in the timed region
         }
         clk_s = clk.summary()
         out["clocks"] = clk_s
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             out["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -26,7 +26,8 @@
  *    after setup and may be used from one host thread at a time.
  *  - Asynchronous kernel faults surface as HM_ERR_CUDA at the next synchronising call;
  *    environment HM_DEBUG=1 synchronises after every launch.
- *  - There is no CPU fallback: without a CUDA device hm_init returns HM_ERR_CUDA.
+ *  - There is no CPU fallback: without a CUDA device hm_init returns HM_ERR_CUDA (device < 0 gives
+ *    a host-only context for trees and shard plans; every compute call then returns an error).
  */
 #ifndef HM_H_
 #define HM_H_
@@ -49,6 +50,11 @@ typedef enum {
     HM_ERR_NOT_READY = 7,            /* handle not built / wrong handle combination          */
     HM_ERR_UNSUPPORTED = 8           /* configuration outside what this build implements     */
 } hm_status;
+
+/* hm_init flags */
+#define HM_FLAG_LOCAL_GROUP 0x1u   /* world > 1 inside ONE process: comm_id points to an int64 group
+                                      key shared by the ranks (one host thread per rank); the exchange
+                                      is done with device copies (tests of the sharded path on one GPU) */
 
 typedef struct hm_ctx hm_ctx;
 typedef struct hm_geom hm_geom;
@@ -74,11 +80,12 @@ typedef struct {
 typedef struct {
     double eps_lu;         /* truncation tolerance of the factor blocks; <= 0 -> eps_aca
                               ("equal to the approximation accuracy used for F")   */
-    int32_t cut_level;     /* level-scheduled substitution: W-form updates for
-                              tree levels < cut_level, then ONE block-diagonal solve with the
-                              inverse factors of the cut_level diagonal blocks (H-format).
-                              cut_level = depth: leaf inverses only (pure level form);
-                              0: C^-1 b = U^-1 (L^-1 b) as two H-applies; < 0: depth          */
+    int32_t cut_level;     /* solve form (reading R27): level-form updates
+                              b_t2 -= W^L_t b_t1 (and W^U_t for the backward sweep) for tree levels
+                              < cut_level, then ONE block-diagonal solve with the inverse factors
+                              of the cut_level diagonal blocks, compressed in F's partition.
+                              < 0 (default) -> 0: C^-1 b = U^-1 (L^-1 b) as two H-matrix products;
+                              >= depth: pure level form (leaf inverses only).                  */
 } hm_lu_params;
 
 /* Storage / traffic accounting (bytes are fp64 payload bytes actually stored in HBM). */
@@ -99,13 +106,27 @@ typedef struct {
     int64_t launches_solve_C;         /* kernel launches per hm_solve_C column (engine: 1)      */
     double setup_seconds[8];          /* tree, aca, dense-fill+pack, rowsum+scale, C-expand,
                                          dense LU+W, W-compress+pack, flux constant g          */
+    int64_t bytes_F_local;            /* world > 1: this rank's stored bytes of F (= bytes_F)   */
+    int64_t bytes_C_local;            /* world > 1: this rank's bytes of the solve operators    */
+    int64_t rank, world;
 } hm_storage;
 
 /* ---- lifetime ------------------------------------------------------------------------- */
-/* device: CUDA ordinal; rank/world: SPMD position (world > 1 not supported in this build:
-   returns HM_ERR_UNSUPPORTED); nccl_unique_id: NULL; flags: reserved, pass 0. */
-hm_status hm_init(int device, int rank, int world, const void* nccl_unique_id, uint32_t flags,
+/* device: CUDA ordinal (< 0: host-only context: hm_build_geometry / hm_local_range / hm_shard_plan /
+   hm_export_* only, no CUDA is touched).  rank / world: SPMD position, world a power of two.
+   world > 1 shards the hot path by row cluster: rank r owns the rows
+   of tree node r at level log2(world) (hm_local_range) and the vectors of hm_apply_F / hm_solve_C /
+   hm_radiative_flux become this rank's SLICE in internal order (n_loc x nrhs, n_loc = end - begin);
+   every rank makes the same calls.  comm_id: world == 1: NULL; world > 1: the 128-byte NCCL unique id
+   from hm_nccl_unique_id() on rank 0, broadcast by the caller (the library owns its communicator and
+   runs ncclAllGather on the call's stream), or with HM_FLAG_LOCAL_GROUP a pointer to an int64 key
+   shared by `world` ranks living in this process (one host thread per rank).  Setup is redundant
+   on every rank (each keeps only its block rows for the hot path).  Returns HM_ERR_CUDA without a
+   device, HM_ERR_NCCL if libnccl.so.2 cannot be opened or the communicator fails. */
+hm_status hm_init(int device, int rank, int world, const void* comm_id, uint32_t flags,
                   hm_ctx** ctx);
+/* 128-byte ncclUniqueId into id_out (rank 0 of a world > 1 job). */
+hm_status hm_nccl_unique_id(void* id_out);
 void hm_finalize(hm_ctx* ctx);
 const char* hm_status_string(hm_status s);
 const char* hm_last_error(const hm_ctx* ctx);
@@ -163,6 +184,11 @@ hm_status hm_export_row_sums(const hm_hmat* F, double* s, double* c);
 hm_status hm_storage_report(const hm_hmat* F, const hm_hlu* LU, hm_storage* out);
 /* Internal-order shard of `rank` among `world` ranks (tree node at level log2(world)). */
 hm_status hm_local_range(const hm_geom* geom, int rank, int world, int64_t* begin, int64_t* end);
+/* Shard plan for `world` ranks (host buffers): begin/end[world] internal row ranges, *maxc the padded
+   segment length of the exchanged vectors, block_owner[n_blocks] (or NULL) the rank owning each block
+   of hm_export_partition's order (-1: its rows straddle ranks). */
+hm_status hm_shard_plan(const hm_geom* geom, int world, int64_t* begin, int64_t* end, int64_t* maxc,
+                        int64_t* block_owner);
 
 /* ---- measurement support (bench.py) ---------------------------------------------------- */
 /* Times the hot-path programs with CUDA events on `stream` (device pointers T, q; nrhs = 1) over

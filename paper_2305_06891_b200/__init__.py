@@ -52,7 +52,8 @@ class hm_storage(C.Structure):
                 ("bytes_C", C.c_int64), ("bytes_C_leaf", C.c_int64), ("n_blocks_C", C.c_int64),
                 ("n_lowrank_C", C.c_int64), ("rank_max_C", C.c_int64), ("rank_mean_C", C.c_double),
                 ("launches_apply_F", C.c_int64), ("launches_solve_C", C.c_int64),
-                ("setup_seconds", C.c_double * 8)]
+                ("setup_seconds", C.c_double * 8), ("bytes_F_local", C.c_int64), ("bytes_C_local", C.c_int64),
+                ("rank", C.c_int64), ("world", C.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "setup_seconds"}
@@ -93,6 +94,8 @@ def load_library(path: str = LIB_PATH):
         "hm_local_range": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(I64), C.POINTER(I64)]),
         "hm_profile_flux": (C.c_int, [P, P, P, P, P, I32, P, P, P]),
         "hm_trace_flux": (C.c_int, [P, P, P, P, P, I32, C.POINTER(I32), P, P, P, P]),
+        "hm_nccl_unique_id": (C.c_int, [P]),
+        "hm_shard_plan": (C.c_int, [P, C.c_int, P, P, C.POINTER(I64), P]),
         "hm_destroy_geom": (None, [P]),
         "hm_destroy_hmat": (None, [P]),
         "hm_destroy_hlu": (None, [P]),
@@ -135,14 +138,31 @@ def _stream(stream, *arrays):
     return 0
 
 
+HM_FLAG_LOCAL_GROUP = 0x1
+
+
 class Context:
-    def __init__(self, device: int = 0):
+    """rank/world: SPMD position (world a power of two).  world > 1 needs comm_id: the 128-byte NCCL
+    unique id (bytes, from hm_nccl_unique_id on rank 0, broadcast by the caller), or with
+    flags=HM_FLAG_LOCAL_GROUP an int group key shared by ranks living in this process.
+    device < 0: host-only context (trees and shard plans, no CUDA)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, comm_id=None, flags: int = 0):
         self.lib = load_library()
         h = C.c_void_p()
-        st = self.lib.hm_init(device, 0, 1, None, 0, C.byref(h))
+        cid = None
+        if comm_id is not None:
+            if flags & HM_FLAG_LOCAL_GROUP:
+                self._cid = C.c_int64(int(comm_id))
+            else:
+                self._cid = C.create_string_buffer(bytes(comm_id), 128)
+            cid = C.cast(C.byref(self._cid), C.c_void_p)
+        st = self.lib.hm_init(device, rank, world, cid, flags, C.byref(h))
         if st != 0:
-            raise HMError(st, f"hm_init(device={device}) failed (no CUDA device? no CPU fallback exists)")
+            raise HMError(st, f"hm_init(device={device}, rank={rank}, world={world}) failed "
+                              "(no CUDA device? no CPU fallback exists)")
         self.h = h
+        self.rank, self.world = rank, world
 
     def check(self, st: int, what: str):
         if st != 0:
@@ -154,8 +174,31 @@ class Context:
             self.h = None
 
 
-def hm_init(device: int = 0) -> Context:
-    return Context(device)
+def hm_init(device: int = 0, rank: int = 0, world: int = 1, comm_id=None, flags: int = 0) -> Context:
+    return Context(device, rank, world, comm_id, flags)
+
+
+def hm_nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    st = lib.hm_nccl_unique_id(buf)
+    if st != 0:
+        raise HMError(st, "hm_nccl_unique_id failed")
+    return buf.raw
+
+
+def hm_shard_plan(geom, world: int):
+    """Row-cluster shard plan: (begin[world], end[world], maxc, block_owner[n_blocks]) -- block_owner[b]
+    is the rank owning block b's rows (-1: the rows straddle ranks)."""
+    b = np.zeros(world, dtype=np.int64)
+    e = np.zeros(world, dtype=np.int64)
+    m = C.c_int64()
+    nb = C.c_int64()
+    geom.ctx.check(geom.ctx.lib.hm_export_partition(geom.h, None, C.byref(nb), None), "partition")
+    own = np.zeros(nb.value, dtype=np.int64)
+    geom.ctx.check(geom.ctx.lib.hm_shard_plan(geom.h, world, b.ctypes.data, e.ctypes.data, C.byref(m),
+                                              own.ctypes.data), "hm_shard_plan")
+    return b, e, m.value, own
 
 
 class Geometry:
@@ -217,6 +260,14 @@ def hm_factor_hlu(ctx: Context, F: HMatrix, emissivity, eps_lu=0.0, cut_level=-1
     return HLU(ctx, h, F)
 
 
+def _rows(F_or_geom_ctx, geom):
+    ctx = geom.ctx
+    if getattr(ctx, "world", 1) > 1:
+        b, e = hm_local_range(geom, ctx.rank, ctx.world)
+        return e - b
+    return geom.n
+
+
 def _nrhs(x, n):
     shp = tuple(x.shape)
     if shp[0] != n or len(shp) > 2:
@@ -228,21 +279,22 @@ def hm_apply_F(ctx: Context, F: HMatrix, x, y, stream=None):
     """y = F x; x, y: (n,) or (n, nrhs) float64, device tensors or host arrays."""
     px, kx = _ptr(x)
     py, ky = _ptr(y)
-    ctx.check(ctx.lib.hm_apply_F(ctx.h, F.h, _nrhs(x, F.geom.n), px, py, _stream(stream, x, y)), "hm_apply_F")
+    ctx.check(ctx.lib.hm_apply_F(ctx.h, F.h, _nrhs(x, _rows(F, F.geom)), px, py, _stream(stream, x, y)), "hm_apply_F")
     return y
 
 
 def hm_solve_C(ctx: Context, LU: HLU, b, z, stream=None):
     pb, kb = _ptr(b)
     pz, kz = _ptr(z)
-    ctx.check(ctx.lib.hm_solve_C(ctx.h, LU.h, _nrhs(b, LU.F.geom.n), pb, pz, _stream(stream, b, z)), "hm_solve_C")
+    ctx.check(ctx.lib.hm_solve_C(ctx.h, LU.h, _nrhs(b, _rows(LU, LU.F.geom)), pb, pz, _stream(stream, b, z)),
+              "hm_solve_C")
     return z
 
 
 def hm_radiative_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, stream=None):
     pT, kT = _ptr(T)
     pq, kq = _ptr(q)
-    ctx.check(ctx.lib.hm_radiative_flux(ctx.h, F.h, LU.h, _nrhs(T, F.geom.n), pT, pq, _stream(stream, T, q)),
+    ctx.check(ctx.lib.hm_radiative_flux(ctx.h, F.h, LU.h, _nrhs(T, _rows(F, F.geom)), pT, pq, _stream(stream, T, q)),
               "hm_radiative_flux")
     return q
 

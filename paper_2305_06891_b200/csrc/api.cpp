@@ -121,27 +121,35 @@ const char* hm_status_string(hm_status s) {
 
 const char* hm_last_error(const hm_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
 
-hm_status hm_init(int device, int rank, int world, const void* nccl_unique_id, uint32_t flags, hm_ctx** out) {
+hm_status hm_init(int device, int rank, int world, const void* comm_id, uint32_t flags, hm_ctx** out) {
     if (!out) return HM_ERR_INVALID_ARG;
     *out = nullptr;
-    if (world != 1 || rank != 0 || nccl_unique_id) return HM_ERR_UNSUPPORTED;
-    int cnt = 0;
-    if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0 || device < 0 || device >= cnt) {
-        cudaGetLastError();
-        return HM_ERR_CUDA;
-    }
+    if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world) return HM_ERR_INVALID_ARG;
     auto* c = new hm_ctx;
     c->c.device = device;
     c->c.rank = rank;
     c->c.world = world;
     c->c.flags = flags;
+    c->c.host_only = device < 0;
     const char* dbg = getenv("HM_DEBUG");
     g_debug = c->c.debug = dbg && dbg[0] == '1';
+    if (c->c.host_only) {   // trees and shard plans only: no CUDA, no exchange
+        *out = c;
+        return HM_OK;
+    }
+    int cnt = 0;
+    if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0 || device >= cnt) {
+        cudaGetLastError();
+        delete c;
+        return HM_ERR_CUDA;
+    }
     hm_status st = guarded(&c->c, [&] {
         HM_CUDA(cudaSetDevice(device));
         HM_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        c->c.ex = make_exchanger(device, rank, world, comm_id, flags).release();
     });
     if (st != HM_OK) {
+        if (c->c.stream) cudaStreamDestroy(c->c.stream);
         delete c;
         return st;
     }
@@ -151,6 +159,7 @@ hm_status hm_init(int device, int rank, int world, const void* nccl_unique_id, u
 
 void hm_finalize(hm_ctx* ctx) {
     if (!ctx) return;
+    delete ctx->c.ex;
     if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
 }
@@ -199,6 +208,12 @@ hm_status hm_build_geometry(hm_ctx* ctx, int64_t n, const double* xyz, const dou
         g.params = *params;
         const double t0 = now_seconds();
         build_trees(g, xyz, nrm, area, facet_aabb);
+        make_shard(g, c->rank, c->world);
+        if (c->host_only) {
+            g.setup_seconds = now_seconds() - t0;
+            *out = guard.release();
+            return;
+        }
         std::vector<double> soa(7 * (size_t)n);
         std::copy(g.cx.begin(), g.cx.end(), soa.begin());
         std::copy(g.cy.begin(), g.cy.end(), soa.begin() + n);
@@ -241,19 +256,7 @@ hm_status hm_export_partition(const hm_geom* geom, const hm_hmat* F, int64_t* n_
 hm_status hm_local_range(const hm_geom* geom, int rank, int world, int64_t* begin, int64_t* end) {
     if (!geom || !begin || !end || world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
         return HM_ERR_INVALID_ARG;
-    // node `rank` at tree level log2(world), walking down the left/right children
-    const Geom& g = geom->g;
-    int node = 0;
-    for (int bit = world >> 1; bit > 0; bit >>= 1) {
-        const Node& N = g.nodes[node];
-        if (N.is_leaf()) {  // too few clusters: later ranks get empty ranges
-            if (rank & (bit * 2 - 1)) { *begin = *end = N.end; return HM_OK; }
-            break;
-        }
-        node = N.child[(rank & bit) ? 1 : 0];
-    }
-    *begin = g.nodes[node].begin;
-    *end = g.nodes[node].end;
+    local_range(geom->g, rank, world, begin, end);   // node `rank` at tree level log2(world)
     return HM_OK;
 }
 
@@ -261,6 +264,10 @@ hm_status hm_local_range(const hm_geom* geom, int rank, int world, int64_t* begi
 hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params* params, hm_hmat** F_out) {
     if (!ctx || !geom || !params || !F_out) return HM_ERR_INVALID_ARG;
     *F_out = nullptr;
+    if (ctx->c.host_only) {
+        ctx->c.last_error = "host-only context (device < 0): trees and shard plans only";
+        return HM_ERR_NOT_READY;
+    }
     Ctx* c = &ctx->c;
     return guarded(c, [&] {
         if (!(params->eps_aca > 0.0) || params->eps_aca >= 1.0)
@@ -365,6 +372,7 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             }
         }
         build_hop(c, g, src, F.op, s);
+        if (g.shard.sharded()) build_hop(c, g, src, F.op_loc, s, &g.shard);   // this rank's block rows
         batches.clear();
         F.setup_seconds[1] = now_seconds() - t0;
 
@@ -398,6 +406,29 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         HM_CUDA(cudaMemcpyAsync(hs.data(), sv.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaMemcpyAsync(hc.data(), cv.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaStreamSynchronize(s));
+        if (g.shard.sharded()) {
+            // the local operator: same closed-cavity scaling, rows indexed in the padded layout
+            const Shard& S = g.shard;
+            if (params->closed_cavity) {
+                std::vector<double> cdiv_pad(S.n_pad(), 1.0);
+                for (int64_t i = S.lb(); i < S.le(); ++i) cdiv_pad[S.pad(i)] = hc[i] != 0.0 ? hc[i] : 1.0;
+                DBuf<double> dcp;
+                dcp.upload(c, cdiv_pad, "row divisors (padded)", s);
+                std::vector<int64_t> tasks;
+                for (const Panel& pn : F.op_loc.p2.panels)
+                    tasks.insert(tasks.end(), {pn.a_off, pn.ld, pn.nrows, pn.ncols, pn.out0});
+                DBuf<int64_t> dt;
+                dt.upload(c, tasks, "scale tasks (local)", s);
+                if (!tasks.empty()) k::scale_rows(dt.p, (int)F.op_loc.p2.panels.size(), F.op_loc.arena.p, dcp.p, s);
+                HM_CUDA(cudaStreamSynchronize(s));
+            }
+            F.xt_loc.alloc(c, (size_t)(S.n_pad() + F.op_loc.n_t), "F xt (local)");
+            Program& P = F.sp_apply.add(F.xt_loc.p, true);
+            P.n_x = S.n_pad();
+            P.add_stream(F.op_loc.p1, F.op_loc, F.xt_loc.p, F.xt_loc.p, OUT_ASSIGN);
+            P.add_stream(F.op_loc.p2, F.op_loc, F.xt_loc.p, nullptr, OUT_LOCAL, DEP_BARRIER, nullptr, IN_PLAIN, -1);
+            F.sp_apply.finalize(c, s, &g);
+        }
         F.s_ext.resize(n);
         F.c_ext.resize(n);
         for (int64_t i = 0; i < n; ++i) {
@@ -431,27 +462,18 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
     Ctx* c = &ctx->c;
     return guarded(c, [&] {
         HMat& F = const_cast<HMat&>(Fh->h);
-        const Geom& g = *F.geom;
-        const int64_t n = g.n;
+        const size_t cnt = (size_t)vec_rows(*F.geom) * nrhs;
         cudaStream_t s = (cudaStream_t)stream;
         bool hin = false;
-        const double* xd = stage_in(c, F.host_stage_in, x, (size_t)n * nrhs, s, hin);
+        const double* xd = stage_in(c, F.host_stage_in, x, cnt, s, hin);
         const bool hout = !is_device_ptr(y);
         double* yd = y;
         if (hout) {
-            if (F.host_stage_out.n < (size_t)n * nrhs) F.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
+            if (F.host_stage_out.n < cnt) F.host_stage_out.alloc(c, cnt, "host staging (out)");
             yd = F.host_stage_out.p;
         }
-        for (int col = 0; col < nrhs; ++col) {
-            ProgArgs a{};
-            a.perm = g.d_perm.p;
-            a.user_in = xd;
-            a.user_out = yd;
-            a.ld = nrhs;
-            a.col = col;
-            F.prog_apply.launch(a, s);
-        }
-        if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        for (int col = 0; col < nrhs; ++col) launch_apply(c, F, xd, yd, nrhs, col, s);
+        if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
@@ -461,27 +483,18 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
     Ctx* c = &ctx->c;
     return guarded(c, [&] {
         HLU& L = const_cast<HLU&>(LUh->h);
-        const Geom& g = *L.F->geom;
-        const int64_t n = g.n;
+        const size_t cnt = (size_t)vec_rows(*L.F->geom) * nrhs;
         cudaStream_t s = (cudaStream_t)stream;
         bool hin = false;
-        const double* bd = stage_in(c, L.host_stage_in, b, (size_t)n * nrhs, s, hin);
+        const double* bd = stage_in(c, L.host_stage_in, b, cnt, s, hin);
         const bool hout = !is_device_ptr(z);
         double* zd = z;
         if (hout) {
-            if (L.host_stage_out.n < (size_t)n * nrhs) L.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
+            if (L.host_stage_out.n < cnt) L.host_stage_out.alloc(c, cnt, "host staging (out)");
             zd = L.host_stage_out.p;
         }
-        for (int col = 0; col < nrhs; ++col) {
-            ProgArgs a{};
-            a.perm = g.d_perm.p;
-            a.user_in = bd;
-            a.user_out = zd;
-            a.ld = nrhs;
-            a.col = col;
-            L.prog_solve.launch(a, s);
-        }
-        if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        for (int col = 0; col < nrhs; ++col) launch_solve(c, L, bd, zd, nrhs, col, s);
+        if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
@@ -489,21 +502,54 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
 }  // extern "C"
 
 namespace hm {
-// One flux evaluation (engine program, one launch) for column `col` (device pointers).
-void launch_flux(HLU& L, const double* Td, double* qd, int ld, int col, cudaStream_t s) {
-    const Geom& g = *L.F->geom;
+// Rows of the caller's vectors: n (external order) or, sharded, this rank's slice (internal order).
+int64_t vec_rows(const Geom& g) { return g.shard.sharded() ? g.shard.le() - g.shard.lb() : g.n; }
+
+static ProgArgs base_args(const Geom& g, const double* in, double* out, int ld, int col) {
     ProgArgs a{};
     a.perm = g.d_perm.p;
-    a.user_in = Td;
-    a.user_out = qd;
+    a.user_in = in;
+    a.user_out = out;
     a.ld = ld;
     a.col = col;
-    a.eps_int = L.eps_int.p;
-    a.eps_ext = L.eps_ext.p;
-    a.area_int = g.d_geo.p + 6 * g.n;
-    a.g_int = L.g_int.p;
+    a.local0 = g.shard.base();
+    return a;
+}
+
+void launch_apply(Ctx* c, HMat& F, const double* xd, double* yd, int ld, int col, cudaStream_t s) {
+    const Geom& g = *F.geom;
+    ProgArgs a = base_args(g, xd, yd, ld, col);
+    if (g.shard.sharded()) F.sp_apply.launch(c, g, a, s);
+    else F.prog_apply.launch(a, s);
+}
+
+void launch_solve(Ctx* c, HLU& L, const double* bd, double* zd, int ld, int col, cudaStream_t s) {
+    const Geom& g = *L.F->geom;
+    ProgArgs a = base_args(g, bd, zd, ld, col);
+    if (g.shard.sharded()) L.sp_solve.launch(c, g, a, s);
+    else L.prog_solve.launch(a, s);
+}
+
+// One flux evaluation (engine program(s)) for column `col` (device pointers).
+void launch_flux(Ctx* c, HLU& L, const double* Td, double* qd, int ld, int col, cudaStream_t s,
+                 unsigned long long* trace) {
+    const Geom& g = *L.F->geom;
+    ProgArgs a = base_args(g, Td, qd, ld, col);
     a.sigma = 5.670374419e-8;  // DESIGN.md reading R2
-    L.prog_flux.launch(a, s);
+    a.trace = trace;
+    if (g.shard.sharded()) {
+        a.eps_int = L.eps_pad.p;
+        a.area_int = L.area_pad.p;
+        a.g_int = L.g_pad.p;
+        a.T_pad = L.xtA_loc.p;
+        L.sp_flux.launch(c, g, a, s);
+    } else {
+        a.eps_int = L.eps_int.p;
+        a.eps_ext = L.eps_ext.p;
+        a.area_int = g.d_geo.p + 6 * g.n;
+        a.g_int = L.g_int.p;
+        L.prog_flux.launch(a, s);
+    }
 }
 
 }  // namespace hm
@@ -520,18 +566,18 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
     Ctx* c = &ctx->c;
     return guarded(c, [&] {
         HLU& L = const_cast<HLU&>(LUh->h);
-        const int64_t n = L.F->geom->n;
+        const size_t cnt = (size_t)vec_rows(*L.F->geom) * nrhs;
         cudaStream_t s = (cudaStream_t)stream;
         bool hin = false;
-        const double* Td = stage_in(c, L.host_stage_in, T, (size_t)n * nrhs, s, hin);
+        const double* Td = stage_in(c, L.host_stage_in, T, cnt, s, hin);
         const bool hout = !is_device_ptr(q);
         double* qd = q;
         if (hout) {
-            if (L.host_stage_out.n < (size_t)n * nrhs) L.host_stage_out.alloc(c, (size_t)n * nrhs, "host staging (out)");
+            if (L.host_stage_out.n < cnt) L.host_stage_out.alloc(c, cnt, "host staging (out)");
             qd = L.host_stage_out.p;
         }
-        for (int col = 0; col < nrhs; ++col) launch_flux(L, Td, qd, nrhs, col, s);
-        if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        for (int col = 0; col < nrhs; ++col) launch_flux(c, L, Td, qd, nrhs, col, s);
+        if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
@@ -543,7 +589,6 @@ hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, con
     return guarded(c, [&] {
         HLU& L = const_cast<HLU&>(LUh->h);
         HMat& F = const_cast<HMat&>(Fh->h);
-        const Geom& g = *F.geom;
         cudaStream_t s = (cudaStream_t)stream;
         cudaEvent_t e0, e1;
         HM_CUDA(cudaEventCreate(&e0));
@@ -558,22 +603,27 @@ hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, con
             HM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
             return (double)ms / iters;
         };
-        ProgArgs a{};
-        a.perm = g.d_perm.p;
-        a.user_in = T;
-        a.user_out = q;
-        a.ld = 1;
-        ms_out[0] = timeit([&] { launch_flux(L, T, q, 1, 0, s); });
-        ms_out[1] = timeit([&] { F.prog_apply.launch(a, s); });
-        ms_out[2] = timeit([&] { L.prog_solve.launch(a, s); });
+        ms_out[0] = timeit([&] { launch_flux(c, L, T, q, 1, 0, s); });
+        ms_out[1] = timeit([&] { launch_apply(c, F, T, q, 1, 0, s); });
+        ms_out[2] = timeit([&] { launch_solve(c, L, T, q, 1, 0, s); });
         for (int i = 3; i < 6; ++i) ms_out[i] = 0.0;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (launches_out) {
-            launches_out[0] = launches_out[1] = launches_out[2] = 1;
-            launches_out[3] = (int64_t)L.prog_flux.h_passes.size();
-            launches_out[4] = (int64_t)L.prog_flux.h_units.size();
-            launches_out[5] = L.prog_flux.grid;
+            const bool sh = F.geom->shard.sharded();
+            launches_out[0] = sh ? (int64_t)L.sp_flux.segs.size() : 1;
+            launches_out[1] = sh ? (int64_t)F.sp_apply.segs.size() : 1;
+            launches_out[2] = sh ? (int64_t)L.sp_solve.segs.size() : 1;
+            int64_t passes = 0, units = 0;
+            if (sh) {
+                for (auto& P : L.sp_flux.segs) { passes += (int64_t)P->h_passes.size(); units += (int64_t)P->h_units.size(); }
+            } else {
+                passes = (int64_t)L.prog_flux.h_passes.size();
+                units = (int64_t)L.prog_flux.h_units.size();
+            }
+            launches_out[3] = passes;
+            launches_out[4] = units;
+            launches_out[5] = engine_grid();
         }
     });
 }
@@ -593,20 +643,8 @@ hm_status hm_trace_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, const
         for (size_t i = 0; i < np; ++i) { init[2 * i] = ~0ull; init[2 * i + 1] = 0ull; }
         if (P.trace.n < 2 * np) P.trace.alloc(c, 2 * np, "engine trace");
         HM_CUDA(cudaMemcpyAsync(P.trace.p, init.data(), 2 * np * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-        const Geom& g = *L.F->geom;
-        ProgArgs a{};
-        a.perm = g.d_perm.p;
-        a.user_in = T;
-        a.user_out = q;
-        a.ld = 1;
-        a.eps_int = L.eps_int.p;
-        a.eps_ext = L.eps_ext.p;
-    a.eps_ext = L.eps_ext.p;
-        a.area_int = g.d_geo.p + 6 * g.n;
-        a.g_int = L.g_int.p;
-        a.sigma = 5.670374419e-8;
-        a.trace = P.trace.p;
-        P.launch(a, s);
+        if (L.F->geom->shard.sharded()) throw Error(HM_ERR_UNSUPPORTED, "hm_trace_flux: world == 1 only");
+        launch_flux(c, L, T, q, 1, 0, s, P.trace.p);
         std::vector<unsigned long long> tr(2 * np);
         HM_CUDA(cudaMemcpyAsync(tr.data(), P.trace.p, 2 * np * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaStreamSynchronize(s));
@@ -642,7 +680,10 @@ hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* ou
     out->bytes_F_phase1 = 8 * F.op.p1_doubles();
     out->bytes_F_phase2 = 8 * F.op.p2_doubles();
     out->bytes_F = out->bytes_F_phase1 + out->bytes_F_phase2;
-    out->launches_apply_F = 1;  // one persistent engine launch
+    out->launches_apply_F = g.shard.sharded() ? (int64_t)F.sp_apply.segs.size() : 1;  // persistent engine launches
+    out->rank = g.shard.rank;
+    out->world = g.shard.world;
+    out->bytes_F_local = g.shard.sharded() ? 8 * (F.op_loc.p1_doubles() + F.op_loc.p2_doubles()) : out->bytes_F;
     for (int q = 0; q < 3; ++q) out->setup_seconds[q] = F.setup_seconds[q];
     out->setup_seconds[0] += g.setup_seconds;
     if (LUh) {
@@ -653,7 +694,10 @@ hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* ou
         out->n_lowrank_C = L.n_lr;
         out->rank_max_C = L.rank_max;
         out->rank_mean_C = L.n_lr ? double(L.rank_sum) / L.n_lr : 0.0;
-        out->launches_solve_C = 1;  // one persistent engine launch
+        out->launches_solve_C = g.shard.sharded() ? (int64_t)L.sp_solve.segs.size() : 1;
+        out->bytes_C_local = g.shard.sharded() ? 8 * (L.leafL_loc.p1_doubles() + L.leafL_loc.p2_doubles() +
+                                                      L.leafU_loc.p1_doubles() + L.leafU_loc.p2_doubles())
+                                               : out->bytes_C;
         for (int q = 0; q < 4; ++q) out->setup_seconds[4 + q] = L.setup_seconds[q];
     }
     return HM_OK;

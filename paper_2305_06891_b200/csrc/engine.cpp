@@ -104,10 +104,6 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
             throw Error(HM_ERR_UNSUPPORTED, "work unit exceeds the engine stage size");
     const int64_t P = (int64_t)h_passes.size();
     if (P > engine_max_passes()) throw Error(HM_ERR_UNSUPPORTED, "program has more passes than the engine's pass table");
-    {
-        const char* e = getenv("HM_PREFETCH");
-        prefetch = e && e[0] == '1';   // default off: measured slower on C2 (extra DRAM reads)
-    }
     const int64_t nn = g ? (int64_t)g->nodes.size() : 0;
     n_counters = P + 4 * nn;
     auto c_p1 = [&](int sw, int node) { return (int32_t)(P + sw * 2 * nn + node); };
@@ -152,6 +148,18 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
         else wait(sweep_dep[sw]);
         if ((kind == DEP_FWD_P2 || kind == DEP_BWD_P2) && !xonly) wait(c_p1(sw, node));
     }
+    for (size_t i = 0; i < h_tasks.size(); ++i) {   // per-chunk copies of the task's dependency record
+        const Task& t = h_tasks[i];
+        for (int64_t q = t.first_unit; q < t.first_unit + t.n_units; ++q) {
+            Unit& u = h_units[q];
+            u.task = (int64_t)i;
+            for (int j = 0; j < 2; ++j) {
+                u.wait_id[j] = t.wait_id[j];
+                u.wait_cnt[j] = t.wait_cnt[j];
+                u.inc_id[j] = t.inc_id[j];
+            }
+        }
+    }
     passes.upload(ctx, h_passes, "engine passes", s);
     units.upload(ctx, h_units, "engine units", s);
     tasks.upload(ctx, h_tasks, "engine tasks", s);
@@ -159,8 +167,6 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
     HM_CUDA(cudaMemsetAsync(done.p, 0, sizeof(unsigned long long) * std::max<int64_t>(n_counters, 1), s));
     queue.alloc(ctx, 1, "engine task queue");
     HM_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(unsigned long long), s));
-    pf.alloc(ctx, 1, "engine prefetch counter");
-    HM_CUDA(cudaMemsetAsync(pf.p, 0, sizeof(unsigned long long), s));
     grid = engine_grid();
     epoch = 0;
     ready = true;
@@ -171,7 +177,6 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
     a.passes = passes.p;
     a.n_passes = (int32_t)h_passes.size();
     a.n_x = n_x;
-    a.prefetch = prefetch ? 1 : 0;
     a.units = units.p;
     a.tasks = tasks.p;
     a.n_tasks = (int64_t)h_tasks.size();
@@ -179,9 +184,6 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
     // every CTA's producer takes exactly one index past the end: the counter advances by
     // n_tasks + grid per launch
     a.queue_base = epoch * (unsigned long long)(h_tasks.size() + grid);
-    // the prefetch warp's 32 lanes each take one index past the end per CTA
-    a.pf_counter = pf.p;
-    a.pf_base = epoch * (unsigned long long)(h_units.size() + 32ull * grid);
     a.n_units = (int64_t)h_units.size();
     a.done = done.p;
     a.epoch = ++epoch;
@@ -201,9 +203,28 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
         fprintf(stderr,
                 "[engine stats] passes %zu units %zu grid %d | per CTA (kcycles): producer wait-empty %.1f meta %.1f "
                 "chunks %.0f | gatherer(sum of warps) wait-full %.1f dep %.1f gather %.1f | consumer wait %.1f "
-                "compute %.1f task-end %.1f | retire wait %.1f work %.1f | TMA issue->land %.0f cycles (n %.0f, landed before gather done %.0f)\n",
+                "compute %.1f task-end %.1f | retire wait %.1f work %.1f | producer wait-pempty %.1f total %.1f | consumer wait-gathered %.1f\n",
                 h_passes.size(), h_units.size(), grid, h[0] / G / 1e3, h[1] / G / 1e3, h[2] / G, h[3] / G / 1e3,
-                h[4] / G / 1e3, h[5] / G / 1e3, h[6] / G / 1e3, h[7] / G / 1e3, h[8] / G / 1e3, h[9] / G / 1e3, h[10] / G / 1e3, h[12] ? (double)h[11] / h[12] : 0.0, (double)h[12], (double)h[13]);
+                h[4] / G / 1e3, h[5] / G / 1e3, h[6] / G / 1e3, h[7] / G / 1e3, h[8] / G / 1e3, h[9] / G / 1e3, h[10] / G / 1e3, h[11] / G / 1e3, h[12] / G / 1e3, h[13] / G / 1e3);
+    }
+}
+
+void SegProgram::launch(Ctx* ctx, const Geom& g, ProgArgs a, cudaStream_t s) {
+    const Shard& S = g.shard;
+    for (size_t i = 0; i < segs.size(); ++i) {
+        if (pre[i]) {
+            if (pre_user[i]) {   // this rank's slice (column a.col of the caller's n_loc x ld array)
+                const int64_t nl = S.le() - S.lb();
+                if (nl > 0)
+                    HM_CUDA(cudaMemcpy2DAsync(pre[i] + S.base(), sizeof(double), a.user_in + a.col,
+                                              sizeof(double) * (size_t)(a.ld ? a.ld : 1), sizeof(double), (size_t)nl,
+                                              cudaMemcpyDeviceToDevice, s));
+            }
+            if (!ctx->ex) throw Error(HM_ERR_NOT_READY, "sharded program without an exchanger");
+            ctx->ex->allgather(pre[i], S.maxc, s);
+            debug_sync(s, "allgather");
+        }
+        segs[i]->launch(a, s);
     }
 }
 

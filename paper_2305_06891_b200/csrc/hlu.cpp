@@ -288,7 +288,11 @@ void factor_hlu(HLU& L, const double* emissivity) {
     const int D = g.depth;
     // cut level: W-form updates for levels < Lc, then block-diagonal solves with the inverse
     // factors of the level-Lc diagonal blocks (Lc = depth: leaf inverses only)
-    const int Lc = (L.params.cut_level < 0 || L.params.cut_level > D) ? D : L.params.cut_level;
+    // cut level (reading R27): < 0 -> 0 (the default: U^-1 (L^-1 b) with the inverse factors
+    // in F's partition, fewest dependent passes, measured fastest on C2); >= depth -> pure level form
+    const int Lc = L.params.cut_level < 0 ? 0 : std::min(L.params.cut_level, D);
+    if (g.shard.sharded() && Lc != 0)
+        throw Error(HM_ERR_UNSUPPORTED, "sharded solve (world > 1) is built in the inverse-factor form: cut_level 0");
     L.cut_level = Lc;
     fz.cut = Lc;
     fz.fwd_src.assign(std::max(Lc, 0), {});
@@ -376,6 +380,10 @@ void factor_hlu(HLU& L, const double* emissivity) {
     }
     build_hop(c, g, srcL, L.leafL, s);
     build_hop(c, g, srcU, L.leafU, s);
+    if (g.shard.sharded()) {   // this rank's rows of L^-1 and U^-1 (inverse-factor form, Lc == 0)
+        build_hop(c, g, srcL, L.leafL_loc, s, &g.shard);
+        build_hop(c, g, srcU, L.leafU_loc, s, &g.shard);
+    }
     account(L, L.leafL);
     account(L, L.leafU);
     maxt = std::max({maxt, L.leafL.n_t, L.leafU.n_t});
@@ -462,6 +470,57 @@ void factor_hlu(HLU& L, const double* emissivity) {
         HM_CUDA(cudaStreamSynchronize(s));
     }
     L.setup_seconds[3] = now_seconds() - t0;
+
+    // ---- sharded hot path (world > 1): exchange steps between the engine programs
+    if (g.shard.sharded()) {
+        const Shard& S = g.shard;
+        const int64_t np = S.n_pad();
+        std::vector<double> gh(n), ep(np, 0.0), ap(np, 1.0), gp(np, 0.0);
+        HM_CUDA(cudaMemcpyAsync(gh.data(), L.g_int.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < n; ++i) {   // every segment: the gathers read all ranks' eps
+            const int64_t j = S.pad(i);
+            ep[j] = eps_int[i];
+            ap[j] = g.area[i];
+            gp[j] = gh[i];
+        }
+        L.eps_pad.upload(c, ep, "eps (padded)", s);
+        L.area_pad.upload(c, ap, "area (padded)", s);
+        L.g_pad.upload(c, gp, "g (padded)", s);
+        L.xtA_loc.alloc(c, (size_t)(np + L.leafL_loc.n_t), "solve xtA (local)");
+        L.xtB_loc.alloc(c, (size_t)(np + L.leafU_loc.n_t), "solve xtB (local)");
+        auto first_op = [&](SegProgram& SP, int in_mode) {   // allgather b (or T) -> L^-1 -> y
+            Program& P = SP.add(L.xtA_loc.p, true);
+            P.n_x = np;
+            P.add_stream(L.leafL_loc.p1, L.leafL_loc, L.xtA_loc.p, L.xtA_loc.p, OUT_ASSIGN, DEP_BARRIER, nullptr, in_mode);
+            P.add_stream(L.leafL_loc.p2, L.leafL_loc, L.xtA_loc.p, L.xtB_loc.p, OUT_ASSIGN, DEP_BARRIER, nullptr,
+                         in_mode, -1);
+        };
+        first_op(L.sp_solve, IN_PLAIN);
+        {
+            Program& P = L.sp_solve.add(L.xtB_loc.p, false);   // allgather y -> U^-1 -> z (local slice)
+            P.n_x = np;
+            P.add_stream(L.leafU_loc.p1, L.leafU_loc, L.xtB_loc.p, L.xtB_loc.p, OUT_ASSIGN);
+            P.add_stream(L.leafU_loc.p2, L.leafU_loc, L.xtB_loc.p, nullptr, OUT_LOCAL, DEP_BARRIER, nullptr, IN_PLAIN, -1);
+        }
+        L.sp_solve.finalize(c, s, &g);
+        first_op(L.sp_flux, IN_FLUXI);
+        {
+            Program& P = L.sp_flux.add(L.xtB_loc.p, false);    // allgather y -> U^-1 -> z into F's x region
+            P.n_x = np;
+            P.add_stream(L.leafU_loc.p1, L.leafU_loc, L.xtB_loc.p, L.xtB_loc.p, OUT_ASSIGN);
+            P.add_stream(L.leafU_loc.p2, L.leafU_loc, L.xtB_loc.p, Fm.xt_loc.p, OUT_ASSIGN, DEP_BARRIER, nullptr,
+                         IN_PLAIN, -1);
+        }
+        {
+            Program& P = L.sp_flux.add(Fm.xt_loc.p, false);    // allgather z -> F -> q (local slice)
+            P.n_x = np;
+            P.add_stream(F.op_loc.p1, F.op_loc, Fm.xt_loc.p, Fm.xt_loc.p, OUT_ASSIGN);
+            P.add_stream(F.op_loc.p2, F.op_loc, Fm.xt_loc.p, nullptr, OUT_FLUX_LOCAL, DEP_BARRIER, nullptr, IN_PLAIN, -1);
+        }
+        L.sp_flux.finalize(c, s, &g);
+        HM_CUDA(cudaStreamSynchronize(s));
+    }
 }
 
 }  // namespace hm

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -55,8 +56,18 @@ struct DBuf {  // owning device buffer
     void reset();
 };
 
+// The exchange step of the sharded hot path: in-place allgather of a padded vector (rank q's
+// segment at buf[q*count, (q+1)*count)), stream-ordered.  shard.cpp.
+struct Exchanger {
+    virtual ~Exchanger() = default;
+    virtual void allgather(double* buf, int64_t count, cudaStream_t s) = 0;
+    virtual const char* kind() const = 0;
+};
+
 struct Ctx {
     int device = 0, rank = 0, world = 1;
+    bool host_only = false;            // device < 0: trees / shard plan only (no CUDA)
+    Exchanger* ex = nullptr;           // world > 1 (owned)
     uint32_t flags = 0;
     cudaStream_t stream = nullptr;  // setup stream
     std::string last_error;
@@ -96,8 +107,28 @@ struct Blk {
     int rank = 0;
 };
 
+// Row-cluster shard of this rank: padded layout of G segments of maxc entries.
+struct Shard {
+    int rank = 0, world = 1;
+    int64_t maxc = 0;
+    std::vector<int64_t> rb, re;   // per-rank internal-order row ranges
+    bool sharded() const { return world > 1; }
+    int64_t lb() const { return rb[rank]; }
+    int64_t le() const { return re[rank]; }
+    int64_t n_pad() const { return (int64_t)world * maxc; }
+    int64_t base() const { return (int64_t)rank * maxc; }
+    int rank_of(int64_t i) const;
+    int64_t pad(int64_t i) const {
+        if (world == 1) return i;
+        const int q = rank_of(i);
+        return (int64_t)q * maxc + (i - rb[q]);
+    }
+    bool owns_row(int64_t i) const { return world == 1 || (i >= lb() && i < le()); }
+};
+
 struct Geom {
     Ctx* ctx;
+    Shard shard;
     int64_t n;
     hm_tree_params params;
     std::vector<int32_t> perm;  // perm[internal] = external
@@ -117,6 +148,9 @@ struct Geom {
 
 void build_trees(Geom& g, const double* xyz, const double* nrm, const double* area,
                  const double* aabb);
+void local_range(const Geom& g, int rank, int world, int64_t* begin, int64_t* end);
+void make_shard(Geom& g, int rank, int world);
+std::unique_ptr<Exchanger> make_exchanger(int device, int rank, int world, const void* comm_id, uint32_t flags);
 
 // ------------------------------------------------------------------ the two-phase stream operator
 // Both phases are "column-stream panels": a column-major matrix (column stride ld, even) whose
@@ -133,7 +167,7 @@ void build_trees(Geom& g, const double* xyz, const double* nrm, const double* ar
 // accumulates in registers and emits once.  Pieces of the same panel (only panels > 512 KB are
 // split) combine deterministically: the last-finishing piece adds the partials in piece order.
 constexpr int kMaxRuns = 16;
-struct Unit {
+struct alignas(16) Unit {
     int64_t a_off;     // arena offset of the chunk payload
     int64_t out0;      // output index of row 0 of the panel
     int64_t part_off;  // partial-sum scratch offset of this piece (nseg > 1)
@@ -154,7 +188,12 @@ struct Unit {
     int32_t nruns;
     int32_t run_src[kMaxRuns];
     uint16_t run_len[kMaxRuns];
+    // the task this chunk belongs to and its dependency record (copied from the Task at program
+    // finalisation, so the engine's chunk header is self-contained)
+    int64_t task;
+    int32_t wait_id[2], wait_cnt[2], inc_id[2];
 };
+static_assert(sizeof(Unit) % 16 == 0, "Unit is TMA-copied");
 enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2 };
 constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage
 constexpr int kUnitMaxCols = 512;
@@ -209,6 +248,7 @@ struct SrcBlock {
 
 struct HOp {
     int64_t n_rows_total = 0;     // n
+    int64_t n_x = 0;              // size of the x region of XT
     DBuf<double> arena;
     StreamPass p1, p2;
     DBuf<int32_t> colsrc;          // per-unit, 16-byte aligned column-source segments
@@ -231,8 +271,10 @@ struct HOp {
     bool empty() const { return p1.empty() && p2.empty(); }
 };
 
-// Build the operator; XT layout is [x (n) | t (n_p1)].
-void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s);
+// Build the operator; XT layout is [x (n_x) | t (n_t)].  With a shard (world > 1) only the block
+// rows of this rank are stored, x indices and phase-2 outputs use the padded layout (n_x = n_pad).
+void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s,
+               const Shard* sh = nullptr);
 
 // ------------------------------------------------------------------ persistent stream engine
 struct Pass {
@@ -253,14 +295,12 @@ struct Pass {
 struct ProgArgs {
     const Pass* passes;
     int32_t n_passes;
-    int32_t prefetch;           // 1: the L2 prefetch warp runs ahead of the task queue
+    int32_t pad0;
     const Unit* units;
     const Task* tasks;
     int64_t n_tasks;
     unsigned long long* queue;  // monotone task counter
     unsigned long long queue_base;  // counter value at the start of this launch
-    unsigned long long* pf_counter; // monotone L2-prefetch chunk counter
-    unsigned long long pf_base;
     int64_t n_units;
     unsigned long long* done;   // dependency counters (passes, then per-node), monotone over launches
     unsigned long long* trace;  // optional: per pass [first gather, last retire] (%globaltimer ns)
@@ -276,10 +316,13 @@ struct ProgArgs {
     const double* area_int;
     const double* g_int;
     double sigma;
+    int64_t local0;             // sharded: padded index of this rank's first row
+    const double* T_pad;        // sharded flux: gathered temperatures (padded internal order)
 };
 
 // input modes of a stream pass: the prologue / permute-in fused into the gather
-enum InMode : int { IN_PLAIN = 0, IN_PERM = 1, IN_FLUX = 2 };
+// IN_FLUXI (sharded flux): x-region input j is T_j (padded internal order), gathered as eps_j T_j^4
+enum InMode : int { IN_PLAIN = 0, IN_PERM = 1, IN_FLUX = 2, IN_FLUXI = 3 };
 
 // A program = passes in topological order; executes in one cooperative launch.
 struct Program {
@@ -290,12 +333,10 @@ struct Program {
     DBuf<Unit> units;
     DBuf<Task> tasks;
     DBuf<unsigned long long> queue;   // monotone task counter (epoch * n_tasks at the end of a launch)
-    DBuf<unsigned long long> pf;      // monotone L2-prefetch counter
     DBuf<unsigned long long> done;
     unsigned long long epoch = 0;
     int grid = 0;
     bool ready = false;
-    bool prefetch = true;
     int64_t n_x = 0;     // x-region size of the programs' XT buffers (fused-prologue gathers)
     std::vector<int32_t> task_kind, task_node;   // dependency kind / tree node of each task
     std::vector<uint8_t> task_xonly;             // task reads only the x region of its input
@@ -315,13 +356,34 @@ struct Program {
     void launch(ProgArgs a, cudaStream_t s);
 };
 
+// Sharded hot path (world > 1): engine programs separated by exchange steps.  Before segment i,
+// if pre[i] != nullptr: (pre_user[i]: copy the caller's local slice, column `col`, into this rank's
+// segment of pre[i]) then allgather pre[i] in place (count = maxc per rank).
+struct SegProgram {
+    std::vector<std::unique_ptr<Program>> segs;
+    std::vector<double*> pre;
+    std::vector<uint8_t> pre_user;
+    Program& add(double* exch_buf, bool user_slice) {
+        segs.emplace_back(new Program());
+        pre.push_back(exch_buf);
+        pre_user.push_back(user_slice ? 1 : 0);
+        return *segs.back();
+    }
+    bool empty() const { return segs.empty(); }
+    void finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
+        for (auto& p : segs) p->finalize(ctx, s, g);
+    }
+    void launch(Ctx* ctx, const Geom& g, ProgArgs a, cudaStream_t s);
+};
+
 size_t engine_smem_bytes();
 int engine_max_passes();
 int engine_grid();
 void engine_launch(const ProgArgs& A, int grid, cudaStream_t s);
 
 // output modes of phase 2
-enum OutMode : int { OUT_ASSIGN = 0, OUT_SUB = 1, OUT_PERM = 2, OUT_FLUX = 3 };
+// OUT_LOCAL / OUT_FLUX_LOCAL (sharded): the caller's vectors are this rank's slice in internal order
+enum OutMode : int { OUT_ASSIGN = 0, OUT_SUB = 1, OUT_PERM = 2, OUT_FLUX = 3, OUT_LOCAL = 4, OUT_FLUX_LOCAL = 5 };
 struct FluxEpi {  // OUT_FLUX: q_ext[perm[i]] = sigma * eps_i / A_i * (acc - eta_i g_i)
     const double* T_ext;
     const int32_t* perm;
@@ -347,6 +409,10 @@ struct HMat {
     DBuf<double> y;    // internal-order output
     DBuf<double> host_stage_in, host_stage_out;
     Program prog_apply;   // permute-in -> F phase 1 -> F phase 2 (+ permute-out)
+    // sharded hot path (world > 1): this rank's block rows, padded vectors
+    HOp op_loc;
+    DBuf<double> xt_loc;  // [x_pad | t]
+    SegProgram sp_apply;  // allgather x -> phase 1 -> phase 2
 };
 
 struct HLU {
@@ -366,6 +432,12 @@ struct HLU {
     int rank_max = 0;
     Program prog_solve;   // permute-in -> forward levels -> leaf L^-1 -> backward levels -> leaf U^-1
     Program prog_flux;    // prologue -> solve passes -> F phase 1 -> F phase 2 + flux epilogue
+    // sharded hot path (world > 1, inverse-factor form): this rank's rows of L^-1, U^-1
+    HOp leafL_loc, leafU_loc;
+    DBuf<double> xtA_loc, xtB_loc;
+    DBuf<double> eps_pad, area_pad, g_pad;
+    SegProgram sp_solve;  // AG b -> L^-1 -> AG y -> U^-1
+    SegProgram sp_flux;   // AG T -> L^-1 (w = eps T^4 fused) -> AG y -> U^-1 -> AG z -> F + flux epilogue
 };
 
 // ------------------------------------------------------------------ kernel launchers (kernels_*.cu)
@@ -407,6 +479,14 @@ void cpaca_batch(double* T, int64_t ldt, const int64_t* blk /*[nb][6] i0,m,j0,n,
 }  // namespace k
 
 double now_seconds();
+
+// hot-path launches for one column (api.cpp): world == 1 -> one engine program; sharded -> the
+// segmented program with its exchange steps
+int64_t vec_rows(const Geom& g);
+void launch_apply(Ctx* c, HMat& F, const double* xd, double* yd, int ld, int col, cudaStream_t s);
+void launch_solve(Ctx* c, HLU& L, const double* bd, double* zd, int ld, int col, cudaStream_t s);
+void launch_flux(Ctx* c, HLU& L, const double* Td, double* qd, int ld, int col, cudaStream_t s,
+                 unsigned long long* trace = nullptr);
 
 }  // namespace hm
 

@@ -136,8 +136,15 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
     HM_CUDA(cudaMemsetAsync(P.counters.p, 0, sizeof(int32_t) * std::max<int32_t>(grp, 1), s));
 }
 
-void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s) {
+void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s, const Shard* sh) {
     const int64_t n = g.n;
+    // sharded: only blocks with rows on this rank; x indices and outputs in the
+    // padded layout (x region of XT = n_pad), t after it
+    const bool shd = sh && sh->sharded();
+    const int64_t nx = shd ? sh->n_pad() : n;
+    auto xi = [&](int64_t i) -> int32_t { return (int32_t)(shd ? sh->pad(i) : i); };
+    auto mine = [&](const SrcBlock& B) { return !shd || (B.r0 < sh->le() && B.r0 + B.m > sh->lb()); };
+    op.n_x = nx;
     const int nleaves = (int)g.leaves.size();
     op.n_rows_total = n;
     op.items.clear();
@@ -157,6 +164,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     std::vector<std::vector<int>> taus;
     for (size_t b = 0; b < blocks.size(); ++b) {
         const SrcBlock& B = blocks[b];
+        if (!mine(B)) continue;
         if (B.kind != KIND_LR) { ++op.n_dense; continue; }
         ++op.n_lr;
         op.rank_sum += B.k;
@@ -179,9 +187,9 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
             while (q1 < members.size() && K + blocks[members[q1]].k <= 128) K += blocks[members[q1++]].k;
             const SrcBlock& B0 = blocks[members[q0]];
             const int64_t ld = align2(K);
-            Panel pn{off, n + tcount, (int32_t)ld, (int32_t)K, (int32_t)B0.n, (int32_t)colsrc.size(), B0.c0,
+            Panel pn{off, nx + tcount, (int32_t)ld, (int32_t)K, (int32_t)B0.n, (int32_t)colsrc.size(), B0.c0,
                      (int32_t)B0.n};
-            for (int64_t j = 0; j < B0.n; ++j) colsrc.push_back((int32_t)(B0.c0 + j));
+            for (int64_t j = 0; j < B0.n; ++j) colsrc.push_back(xi(B0.c0 + j));
             int64_t local = 0;
             for (size_t q = q0; q < q1; ++q) {
                 const int b = members[q];
@@ -213,9 +221,10 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     for (int l = 0; l < nleaves; ++l) {
         if (items[l].empty()) continue;
         const Node& L = g.nodes[g.leaves[l]];
+        if (shd && !(L.begin >= sh->lb() && L.end <= sh->le())) continue;   // another rank's leaf row
         for (int64_t rc = L.begin; rc < L.end; rc += 128) {   // row chunks of <= 128
             const int64_t lr0 = rc, lm = std::min<int64_t>(128, L.end - rc), ld = align2(lm);
-            Panel pn{off, lr0, (int32_t)ld, (int32_t)lm, 0, (int32_t)colsrc.size(), lr0, 0};
+            Panel pn{off, xi(lr0), (int32_t)ld, (int32_t)lm, 0, (int32_t)colsrc.size(), lr0, 0};
             // dense blocks first (they read only x), then the U factors (they read t)
             std::vector<int> order;
             for (int b : items[l]) if (blocks[b].kind != KIND_LR) order.push_back(b);
@@ -230,14 +239,14 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
                         fill.insert(fill.end(), {off, lr0, lm, B.c0, B.n, ld});
                     else
                         pack.insert(pack.end(), {off, (int64_t)(uintptr_t)(B.dense + ro * B.d_rs), lm, B.n, B.d_rs, B.d_cs, ld});
-                    for (int64_t j = 0; j < B.n; ++j) colsrc.push_back((int32_t)(B.c0 + j));
+                    for (int64_t j = 0; j < B.n; ++j) colsrc.push_back(xi(B.c0 + j));
                     op.items.push_back(HOp::ItemRec{off, ld, -1, 0, lr0, lm, B.c0, B.n, 0});
                     off += ld * B.n;
                     pn.ncols += (int32_t)B.n;
                     op.p2.doubles += lm * B.n;
                 } else {
                     pack.insert(pack.end(), {off, (int64_t)(uintptr_t)(B.U + ro), lm, (int64_t)B.k, 1, B.u_ld, ld});
-                    for (int q = 0; q < B.k; ++q) colsrc.push_back((int32_t)(n + tbase[b] + q));
+                    for (int q = 0; q < B.k; ++q) colsrc.push_back((int32_t)(nx + tbase[b] + q));
                     op.items.push_back(HOp::ItemRec{off, ld, voff[b], vld[b], lr0, lm, B.c0, B.n, B.k});
                     off += ld * B.k;
                     pn.ncols += B.k;
@@ -247,7 +256,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
             op.p2.panels.push_back(pn);
         }
     }
-    if ((int64_t)n + tcount >= INT32_MAX || (int64_t)colsrc.size() >= INT32_MAX)
+    if (nx + tcount >= INT32_MAX || (int64_t)colsrc.size() >= INT32_MAX)
         throw Error(HM_ERR_UNSUPPORTED, "index space exceeds int32");
 
     op.arena.alloc(ctx, (size_t)std::max<int64_t>(off, 2), "operator arena");
@@ -258,9 +267,11 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     op.colsrc.upload(ctx, ucs, "colsrc", s);
     // the same column sources for passes that gather straight from the caller's external-order
     // vector (fused prologue): x-region index j becomes -(perm[j] + 1)
-    for (int32_t& j : ucs)
-        if (j < n) j = -(g.perm[j] + 1);
-    op.colsrc_ext.upload(ctx, ucs, "colsrc (external)", s);
+    if (!shd) {
+        for (int32_t& j : ucs)
+            if (j < n) j = -(g.perm[j] + 1);
+        op.colsrc_ext.upload(ctx, ucs, "colsrc (external)", s);
+    }
     DBuf<int64_t> d_pack, d_fill;
     d_pack.upload(ctx, pack, "pack tasks", s);
     d_fill.upload(ctx, fill, "fill tasks", s);

@@ -29,35 +29,35 @@ namespace hm {
 namespace {
 
 // warp roles
-constexpr int kGatherers = 5;                       // warps 1..5 (gatherer w owns stage w-1)
-constexpr int kConsumerWarps = 8;                   // warps 6..13
+constexpr int kGatherers = 4;                       // warps 1..4 (gatherer w owns header slots k = w-1 mod 4)
+constexpr int kConsumerWarps = 8;                   // warps 5..12
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kConsumer0 = 32 * (1 + kGatherers);
-constexpr int kRetireWarp = 1 + kGatherers + kConsumerWarps;   // warps 14..15
+constexpr int kRetireWarp = 1 + kGatherers + kConsumerWarps;   // warps 13..14
 constexpr int kRetireWarps = 2;
-constexpr int kPrefetchWarp = kRetireWarp + kRetireWarps;     // warp 16
-constexpr int kThreads = 32 * (kPrefetchWarp + 1);            // 544
-constexpr int64_t kPrefetchWindow = 1536;   // chunks (~48 MB) ahead of the task-queue frontier
-constexpr int kStages = 5;         // multiple of kGatherers
+constexpr int kThreads = 32 * (kRetireWarp + kRetireWarps);  // 480
+
+// Two rings: payload stages (TMA of the factor bytes) and header/gather slots (chunk descriptor +
+// gathered inputs).  The producer posts a chunk's header kLookahead chunks before it issues its
+// payload, so the input gather (an L2 round trip) is finished by the time the payload lands.
+constexpr int kPStages = 4;
+constexpr int kGSlots = 12;
+constexpr int kLookahead = kGSlots - kPStages;
 constexpr int kRetireSlots = 4;    // task-end handoff buffers (consumers -> retire warps)
 constexpr int kMaxCols = 512;      // per chunk; payload <= 32 KB
 constexpr int kMaxPasses = 96;     // pass table held in shared memory
-static_assert(kStages % kGatherers == 0, "stage ownership");
+static_assert(kGSlots % kGatherers == 0, "slot ownership");
 
-struct __align__(16) Stage {
+struct __align__(16) PStage {
     double payload[kUnitPayloadDoubles];
-    double xs[kMaxCols];
-    int32_t cs[kMaxCols];
 };
 
-// Per-stage header written by the producer: everything the gatherers and consumers need about the
-// chunk in flight, so that no role issues a dependent global-memory load per chunk.
-struct StageHdr {
-    Unit u;            // the chunk's descriptor (u.type < 0: end-of-work marker)
-    int64_t task;      // task index
-    int32_t wait_id[2], wait_cnt[2], inc_id[2];
-    int32_t pad[2];
-    long long t_issue;  // stats only: clock64 at TMA issue
+// Header/gather slot: the chunk's descriptor (TMA-copied by the producer: everything the gatherers
+// and consumers need, so that no role issues a dependent global-memory load per chunk) and the
+// gathered inputs.  hdr.type < 0: end-of-work marker.
+struct __align__(16) GSlot {
+    Unit hdr;
+    double xs[kMaxCols];
 };
 
 // Task-end handoff: the consumers deposit their per-thread partial sums and the task's descriptor,
@@ -73,11 +73,12 @@ struct RetireSlot {
 };
 
 struct EngineSmem {
-    Stage st[kStages];
-    StageHdr hdr[kStages];
+    PStage st[kPStages];
+    GSlot gs[kGSlots];
     Pass passes[kMaxPasses];   // the program's pass table, copied once per launch
     RetireSlot rs[kRetireSlots];
-    unsigned long long csfull[kStages], full[kStages], gathered[kStages], empty[kStages];
+    unsigned long long gready[kGSlots], gathered[kGSlots], gempty[kGSlots];
+    unsigned long long full[kPStages], pempty[kPStages];
     unsigned long long rfull[kRetireSlots], rempty[kRetireSlots];
 };
 
@@ -116,9 +117,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(smem_u32(b))
         : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 // split-K arrival: release this thread's (and, cumulatively, its warp's) partial-sum writes,
 // acquire the other pieces' when last
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
@@ -146,6 +144,13 @@ __device__ __forceinline__ void emit(const ProgArgs& A, const Pass& P, int64_t r
         case OUT_ASSIGN: P.out[row] = s; break;
         case OUT_SUB: P.out[row] = __ldcg(P.out + row) - s; break;
         case OUT_PERM: A.user_out[(int64_t)A.perm[row] * A.ld + A.col] = s; break;
+        case OUT_LOCAL: A.user_out[(row - A.local0) * A.ld + A.col] = s; break;
+        case OUT_FLUX_LOCAL: {
+            const double eta = pow4(__ldcg(A.T_pad + row));
+            A.user_out[(row - A.local0) * A.ld + A.col] =
+                A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row]);
+            break;
+        }
         default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form)
             const int64_t e = A.perm[row];
             const double eta = pow4(A.user_in[e * A.ld + A.col]);
@@ -173,11 +178,14 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&S.csfull[s], 1);
-            mbar_init(&S.full[s], 1);
-            mbar_init(&S.gathered[s], 1);
-            mbar_init(&S.empty[s], kConsumerWarps);
+        for (int g = 0; g < kGSlots; ++g) {
+            mbar_init(&S.gready[g], 1);
+            mbar_init(&S.gathered[g], 1);
+            mbar_init(&S.gempty[g], kConsumerWarps);
+        }
+        for (int p = 0; p < kPStages; ++p) {
+            mbar_init(&S.full[p], 1);
+            mbar_init(&S.pempty[p], kConsumerWarps);
         }
         for (int r = 0; r < kRetireSlots; ++r) {
             mbar_init(&S.rfull[r], kConsumerWarps);
@@ -189,165 +197,172 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
     __syncthreads();
 
     if (warp == 0) {
-        // ------------------------------------------------ producer warp: grab tasks, TMA their chunks.
-        // The next task index is requested while the current task streams, and the unit descriptors
-        // of a task are loaded 32 at a time (one per lane), so the TMA issue loop never waits on a
-        // dependent global load.
-        unsigned long long nxt = 0, st_empty = 0, st_meta = 0, st_chunks = 0;
-        if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - A.queue_base;
-        nxt = __shfl_sync(0xffffffffu, nxt, 0);
-        int64_t k = 0;
-        while (true) {
-            const unsigned long long t = nxt;
-            const bool end = t >= (unsigned long long)A.n_tasks;
-            Task task{};
+        // ------------------------------------------------ producer (one thread): grab tasks; per chunk,
+        // TMA its descriptor into a header slot (the gather starts when it lands) and, kLookahead chunks
+        // behind, TMA its payload.  The next task index (atomic) and its Task record are requested one
+        // task ahead, so the issue loop never waits on a global load.
+        if (lane != 0) return;
+        unsigned long long st_empty = 0, st_meta = 0, st_chunks = 0, st_pempty = 0;
+        const long long t_start = clock64();
+        int64_t k = 0;     // headers posted
+        int64_t kp = 0;    // payloads issued
+        auto issue_payload = [&]() {
+            const int p = (int)(kp % kPStages);
+            const int g = (int)(kp % kGSlots);
             long long c0 = clock64();
-            if (!end) {
-                task = A.tasks[t];
-                if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - A.queue_base;
+            mbar_wait(&S.gready[g], (uint32_t)((kp / kGSlots) & 1));   // its descriptor has landed
+            if (kp >= kPStages) mbar_wait(&S.pempty[p], (uint32_t)(((kp / kPStages) - 1) & 1));
+            st_pempty += clock64() - c0;
+            const Unit& u = S.gs[g].hdr;
+            if (u.type == UNIT_STREAM) {
+                const uint32_t pb = (uint32_t)u.ncols * (uint32_t)u.ld * 8u;
+                mbar_expect_tx(&S.full[p], pb);
+                tma_load_1d(S.st[p].payload, S.passes[u.pass].arena + u.a_off, pb, &S.full[p]);
+            } else {
+                mbar_arrive(&S.full[p]);
             }
-            // end of work: one marker per gatherer warp (each owns its own stages)
-            const int nch = end ? kGatherers : task.n_units;
-            for (int base = 0; base < nch; base += 32) {
-                Unit mine{};
-                if (!end && base + lane < nch) mine = A.units[task.first_unit + base + lane];
-                __syncwarp();
-                st_meta += clock64() - c0;
-                const int cnt = min(32, nch - base);
-                for (int c = 0; c < cnt; ++c, ++k) {
-                    const int s = (int)(k % kStages);
-                    c0 = clock64();
-                    if (k >= kStages && lane == 0) mbar_wait(&S.empty[s], (uint32_t)(((k / kStages) - 1) & 1));
-                    __syncwarp();
-                    st_empty += clock64() - c0;
-                    ++st_chunks;
-                    StageHdr& H = S.hdr[s];
-                    if (lane == c) {
-                        if (end) {
-                            H.u.type = -1;
-                        } else {
-                            H.u = mine;
-                            H.task = (int64_t)t;
-                            H.wait_id[0] = task.wait_id[0]; H.wait_id[1] = task.wait_id[1];
-                            H.wait_cnt[0] = task.wait_cnt[0]; H.wait_cnt[1] = task.wait_cnt[1];
-                            H.inc_id[0] = task.inc_id[0]; H.inc_id[1] = task.inc_id[1];
-                            if (mine.type == UNIT_STREAM) {
-                                const Pass& P = S.passes[mine.pass];
-                                const uint32_t pb = (uint32_t)mine.ncols * (uint32_t)mine.ld * 8u;
-                                const uint32_t cb = (((uint32_t)mine.ncols + 3u) & ~3u) * 4u;
-                                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                                // column sources first, on their own barrier: the gather overlaps the
-                                // payload's flight (run-encoded chunks need no column-source copy)
-                                if (mine.nruns > 0 && P.in_mode == IN_PLAIN) {
-                                    mbar_arrive(&S.csfull[s]);
-                                } else {
-                                    mbar_expect_tx(&S.csfull[s], cb);
-                                    tma_load_1d(S.st[s].cs, P.colsrc + mine.cs_off, cb, &S.csfull[s]);
-                                }
-                                if (A.stats) H.t_issue = clock64();
-                                mbar_expect_tx(&S.full[s], pb);
-                                tma_load_1d(S.st[s].payload, P.arena + mine.a_off, pb, &S.full[s]);
-                            } else {
-                                mbar_arrive(&S.csfull[s]);
-                                mbar_arrive(&S.full[s]);
-                            }
-                        }
-                        if (end) {
-                            mbar_arrive(&S.csfull[s]);
-                            mbar_arrive(&S.full[s]);
-                        }
-                    }
-                }
-                nxt = __shfl_sync(0xffffffffu, nxt, 0);
-                c0 = clock64();
-            }
-            if (end) break;
+            ++kp;
+        };
+        auto wait_slot = [&](int64_t kk) {
+            const int g = (int)(kk % kGSlots);
+            long long c0 = clock64();
+            if (kk >= kGSlots) mbar_wait(&S.gempty[g], (uint32_t)(((kk / kGSlots) - 1) & 1));
+            st_empty += clock64() - c0;
+            return g;
+        };
+        unsigned long long t = atomicAdd(A.queue, 1ull) - A.queue_base;
+        bool have_t = t < (unsigned long long)A.n_tasks;
+        unsigned long long tn = ~0ull;   // pending grab of the next task index
+        Task task{};
+        if (have_t) {
+            tn = atomicAdd(A.queue, 1ull) - A.queue_base;
+            task = A.tasks[t];
         }
-        if (A.stats && lane == 0) {
+        while (have_t) {
+            long long c0 = clock64();
+            const bool have_n = tn < (unsigned long long)A.n_tasks;
+            Task task_n{};
+            unsigned long long tnn = ~0ull;
+            if (have_n) {
+                task_n = A.tasks[tn];
+                tnn = atomicAdd(A.queue, 1ull) - A.queue_base;
+            }
+            st_meta += clock64() - c0;
+            const int nch = task.n_units;
+            for (int c = 0; c < nch; ++c) {
+                const int g = wait_slot(k);
+                ++st_chunks;
+                mbar_expect_tx(&S.gready[g], (uint32_t)sizeof(Unit));
+                tma_load_1d(&S.gs[g].hdr, A.units + task.first_unit + c, (uint32_t)sizeof(Unit), &S.gready[g]);
+                ++k;
+                if (k - kp > kLookahead) issue_payload();
+            }
+            t = tn;
+            tn = tnn;
+            task = task_n;
+            have_t = have_n;
+        }
+        while (kp < k) issue_payload();
+        // end of work: one marker per gatherer warp (each owns its own slots); no payload
+        for (int c = 0; c < kGatherers; ++c) {
+            const int g = wait_slot(k);
+            S.gs[g].hdr.type = -1;
+            mbar_arrive(&S.gready[g]);
+            ++k;
+        }
+        if (A.stats) {
             atomicAdd(A.stats + 0, st_empty);
             atomicAdd(A.stats + 1, st_meta);
             atomicAdd(A.stats + 2, st_chunks);
-        }
-        return;
-    }
-    if (warp == kPrefetchWarp) {
-        // ------------------------------------------------ L2 prefetcher: stream the program's chunks into
-        // L2 in program order, at most kPrefetchWindow chunks ahead of the task-queue frontier, so HBM
-        // stays busy while tasks wait on their dependencies
-        if (!A.prefetch) return;
-        while (true) {
-            const unsigned long long p = atomicAdd(A.pf_counter, 1ull) - A.pf_base;
-            if (p >= (unsigned long long)A.n_units) break;
-            unsigned ns = 64;
-            while (true) {
-                unsigned long long q;
-                asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(q) : "l"(A.queue) : "memory");
-                q -= A.queue_base;
-                const int64_t frontier = q < (unsigned long long)A.n_tasks ? A.tasks[q].first_unit : A.n_units;
-                if ((int64_t)p < frontier + kPrefetchWindow) break;
-                __nanosleep(ns);
-                if (ns < 1024) ns <<= 1;
-            }
-            const Unit& u = A.units[p];
-            if (u.type == UNIT_STREAM) {
-                const Pass& P = S.passes[u.pass];
-                prefetch_l2(P.arena + u.a_off, (uint32_t)u.ncols * (uint32_t)u.ld * 8u);
-            }
+            atomicAdd(A.stats + 11, st_pempty);
+            atomicAdd(A.stats + 12, (unsigned long long)(clock64() - t_start));
         }
         return;
     }
     if (warp >= 1 && warp <= kGatherers) {
-        // ------------------------------------------------ gatherers: warp w owns stages s = w-1 (mod kGatherers)
+        // ------------------------------------------------ gatherers: warp w owns header slots k = w-1 (mod kGatherers)
         int64_t verified = -1;  // last task whose waits this warp has checked
-        unsigned long long st_full = 0, st_dep = 0, st_gather = 0, st_lat = 0, st_nlat = 0, st_early = 0;
+        int sat_id[2] = {-1, -1};                 // recently satisfied counters (lane 0)
+        unsigned long long sat_tgt[2] = {0, 0};
+        unsigned long long st_full = 0, st_dep = 0, st_gather = 0;
         for (int64_t k = warp - 1;; k += kGatherers) {
-            const int s = (int)(k % kStages);
+            const int s = (int)(k % kGSlots);
             long long c0 = clock64();
-            mbar_wait(&S.csfull[s], (uint32_t)((k / kStages) & 1));
+            mbar_wait(&S.gready[s], (uint32_t)((k / kGSlots) & 1));
             long long c1 = clock64();
             st_full += c1 - c0;
-            const StageHdr& H = S.hdr[s];
-            const int type = H.u.type;
+            const Unit& H = S.gs[s].hdr;
+            const int type = H.type;
             if (type >= 0) {
                 const int64_t ti = H.task;
                 if (ti != verified) {
+                    // dependency waits (acquire); counters only grow, so a (counter, target) pair
+                    // already seen satisfied by this warp is not polled again
                     if (lane == 0) {
-                        if (H.wait_id[0] >= 0) wait_counter(A, H.wait_id[0], H.wait_cnt[0]);
-                        if (H.wait_id[1] >= 0) wait_counter(A, H.wait_id[1], H.wait_cnt[1]);
-                        if (A.trace && H.u.chunk == 0) atomicMin(A.trace + 2 * H.u.pass, gtimer());
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const int id = H.wait_id[q];
+                            if (id < 0) continue;
+                            const unsigned long long tgt = A.epoch * (unsigned long long)H.wait_cnt[q];
+                            if (id == sat_id[0] && tgt <= sat_tgt[0]) continue;
+                            if (id == sat_id[1] && tgt <= sat_tgt[1]) continue;
+                            wait_counter(A, id, H.wait_cnt[q]);
+                            sat_id[1] = sat_id[0]; sat_tgt[1] = sat_tgt[0];
+                            sat_id[0] = id; sat_tgt[0] = tgt;
+                        }
+                        if (A.trace && H.chunk == 0) atomicMin(A.trace + 2 * H.pass, gtimer());
                     }
                     __syncwarp();
-                    __threadfence();
                     verified = ti;
                 }
                 c0 = clock64();
                 st_dep += c0 - c1;
                 if (type == UNIT_STREAM) {
-                    const Pass& P = S.passes[H.u.pass];
+                    const Pass& P = S.passes[H.pass];
                     const double* in = P.in ? P.in : A.user_in;
-                    const int32_t* cs = S.st[s].cs;
-                    const int ncols = H.u.ncols;
+                    const int32_t* cs = P.colsrc + H.cs_off;   // global (static): chunks without runs
+                    const int ncols = H.ncols;
                     const int im = P.in_mode;
                     constexpr int kPer = kMaxCols / 32;
                     double v[kPer];
-                    if (im == IN_PLAIN && H.u.nruns > 0) {
-                        // run-encoded column sources: lane's columns c = lane + 32 q are increasing
-                        const int nr = H.u.nruns;
-                        int r = 0, rs = 0;
+                    if ((im == IN_PLAIN || im == IN_FLUXI) && H.nruns > 0) {
+                        // run-encoded column sources: lane's columns c = lane + 32 q are increasing, so
+                        // its run index only moves forward
+                        const int nr = H.nruns;
+                        int r = 0, rs = 0, rl = H.run_len[0];
+                        int32_t rsrc = H.run_src[0];
                         int32_t idx[kPer];
 #pragma unroll
                         for (int q = 0; q < kPer; ++q) {
                             const int c = lane + 32 * q;
-                            while (r < nr - 1 && c >= rs + (int)H.u.run_len[r]) { rs += H.u.run_len[r]; ++r; }
-                            idx[q] = c < ncols ? H.u.run_src[r] + (c - rs) : -1;
+                            while (r < nr - 1 && c >= rs + rl) {
+                                rs += rl;
+                                ++r;
+                                rl = H.run_len[r];
+                                rsrc = H.run_src[r];
+                            }
+                            idx[q] = c < ncols ? rsrc + (c - rs) : -1;
                         }
 #pragma unroll
                         for (int q = 0; q < kPer; ++q) v[q] = idx[q] >= 0 ? __ldcg(in + idx[q]) : 0.0;
-                    } else if (im == IN_PLAIN) {
+                        if (im == IN_FLUXI) {   // sharded flux prologue: w_j = eps_j T_j^4 (x region)
+#pragma unroll
+                            for (int q = 0; q < kPer; ++q)
+                                if (idx[q] >= 0 && idx[q] < A.n_x) v[q] = __ldg(A.eps_int + idx[q]) * pow4(v[q]);
+                        }
+                    } else if (im == IN_PLAIN || im == IN_FLUXI) {
+                        int32_t idx[kPer];
 #pragma unroll
                         for (int q = 0; q < kPer; ++q) {
                             const int c = lane + 32 * q;
-                            v[q] = c < ncols ? __ldcg(in + cs[c]) : 0.0;
+                            idx[q] = c < ncols ? __ldg(cs + c) : -1;
+                        }
+#pragma unroll
+                        for (int q = 0; q < kPer; ++q) v[q] = idx[q] >= 0 ? __ldcg(in + idx[q]) : 0.0;
+                        if (im == IN_FLUXI) {
+#pragma unroll
+                            for (int q = 0; q < kPer; ++q)
+                                if (idx[q] >= 0 && idx[q] < A.n_x) v[q] = __ldg(A.eps_int + idx[q]) * pow4(v[q]);
                         }
                     } else {
                         // fused prologue: x-region inputs come straight from the caller's external-order
@@ -356,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
 #pragma unroll
                         for (int q = 0; q < kPer; ++q) {
                             const int c = lane + 32 * q;
-                            const int32_t j = c < ncols ? cs[c] : 0;
+                            const int32_t j = c < ncols ? __ldg(cs + c) : 0;
                             if (c >= ncols) {
                                 v[q] = 0.0;
                             } else if (j >= 0) {
@@ -371,19 +386,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
 #pragma unroll
                     for (int q = 0; q < kPer; ++q) {
                         const int c = lane + 32 * q;
-                        if (c < ncols) S.st[s].xs[c] = v[q];
+                        if (c < ncols) S.gs[s].xs[c] = v[q];
                     }
                 }
             }
             __syncwarp();
             if (type >= 0) st_gather += clock64() - c0;
-            if (A.stats && type == UNIT_STREAM) {   // landing probe: issue -> payload complete
-                const long long ti = H.t_issue;
-                const bool pending = !mbar_test(&S.full[s], (uint32_t)((k / kStages) & 1));
-                mbar_wait(&S.full[s], (uint32_t)((k / kStages) & 1));
-                if (pending) { st_lat += clock64() - ti; ++st_nlat; }
-                else ++st_early;
-            }
             if (lane == 0) mbar_arrive(&S.gathered[s]);
             if (type < 0) break;
         }
@@ -391,9 +399,6 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             atomicAdd(A.stats + 3, st_full);
             atomicAdd(A.stats + 4, st_dep);
             atomicAdd(A.stats + 5, st_gather);
-            atomicAdd(A.stats + 11, st_lat);
-            atomicAdd(A.stats + 12, st_nlat);
-            atomicAdd(A.stats + 13, st_early);
         }
         return;
     }
@@ -497,21 +502,24 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
     // registers; at the task's last chunk hand the per-thread partials to the retire warp
     const int ct = tid - kConsumer0;
     double2 acc = make_double2(0.0, 0.0), acc2 = acc;
-    unsigned long long st_wait = 0, st_comp = 0, st_task = 0;
+    unsigned long long st_wait = 0, st_comp = 0, st_task = 0, st_wg = 0;
     int64_t ntask = 0;
     long long c0 = clock64();
     for (int64_t k = 0;; ++k) {
-        const int s = (int)(k % kStages);
-        mbar_wait(&S.gathered[s], (uint32_t)((k / kStages) & 1));
-        mbar_wait(&S.full[s], (uint32_t)((k / kStages) & 1));
+        const int gsl = (int)(k % kGSlots);
+        const int s = (int)(k % kPStages);
+        mbar_wait(&S.gathered[gsl], (uint32_t)((k / kGSlots) & 1));
+        const long long cg = clock64();
+        st_wg += cg - c0;
+        const Unit& H = S.gs[gsl].hdr;
+        struct { int32_t type, pass, nrows, ld, ncols, chunk, nchunks, grp, nseg, seg; int64_t out0, part_off; } u;
+        u.type = H.type; u.pass = H.pass; u.nrows = H.nrows; u.ld = H.ld; u.ncols = H.ncols;
+        u.chunk = H.chunk; u.nchunks = H.nchunks; u.out0 = H.out0;
+        u.grp = H.grp; u.nseg = H.nseg; u.seg = H.seg; u.part_off = H.part_off;
+        const int32_t inc0 = H.inc_id[0], inc1 = H.inc_id[1];
+        if (u.type >= 0) mbar_wait(&S.full[s], (uint32_t)((k / kPStages) & 1));
         long long c1 = clock64();
         st_wait += c1 - c0;
-        const StageHdr& H = S.hdr[s];
-        struct { int32_t type, pass, nrows, ld, ncols, chunk, nchunks, grp, nseg, seg; int64_t out0, part_off; } u;
-        u.type = H.u.type; u.pass = H.u.pass; u.nrows = H.u.nrows; u.ld = H.u.ld; u.ncols = H.u.ncols;
-        u.chunk = H.u.chunk; u.nchunks = H.u.nchunks; u.out0 = H.u.out0;
-        u.grp = H.u.grp; u.nseg = H.u.nseg; u.seg = H.u.seg; u.part_off = H.u.part_off;
-        const int32_t inc0 = H.inc_id[0], inc1 = H.inc_id[1];
         if (u.type < 0) {   // end of work: one marker per retire warp
             for (int w = 0; w < kRetireWarps; ++w, ++ntask) {
                 const int r = (int)(ntask % kRetireSlots);
@@ -531,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             if (u.chunk == 0) acc = acc2 = make_double2(0.0, 0.0);
             if (g < G) {
                 const double2* a = reinterpret_cast<const double2*>(S.st[s].payload) + p;
-                const double* xs = S.st[s].xs;
+                const double* xs = S.gs[gsl].xs;
                 const int ld2 = u.ld >> 1;
                 const int nc = u.ncols;
                 int c = g;
@@ -562,9 +570,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                 P.out[row] = u.type == UNIT_PROLOGUE ? A.eps_int[row] * pow4(v) : v;
             }
         }
-        // stage consumed: release it to the producer (per warp, no CTA-wide barrier)
+        // chunk consumed: release its payload stage and header slot (per warp, no CTA-wide barrier)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[s]);
+        if (lane == 0) {
+            mbar_arrive(&S.pempty[s]);
+            mbar_arrive(&S.gempty[gsl]);
+        }
         c0 = clock64();
         st_comp += c0 - c1;
         if (u.chunk != u.nchunks - 1) continue;
@@ -589,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
         atomicAdd(A.stats + 6, st_wait);
         atomicAdd(A.stats + 7, st_comp);
         atomicAdd(A.stats + 8, st_task);
+        atomicAdd(A.stats + 13, st_wg);
     }
 }
 

@@ -6,12 +6,14 @@ timeout 200 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 tail -3 gpurun_out/smoke.log
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
 tail -15 gpurun_out/pytest_gpu.log
-timeout 400 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
 cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?
+cat gpurun_out/bench_ref.json
 if [ "${NCU:-1}" = 1 ]; then
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --profile-iters 2 > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
-timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:engine_kernel -c 2 \
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-level-form --profile-iters 2 > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
+timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:engine_kernel -c 1 \
   -o gpurun_out/prof_engine -f python scripts/prof_step.py --steps 1 > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
 tail -3 gpurun_out/ncu_full.log
 fi

@@ -15,7 +15,7 @@ def main(cfg_id=2):
     ctx = hm.hm_init(0)
     g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
     F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
-    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=int(os.environ.get('CUT', '-1')))
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=int(os.environ.get('CUT', '0')))
     T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
     q = torch.empty_like(T)
     for _ in range(5):

@@ -77,6 +77,52 @@ __global__ void tma_ring(const char* __restrict__ a, int64_t nchunks, int chunk,
     if (acc == 123.456) out[0] = acc;
 }
 
+// ring with (a) chunk byte offset `off` (16-B aligned, not 128-B), (b) permuted chunk order,
+// (c) a gather step: after the payload lands the consumer warps first load `ng` x values from an
+// L2-resident vector through the indices stored in the chunk's first bytes (like the engine)
+__global__ void tma_ring2(const char* __restrict__ a, int64_t nchunks, int chunk, int stages, int off,
+                          const int64_t* __restrict__ order, const double* __restrict__ xv, int ng, double* out) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    unsigned long long* full = (unsigned long long*)sm;
+    unsigned long long* empty = full + 32;
+    char* buf = (char*)(sm + 1024);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int CW = (blockDim.x >> 5) - 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, CW); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            int64_t k = 0;
+            for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++k) {
+                const int s = (int)(k % stages);
+                if (k >= stages) mbar_wait(empty + s, (uint32_t)(((k / stages) - 1) & 1));
+                mbar_expect_tx(full + s, chunk);
+                const int64_t cc = order ? order[c] : c;
+                tma_load_1d(buf + (size_t)s * chunk, a + cc * (chunk + off), chunk, full + s);
+            }
+        }
+        return;
+    }
+    double acc = 0;
+    int64_t k = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++k) {
+        const int s = (int)(k % stages);
+        mbar_wait(full + s, (uint32_t)((k / stages) & 1));
+        const double2* p = (const double2*)(buf + (size_t)s * chunk);
+        if (ng) {
+            const int* idx = (const int*)p;
+            for (int i = threadIdx.x - 32; i < ng; i += 32 * CW) acc += __ldcg(xv + (idx[i] & 262143));
+        }
+        for (int i = threadIdx.x - 32; i < chunk / 16; i += 32 * CW) { double2 v = p[i]; acc += v.x + v.y; }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
 int main() {
     int sms;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -119,6 +165,28 @@ int main() {
                 double gbs = timeit([&] { tma_ring<4><<<sms * ctas, 160, sm>>>(a, nch, chunk, stages, out); });
                 printf("tma_ring chunk %6d stages %2d ctas/SM %d (in flight/SM %4zu KB): %.0f GB/s\n", chunk, stages, ctas,
                        (size_t)stages * chunk * ctas / 1024, gbs);
+            }
+        }
+    }
+    {
+        const int chunk = 32768;
+        const int64_t nch = bytes / (chunk + 16) - 1;
+        std::vector<int64_t> h(nch);
+        for (int64_t i = 0; i < nch; ++i) h[i] = i;
+        uint64_t z = 12345;
+        for (int64_t i = nch - 1; i > 0; --i) { z = z * 6364136223846793005ull + 1442695040888963407ull; int64_t j = (int64_t)((z >> 33) % (uint64_t)(i + 1)); std::swap(h[i], h[j]); }
+        int64_t* ord;
+        double* xv;
+        CK(cudaMalloc(&ord, nch * 8));
+        CK(cudaMalloc(&xv, 262144 * 8));
+        CK(cudaMemset(xv, 0, 262144 * 8));
+        CK(cudaMemcpy(ord, h.data(), nch * 8, cudaMemcpyHostToDevice));
+        for (int stages : {4}) {
+            const size_t sm = 1024 + (size_t)stages * chunk;
+            CK(cudaFuncSetAttribute(tma_ring2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            for (int off : {0, 16}) for (int rnd : {0, 1}) for (int ng : {0, 128, 512}) for (int cw : {4, 8}) {
+                double gbs = timeit([&] { tma_ring2<<<sms, 32 * (cw + 1), sm>>>(a, nch, chunk, stages, off, rnd ? ord : nullptr, xv, ng, out); });
+                printf("tma_ring2 chunk 32K stages %d off %2d random %d gather %3d consumer warps %d: %.0f GB/s\n", stages, off, rnd, ng, cw, gbs * (double)nch * chunk / bytes);
             }
         }
     }

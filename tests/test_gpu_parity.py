@@ -98,9 +98,10 @@ def test_apply_equals_oracle_hmatrix_and_dense(hm, case):
     assert rel(y, Fd @ x) <= 10 * cfg.eps_aca
 
 
-@pytest.mark.parametrize("cut", [-1, 0, 2])
+@pytest.mark.parametrize("cut", [-1, 0, 2, 99])
 def test_solve_and_flux_match_dense_oracle(hm, case, cut):
-    """cut -1: pure level form (leaf inverses); 0: U^-1 (L^-1 b) as two H-applies; 2: mixed."""
+    """cut -1: default (= 0); 0: U^-1 (L^-1 b) as two H-applies; 2: mixed; 99 (>= depth): pure level
+    form (level-scheduled W updates + leaf inverses)."""
     import torch
     cfg, F, f = case["cfg"], case["F"], case["f"]
     ctx = F.ctx

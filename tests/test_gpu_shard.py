@@ -1,0 +1,106 @@
+"""Sharded hot path on one GPU ("virtual shards"): G ranks in one process, one host
+thread each, HM_FLAG_LOCAL_GROUP (the allgather done with device copies ordered by events), the same
+segmented engine programs the NCCL path runs.  Results must equal the world = 1 path (only the
+split-K summation order may differ) and the dense oracle within 10 eps_ACA.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import viewfactor as vf
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def _run_rank(hm, rank, world, key, cfg, out, errs):
+    try:
+        f = cfg.facets
+        ctx = hm.hm_init(0, rank, world, key, hm.HM_FLAG_LOCAL_GROUP)
+        g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
+        F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+        LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+        perm = hm.hm_export_perm(g)
+        b, e = hm.hm_local_range(g, rank, world)
+        rows = perm[b:e]                                    # external ids of this rank's internal rows
+        x = np.ascontiguousarray(cfg.rhs()[rows, :1])
+        T = np.ascontiguousarray(cfg.T[rows, :1])
+        y = np.empty_like(x)
+        z = np.empty_like(x)
+        q = np.empty_like(x)
+        hm.hm_apply_F(ctx, F, x, y)
+        hm.hm_solve_C(ctx, LU, x, z)
+        hm.hm_radiative_flux(ctx, F, LU, T, q)
+        for _ in range(3):                                  # repeated calls: exchange state reuse
+            hm.hm_radiative_flux(ctx, F, LU, T, q)
+        out[rank] = dict(rows=rows, y=y[:, 0], z=z[:, 0], q=q[:, 0])
+        del LU, F, g
+        ctx.close()
+    except Exception as ex:                                 # noqa: BLE001 -- reported by the test
+        errs.append(f"rank {rank}: {ex!r}")
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_virtual_shards_match_single_rank_and_oracle(world):
+    import paper_2305_06891_b200 as hm
+    cfg = synth.make_config(2, geometry=synth.icosphere(4))
+    f = cfg.facets
+    out, errs = {}, []
+    th = [threading.Thread(target=_run_rank, args=(hm, r, world, 1000 + world, cfg, out, errs)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    n = f.n
+    Y, Z, Q = np.empty(n), np.empty(n), np.empty(n)
+    for r in range(world):
+        o = out[r]
+        Y[o["rows"]], Z[o["rows"]], Q[o["rows"]] = o["y"], o["z"], o["q"]
+    # world = 1 on the same operators
+    ctx = hm.hm_init(0)
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    x = cfg.rhs()[:, 0].copy()
+    y1, z1, q1 = np.empty(n), np.empty(n), np.empty(n)
+    hm.hm_apply_F(ctx, F, x, y1)
+    hm.hm_solve_C(ctx, LU, x, z1)
+    hm.hm_radiative_flux(ctx, F, LU, cfg.T[:, 0].copy(), q1)
+    assert rel(Y, y1) <= 1e-13
+    assert rel(Z, z1) <= 1e-13
+    assert rel(Q, q1) <= 1e-12
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
+    assert rel(Y, Fd @ x) <= 10 * cfg.eps_aca
+    assert rel(Z, vf.solve(C, x)) <= 10 * cfg.eps_aca
+    assert rel(Q, vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]) <= 10 * cfg.eps_aca
+
+
+def test_sharded_level_form_is_rejected():
+    import paper_2305_06891_b200 as hm
+    cfg = synth.make_config(2, geometry=synth.icosphere(3))
+    f = cfg.facets
+    errs = []
+
+    def run(rank):
+        try:
+            ctx = hm.hm_init(0, rank, 2, 77, hm.HM_FLAG_LOCAL_GROUP)
+            g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min)
+            F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+            with pytest.raises(hm.HMError) as ei:
+                hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=3)
+            assert ei.value.status == "HM_ERR_UNSUPPORTED"
+        except Exception as ex:                             # noqa: BLE001
+            errs.append(repr(ex))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
