@@ -19,7 +19,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", CSRC,
           "-I", os.path.join(os.path.dirname(HERE), "include")]
 SOURCES = ["tree.cpp", "hop.cpp", "api.cpp", "hlu.cpp", "engine.cpp", "shard.cpp",
-           "kernels_assembly.cu", "kernels_apply.cu", "kernels_dense.cu", "kernels_engine.cu"]
+           "kernels_assembly.cu", "kernels_apply.cu", "kernels_dense.cu", "kernels_engine.cu",
+           "kernels_mrhs.cu"]
 
 
 def _digest() -> str:
@@ -56,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-ldl"]
+    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-Xlinker", "--no-undefined", "-o", tmp] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

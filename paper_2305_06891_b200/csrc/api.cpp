@@ -441,6 +441,17 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         F.prog_apply.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PERM);
         F.prog_apply.add_stream(F.op.p2, F.op, F.xt.p, nullptr, OUT_PERM, DEP_BARRIER, nullptr, IN_PERM, -1);
         F.prog_apply.finalize(c, s);
+        if (!g.shard.sharded()) {   // multi-RHS program: blocks of kMrhsMax columns, DMMA engine
+            F.xt_m.alloc(c, (size_t)(n + F.op.n_t) * kMrhsMax, "F xt (multi-RHS)");
+            F.y_m.alloc(c, (size_t)n * kMrhsMax, "F y (multi-RHS)");
+            Program& P = F.prog_apply_m;
+            P.mrhs = true;
+            P.n_x = n;
+            P.add_stream(F.op.p1m, F.op, F.xt_m.p, F.xt_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PERM);
+            P.add_stream(F.op.p2m, F.op, F.xt_m.p, F.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PERM, -1);
+            P.add_elementwise(UNIT_EPILOGUE, n, nullptr, 128, F.y_m.p, OUT_PERM);
+            P.finalize(c, s);
+        }
         HM_CUDA(cudaStreamSynchronize(s));
         F.setup_seconds[2] = now_seconds() - t0;
         *F_out = guard.release();
@@ -472,7 +483,15 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
             if (F.host_stage_out.n < cnt) F.host_stage_out.alloc(c, cnt, "host staging (out)");
             yd = F.host_stage_out.p;
         }
-        for (int col = 0; col < nrhs; ++col) launch_apply(c, F, xd, yd, nrhs, col, s);
+        if (nrhs >= 2 && F.prog_apply_m.ready) {   // multi-RHS engine, kMrhsMax columns per launch
+            for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
+                ProgArgs a = base_args(*F.geom, xd + c0, yd + c0, nrhs, 0);
+                a.nrhs = std::min(kMrhsMax, nrhs - c0);
+                F.prog_apply_m.launch(a, s);
+            }
+        } else {
+            for (int col = 0; col < nrhs; ++col) launch_apply(c, F, xd, yd, nrhs, col, s);
+        }
         if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
     });
@@ -493,7 +512,15 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
             if (L.host_stage_out.n < cnt) L.host_stage_out.alloc(c, cnt, "host staging (out)");
             zd = L.host_stage_out.p;
         }
-        for (int col = 0; col < nrhs; ++col) launch_solve(c, L, bd, zd, nrhs, col, s);
+        if (nrhs >= 2 && L.prog_solve_m.ready) {
+            for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
+                ProgArgs a = base_args(*L.F->geom, bd + c0, zd + c0, nrhs, 0);
+                a.nrhs = std::min(kMrhsMax, nrhs - c0);
+                L.prog_solve_m.launch(a, s);
+            }
+        } else {
+            for (int col = 0; col < nrhs; ++col) launch_solve(c, L, bd, zd, nrhs, col, s);
+        }
         if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
     });
@@ -505,7 +532,7 @@ namespace hm {
 // Rows of the caller's vectors: n (external order) or, sharded, this rank's slice (internal order).
 int64_t vec_rows(const Geom& g) { return g.shard.sharded() ? g.shard.le() - g.shard.lb() : g.n; }
 
-static ProgArgs base_args(const Geom& g, const double* in, double* out, int ld, int col) {
+ProgArgs base_args(const Geom& g, const double* in, double* out, int ld, int col) {
     ProgArgs a{};
     a.perm = g.d_perm.p;
     a.user_in = in;
@@ -552,6 +579,19 @@ void launch_flux(Ctx* c, HLU& L, const double* Td, double* qd, int ld, int col, 
     }
 }
 
+// Multi-RHS flux: r <= kMrhsMax columns starting at Td / qd (caller's arrays, row stride ld).
+void launch_flux_m(HLU& L, const double* Td, double* qd, int ld, int r, cudaStream_t s) {
+    const Geom& g = *L.F->geom;
+    ProgArgs a = base_args(g, Td, qd, ld, 0);
+    a.nrhs = r;
+    a.sigma = 5.670374419e-8;  // DESIGN.md reading R2
+    a.eps_int = L.eps_int.p;
+    a.eps_ext = L.eps_ext.p;
+    a.area_int = g.d_geo.p + 6 * g.n;
+    a.g_int = L.g_int.p;
+    L.prog_flux_m.launch(a, s);
+}
+
 }  // namespace hm
 
 extern "C" {
@@ -576,7 +616,11 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
             if (L.host_stage_out.n < cnt) L.host_stage_out.alloc(c, cnt, "host staging (out)");
             qd = L.host_stage_out.p;
         }
-        for (int col = 0; col < nrhs; ++col) launch_flux(c, L, Td, qd, nrhs, col, s);
+        if (nrhs >= 2 && L.prog_flux_m.ready) {
+            for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) launch_flux_m(L, Td + c0, qd + c0, nrhs, std::min(kMrhsMax, nrhs - c0), s);
+        } else {
+            for (int col = 0; col < nrhs; ++col) launch_flux(c, L, Td, qd, nrhs, col, s);
+        }
         if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
     });

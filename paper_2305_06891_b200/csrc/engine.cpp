@@ -62,18 +62,19 @@ void Program::add_stream(const StreamPass& sp, const HOp& op, const double* in, 
     add_stream_impl(*this, sp, op, in, out, mode, kind, panel_node, in_mode, xdep);
 }
 
-void Program::add_elementwise(int type, int64_t n, double* out) {
+void Program::add_elementwise(int type, int64_t n, double* out, int rows_per_unit, const double* in, int mode) {
     Pass p{};
     p.type = type;
     p.dep = (int32_t)h_passes.size() - 1;
-    p.mode = OUT_ASSIGN;
+    p.mode = mode;
     p.first_unit = (int64_t)h_units.size();
     p.out = out;
+    p.in = in;
     const int32_t idx = (int32_t)h_passes.size();
-    for (int64_t r = 0; r < n; r += 1024) {   // four rows per consumer thread
+    for (int64_t r = 0; r < n; r += rows_per_unit) {
         Unit u{};
         u.out0 = r;
-        u.nrows = (int32_t)std::min<int64_t>(1024, n - r);
+        u.nrows = (int32_t)std::min<int64_t>(rows_per_unit, n - r);
         u.grp = -1;
         u.nseg = 1;
         u.pass = idx;
@@ -100,7 +101,8 @@ void Program::add_elementwise(int type, int64_t n, double* out) {
 
 void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
     for (const Unit& u : h_units)
-        if (u.type == UNIT_STREAM && (u.ncols > kUnitMaxCols || u.ld > 128 || (int64_t)u.ncols * u.ld > kUnitPayloadDoubles))
+        if (u.type == UNIT_STREAM && (u.ncols > (mrhs ? kMrhsMaxCols : kUnitMaxCols) || u.ld > 128 ||
+                                      (int64_t)u.ncols * u.ld > kUnitPayloadDoubles))
             throw Error(HM_ERR_UNSUPPORTED, "work unit exceeds the engine stage size");
     const int64_t P = (int64_t)h_passes.size();
     if (P > engine_max_passes()) throw Error(HM_ERR_UNSUPPORTED, "program has more passes than the engine's pass table");
@@ -167,7 +169,7 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
     HM_CUDA(cudaMemsetAsync(done.p, 0, sizeof(unsigned long long) * std::max<int64_t>(n_counters, 1), s));
     queue.alloc(ctx, 1, "engine task queue");
     HM_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(unsigned long long), s));
-    grid = engine_grid();
+    grid = mrhs ? engine_mrhs_grid() : engine_grid();
     epoch = 0;
     ready = true;
 }
@@ -194,7 +196,8 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
         HM_CUDA(cudaMemsetAsync(stats.p, 0, 16 * sizeof(unsigned long long), s));
         a.stats = stats.p;
     }
-    engine_launch(a, grid, s);
+    if (mrhs) engine_mrhs_launch(a, grid, s);
+    else engine_launch(a, grid, s);
     if (want_stats) {
         unsigned long long h[16];
         HM_CUDA(cudaMemcpyAsync(h, stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -471,6 +471,32 @@ void factor_hlu(HLU& L, const double* emissivity) {
     }
     L.setup_seconds[3] = now_seconds() - t0;
 
+    // ---- multi-RHS programs (world == 1, inverse-factor form): blocks of kMrhsMax columns
+    if (!g.shard.sharded() && Lc == 0) {
+        L.xtA_m.alloc(c, (size_t)(n + L.leafL.n_t) * kMrhsMax, "solve xtA (multi-RHS)");
+        L.xtB_m.alloc(c, (size_t)(n + L.leafU.n_t) * kMrhsMax, "solve xtB (multi-RHS)");
+        auto mprog = [&](Program& P, int in_mode, double* out_u, int mode_u) {
+            P.mrhs = true;
+            P.n_x = n;
+            P.add_stream(L.leafL.p1m, L.leafL, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, in_mode);
+            P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, in_mode, -1);
+            P.add_stream(L.leafU.p1m, L.leafU, L.xtB_m.p, L.xtB_m.p, OUT_ASSIGN);
+            P.add_stream(L.leafU.p2m, L.leafU, L.xtB_m.p, out_u, mode_u, DEP_BARRIER, nullptr, IN_PLAIN,
+                         (int)P.h_passes.size() - 2);
+        };
+        // final results go to an internal n x 64 buffer, then an element-wise epilogue pass emits them
+        // (permute-out / flux epilogue) coalesced and fully parallel
+        mprog(L.prog_solve_m, IN_PERM, Fm.y_m.p, OUT_ASSIGN);
+        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 128, Fm.y_m.p, OUT_PERM);
+        L.prog_solve_m.finalize(c, s, &g);
+        mprog(L.prog_flux_m, IN_FLUX, Fm.xt_m.p, OUT_ASSIGN);
+        L.prog_flux_m.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
+        L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
+                                 (int)L.prog_flux_m.h_passes.size() - 2);
+        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 128, Fm.y_m.p, OUT_FLUX);
+        L.prog_flux_m.finalize(c, s, &g);
+    }
+
     // ---- sharded hot path (world > 1): exchange steps between the engine programs
     if (g.shard.sharded()) {
         const Shard& S = g.shard;

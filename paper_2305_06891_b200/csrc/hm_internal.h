@@ -194,8 +194,12 @@ struct alignas(16) Unit {
     int32_t wait_id[2], wait_cnt[2], inc_id[2];
 };
 static_assert(sizeof(Unit) % 16 == 0, "Unit is TMA-copied");
-enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2 };
+// UNIT_EPILOGUE (multi-RHS): rows of an internal n x kMrhsMax result emitted through the pass's output
+// mode (permute-out / flux epilogue) by element-wise units, coalesced and fully parallel
+enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2, UNIT_EPILOGUE = 3 };
 constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage
+constexpr int kMrhsMax = 64;                // multi-RHS block width (columns of X per program launch)
+constexpr int kMrhsMaxCols = 64;            // multi-RHS chunk: <= 64 panel columns (X tile 64 x 64)
 constexpr int kUnitMaxCols = 512;
 constexpr int64_t kPieceDoubles = 65536;    // panels above 512 KB are split into pieces
 
@@ -251,6 +255,7 @@ struct HOp {
     int64_t n_x = 0;              // size of the x region of XT
     DBuf<double> arena;
     StreamPass p1, p2;
+    StreamPass p1m, p2m;           // the same panels chunked for the multi-RHS kernel (world == 1)
     DBuf<int32_t> colsrc;          // per-unit, 16-byte aligned column-source segments
     DBuf<int32_t> colsrc_ext;      // same, x-region entries as -(external index + 1) (fused prologue)
     int64_t n_t = 0;              // total rank (size of t)
@@ -317,6 +322,7 @@ struct ProgArgs {
     const double* g_int;
     double sigma;
     int64_t local0;             // sharded: padded index of this rank's first row
+    int32_t nrhs;               // multi-RHS: columns of this launch (<= kMrhsMax; user arrays have ld >= nrhs)
     const double* T_pad;        // sharded flux: gathered temperatures (padded internal order)
 };
 
@@ -337,6 +343,7 @@ struct Program {
     unsigned long long epoch = 0;
     int grid = 0;
     bool ready = false;
+    bool mrhs = false;   // multi-RHS program (engine_mrhs_kernel, kMrhsMax columns per launch)
     int64_t n_x = 0;     // x-region size of the programs' XT buffers (fused-prologue gathers)
     std::vector<int32_t> task_kind, task_node;   // dependency kind / tree node of each task
     std::vector<uint8_t> task_xonly;             // task reads only the x region of its input
@@ -351,7 +358,8 @@ struct Program {
     void add_stream(const StreamPass& sp, const HOp& op, const double* in, double* out, int mode,
                     int kind = DEP_BARRIER, const std::vector<int32_t>* panel_node = nullptr, int in_mode = IN_PLAIN,
                     int xdep = -2);
-    void add_elementwise(int type, int64_t n, double* out);
+    void add_elementwise(int type, int64_t n, double* out, int rows_per_unit = 1024, const double* in = nullptr,
+                         int mode = 0 /* OUT_ASSIGN */);
     void finalize(Ctx* ctx, cudaStream_t s, const Geom* g = nullptr);
     void launch(ProgArgs a, cudaStream_t s);
 };
@@ -377,6 +385,8 @@ struct SegProgram {
 };
 
 size_t engine_smem_bytes();
+int engine_mrhs_grid();
+void engine_mrhs_launch(const ProgArgs& A, int grid, cudaStream_t s);
 int engine_max_passes();
 int engine_grid();
 void engine_launch(const ProgArgs& A, int grid, cudaStream_t s);
@@ -413,6 +423,10 @@ struct HMat {
     HOp op_loc;
     DBuf<double> xt_loc;  // [x_pad | t]
     SegProgram sp_apply;  // allgather x -> phase 1 -> phase 2
+    // multi-RHS hot path (world == 1): blocks of kMrhsMax columns, row-major n x kMrhsMax vectors
+    DBuf<double> xt_m;
+    Program prog_apply_m;
+    DBuf<double> y_m;     // internal n x kMrhsMax result (epilogue pass input)
 };
 
 struct HLU {
@@ -438,6 +452,9 @@ struct HLU {
     DBuf<double> eps_pad, area_pad, g_pad;
     SegProgram sp_solve;  // AG b -> L^-1 -> AG y -> U^-1
     SegProgram sp_flux;   // AG T -> L^-1 (w = eps T^4 fused) -> AG y -> U^-1 -> AG z -> F + flux epilogue
+    // multi-RHS hot path (world == 1, inverse-factor form)
+    DBuf<double> xtA_m, xtB_m;
+    Program prog_solve_m, prog_flux_m;
 };
 
 // ------------------------------------------------------------------ kernel launchers (kernels_*.cu)
@@ -483,6 +500,8 @@ double now_seconds();
 // hot-path launches for one column (api.cpp): world == 1 -> one engine program; sharded -> the
 // segmented program with its exchange steps
 int64_t vec_rows(const Geom& g);
+ProgArgs base_args(const Geom& g, const double* in, double* out, int ld, int col);
+void launch_flux_m(HLU& L, const double* Td, double* qd, int ld, int r, cudaStream_t s);
 void launch_apply(Ctx* c, HMat& F, const double* xd, double* yd, int ld, int col, cudaStream_t s);
 void launch_solve(Ctx* c, HLU& L, const double* bd, double* zd, int ld, int col, cudaStream_t s);
 void launch_flux(Ctx* c, HLU& L, const double* Td, double* qd, int ld, int col, cudaStream_t s,

@@ -20,8 +20,10 @@ static inline int64_t align2(int64_t x) { return (x + 1) & ~int64_t(1); }
 // Cut panels into pieces (only panels above 512 KB are split, for load balance) and pieces into
 // chunks of <= 32 KB contiguous payload (<= 512 columns), each chunk with its own 16-byte
 // aligned column-source segment (so the engine can TMA both).
+// max_cols: columns per chunk (single vector: kUnitMaxCols; multi-RHS: kMrhsMaxCols); part_scale:
+// partial-sum doubles per panel row (1, or kMrhsMax for the multi-RHS units)
 static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs, std::vector<int32_t>& ucs,
-                       cudaStream_t s) {
+                       cudaStream_t s, int max_cols = kUnitMaxCols, int part_scale = 1) {
     std::vector<Unit>& units = P.h_units;
     units.clear();
     P.unit_panel.clear();
@@ -60,7 +62,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
             for (int32_t q = 0; q < sg.np; ++q, ++pc) {
                 const int64_t p0 = sg.c0 + q * Cp, p1 = std::min<int64_t>(sg.c1, p0 + Cp);
                 if (p1 <= p0) { --pc; continue; }
-                int64_t C = std::min<int64_t>(kUnitMaxCols, kUnitPayloadDoubles / pn.ld);
+                int64_t C = std::min<int64_t>(max_cols, kUnitPayloadDoubles / pn.ld);
                 const int32_t nch = (int32_t)((p1 - p0 + C - 1) / C);
                 C = (p1 - p0 + nch - 1) / nch;
                 Piece PC;
@@ -73,7 +75,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
                     u.ncols = (int32_t)std::min<int64_t>(C, p1 - c0);
                     u.a_off = pn.a_off + c0 * pn.ld;
                     u.out0 = pn.out0;
-                    u.part_off = part + (npieces > 1 ? (int64_t)pc * pn.ld : 0);
+                    u.part_off = (part + (npieces > 1 ? (int64_t)pc * pn.ld : 0)) * part_scale;
                     u.cs_off = (int64_t)PC.cs.size();   // relative; rebased below
                     for (int32_t c = 0; c < u.ncols; ++c) PC.cs.push_back(pcs[pn.cs_off + c0 + c]);
                     {   // run-length form of the column sources
@@ -131,7 +133,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
         }
     }
     P.n_units = (int64_t)units.size();
-    P.part.alloc(ctx, (size_t)std::max<int64_t>(part, 2), "split-K partials");
+    P.part.alloc(ctx, (size_t)std::max<int64_t>(part * part_scale, 2), "split-K partials");
     P.counters.alloc(ctx, (size_t)std::max<int32_t>(grp, 1), "split-K counters");
     HM_CUDA(cudaMemsetAsync(P.counters.p, 0, sizeof(int32_t) * std::max<int32_t>(grp, 1), s));
 }
@@ -264,6 +266,14 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     std::vector<int32_t> ucs;
     make_units(ctx, op.p1, colsrc, ucs, s);
     make_units(ctx, op.p2, colsrc, ucs, s);
+    if (!shd) {   // multi-RHS chunking of the same panels (<= kMrhsMaxCols columns: X tile in smem)
+        op.p1m.panels = op.p1.panels;
+        op.p2m.panels = op.p2.panels;
+        op.p1m.doubles = op.p1.doubles;
+        op.p2m.doubles = op.p2.doubles;
+        make_units(ctx, op.p1m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax);
+        make_units(ctx, op.p2m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax);
+    }
     op.colsrc.upload(ctx, ucs, "colsrc", s);
     // the same column sources for passes that gather straight from the caller's external-order
     // vector (fused prologue): x-region index j becomes -(perm[j] + 1)

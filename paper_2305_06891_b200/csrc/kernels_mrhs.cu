@@ -1,0 +1,469 @@
+// Multi-RHS stream engine: the same programs as the single-vector engine
+// (kernels_engine.cu) applied to a block of up to kMrhsMax = 64 right-hand sides at once, so every
+// stored factor byte is read ONCE per 64 columns and the apply becomes a dense contraction
+// (2 x 64 flop per 8 stored bytes = 16 flop/B, above the FP64 ridge): each chunk
+//     out[rows, 0:r] += A[rows, cols] @ X[cols, 0:r]
+// runs on the FP64 tensor pipe (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; sm_100a's tcgen05 has no f64
+// kind).  Vectors are row-major n x kMrhsMax (row i: its r values contiguous, 512 B).
+//
+// One CTA per SM, cooperative launch, warp-specialised over a 3-stage ring; each stage holds a
+// chunk's descriptor, its payload (<= 32 KB, 1-D TMA) and its gathered X tile (<= 64 x 64):
+//   warp 0      producer: tasks from the monotone queue, descriptors (lane-parallel loads), TMA;
+//   warps 1-2   gatherers: dependency waits, then X rows (512 B each, coalesced) into the stage;
+//   warps 3-10  consumers: DMMA over the chunk, accumulators (8x8 tiles) in registers across the
+//               task; at the task's last chunk they emit (split panels: partial + last-arriver sum
+//               in piece order) and publish the task (release fence, counters).
+#include <cstdint>
+
+#include "engine.h"
+#include "engine_dev.cuh"
+#include "hm_internal.h"
+
+namespace hm {
+namespace {
+using namespace dev;
+
+constexpr int kMGatherers = 2;
+constexpr int kMConsumerWarps = 8;
+constexpr int kMConsumers = 32 * kMConsumerWarps;
+constexpr int kMConsumer0 = 32 * (1 + kMGatherers);
+constexpr int kMThreads = 32 * (1 + kMGatherers + kMConsumerWarps);   // 352
+constexpr int kMStages = 3;
+constexpr int kXStride = 72;          // X tile row stride (doubles): conflict-free B fragments
+constexpr int kMaxPassesM = 96;
+constexpr int kMaxTiles = 16;         // 8x8 accumulator tiles per consumer warp (128 rows x 64 cols / 8 warps)
+
+struct __align__(16) MStage {
+    Unit hdr;
+    double payload[kUnitPayloadDoubles];
+    double X[kMrhsMaxCols * kXStride];
+};
+
+struct MSmem {
+    MStage st[kMStages];
+    Pass passes[kMaxPassesM];
+    unsigned long long posted[kMStages], full[kMStages], gathered[kMStages], empty[kMStages];
+    int last;
+};
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kMConsumers) : "memory"); }
+
+// out[row, col] for the program's output mode; vectors inside the library are row-major with
+// stride kMrhsMax, the caller's arrays with stride A.ld (external order)
+__device__ __forceinline__ void emit_m(const ProgArgs& A, const Pass& P, int64_t row, int col, double s) {
+    switch (P.mode) {
+        case OUT_ASSIGN: P.out[row * kMrhsMax + col] = s; break;
+        case OUT_SUB: P.out[row * kMrhsMax + col] = __ldcg(P.out + row * kMrhsMax + col) - s; break;
+        case OUT_PERM: A.user_out[(int64_t)A.perm[row] * A.ld + col] = s; break;
+        default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form)
+            const int64_t e = A.perm[row];
+            const double eta = pow4(A.user_in[e * A.ld + col]);
+            A.user_out[e * A.ld + col] = A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArgs A) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    MSmem& S = *reinterpret_cast<MSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int R = A.nrhs;                       // columns of this launch (<= 64)
+    const int N8 = (R + 7) >> 3;                // 8-wide column tiles
+    if (tid == 0) {
+        for (int s = 0; s < kMStages; ++s) {
+            mbar_init(&S.posted[s], 1);
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.gathered[s], kMGatherers);
+            mbar_init(&S.empty[s], kMConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < A.n_passes; i += kMThreads) S.passes[i] = A.passes[i];
+    __syncthreads();
+
+    if (warp == 0) {
+        // ------------------------------------------------ producer
+        unsigned long long nxt = 0, st_e = 0, st_m = 0;
+        const long long t0 = clock64();
+        if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - A.queue_base;
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        int64_t k = 0;
+        while (true) {
+            const unsigned long long t = nxt;
+            const bool end = t >= (unsigned long long)A.n_tasks;
+            Task task{};
+            if (!end) {
+                task = A.tasks[t];
+                if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - A.queue_base;
+            }
+            const int nch = end ? 1 : task.n_units;
+            for (int base = 0; base < nch; base += 32) {
+                long long c0 = clock64();
+                Unit mine{};
+                if (!end && base + lane < nch) mine = A.units[task.first_unit + base + lane];
+                __syncwarp();
+                st_m += clock64() - c0;
+                const int cnt = min(32, nch - base);
+                for (int c = 0; c < cnt; ++c, ++k) {
+                    const int s = (int)(k % kMStages);
+                    c0 = clock64();
+                    if (k >= kMStages && lane == 0) mbar_wait(&S.empty[s], (uint32_t)(((k / kMStages) - 1) & 1));
+                    __syncwarp();
+                    st_e += clock64() - c0;
+                    if (lane == c) {
+                        MStage& St = S.st[s];
+                        if (end) {
+                            St.hdr.type = -1;
+                            mbar_arrive(&S.posted[s]);
+                            mbar_arrive(&S.full[s]);
+                        } else {
+                            St.hdr = mine;
+                            mbar_arrive(&S.posted[s]);
+                            if (mine.type == UNIT_STREAM) {
+                                const uint32_t pb = (uint32_t)mine.ncols * (uint32_t)mine.ld * 8u;
+                                mbar_expect_tx(&S.full[s], pb);
+                                tma_load_1d(St.payload, S.passes[mine.pass].arena + mine.a_off, pb, &S.full[s]);
+                            } else {
+                                mbar_arrive(&S.full[s]);
+                            }
+                        }
+                    }
+                }
+                nxt = __shfl_sync(0xffffffffu, nxt, 0);
+            }
+            if (end) break;
+        }
+        if (A.stats && lane == 0) {
+            atomicAdd(A.stats + 0, st_e);
+            atomicAdd(A.stats + 1, st_m);
+            atomicAdd(A.stats + 12, (unsigned long long)(clock64() - t0));
+        }
+        return;
+    }
+    if (warp <= kMGatherers) {
+        // ------------------------------------------------ gatherers (both warps on every stage,
+        // columns split between them): dependency waits, then the X rows of the chunk
+        const int gw = warp - 1;
+        int64_t verified = -1;
+        unsigned long long st_p = 0, st_d = 0, st_g = 0;
+        for (int64_t k = 0;; ++k) {
+            const int s = (int)(k % kMStages);
+            long long c0 = clock64();
+            mbar_wait(&S.posted[s], (uint32_t)((k / kMStages) & 1));
+            long long c1 = clock64();
+            st_p += c1 - c0;
+            MStage& St = S.st[s];
+            const Unit& H = St.hdr;
+            const int type = H.type;
+            if (type >= 0 && H.task != verified) {
+                if (lane == 0) {
+                    if (H.wait_id[0] >= 0) wait_counter(A, H.wait_id[0], H.wait_cnt[0]);
+                    if (H.wait_id[1] >= 0) wait_counter(A, H.wait_id[1], H.wait_cnt[1]);
+                }
+                __syncwarp();
+                fence_proxy_async_global();
+                verified = H.task;
+            }
+            c0 = clock64();
+            st_d += c0 - c1;
+            if (type == UNIT_STREAM) {
+                const Pass& P = S.passes[H.pass];
+                const double* in = P.in;
+                const int ncols = H.ncols;
+                const int im = P.in_mode;
+                const int32_t* cs = P.colsrc + H.cs_off;   // colsrc_ext for fused-prologue passes
+                const int ncol4 = (ncols + 3) & ~3;
+                if (im == IN_PLAIN) {
+                    // each X row (512 B, written by an earlier pass) arrives by a 1-D TMA bulk copy:
+                    // warp gw, lane l -> column c = gw + kMGatherers * l
+                    const int c = gw + kMGatherers * lane;
+                    const int mine = c < ncols ? 1 : 0;
+                    const int cnt = __popc(__ballot_sync(0xffffffffu, mine));
+                    if (lane == 0 && cnt) mbar_add_tx(&S.gathered[s], (uint32_t)cnt * kMrhsMax * 8u);
+                    __syncwarp();
+                    if (mine) {
+                        const int32_t j = __ldg(cs + c);
+                        tma_load_1d(St.X + c * kXStride, in + (int64_t)j * kMrhsMax, kMrhsMax * 8u, &S.gathered[s]);
+                    } else if (c < ncol4) {   // k-step padding columns: zero (consumers multiply them)
+#pragma unroll
+                        for (int q = 0; q < kMrhsMax; ++q) St.X[c * kXStride + q] = 0.0;
+                    }
+                } else {
+                    // fused prologue: rows of the caller's external-order array (stride ld), IN_FLUX:
+                    // w = eps T^4; 8 columns in flight per warp, lanes cover the 64 values as double2
+                    const int q = 2 * lane;
+                    for (int c0 = gw; c0 < ncol4; c0 += 8 * kMGatherers) {
+                        double2 v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int c = c0 + u * kMGatherers;
+                            v[u] = make_double2(0.0, 0.0);
+                            if (c < ncols) {
+                                const int32_t j = __ldg(cs + c);
+                                if (j >= 0) {
+                                    v[u] = __ldcg(reinterpret_cast<const double2*>(in + (int64_t)j * kMrhsMax) + lane);
+                                } else {
+                                    const int64_t e = -(int64_t)j - 1;
+                                    const double* src = A.user_in + e * A.ld;
+                                    v[u].x = q < R ? __ldg(src + q) : 0.0;
+                                    v[u].y = q + 1 < R ? __ldg(src + q + 1) : 0.0;
+                                    if (im == IN_FLUX) {
+                                        const double ee = __ldg(A.eps_ext + e);
+                                        v[u].x = ee * pow4(v[u].x);
+                                        v[u].y = ee * pow4(v[u].y);
+                                    }
+                                }
+                                if (q >= R) v[u].x = 0.0;
+                                if (q + 1 >= R) v[u].y = 0.0;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int c = c0 + u * kMGatherers;
+                            if (c < ncol4) reinterpret_cast<double2*>(St.X + c * kXStride)[lane] = v[u];
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            st_g += clock64() - c0;
+            if (lane == 0) mbar_arrive(&S.gathered[s]);
+            if (type < 0) break;
+        }
+        if (A.stats && lane == 0) {
+            atomicAdd(A.stats + 3, st_p);
+            atomicAdd(A.stats + 4, st_d);
+            atomicAdd(A.stats + 5, st_g);
+        }
+        return;
+    }
+    // ---------------------------------------------------- consumers: DMMA, task accumulators in registers
+    const int cw = warp - 1 - kMGatherers;   // consumer warp 0..7
+    const int ct = tid - kMConsumer0;
+    double acc[kMaxTiles][2];
+#pragma unroll
+    for (int i = 0; i < kMaxTiles; ++i) acc[i][0] = acc[i][1] = 0.0;
+    const int ar = lane >> 2, ak = lane & 3;     // fragment coordinates
+    unsigned long long st_wg = 0, st_wf = 0, st_c = 0, st_t = 0;
+    long long c0 = clock64();
+    for (int64_t k = 0;; ++k) {
+        const int s = (int)(k % kMStages);
+        mbar_wait(&S.gathered[s], (uint32_t)((k / kMStages) & 1));
+        long long c1 = clock64();
+        st_wg += c1 - c0;
+        MStage& St = S.st[s];
+        const int type = St.hdr.type;
+        if (type < 0) break;
+        mbar_wait(&S.full[s], (uint32_t)((k / kMStages) & 1));
+        long long c2 = clock64();
+        st_wf += c2 - c1;
+        const int pass = St.hdr.pass, nrows = St.hdr.nrows, ld = St.hdr.ld, ncols = St.hdr.ncols;
+        const int chunk = St.hdr.chunk, nchunks = St.hdr.nchunks;
+        const int grp = St.hdr.grp, nseg = St.hdr.nseg, seg = St.hdr.seg;
+        const int64_t out0 = St.hdr.out0, part_off = St.hdr.part_off;
+        const int32_t inc0 = St.hdr.inc_id[0], inc1 = St.hdr.inc_id[1];
+        const Pass& P = S.passes[pass];
+        const int M8 = (nrows + 7) >> 3;
+        const int ntile = M8 * N8;
+        if (type == UNIT_STREAM) {
+            if (chunk == 0) {
+#pragma unroll
+                for (int i = 0; i < kMaxTiles; ++i) acc[i][0] = acc[i][1] = 0.0;
+            }
+            const double* Ap = St.payload;
+            const double* Xp = St.X;
+            // this warp's tiles t = cw + 8 i: fragment offsets hoisted out of the k loop
+            int arow[kMaxTiles], bcol[kMaxTiles];
+            int nmine = 0;
+#pragma unroll
+            for (int i = 0; i < kMaxTiles; ++i) {
+                const int t = cw + 8 * i;
+                arow[i] = -1;
+                bcol[i] = 0;
+                if (t < ntile) {
+                    const int mt = t / N8, nt = t - mt * N8;
+                    const int row = mt * 8 + ar;
+                    arow[i] = row < ld ? row : -1;
+                    bcol[i] = nt * 8 + ar;
+                    nmine = i + 1;
+                }
+            }
+            if (N8 == 8) {   // r = 64: a warp's tiles share one column tile -> one B fragment per k-step
+                const int bc = cw * 8 + ar;
+                for (int k4 = 0; k4 < ncols; k4 += 4) {
+                    const int kk = k4 + ak;
+                    const bool kv = kk < ncols;
+                    const double* Ak = Ap + kk * ld;
+                    const double b = Xp[kk * kXStride + bc];
+#pragma unroll
+                    for (int i = 0; i < kMaxTiles; ++i) {
+                        if (i < nmine) {
+                            const double a = (kv && arow[i] >= 0) ? Ak[arow[i]] : 0.0;
+                            dmma(acc[i], a, b);
+                        }
+                    }
+                }
+            } else {
+                for (int k4 = 0; k4 < ncols; k4 += 4) {
+                    const int kk = k4 + ak;
+                    const bool kv = kk < ncols;
+                    const double* Ak = Ap + kk * ld;
+                    const double* Xk = Xp + kk * kXStride;
+#pragma unroll
+                    for (int i = 0; i < kMaxTiles; ++i) {
+                        if (i < nmine) {
+                            const double a = (kv && arow[i] >= 0) ? Ak[arow[i]] : 0.0;
+                            dmma(acc[i], a, Xk[bcol[i]]);
+                        }
+                    }
+                }
+            }
+        } else if (type == UNIT_EPILOGUE) {
+            // rows x R of the internal result through the pass's output mode (permute-out / flux
+            // epilogue); 4 independent elements per thread in flight
+            const int tot = nrows * R;
+            for (int e0 = ct; e0 < tot; e0 += 4 * kMConsumers) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kMConsumers;
+                    v[u] = e < tot ? __ldcg(P.in + (out0 + e / R) * kMrhsMax + (e % R)) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kMConsumers;
+                    if (e < tot) emit_m(A, P, out0 + e / R, e % R, v[u]);
+                }
+            }
+        } else {
+            for (int i = ct; i < nrows; i += kMConsumers) {   // element-wise pass: rows x R
+                const int64_t row = out0 + i;
+                const int64_t e = A.perm[row];
+                for (int q = 0; q < R; ++q) {
+                    const double v = A.user_in[e * A.ld + q];
+                    P.out[row * kMrhsMax + q] = type == UNIT_PROLOGUE ? A.eps_int[row] * pow4(v) : v;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+        c0 = clock64();
+        st_c += c0 - c2;
+        if (chunk != nchunks - 1) continue;
+        // ---- last chunk of the task: emit (split panels combine deterministically), publish
+        if (type == UNIT_STREAM) {
+            if (grp < 0) {
+#pragma unroll
+                for (int i = 0; i < kMaxTiles; ++i) {
+                    const int t = cw + 8 * i;
+                    if (t >= ntile) break;
+                    const int mt = t / N8, nt = t - (t / N8) * N8;
+                    const int row = mt * 8 + ar;
+                    const int col = nt * 8 + 2 * ak;
+                    if (row < nrows) {
+                        if (col < R) emit_m(A, P, out0 + row, col, acc[i][0]);
+                        if (col + 1 < R) emit_m(A, P, out0 + row, col + 1, acc[i][1]);
+                    }
+                }
+            } else {
+                double* part = P.part + part_off;
+#pragma unroll
+                for (int i = 0; i < kMaxTiles; ++i) {
+                    const int t = cw + 8 * i;
+                    if (t >= ntile) break;
+                    const int mt = t / N8, nt = t - (t / N8) * N8;
+                    const int row = mt * 8 + ar;
+                    const int col = nt * 8 + 2 * ak;
+                    if (row < nrows) {
+                        part[row * kMrhsMax + col] = acc[i][0];
+                        part[row * kMrhsMax + col + 1] = acc[i][1];
+                    }
+                }
+                cons_sync();
+                if (ct == 0) {
+                    __threadfence();
+                    S.last = (atomicAdd(P.counters + grp, 1) == nseg - 1);
+                    if (S.last) __threadfence();
+                }
+                cons_sync();
+                if (S.last) {
+                    const int64_t pstride = (int64_t)ld * kMrhsMax;   // piece q's partial: (q - seg) * pstride away
+                    const int tot = nrows * R;
+                    for (int e0 = ct; e0 < tot; e0 += 4 * kMConsumers) {   // 4 elements in flight
+                        double v[4] = {0.0, 0.0, 0.0, 0.0};
+                        for (int q = 0; q < nseg; ++q) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int e = e0 + u * kMConsumers;
+                                if (e < tot)
+                                    v[u] += __ldcg(part + (int64_t)(q - seg) * pstride + (e / R) * kMrhsMax + (e % R));
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int e = e0 + u * kMConsumers;
+                            if (e < tot) emit_m(A, P, out0 + e / R, e % R, v[u]);
+                        }
+                    }
+                    if (ct == 0) P.counters[grp] = 0;
+                }
+            }
+        }
+        cons_sync();
+        if (ct == 0) {
+            __threadfence();
+            atomicAdd(A.done + pass, 1ull);
+            if (inc0 >= 0) atomicAdd(A.done + inc0, 1ull);
+            if (inc1 >= 0) atomicAdd(A.done + inc1, 1ull);
+        }
+        const long long c3 = clock64();
+        st_t += c3 - c0;
+        c0 = c3;
+    }
+    if (A.stats && ct == 0) {
+        atomicAdd(A.stats + 6, st_wg);
+        atomicAdd(A.stats + 13, st_wf);
+        atomicAdd(A.stats + 7, st_c);
+        atomicAdd(A.stats + 8, st_t);
+    }
+}
+
+}  // namespace
+
+static size_t mrhs_smem_bytes() { return sizeof(MSmem) + 128; }
+
+static void mrhs_set_attr() {
+    static bool attr = false;
+    if (!attr) {
+        HM_CUDA(cudaFuncSetAttribute(engine_mrhs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)mrhs_smem_bytes()));
+        attr = true;
+    }
+}
+
+void engine_mrhs_launch(const ProgArgs& A, int grid, cudaStream_t s) {
+    mrhs_set_attr();
+    void* args[] = {const_cast<ProgArgs*>(&A)};
+    HM_CUDA(cudaLaunchCooperativeKernel((const void*)engine_mrhs_kernel, dim3(grid), dim3(kMThreads), args,
+                                        mrhs_smem_bytes(), s));
+    debug_sync(s, "engine_mrhs_kernel");
+}
+
+int engine_mrhs_grid() {
+    int dev = 0, sms = 0, per = 0;
+    HM_CUDA(cudaGetDevice(&dev));
+    HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    mrhs_set_attr();
+    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, engine_mrhs_kernel, kMThreads, mrhs_smem_bytes()));
+    if (per < 1) throw Error(HM_ERR_CUDA, "multi-RHS engine kernel does not fit on an SM");
+    return sms * per;
+}
+
+}  // namespace hm

@@ -136,6 +136,42 @@ def test_host_pointers_and_multiple_rhs(hm, case):
         assert rel(Yh[:, c], case["H"].apply(X[:, c])) <= TOL_EXACT
 
 
+@pytest.mark.parametrize("nrhs", [8, 64, 70])
+def test_multi_rhs_dmma_matches_single_columns_and_oracle(hm, case, nrhs):
+    """blocks of 64 right-hand sides through the DMMA engine (apply, solve, flux)
+    equal the single-vector path column by column (summation order differs: 1e-12) and the dense
+    oracle (10 eps_ACA).  nrhs = 70 exercises a 64 + 6 split."""
+    import torch
+    cfg, F, f = case["cfg"], case["F"], case["f"]
+    ctx = F.ctx
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    T = 300.0 + 700.0 * np.stack([synth.uniform(100 + c, f.n) for c in range(nrhs)], axis=1)
+    X = vf.SIGMA_SB * T ** 4
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
+    outs = {}
+    for name, fn, inp in [("apply", hm.hm_apply_F, X), ("solve", hm.hm_solve_C, X), ("flux", hm.hm_radiative_flux, T)]:
+        op = F if name == "apply" else LU
+        Yd = torch.empty(f.n, nrhs, dtype=torch.float64, device="cuda")
+        args = (ctx, F, LU) if name == "flux" else (ctx, op)
+        fn(*args, torch.from_numpy(inp).cuda(), Yd)
+        torch.cuda.synchronize()
+        Y = Yd.cpu().numpy()
+        outs[name] = Y
+        for c in (0, nrhs // 2, nrhs - 1):
+            y1 = torch.empty(f.n, dtype=torch.float64, device="cuda")
+            fn(*args, torch.from_numpy(inp[:, c].copy()).cuda(), y1)
+            torch.cuda.synchronize()
+            assert rel(Y[:, c], y1.cpu().numpy()) <= 1e-12, (name, c)
+    Yo = Fd @ X
+    Zo = np.linalg.solve(C, X)
+    for c in range(0, nrhs, 7):
+        assert rel(outs["apply"][:, c], Yo[:, c]) <= 10 * cfg.eps_aca
+        assert rel(outs["solve"][:, c], Zo[:, c]) <= 10 * cfg.eps_aca
+    qo = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, T[:, :3])
+    for c in range(3):
+        assert rel(outs["flux"][:, c], qo[:, c]) <= 10 * cfg.eps_aca
+
+
 # ---------------------------------------------------------------- edge cases
 def test_single_dense_leaf_equals_dense(hm, ctx):
     f = synth.icosphere(1)             # n = 80 <= n_min
