@@ -478,8 +478,12 @@ void factor_hlu(HLU& L, const double* emissivity) {
         auto mprog = [&](Program& P, int in_mode, double* out_u, int mode_u) {
             P.mrhs = true;
             P.n_x = n;
-            P.add_stream(L.leafL.p1m, L.leafL, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, in_mode);
-            P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, in_mode, -1);
+            // prologue: b (or w = eps T^4) into the internal n x 64 layout, then every gather is a
+            // 512-byte TMA row copy
+            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, 128);
+            P.add_stream(L.leafL.p1m, L.leafL, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN);
+            P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
+                         (int)P.h_passes.size() - 2);
             P.add_stream(L.leafU.p1m, L.leafU, L.xtB_m.p, L.xtB_m.p, OUT_ASSIGN);
             P.add_stream(L.leafU.p2m, L.leafU, L.xtB_m.p, out_u, mode_u, DEP_BARRIER, nullptr, IN_PLAIN,
                          (int)P.h_passes.size() - 2);

@@ -23,7 +23,7 @@ static inline int64_t align2(int64_t x) { return (x + 1) & ~int64_t(1); }
 // max_cols: columns per chunk (single vector: kUnitMaxCols; multi-RHS: kMrhsMaxCols); part_scale:
 // partial-sum doubles per panel row (1, or kMrhsMax for the multi-RHS units)
 static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs, std::vector<int32_t>& ucs,
-                       cudaStream_t s, int max_cols = kUnitMaxCols, int part_scale = 1) {
+                       cudaStream_t s, int max_cols = kUnitMaxCols, int part_scale = 1, bool split_xonly = true) {
     std::vector<Unit>& units = P.h_units;
     units.clear();
     P.unit_panel.clear();
@@ -45,7 +45,10 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
         // two column segments: [0, ndense) reads only x (may run before the t values exist),
         // [ndense, ncols) reads t; each is cut into pieces, all pieces of the panel combine
         struct Seg { int64_t c0, c1; int32_t np; };
-        Seg segs[2] = {{0, pn.ndense, 0}, {pn.ndense, pn.ncols, 0}};
+        // (multi-RHS: no split -- the kernel is compute-bound, and every extra piece costs a
+        // rows x 64 partial write + combine)
+        const int64_t nd = split_xonly ? pn.ndense : 0;
+        Seg segs[2] = {{0, nd, 0}, {nd, pn.ncols, 0}};
         int32_t npieces = 0;
         for (Seg& sg : segs) {
             const int64_t w = sg.c1 - sg.c0;
@@ -68,7 +71,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
                 Piece PC;
                 PC.panel = (int32_t)pi;
                 PC.doubles = (p1 - p0) * pn.ld;
-                PC.xonly = sgi == 0 ? 1 : 0;
+                PC.xonly = p1 <= pn.ndense ? 1 : 0;   // reads only x (no t)
                 for (int32_t ch = 0; ch < nch; ++ch) {
                     Unit u{};
                     const int64_t c0 = p0 + ch * C;
@@ -271,8 +274,8 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
         op.p2m.panels = op.p2.panels;
         op.p1m.doubles = op.p1.doubles;
         op.p2m.doubles = op.p2.doubles;
-        make_units(ctx, op.p1m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax);
-        make_units(ctx, op.p2m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax);
+        make_units(ctx, op.p1m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax, false);
+        make_units(ctx, op.p2m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax, false);
     }
     op.colsrc.upload(ctx, ucs, "colsrc", s);
     // the same column sources for passes that gather straight from the caller's external-order

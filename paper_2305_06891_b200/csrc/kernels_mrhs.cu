@@ -52,6 +52,51 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// One chunk's contraction for a warp owning TM tiles t = cw + 8 i: acc[i] += A[rows(t), :] X[:, cols(t)].
+// Rows beyond the panel (garbage) only feed accumulator rows that are never emitted, so the full
+// k-steps need no predicates; the k tail (ncols % 4) zeroes A (X rows there are zero, but stale A
+// could be NaN).
+template <int TM>
+__device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const double* __restrict__ Ap,
+                                          const double* __restrict__ Xp, int ld, int ncols, int cw, int N8, int ar,
+                                          int ak) {
+    int arow[TM], bcol[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int t = cw + 8 * i;
+        const int mt = t / N8, nt = t - mt * N8;
+        arow[i] = mt * 8 + ar;
+        bcol[i] = nt * 8 + ar;
+    }
+    const int nfull = ncols & ~3;
+    for (int k4 = 0; k4 < nfull; k4 += 4) {
+        const double* Ak = Ap + (k4 + ak) * ld;
+        const double* Xk = Xp + (k4 + ak) * kXStride;
+        double a[TM], b[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            a[i] = Ak[arow[i]];
+            b[i] = Xk[bcol[i]];
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i) dmma(acc[i], a[i], b[i]);
+    }
+    if (nfull < ncols) {
+        const int kk = nfull + ak;
+        const bool kv = kk < ncols;
+        const double* Ak = Ap + kk * ld;
+        const double* Xk = Xp + kk * kXStride;
+        double a[TM], b[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            a[i] = kv ? Ak[arow[i]] : 0.0;
+            b[i] = Xk[bcol[i]];
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i) dmma(acc[i], a[i], b[i]);
+    }
+}
+
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kMConsumers) : "memory"); }
 
 // out[row, col] for the program's output mode; vectors inside the library are row-major with
@@ -279,51 +324,22 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             }
             const double* Ap = St.payload;
             const double* Xp = St.X;
-            // this warp's tiles t = cw + 8 i: fragment offsets hoisted out of the k loop
-            int arow[kMaxTiles], bcol[kMaxTiles];
+            // this warp's tiles t = cw + 8 i (row tiles mt, column tile nt); the k loop is
+            // specialised on the tile count so the fragments of a k-step are loaded as a batch into
+            // distinct registers and then feed back-to-back DMMAs
             int nmine = 0;
 #pragma unroll
-            for (int i = 0; i < kMaxTiles; ++i) {
-                const int t = cw + 8 * i;
-                arow[i] = -1;
-                bcol[i] = 0;
-                if (t < ntile) {
-                    const int mt = t / N8, nt = t - mt * N8;
-                    const int row = mt * 8 + ar;
-                    arow[i] = row < ld ? row : -1;
-                    bcol[i] = nt * 8 + ar;
-                    nmine = i + 1;
-                }
-            }
-            if (N8 == 8) {   // r = 64: a warp's tiles share one column tile -> one B fragment per k-step
-                const int bc = cw * 8 + ar;
-                for (int k4 = 0; k4 < ncols; k4 += 4) {
-                    const int kk = k4 + ak;
-                    const bool kv = kk < ncols;
-                    const double* Ak = Ap + kk * ld;
-                    const double b = Xp[kk * kXStride + bc];
-#pragma unroll
-                    for (int i = 0; i < kMaxTiles; ++i) {
-                        if (i < nmine) {
-                            const double a = (kv && arow[i] >= 0) ? Ak[arow[i]] : 0.0;
-                            dmma(acc[i], a, b);
-                        }
-                    }
-                }
-            } else {
-                for (int k4 = 0; k4 < ncols; k4 += 4) {
-                    const int kk = k4 + ak;
-                    const bool kv = kk < ncols;
-                    const double* Ak = Ap + kk * ld;
-                    const double* Xk = Xp + kk * kXStride;
-#pragma unroll
-                    for (int i = 0; i < kMaxTiles; ++i) {
-                        if (i < nmine) {
-                            const double a = (kv && arow[i] >= 0) ? Ak[arow[i]] : 0.0;
-                            dmma(acc[i], a, Xk[bcol[i]]);
-                        }
-                    }
-                }
+            for (int i = 0; i < kMaxTiles; ++i)
+                if (cw + 8 * i < ntile) nmine = i + 1;
+            switch (nmine) {
+#define HM_MMA_CASE(TM) \
+    case TM: mma_chunk<TM>(acc, Ap, Xp, ld, ncols, cw, N8, ar, ak); break;
+                HM_MMA_CASE(1) HM_MMA_CASE(2) HM_MMA_CASE(3) HM_MMA_CASE(4)
+                HM_MMA_CASE(5) HM_MMA_CASE(6) HM_MMA_CASE(7) HM_MMA_CASE(8)
+                HM_MMA_CASE(9) HM_MMA_CASE(10) HM_MMA_CASE(11) HM_MMA_CASE(12)
+                HM_MMA_CASE(13) HM_MMA_CASE(14) HM_MMA_CASE(15) HM_MMA_CASE(16)
+#undef HM_MMA_CASE
+                default: break;
             }
         } else if (type == UNIT_EPILOGUE) {
             // rows x R of the internal result through the pass's output mode (permute-out / flux
@@ -343,14 +359,30 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 }
             }
         } else {
-            for (int i = ct; i < nrows; i += kMConsumers) {   // element-wise pass: rows x R
-                const int64_t row = out0 + i;
-                const int64_t e = A.perm[row];
-                for (int q = 0; q < R; ++q) {
-                    const double v = A.user_in[e * A.ld + q];
-                    P.out[row * kMrhsMax + q] = type == UNIT_PROLOGUE ? A.eps_int[row] * pow4(v) : v;
+            // element-wise prologue: rows x R of the caller's external-order array permuted into the
+            // internal n x 64 layout (UNIT_PROLOGUE: w = eps T^4); coalesced, 4 elements in flight
+            const int tot = nrows * R;
+            for (int e0 = ct; e0 < tot; e0 += 4 * kMConsumers) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kMConsumers;
+                    v[u] = 0.0;
+                    if (e < tot) {
+                        const int64_t row = out0 + e / R;
+                        v[u] = __ldg(A.user_in + (int64_t)__ldg(A.perm + row) * A.ld + (e % R));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kMConsumers;
+                    if (e < tot) {
+                        const int64_t row = out0 + e / R;
+                        P.out[row * kMrhsMax + (e % R)] = type == UNIT_PROLOGUE ? __ldg(A.eps_int + row) * pow4(v[u]) : v[u];
+                    }
                 }
             }
+            // the rest of the 64-wide rows stays zero-free of stale values: columns R..63 are never read
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[s]);
