@@ -336,13 +336,35 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             std::vector<int32_t> hrank(ids.size());
             HM_CUDA(cudaMemcpyAsync(hrank.data(), drank.p, ids.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
             HM_CUDA(cudaStreamSynchronize(s));
+            // compact the batch: keep only the first k columns of U and V of the low-rank blocks
+            // (scratch is sized for the rank cap; stored factors are a small fraction of it)
+            std::vector<int64_t> ctasks;
+            int64_t ctot = 0;
             for (size_t q = 0; q < ids.size(); ++q) {
                 const size_t bb = ids[q];
+                const Blk& B = g.blocks[bb];
+                const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0, kq = hrank[q];
                 F.blk_rank[bb] = hrank[q];
                 F.blk_kind[bb] = hrank[q] >= hkcap[q] ? KIND_ADM_DENSE : KIND_LR;
-                rec[bb] = AcaRec{(int)batches.size(), huoff[q], hvoff[q], hkcap[q]};
+                if (F.blk_kind[bb] != KIND_LR) continue;
+                const int64_t uo = ctot, vo = ctot + ((m * kq + 1) & ~1LL);
+                ctot = vo + ((nn * kq + 1) & ~1LL);
+                if (kq > 0) {
+                    ctasks.insert(ctasks.end(), {uo, (int64_t)(uintptr_t)(scratch.p + huoff[q]), m * kq, 1, 1, 0, m * kq});
+                    ctasks.insert(ctasks.end(), {vo, (int64_t)(uintptr_t)(scratch.p + hvoff[q]), nn * kq, 1, 1, 0, nn * kq});
+                }
+                rec[bb] = AcaRec{(int)batches.size(), uo, vo, hkcap[q]};
             }
-            batches.push_back(std::move(scratch));
+            DBuf<double> compact;
+            compact.alloc(c, (size_t)std::max<int64_t>(ctot, 2), "ACA factors");
+            if (!ctasks.empty()) {
+                DBuf<int64_t> dct;
+                dct.upload(c, ctasks, "compaction tasks", s);
+                k::pack(dct.p, (int)(ctasks.size() / 7), compact.p, s);
+                HM_CUDA(cudaStreamSynchronize(s));
+            }
+            scratch.reset();
+            batches.push_back(std::move(compact));
         }
         int32_t herr[4];
         HM_CUDA(cudaMemcpy(herr, err.p, sizeof(herr), cudaMemcpyDeviceToHost));

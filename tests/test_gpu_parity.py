@@ -304,3 +304,90 @@ def test_config2_full_size(hm, ctx):
     torch.cuda.synchronize()
     sig = vf.SIGMA_SB * 700.0 ** 4
     assert np.abs(q.cpu().numpy()).max() <= 10 * cfg.eps_aca * sig
+
+
+# ---------------------------------------------------------------- BASELINE configs[2] (C3, 82,000 facets)
+@pytest.mark.slow
+def test_config3_capped_cylinder_sampled(hm, ctx):
+    """C3 (capped cylinder R = 1, L = 4, reading R17 B: 82,000 facets) at full size: exact partition vs
+    the oracle's own Alg. 1 / Alg. 2, F x and a block of 8 right-hand sides (DMMA engine) vs 2,000 sampled
+    dense rows, and the solve residual on the sampled rows (kappa(C) ~ 1.7), all within 10 eps_ACA."""
+    import torch
+    from oracle import tree as otree
+    cfg = synth.make_config(3, nrhs=8)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    tr = otree.build_cluster_tree(f.centroid, cfg.n_min)
+    assert (hm.hm_export_perm(g) == tr.perm).all()
+    Q = otree.partition_table(otree.build_block_tree(tr, 1.0))
+    P = hm.hm_export_partition(g, F)
+    assert P.shape[0] == Q.shape[0] and (P[:, :6] == Q[:, :6]).all()
+    rows = synth.sample_rows(synth.stream_seed(cfg.seed, 999), f.n, 2000)
+    X = cfg.rhs()
+    Y = torch.empty(f.n, 8, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, torch.from_numpy(X).cuda(), Y)
+    y1 = torch.empty(f.n, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, torch.from_numpy(X[:, 0].copy()).cuda(), y1)
+    torch.cuda.synchronize()
+    Ys = vf.sampled_apply(f.centroid, f.normal, f.area, rows, X)
+    Yh = Y.cpu().numpy()
+    for c in range(8):
+        assert rel(Yh[rows, c], Ys[:, c]) <= 10 * cfg.eps_aca
+    assert rel(y1.cpu().numpy()[rows], Ys[:, 0]) <= 10 * cfg.eps_aca
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, X[:, 0].copy(), z)
+    r = vf.sampled_residual(f.centroid, f.normal, f.area, cfg.emissivity, rows, z[:, None], X[:, :1])[:, 0]
+    assert np.linalg.norm(r) / np.linalg.norm(X[rows, 0]) <= 10 * cfg.eps_aca
+
+
+# ---------------------------------------------------------------- BASELINE configs[3], configs[4] (F apply)
+# Their solve needs the H-arithmetic H-LU (DESIGN.md §9); the F apply runs at full size.
+@pytest.mark.slow
+def test_config4_apply_sampled(hm, ctx):
+    """C4 (icosphere sub 7, 327,680 facets, leaf 128): F x, single vector and 64 right-hand sides (DMMA
+    engine), vs 300 sampled dense rows within 10 eps_ACA; the stage-A factorisation reports
+    HM_ERR_UNSUPPORTED (needs ~2.4 TB dense) instead of failing."""
+    import torch
+    cfg = synth.make_config(4, nrhs=64)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    rows = synth.sample_rows(synth.stream_seed(cfg.seed, 999), f.n, 300)
+    X = cfg.rhs()
+    Y = torch.empty(f.n, 64, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, torch.from_numpy(X).cuda(), Y)
+    y1 = torch.empty(f.n, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, torch.from_numpy(X[:, 0].copy()).cuda(), y1)
+    torch.cuda.synchronize()
+    Ys = vf.sampled_apply(f.centroid, f.normal, f.area, rows, X)
+    Yh = Y.cpu().numpy()
+    assert max(rel(Yh[rows, c], Ys[:, c]) for c in range(64)) <= 10 * cfg.eps_aca
+    assert rel(y1.cpu().numpy()[rows], Ys[:, 0]) <= 10 * cfg.eps_aca
+    with pytest.raises(hm.HMError) as ei:
+        hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    assert ei.value.status == "HM_ERR_UNSUPPORTED"
+
+
+@pytest.mark.slow
+def test_config5_sphere_exact_rank_one_and_closed_form(hm, ctx):
+    """C5 geometry (icosphere sub 8, 1,310,720 facets, eps_ACA = 1e-5) in sphere-exact mode: every admissible
+    block is exactly rank 1 (A_sigma A_tau^T / 4 pi) -- an integer pin at a size no dense oracle reaches --
+    and F x (64 right-hand sides through the DMMA engine) equals the closed form (a (a^T x) - a o a o x) /
+    (4 pi c) (SURVEY.md §8(c) pins) to rounding."""
+    import torch
+    cfg = synth.make_config(5, exact=True, nrhs=64)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    P = hm.hm_export_partition(g, F)
+    lr = P[:, 6] == 1
+    assert lr.sum() > 800000 and (P[lr, 7] == 1).all()
+    X = cfg.rhs()
+    Y = torch.empty(f.n, 64, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, torch.from_numpy(X).cuda(), Y)
+    torch.cuda.synchronize()
+    A = f.area
+    cvec = np.minimum((A.sum() - A) / (4 * np.pi), 1.0)
+    Yh = Y.cpu().numpy()
+    for c in (0, 17, 63):
+        Fx = (A * (A @ X[:, c]) - A * A * X[:, c]) / (4 * np.pi) / cvec
+        assert rel(Yh[:, c], Fx) <= 1e-12
