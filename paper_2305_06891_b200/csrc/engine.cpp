@@ -162,6 +162,23 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
             }
         }
     }
+    {   // HM_ENGINE_STATS=2: per-pass shape of the program (diagnostics)
+        const char* e = getenv("HM_ENGINE_STATS");
+        if (e && e[0] == '2') {
+            for (size_t p = 0; p < h_passes.size(); ++p) {
+                const Pass& P = h_passes[p];
+                int64_t bytes = 0, nu = P.n_units, small = 0;
+                for (int64_t u = P.first_unit; u < P.first_unit + P.n_units; ++u) {
+                    const int64_t b = 8LL * h_units[u].ncols * h_units[u].ld;
+                    bytes += b;
+                    small += b < 16384;
+                }
+                fprintf(stderr, "[program %s] pass %zu type %d mode %d in %d: units %lld tasks %lld bytes %.1f MB "
+                        "avg %.1f KB (<16KB: %lld)\n", mrhs ? "mrhs" : "1rhs", p, P.type, P.mode, P.in_mode,
+                        (long long)nu, (long long)P.n_tasks, bytes / 1e6, nu ? bytes / 1e3 / nu : 0.0, (long long)small);
+            }
+        }
+    }
     passes.upload(ctx, h_passes, "engine passes", s);
     units.upload(ctx, h_units, "engine units", s);
     tasks.upload(ctx, h_tasks, "engine tasks", s);
