@@ -209,14 +209,14 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
     if (a.ld == 0) a.ld = 1;
     static const bool want_stats = [] { const char* e = getenv("HM_ENGINE_STATS"); return e && e[0] == '1'; }();
     if (want_stats) {
-        if (!stats.p) stats.alloc(nullptr, 16, "engine stats");
-        HM_CUDA(cudaMemsetAsync(stats.p, 0, 16 * sizeof(unsigned long long), s));
+        if (!stats.p) stats.alloc(nullptr, 16 + 64, "engine stats");
+        HM_CUDA(cudaMemsetAsync(stats.p, 0, (16 + 64) * sizeof(unsigned long long), s));
         a.stats = stats.p;
     }
     if (mrhs) engine_mrhs_launch(a, grid, s);
     else engine_launch(a, grid, s);
     if (want_stats) {
-        unsigned long long h[16];
+        unsigned long long h[16 + 64];
         HM_CUDA(cudaMemcpyAsync(h, stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaStreamSynchronize(s));
         const double G = (double)grid;
@@ -226,6 +226,13 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
                 "compute %.1f task-end %.1f | retire wait %.1f work %.1f | producer wait-pempty %.1f total %.1f | consumer wait-gathered %.1f\n",
                 h_passes.size(), h_units.size(), grid, h[0] / G / 1e3, h[1] / G / 1e3, h[2] / G, h[3] / G / 1e3,
                 h[4] / G / 1e3, h[5] / G / 1e3, h[6] / G / 1e3, h[7] / G / 1e3, h[8] / G / 1e3, h[9] / G / 1e3, h[10] / G / 1e3, h[11] / G / 1e3, h[12] / G / 1e3, h[13] / G / 1e3);
+        if (!mrhs)
+            for (size_t p = 0; p < h_passes.size() && p < 16; ++p) {
+                const unsigned long long* q = h + 16 + 4 * p;
+                fprintf(stderr, "   pass %zu: chunks/CTA %.1f | consumer kcycles/CTA: wait-gathered %.1f wait-payload %.1f "
+                        "compute %.1f (%.0f cycles/chunk)\n", p, q[3] / G, q[0] / G / 1e3, q[1] / G / 1e3, q[2] / G / 1e3,
+                        q[3] ? (double)q[2] / q[3] : 0.0);
+            }
     }
 }
 
