@@ -592,7 +592,7 @@ void launch_flux(Ctx* c, HLU& L, const double* Td, double* qd, int ld, int col, 
         a.eps_int = L.eps_pad.p;
         a.area_int = L.area_pad.p;
         a.g_int = L.g_pad.p;
-        a.T_pad = L.xtA_loc.p;
+        a.T_pad = L.T_pad;
         L.sp_flux.launch(c, g, a, s);
     } else {
         a.eps_int = L.eps_int.p;

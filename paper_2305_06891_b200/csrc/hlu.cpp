@@ -291,8 +291,6 @@ void factor_hlu(HLU& L, const double* emissivity) {
     // cut level (reading R27): < 0 -> 0 (the default: U^-1 (L^-1 b) with the inverse factors
     // in F's partition, fewest dependent passes, measured fastest on C2); >= depth -> pure level form
     const int Lc = L.params.cut_level < 0 ? 0 : std::min(L.params.cut_level, D);
-    if (g.shard.sharded() && Lc != 0)
-        throw Error(HM_ERR_UNSUPPORTED, "sharded solve (world > 1) is built in the inverse-factor form: cut_level 0");
     L.cut_level = Lc;
     fz.cut = Lc;
     fz.fwd_src.assign(std::max(Lc, 0), {});
@@ -370,27 +368,42 @@ void factor_hlu(HLU& L, const double* emissivity) {
     L.bwd.resize(std::max(Lc, 0));
     L.bytes = L.bytes_leaf = L.n_blocks = L.n_lr = L.rank_sum = 0;
     L.rank_max = 0;
-    int64_t maxt = 0;
+    // t slots: disjoint per operator within a sweep's buffer (xtA: forward levels then leafL; xtB:
+    // backward levels then leafU)
+    int64_t tA = 0, tB = 0;
     for (int lv = 0; lv < Lc; ++lv) {
-        build_hop(c, g, fz.fwd_src[lv], L.fwd[lv], s);
-        build_hop(c, g, fz.bwd_src[lv], L.bwd[lv], s);
+        build_hop(c, g, fz.fwd_src[lv], L.fwd[lv], s, nullptr, tA);
+        build_hop(c, g, fz.bwd_src[lv], L.bwd[lv], s, nullptr, tB);
         account(L, L.fwd[lv]);
         account(L, L.bwd[lv]);
-        maxt = std::max({maxt, L.fwd[lv].n_t, L.bwd[lv].n_t});
+        tA += L.fwd[lv].n_t;
+        tB += L.bwd[lv].n_t;
     }
-    build_hop(c, g, srcL, L.leafL, s);
-    build_hop(c, g, srcU, L.leafU, s);
-    if (g.shard.sharded()) {   // this rank's rows of L^-1 and U^-1 (inverse-factor form, Lc == 0)
-        build_hop(c, g, srcL, L.leafL_loc, s, &g.shard);
-        build_hop(c, g, srcU, L.leafU_loc, s, &g.shard);
+    build_hop(c, g, srcL, L.leafL, s, nullptr, tA);
+    build_hop(c, g, srcU, L.leafU, s, nullptr, tB);
+    tA += L.leafL.n_t;
+    tB += L.leafU.n_t;
+    int64_t tA_loc = 0, tB_loc = 0;
+    if (g.shard.sharded()) {   // this rank's rows of the level-form W operators and the cut inverse factors
+        L.fwd_loc.resize(std::max(Lc, 0));
+        L.bwd_loc.resize(std::max(Lc, 0));
+        for (int lv = 0; lv < Lc; ++lv) {
+            build_hop(c, g, fz.fwd_src[lv], L.fwd_loc[lv], s, &g.shard, tA_loc);
+            build_hop(c, g, fz.bwd_src[lv], L.bwd_loc[lv], s, &g.shard, tB_loc);
+            tA_loc += L.fwd_loc[lv].n_t;
+            tB_loc += L.bwd_loc[lv].n_t;
+        }
+        build_hop(c, g, srcL, L.leafL_loc, s, &g.shard, tA_loc);
+        build_hop(c, g, srcU, L.leafU_loc, s, &g.shard, tB_loc);
+        tA_loc += L.leafL_loc.n_t;
+        tB_loc += L.leafU_loc.n_t;
     }
     account(L, L.leafL);
     account(L, L.leafU);
-    maxt = std::max({maxt, L.leafL.n_t, L.leafU.n_t});
     L.bytes_leaf = L.leafL.p1_doubles() + L.leafL.p2_doubles() + L.leafU.p1_doubles() + L.leafU.p2_doubles();
     fz.staging.clear();
-    L.xtA.alloc(c, (size_t)(n + maxt), "solve xtA");
-    L.xtB.alloc(c, (size_t)(n + maxt), "solve xtB");
+    L.xtA.alloc(c, (size_t)(n + tA), "solve xtA");
+    L.xtB.alloc(c, (size_t)(n + tB), "solve xtB");
     L.z.alloc(c, (size_t)n, "solve z");
     L.setup_seconds[2] = now_seconds() - t0;
 
@@ -517,30 +530,63 @@ void factor_hlu(HLU& L, const double* emissivity) {
         L.eps_pad.upload(c, ep, "eps (padded)", s);
         L.area_pad.upload(c, ap, "area (padded)", s);
         L.g_pad.upload(c, gp, "g (padded)", s);
-        L.xtA_loc.alloc(c, (size_t)(np + L.leafL_loc.n_t), "solve xtA (local)");
-        L.xtB_loc.alloc(c, (size_t)(np + L.leafU_loc.n_t), "solve xtB (local)");
-        auto first_op = [&](SegProgram& SP, int in_mode) {   // allgather b (or T) -> L^-1 -> y
-            Program& P = SP.add(L.xtA_loc.p, true);
-            P.n_x = np;
-            P.add_stream(L.leafL_loc.p1, L.leafL_loc, L.xtA_loc.p, L.xtA_loc.p, OUT_ASSIGN, DEP_BARRIER, nullptr, in_mode);
-            P.add_stream(L.leafL_loc.p2, L.leafL_loc, L.xtA_loc.p, L.xtB_loc.p, OUT_ASSIGN, DEP_BARRIER, nullptr,
-                         in_mode, -1);
+        L.xtA_loc.alloc(c, (size_t)(np + tA_loc), "solve xtA (local)");
+        L.xtB_loc.alloc(c, (size_t)(np + tB_loc), "solve xtB (local)");
+        // Exchange points: the input is allgathered first; a level-form update at a
+        // tree level lv < log2(world) reads rows updated on other ranks, so it is preceded by an
+        // allgather of the vector it reads (levels >= log2(world) are rank-local); so are the cut-level
+        // inverse factors when the cut is above log2(world), and the first backward level (L^-1 produced
+        // only this rank's rows).
+        int gl = 0;
+        while ((1 << gl) < S.world) ++gl;
+        // flux: T is gathered into xtA's x region (cut 0: the first operator's gathers form w = eps T^4
+        // on the fly) or, in the level form whose updates overwrite b in place, into T_loc, from which
+        // a prologue pass materialises w; the epilogue reads T from there
+        if (Lc > 0) L.T_loc.alloc(c, (size_t)np, "T (padded)");
+        L.T_pad = Lc > 0 ? L.T_loc.p : L.xtA_loc.p;
+        auto sweeps = [&](SegProgram& SP, int in_mode) -> Program* {
+            const bool pro = Lc > 0 && in_mode == IN_FLUXI;
+            Program* P = &SP.add(pro ? L.T_loc.p : L.xtA_loc.p, true);
+            P->n_x = np;
+            int im = in_mode;
+            if (pro) {
+                P->add_elementwise(UNIT_PROLOGUE_INT, np, L.xtA_loc.p, 1024, L.T_loc.p);
+                P->sweep_dep[0] = (int32_t)P->h_passes.size() - 1;   // the sweep's root waits for it
+                im = IN_PLAIN;
+            }
+            for (int lv = 0; lv < Lc; ++lv) {
+                if (lv > 0 && lv < gl) { P = &SP.add(L.xtA_loc.p, false); P->n_x = np; }
+                HOp& op = L.fwd_loc[lv];
+                const auto m1 = node_map(op.p1, lv), m2 = node_map(op.p2, lv);
+                P->add_stream(op.p1, op, L.xtA_loc.p, L.xtA_loc.p, OUT_ASSIGN, DEP_FWD_P1, &m1);
+                P->add_stream(op.p2, op, L.xtA_loc.p, L.xtA_loc.p, OUT_SUB, DEP_FWD_P2, &m2);
+            }
+            if (Lc > 0 && Lc < gl) { P = &SP.add(L.xtA_loc.p, false); P->n_x = np; }
+            const auto l1 = node_map(L.leafL_loc.p1, Lc), l2 = node_map(L.leafL_loc.p2, Lc);
+            P->add_stream(L.leafL_loc.p1, L.leafL_loc, L.xtA_loc.p, L.xtA_loc.p, OUT_ASSIGN, DEP_FWD_P1, &l1, im);
+            P->add_stream(L.leafL_loc.p2, L.leafL_loc, L.xtA_loc.p, L.xtB_loc.p, OUT_ASSIGN, DEP_FWD_P2, &l2, im);
+            for (int lv = 0; lv < Lc; ++lv) {
+                if (lv < gl) { P = &SP.add(L.xtB_loc.p, false); P->n_x = np; }
+                HOp& op = L.bwd_loc[lv];
+                const auto m1 = node_map(op.p1, lv), m2 = node_map(op.p2, lv);
+                P->add_stream(op.p1, op, L.xtB_loc.p, L.xtB_loc.p, OUT_ASSIGN, DEP_BWD_P1, &m1);
+                P->add_stream(op.p2, op, L.xtB_loc.p, L.xtB_loc.p, OUT_SUB, DEP_BWD_P2, &m2);
+            }
+            if (Lc < gl) { P = &SP.add(L.xtB_loc.p, false); P->n_x = np; }
+            return P;
         };
-        first_op(L.sp_solve, IN_PLAIN);
         {
-            Program& P = L.sp_solve.add(L.xtB_loc.p, false);   // allgather y -> U^-1 -> z (local slice)
-            P.n_x = np;
-            P.add_stream(L.leafU_loc.p1, L.leafU_loc, L.xtB_loc.p, L.xtB_loc.p, OUT_ASSIGN);
-            P.add_stream(L.leafU_loc.p2, L.leafU_loc, L.xtB_loc.p, nullptr, OUT_LOCAL, DEP_BARRIER, nullptr, IN_PLAIN, -1);
+            Program* P = sweeps(L.sp_solve, IN_PLAIN);
+            const auto u1 = node_map(L.leafU_loc.p1, Lc), u2 = node_map(L.leafU_loc.p2, Lc);
+            P->add_stream(L.leafU_loc.p1, L.leafU_loc, L.xtB_loc.p, L.xtB_loc.p, OUT_ASSIGN, DEP_BWD_P1, &u1);
+            P->add_stream(L.leafU_loc.p2, L.leafU_loc, L.xtB_loc.p, nullptr, OUT_LOCAL, DEP_BWD_P2, &u2);
         }
         L.sp_solve.finalize(c, s, &g);
-        first_op(L.sp_flux, IN_FLUXI);
         {
-            Program& P = L.sp_flux.add(L.xtB_loc.p, false);    // allgather y -> U^-1 -> z into F's x region
-            P.n_x = np;
-            P.add_stream(L.leafU_loc.p1, L.leafU_loc, L.xtB_loc.p, L.xtB_loc.p, OUT_ASSIGN);
-            P.add_stream(L.leafU_loc.p2, L.leafU_loc, L.xtB_loc.p, Fm.xt_loc.p, OUT_ASSIGN, DEP_BARRIER, nullptr,
-                         IN_PLAIN, -1);
+            Program* P = sweeps(L.sp_flux, IN_FLUXI);
+            const auto u1 = node_map(L.leafU_loc.p1, Lc), u2 = node_map(L.leafU_loc.p2, Lc);
+            P->add_stream(L.leafU_loc.p1, L.leafU_loc, L.xtB_loc.p, L.xtB_loc.p, OUT_ASSIGN, DEP_BWD_P1, &u1);
+            P->add_stream(L.leafU_loc.p2, L.leafU_loc, L.xtB_loc.p, Fm.xt_loc.p, OUT_ASSIGN, DEP_BWD_P2, &u2);
         }
         {
             Program& P = L.sp_flux.add(Fm.xt_loc.p, false);    // allgather z -> F -> q (local slice)

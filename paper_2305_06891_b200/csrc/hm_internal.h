@@ -196,7 +196,8 @@ struct alignas(16) Unit {
 static_assert(sizeof(Unit) % 16 == 0, "Unit is TMA-copied");
 // UNIT_EPILOGUE (multi-RHS): rows of an internal n x kMrhsMax result emitted through the pass's output
 // mode (permute-out / flux epilogue) by element-wise units, coalesced and fully parallel
-enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2, UNIT_EPILOGUE = 3 };
+// UNIT_PROLOGUE_INT (sharded level form): out[row] = eps[row] * in[row]^4 on padded internal rows
+enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2, UNIT_EPILOGUE = 3, UNIT_PROLOGUE_INT = 4 };
 constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage
 constexpr int kMrhsMax = 64;                // multi-RHS block width (columns of X per program launch)
 constexpr int kMrhsMaxCols = 64;            // multi-RHS chunk: <= 64 panel columns (X tile 64 x 64)
@@ -278,8 +279,11 @@ struct HOp {
 
 // Build the operator; XT layout is [x (n_x) | t (n_t)].  With a shard (world > 1) only the block
 // rows of this rank are stored, x indices and phase-2 outputs use the padded layout (n_x = n_pad).
+// t_off: first t slot of this operator in its XT buffer (operators of different levels that share a
+// buffer get disjoint t regions, so a level's phase 1 never overwrites t still to be read by another
+// subtree's phase 2 of an earlier level)
 void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s,
-               const Shard* sh = nullptr);
+               const Shard* sh = nullptr, int64_t t_off = 0);
 
 // ------------------------------------------------------------------ persistent stream engine
 struct Pass {
@@ -448,6 +452,9 @@ struct HLU {
     Program prog_flux;    // prologue -> solve passes -> F phase 1 -> F phase 2 + flux epilogue
     // sharded hot path (world > 1, inverse-factor form): this rank's rows of L^-1, U^-1
     HOp leafL_loc, leafU_loc;
+    std::vector<HOp> fwd_loc, bwd_loc;   // level-form W operators, this rank's rows
+    DBuf<double> T_loc;                  // sharded level-form flux: gathered temperatures (padded)
+    const double* T_pad = nullptr;       // where the sharded flux epilogue reads T
     DBuf<double> xtA_loc, xtB_loc;
     DBuf<double> eps_pad, area_pad, g_pad;
     SegProgram sp_solve;  // AG b -> L^-1 -> AG y -> U^-1

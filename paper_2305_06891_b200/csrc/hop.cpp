@@ -141,7 +141,8 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
     HM_CUDA(cudaMemsetAsync(P.counters.p, 0, sizeof(int32_t) * std::max<int32_t>(grp, 1), s));
 }
 
-void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s, const Shard* sh) {
+void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s, const Shard* sh,
+               int64_t t_off) {
     const int64_t n = g.n;
     // sharded: only blocks with rows on this rank; x indices and outputs in the
     // padded layout (x region of XT = n_pad), t after it
@@ -192,7 +193,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
             while (q1 < members.size() && K + blocks[members[q1]].k <= 128) K += blocks[members[q1++]].k;
             const SrcBlock& B0 = blocks[members[q0]];
             const int64_t ld = align2(K);
-            Panel pn{off, nx + tcount, (int32_t)ld, (int32_t)K, (int32_t)B0.n, (int32_t)colsrc.size(), B0.c0,
+            Panel pn{off, nx + t_off + tcount, (int32_t)ld, (int32_t)K, (int32_t)B0.n, (int32_t)colsrc.size(), B0.c0,
                      (int32_t)B0.n};
             for (int64_t j = 0; j < B0.n; ++j) colsrc.push_back(xi(B0.c0 + j));
             int64_t local = 0;
@@ -251,7 +252,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
                     op.p2.doubles += lm * B.n;
                 } else {
                     pack.insert(pack.end(), {off, (int64_t)(uintptr_t)(B.U + ro), lm, (int64_t)B.k, 1, B.u_ld, ld});
-                    for (int q = 0; q < B.k; ++q) colsrc.push_back((int32_t)(nx + tbase[b] + q));
+                    for (int q = 0; q < B.k; ++q) colsrc.push_back((int32_t)(nx + t_off + tbase[b] + q));
                     op.items.push_back(HOp::ItemRec{off, ld, voff[b], vld[b], lr0, lm, B.c0, B.n, B.k});
                     off += ld * B.k;
                     pn.ncols += B.k;
@@ -261,7 +262,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
             op.p2.panels.push_back(pn);
         }
     }
-    if (nx + tcount >= INT32_MAX || (int64_t)colsrc.size() >= INT32_MAX)
+    if (nx + t_off + tcount >= INT32_MAX || (int64_t)colsrc.size() >= INT32_MAX)
         throw Error(HM_ERR_UNSUPPORTED, "index space exceeds int32");
 
     op.arena.alloc(ctx, (size_t)std::max<int64_t>(off, 2), "operator arena");

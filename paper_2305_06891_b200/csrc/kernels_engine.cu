@@ -496,10 +496,17 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                 }
             }
         } else {
-            for (int i = ct; i < u.nrows; i += kConsumers) {   // element-wise: rows [out0, out0 + nrows)
-                const int64_t row = u.out0 + i;
-                const double v = A.user_in[(int64_t)A.perm[row] * A.ld + A.col];
-                P.out[row] = u.type == UNIT_PROLOGUE ? A.eps_int[row] * pow4(v) : v;
+            if (u.type == UNIT_PROLOGUE_INT) {   // sharded: w = eps T^4 in place on padded internal rows
+                for (int i = ct; i < u.nrows; i += kConsumers) {
+                    const int64_t row = u.out0 + i;
+                    P.out[row] = A.eps_int[row] * pow4(P.in[row]);
+                }
+            } else {
+                for (int i = ct; i < u.nrows; i += kConsumers) {   // element-wise: rows [out0, out0 + nrows)
+                    const int64_t row = u.out0 + i;
+                    const double v = A.user_in[(int64_t)A.perm[row] * A.ld + A.col];
+                    P.out[row] = u.type == UNIT_PROLOGUE ? A.eps_int[row] * pow4(v) : v;
+                }
             }
         }
         // chunk consumed: release its payload stage and header slot (per warp, no CTA-wide barrier)

@@ -391,3 +391,28 @@ def test_config5_sphere_exact_rank_one_and_closed_form(hm, ctx):
     for c in (0, 17, 63):
         Fx = (A * (A @ X[:, c]) - A * A * X[:, c]) / (4 * np.pi) / cvec
         assert rel(Yh[:, c], Fx) <= 1e-12
+
+
+def test_level_form_repeatable_bitwise(hm, ctx):
+    """The level-scheduled solve (cut = depth) and flux repeated 30 times give bitwise identical results
+    (no floating-point atomics; every level's phase-1 values live in their own slots, so no subtree's
+    phase 1 can overwrite values another subtree's phase 2 of an earlier level still reads)."""
+    import torch
+    cfg = synth.make_config(2, geometry=synth.icosphere(5))
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=99)
+    b = torch.from_numpy(cfg.rhs()[:, 0].copy()).cuda()
+    T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+    z = torch.empty_like(b)
+    q = torch.empty_like(b)
+    hm.hm_solve_C(ctx, LU, b, z)
+    hm.hm_radiative_flux(ctx, F, LU, T, q)
+    torch.cuda.synchronize()
+    z0, q0 = z.cpu().numpy().copy(), q.cpu().numpy().copy()
+    for _ in range(30):
+        hm.hm_solve_C(ctx, LU, b, z)
+        hm.hm_radiative_flux(ctx, F, LU, T, q)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.cpu().numpy(), z0)
+    assert np.array_equal(q.cpu().numpy(), q0)
