@@ -23,7 +23,8 @@
  *    (NULL = legacy default stream).
  *  - Ownership: the caller owns all argument buffers.  The library owns its handles and all
  *    device memory it allocates; hm_destroy_* / hm_finalize free them.  Handles are immutable
- *    after setup and may be used from one host thread at a time.
+ *    after setup and may be used from one host thread and one stream at a time (the hot-path
+ *    calls of an F / LU pair share their device workspace; calls are stream-ordered).
  *  - Asynchronous kernel faults surface as HM_ERR_CUDA at the next synchronising call;
  *    environment HM_DEBUG=1 synchronises after every launch.
  *  - There is no CPU fallback: without a CUDA device hm_init returns HM_ERR_CUDA (device < 0 gives
