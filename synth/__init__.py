@@ -88,6 +88,8 @@ class Facets:
     aabb: np.ndarray          # (n,6) lo_x lo_y lo_z hi_x hi_y hi_z of the triangle
     tris: np.ndarray | None = None   # (n,3,3) vertices, kept for diagnostics
     name: str = ""
+    vert: np.ndarray | None = None   # (n,3) int64 vertex (node) ids of each triangle
+    n_nodes: int = 0                 # number of mesh vertices (finite-element nodes)
 
     @property
     def n(self) -> int:
@@ -107,7 +109,7 @@ def _facets_from_tris(V: np.ndarray, T: np.ndarray, interior=(0.0, 0.0, 0.0), na
     tri = np.stack([v0, v1, v2], axis=1)
     aabb = np.concatenate([tri.min(axis=1), tri.max(axis=1)], axis=1)
     return Facets(np.ascontiguousarray(cen), np.ascontiguousarray(nrm), np.ascontiguousarray(area),
-                  np.ascontiguousarray(aabb), tri, name)
+                  np.ascontiguousarray(aabb), tri, name, np.ascontiguousarray(T, dtype=np.int64), int(V.shape[0]))
 
 
 def icosphere_mesh(sub: int):
@@ -229,6 +231,23 @@ def temperatures(seed: int, n: int, nrhs: int) -> np.ndarray:
 
 def emissivities(seed: int, n: int, lo=0.3, hi=0.95) -> np.ndarray:
     return lo + (hi - lo) * uniform(stream_seed(seed, 0), n)
+
+
+def projection_csr(f: Facets):
+    """The facet <- node projection of PAPER.md:168-183 (eqn:projection_operator) for linear triangles:
+    row i (external facet order) has the triangle's three vertex ids.  Returned as CSR arrays
+    (row_ptr int64 [n+1], col int32 [3n], val float64 [3n]); the values are the mesh's linear-basis
+    averages (1/A_i) int phi_M dS over a flat triangle, 1/3 each (an input, like the geometry)."""
+    n = f.n
+    row_ptr = np.arange(0, 3 * n + 1, 3, dtype=np.int64)
+    col = np.ascontiguousarray(f.vert.reshape(-1).astype(np.int32))
+    val = np.full(3 * n, 1.0 / 3.0)
+    return row_ptr, col, val
+
+
+def node_temperatures(seed: int, n_nodes: int) -> np.ndarray:
+    """Nodal temperatures T_M ~ U[300, 1000] K (stream k = 2000)."""
+    return 300.0 + 700.0 * uniform(stream_seed(seed, 2000), n_nodes)
 
 
 def make_config(cfg: int, *, exact: bool = False, geometry: Facets | None = None,
