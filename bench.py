@@ -285,6 +285,23 @@ def main():
                       "bytes_C": rep_lf["bytes_C"],
                       "solve_hbm_gbs": rep_lf["bytes_C"] / (lf_ms["solve_C"] * 1e-3) / 1e9}
         del LU_lf
+    # NEXT-1: the cavity Jacobian action J^cav x = 4 P^T Rbar P (T^3 o x) (eq:Jcav) GMRES applies, on the
+    # same operators (one projection + the flux program + one transpose projection)
+    jcav = None
+    if world == 1 and f.vert is not None:
+        Pj = hm.hm_projection_create(ctx, g, f.n_nodes, *synth.projection_csr(f))
+        Tn = torch.from_numpy(synth.node_temperatures(cfg.seed, f.n_nodes)).cuda()
+        xn = torch.from_numpy(synth.uniform(6, f.n_nodes) - 0.5).cuda()
+        yn = torch.empty_like(xn)
+        for _ in range(3):
+            hm.hm_cavity_jacobian(ctx, F, LU, Pj, Tn, xn, yn, stream=stream.cuda_stream)
+        ej0, ej1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ej0.record(stream)
+        for _ in range(args.profile_iters):
+            hm.hm_cavity_jacobian(ctx, F, LU, Pj, Tn, xn, yn, stream=stream.cuda_stream)
+        ej1.record(stream)
+        torch.cuda.synchronize()
+        jcav = {"ms": ej0.elapsed_time(ej1) / args.profile_iters, "n_nodes": f.n_nodes}
     peak, peak_src = peaks()
     bytes_step = rep["bytes_F"] + rep["bytes_C"]
     bytes_local = rep["bytes_F_local"] + rep["bytes_C_local"]    # this rank's stored bytes (= bytes_step at N=1)
@@ -315,7 +332,7 @@ def main():
                        "ranks_C": {"mean": rep["rank_mean_C"], "max": rep["rank_max_C"]},
                        "setup_s": dict(rep["setup_seconds"], wall=setup_wall),
                        "solve_form": "inverse factors (cut level 0, DESIGN.md R27)",
-                       "level_form": level_form},
+                       "level_form": level_form, "cavity_jacobian_action": jcav},
             "roofline": {"bound": "hbm", "kernel": "engine_kernel (flux program)" + (" + NCCL allgathers, rank 0" if world > 1 else ""),
                          "achieved": achieved,
                          "peak": peak, "unit": "GB/s",

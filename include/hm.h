@@ -61,6 +61,7 @@ typedef struct hm_ctx hm_ctx;
 typedef struct hm_geom hm_geom;
 typedef struct hm_hmat hm_hmat;
 typedef struct hm_hlu hm_hlu;
+typedef struct hm_proj hm_proj;
 
 /* Alg. 1 / Alg. 2 parameters. */
 typedef struct {
@@ -171,6 +172,25 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LU, int32_t nrhs, const double* 
    factored from F. */
 hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, int32_t nrhs,
                             const double* T, double* q, void* stream);
+
+/* ---- cavity operator around the hot path (world == 1) ---------- */
+/* Facet <- node projection P (n_facets x n_nodes, PAPER.md:175-183 eqn:projection_operator,
+   P_iM = (1/A_i) int_{Gamma_i} phi_M dS) as host CSR arrays in EXTERNAL facet order: row_ptr[n+1]
+   (int64, row_ptr[0] = 0), col[nnz] node ids in [0, n_nodes), val[nnz].  The library copies them. */
+hm_status hm_projection_create(hm_ctx* ctx, const hm_geom* geom, int64_t n_nodes, const int64_t* row_ptr,
+                               const int32_t* col, const double* val, hm_proj** out);
+void hm_destroy_projection(hm_proj* P);
+/* Q = S eta with S = P^T Rbar P and eta_M = T_M^4 (eqn:flux_residual_3, eqn:S_def_matrix; R, Rbar of
+   eq:Rdef / eq:Rbardef): Q_N = sum_i q_i A_i P_iN with q of eq:qi_new_location at eta = P T^4 -- one
+   projection, one C^-1 solve, one F apply, one transpose projection.  T_nodes, Q_nodes: n_nodes x nrhs
+   (device or host, as for hm_radiative_flux).  LU must have been factored from F, P built on F's
+   geometry. */
+hm_status hm_cavity_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, hm_proj* P, int32_t nrhs,
+                         const double* T_nodes, double* Q_nodes, void* stream);
+/* y = J^cav x = 4 S (T^3 o x) (eq:Jcav): the action GMRES needs,
+   without forming the dense n_nodes x n_nodes J^cav.  Same layout as hm_cavity_flux. */
+hm_status hm_cavity_jacobian(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, hm_proj* P, int32_t nrhs,
+                             const double* T_nodes, const double* x_nodes, double* y_nodes, void* stream);
 
 /* ---- introspection (host buffers) ----------------------------------------------------- */
 hm_status hm_export_perm(const hm_geom* geom, int32_t* perm /* n: perm[internal] = external */);

@@ -95,6 +95,10 @@ def load_library(path: str = LIB_PATH):
         "hm_profile_flux": (C.c_int, [P, P, P, P, P, I32, P, P, P]),
         "hm_trace_flux": (C.c_int, [P, P, P, P, P, I32, C.POINTER(I32), P, P, P, P]),
         "hm_nccl_unique_id": (C.c_int, [P]),
+        "hm_projection_create": (C.c_int, [P, P, I64, P, P, P, C.POINTER(P)]),
+        "hm_destroy_projection": (None, [P]),
+        "hm_cavity_flux": (C.c_int, [P, P, P, P, I32, P, P, P]),
+        "hm_cavity_jacobian": (C.c_int, [P, P, P, P, I32, P, P, P, P]),
         "hm_shard_plan": (C.c_int, [P, C.c_int, P, P, C.POINTER(I64), P]),
         "hm_destroy_geom": (None, [P]),
         "hm_destroy_hmat": (None, [P]),
@@ -358,3 +362,40 @@ def hm_trace_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, max_passes: int = 256
                                     e.ctypes.data, by.ctypes.data, _stream(stream, T, q)), "hm_trace_flux")
     m = min(npass.value, max_passes)
     return [(i, float(b[i]), float(e[i]), int(by[i])) for i in range(m)]
+
+
+class Projection:
+    def __init__(self, ctx, h, geom, n_nodes):
+        self.ctx, self.h, self.geom, self.n_nodes = ctx, h, geom, n_nodes
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.hm_destroy_projection(self.h)
+            self.h = None
+
+
+def hm_projection_create(ctx: Context, geom: Geometry, n_nodes: int, row_ptr, col, val) -> Projection:
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col, dtype=np.int32)
+    cv = np.ascontiguousarray(val, dtype=np.float64)
+    h = C.c_void_p()
+    ctx.check(ctx.lib.hm_projection_create(ctx.h, geom.h, int(n_nodes), rp.ctypes.data, ci.ctypes.data,
+                                           cv.ctypes.data, C.byref(h)), "hm_projection_create")
+    return Projection(ctx, h, geom, int(n_nodes))
+
+
+def hm_cavity_flux(ctx: Context, F: HMatrix, LU: HLU, P: Projection, T_nodes, Q_nodes, stream=None):
+    pT, kT = _ptr(T_nodes)
+    pQ, kQ = _ptr(Q_nodes)
+    ctx.check(ctx.lib.hm_cavity_flux(ctx.h, F.h, LU.h, P.h, _nrhs(T_nodes, P.n_nodes), pT, pQ,
+                                     _stream(stream, T_nodes, Q_nodes)), "hm_cavity_flux")
+    return Q_nodes
+
+
+def hm_cavity_jacobian(ctx: Context, F: HMatrix, LU: HLU, P: Projection, T_nodes, x_nodes, y_nodes, stream=None):
+    pT, kT = _ptr(T_nodes)
+    px, kx = _ptr(x_nodes)
+    py, ky = _ptr(y_nodes)
+    ctx.check(ctx.lib.hm_cavity_jacobian(ctx.h, F.h, LU.h, P.h, _nrhs(T_nodes, P.n_nodes), pT, px, py,
+                                         _stream(stream, T_nodes, y_nodes)), "hm_cavity_jacobian")
+    return y_nodes

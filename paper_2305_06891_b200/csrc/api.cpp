@@ -772,3 +772,121 @@ hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* ou
 }
 
 }  // extern "C"
+
+// ============================================================================ cavity operator (NEXT-1)
+namespace {
+// y_facets = A o q(eta) = Rbar eta (eq:Rbardef) by the flux program with the eta input / Rbar output
+// modes, then Q_nodes = P^T y (eqn:S_def_matrix)
+void cavity_column(Ctx* c, HLU& L, Proj& P, const double* Tn, const double* xn, int mode, int ld, int col, double* Qn,
+                   cudaStream_t s) {
+    const Geom& g = *L.F->geom;
+    k::proj_facets(P.rp.p, P.ci.p, P.cv.p, Tn, xn, mode, ld, col, P.eta.p, P.n_facets, s);
+    ProgArgs a = base_args(g, P.eta.p, P.rbar.p, 1, 0);
+    a.sigma = 5.670374419e-8;  // DESIGN.md reading R2
+    a.eps_int = L.eps_int.p;
+    a.eps_ext = L.eps_ext.p;
+    a.area_int = g.d_geo.p + 6 * g.n;
+    a.g_int = L.g_int.p;
+    a.eta_in = 1;
+    a.rbar_out = 1;
+    L.prog_flux.launch(a, s);
+    k::proj_nodes(P.tp.p, P.ti.p, P.tv.p, P.rbar.p, ld, col, Qn, P.n_nodes, s);
+}
+
+hm_status cavity_call(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, hm_proj* Ph, int32_t nrhs, const double* T,
+                      const double* x, double* out, void* stream, int mode) {
+    if (!ctx || !Fh || !LUh || !Ph || !T || !out || nrhs < 1 || (mode == 1 && !x)) return HM_ERR_INVALID_ARG;
+    if (LUh->h.F != &Fh->h || Ph->p.geom != Fh->h.geom) {
+        ctx->c.last_error = "cavity operator: LU / projection not built for this F";
+        return HM_ERR_NOT_READY;
+    }
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        if (Fh->h.geom->shard.sharded())
+            throw Error(HM_ERR_UNSUPPORTED, "cavity operator: world == 1 only in this build");
+        HLU& L = const_cast<HLU&>(LUh->h);
+        Proj& P = Ph->p;
+        const size_t cnt = (size_t)P.n_nodes * nrhs;
+        cudaStream_t s = (cudaStream_t)stream;
+        bool h1 = false, h2 = false;
+        const double* Td = stage_in(c, P.host_in, T, cnt, s, h1);
+        const double* xd = mode == 1 ? stage_in(c, P.host_in2, x, cnt, s, h2) : nullptr;
+        const bool hout = !is_device_ptr(out);
+        double* od = out;
+        if (hout) {
+            if (P.host_out.n < cnt) P.host_out.alloc(c, cnt, "host staging (out)");
+            od = P.host_out.p;
+        }
+        for (int col = 0; col < nrhs; ++col) cavity_column(c, L, P, Td, xd, mode, nrhs, col, od, s);
+        if (hout) HM_CUDA(cudaMemcpyAsync(out, od, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (h1 || h2 || hout) HM_CUDA(cudaStreamSynchronize(s));
+    });
+}
+}  // namespace
+
+extern "C" {
+
+hm_status hm_projection_create(hm_ctx* ctx, const hm_geom* geom, int64_t n_nodes, const int64_t* row_ptr,
+                               const int32_t* col, const double* val, hm_proj** out) {
+    if (!ctx || !geom || !row_ptr || !col || !val || !out || n_nodes < 1) return HM_ERR_INVALID_ARG;
+    *out = nullptr;
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        if (c->host_only) throw Error(HM_ERR_NOT_READY, "host-only context");
+        const int64_t n = geom->g.n;
+        if (row_ptr[0] != 0) throw Error(HM_ERR_INVALID_ARG, "projection: row_ptr[0] must be 0");
+        for (int64_t i = 0; i < n; ++i)
+            if (row_ptr[i + 1] < row_ptr[i]) throw Error(HM_ERR_INVALID_ARG, "projection: row_ptr not monotone");
+        const int64_t nnz = row_ptr[n];
+        for (int64_t q = 0; q < nnz; ++q) {
+            if (col[q] < 0 || col[q] >= n_nodes)
+                throw Error(HM_ERR_INVALID_ARG, "projection: node id out of range at entry " + std::to_string(q));
+            if (!std::isfinite(val[q])) throw Error(HM_ERR_INVALID_ARG, "projection: non-finite value");
+        }
+        auto* H = new hm_proj;
+        std::unique_ptr<hm_proj> guard(H);
+        Proj& P = H->p;
+        P.ctx = c;
+        P.geom = &geom->g;
+        P.n_facets = n;
+        P.n_nodes = n_nodes;
+        const cudaStream_t s = c->stream;
+        P.rp.upload(c, std::vector<int64_t>(row_ptr, row_ptr + n + 1), "P row_ptr", s);
+        P.ci.upload(c, std::vector<int32_t>(col, col + nnz), "P col", s);
+        P.cv.upload(c, std::vector<double>(val, val + nnz), "P val", s);
+        // transpose (node -> facets), entries in increasing facet order: fixed summation order
+        std::vector<int64_t> tp(n_nodes + 1, 0);
+        for (int64_t q = 0; q < nnz; ++q) ++tp[col[q] + 1];
+        for (int64_t m = 0; m < n_nodes; ++m) tp[m + 1] += tp[m];
+        std::vector<int32_t> ti(nnz);
+        std::vector<double> tv(nnz);
+        std::vector<int64_t> fill(tp.begin(), tp.end() - 1);
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; ++q) {
+                const int64_t d = fill[col[q]]++;
+                ti[d] = (int32_t)i;
+                tv[d] = val[q];
+            }
+        P.tp.upload(c, tp, "P^T row_ptr", s);
+        P.ti.upload(c, ti, "P^T facets", s);
+        P.tv.upload(c, tv, "P^T val", s);
+        P.eta.alloc(c, (size_t)n, "cavity eta");
+        P.rbar.alloc(c, (size_t)n, "cavity Rbar eta");
+        HM_CUDA(cudaStreamSynchronize(s));
+        *out = guard.release();
+    });
+}
+
+void hm_destroy_projection(hm_proj* P) { delete P; }
+
+hm_status hm_cavity_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, hm_proj* P, int32_t nrhs, const double* T_nodes,
+                         double* Q_nodes, void* stream) {
+    return cavity_call(ctx, F, LU, P, nrhs, T_nodes, nullptr, Q_nodes, stream, 0);
+}
+
+hm_status hm_cavity_jacobian(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, hm_proj* P, int32_t nrhs,
+                             const double* T_nodes, const double* x_nodes, double* y_nodes, void* stream) {
+    return cavity_call(ctx, F, LU, P, nrhs, T_nodes, x_nodes, y_nodes, stream, 1);
+}
+
+}  // extern "C"

@@ -325,6 +325,8 @@ struct ProgArgs {
     const double* area_int;
     const double* g_int;
     double sigma;
+    int32_t eta_in;             // 1: the flux input is the facet power eta itself (not T: no T^4)
+    int32_t rbar_out;           // 1: emit A o q = (Rbar eta) (eq:Rbardef) instead of q
     int64_t local0;             // sharded: padded index of this rank's first row
     int32_t nrhs;               // multi-RHS: columns of this launch (<= kMrhsMax; user arrays have ld >= nrhs)
     const double* T_pad;        // sharded flux: gathered temperatures (padded internal order)
@@ -484,6 +486,10 @@ void permute_out(const double* y_int, const int32_t* perm, double* y_ext, int ld
 void flux_prologue(const double* T_ext, int ld, int col, const int32_t* perm, const double* eps_int,
                    double* w_int, int64_t n, cudaStream_t s);
 void fill_value(double* p, int64_t n, double v, cudaStream_t s);
+void proj_facets(const int64_t* rp, const int32_t* col_idx, const double* val, const double* T, const double* x,
+                 int mode, int ld, int col, double* eta, int64_t n, cudaStream_t s);
+void proj_nodes(const int64_t* tp, const int32_t* tidx, const double* tval, const double* y, int ld, int col, double* Q,
+                int64_t n_nodes, cudaStream_t s);
 void row_sums_clamp(const double* y, const double* area, double* sv, double* c, double* cdiv,
                     int64_t n, cudaStream_t s);
 // dense linear algebra (setup)
@@ -520,3 +526,17 @@ struct hm_ctx { hm::Ctx c; };
 struct hm_geom { hm::Geom g; };
 struct hm_hmat { hm::HMat h; };
 struct hm_hlu { hm::HLU h; };
+namespace hm {
+// Facet <- node projection P and its transpose, CSR on the device (NEXT-1).
+struct Proj {
+    Ctx* ctx;
+    const Geom* geom;
+    int64_t n_facets = 0, n_nodes = 0;
+    DBuf<int64_t> rp, tp;       // rows: facets (external order) / nodes
+    DBuf<int32_t> ci, ti;       // node ids / facet ids
+    DBuf<double> cv, tv;
+    DBuf<double> eta, rbar;     // facet workspaces (external order)
+    DBuf<double> host_in, host_in2, host_out;
+};
+}  // namespace hm
+struct hm_proj { hm::Proj p; };

@@ -55,6 +55,36 @@ __global__ void row_sums_kernel(const double* __restrict__ y, const double* __re
     cdiv[i] = ci != 0.0 ? ci : 1.0;
 }
 
+// Facet <- node projection (eqn:P_fi_definition), one facet row per thread:
+// mode 0: eta_i = sum_M P_iM T_M^4 (eqn:flux_residual_3 input); mode 1: eta_i = sum_M P_iM 4 T_M^3 x_M
+// (eq:Jcav input).  T, x: n_nodes x ld, column col.
+__global__ void proj_facets_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col_idx,
+                                   const double* __restrict__ val, const double* __restrict__ T,
+                                   const double* __restrict__ x, int mode, int ld, int col, double* __restrict__ eta,
+                                   int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        const int64_t M = col_idx[q];
+        const double t = T[M * ld + col];
+        const double t3 = t * t * t;
+        s += val[q] * (mode == 0 ? t3 * t : 4.0 * t3 * x[M * ld + col]);
+    }
+    eta[i] = s;
+}
+// Node <- facet transpose (P^T, eqn:S_def_matrix): Q_M = sum_{i ~ M} P_iM y_i in fixed facet order
+// (deterministic, no atomics); Q: n_nodes x ld, column col.
+__global__ void proj_nodes_kernel(const int64_t* __restrict__ tp, const int32_t* __restrict__ tidx,
+                                  const double* __restrict__ tval, const double* __restrict__ y, int ld, int col,
+                                  double* __restrict__ Q, int64_t n_nodes) {
+    const int64_t M = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (M >= n_nodes) return;
+    double s = 0.0;
+    for (int64_t q = tp[M]; q < tp[M + 1]; ++q) s += tval[q] * y[tidx[q]];
+    Q[M * ld + col] = s;
+}
+
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -76,6 +106,20 @@ void flux_prologue(const double* T_ext, int ld, int col, const int32_t* perm, co
     flux_prologue_kernel<<<nblk(n, 256), 256, 0, s>>>(T_ext, ld, col, perm, eps_int, w_int, n);
     HM_CUDA(cudaGetLastError());
     debug_sync(s, "flux_prologue");
+}
+void proj_facets(const int64_t* rp, const int32_t* col_idx, const double* val, const double* T, const double* x,
+                 int mode, int ld, int col, double* eta, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    proj_facets_kernel<<<nblk(n, 256), 256, 0, s>>>(rp, col_idx, val, T, x, mode, ld, col, eta, n);
+    HM_CUDA(cudaGetLastError());
+    debug_sync(s, "proj_facets");
+}
+void proj_nodes(const int64_t* tp, const int32_t* tidx, const double* tval, const double* y, int ld, int col, double* Q,
+                int64_t n_nodes, cudaStream_t s) {
+    if (n_nodes == 0) return;
+    proj_nodes_kernel<<<nblk(n_nodes, 256), 256, 0, s>>>(tp, tidx, tval, y, ld, col, Q, n_nodes);
+    HM_CUDA(cudaGetLastError());
+    debug_sync(s, "proj_nodes");
 }
 void fill_value(double* p, int64_t n, double v, cudaStream_t s) {
     if (n == 0) return;

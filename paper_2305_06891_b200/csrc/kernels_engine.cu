@@ -96,10 +96,13 @@ __device__ __forceinline__ void emit(const ProgArgs& A, const Pass& P, int64_t r
                 A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row]);
             break;
         }
-        default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form)
+        default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form);
+                    // rbar_out: A o q = (Rbar eta)_i (eq:Rbardef)
             const int64_t e = A.perm[row];
-            const double eta = pow4(A.user_in[e * A.ld + A.col]);
-            A.user_out[e * A.ld + A.col] = A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row]);
+            const double in = A.user_in[e * A.ld + A.col];
+            const double eta = A.eta_in ? in : pow4(in);
+            const double sc = A.rbar_out ? A.eps_int[row] : A.eps_int[row] / A.area_int[row];
+            A.user_out[e * A.ld + A.col] = A.sigma * sc * (s - eta * A.g_int[row]);
         }
     }
 }
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                             } else {
                                 const int64_t e = -(int64_t)j - 1;
                                 const double t = __ldg(A.user_in + e * A.ld + A.col);
-                                v[q] = im == IN_PERM ? t : __ldg(A.eps_ext + e) * pow4(t);
+                                v[q] = im == IN_PERM ? t : __ldg(A.eps_ext + e) * (A.eta_in ? t : pow4(t));
                             }
                         }
                     }
@@ -505,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                 for (int i = ct; i < u.nrows; i += kConsumers) {   // element-wise: rows [out0, out0 + nrows)
                     const int64_t row = u.out0 + i;
                     const double v = A.user_in[(int64_t)A.perm[row] * A.ld + A.col];
-                    P.out[row] = u.type == UNIT_PROLOGUE ? A.eps_int[row] * pow4(v) : v;
+                    P.out[row] = u.type == UNIT_PROLOGUE ? A.eps_int[row] * (A.eta_in ? v : pow4(v)) : v;
                 }
             }
         }
