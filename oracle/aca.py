@@ -39,9 +39,14 @@ class ACAResult:
         return self.U.shape[1]
 
 
-def aca_partial(row_fn, col_fn, m: int, n: int, eps: float, kcap: int | None = None) -> ACAResult:
+def aca_partial(row_fn, col_fn, m: int, n: int, eps: float, kcap: int | None = None, probes: int = 0) -> ACAResult:
+    """probes > 0 (reading R30): when the stop test (g) fires, first try up to `probes` rows
+    spread over the block -- the smallest unused row at or after m (q+1) / (probes+1), q = 0, 1, ...
+    (wrapping to the smallest unused row) -- as the next pivot row; a probe whose cross passes (g) is
+    appended and the iteration goes on; the iteration stops once a stop fires with no probe left."""
     if kcap is None:
         kcap = min(m, n)
+    probe_q = 0
     Us: list = []
     Vs: list = []
     k = 0
@@ -81,6 +86,15 @@ def aca_partial(row_fn, col_fn, m: int, n: int, eps: float, kcap: int | None = N
         if rhs > 0.0:
             margin = min(margin, abs(lhs / rhs - 1.0))
         if lhs <= rhs:                                               # (g)
+            if probe_q < probes:                                     # R30 probe
+                pos = (m * (probe_q + 1)) // (probes + 1)
+                probe_q += 1
+                free = np.nonzero(~used_r)[0]
+                if len(free) == 0:
+                    break
+                after = free[free >= pos]
+                istar = int(after[0]) if len(after) else int(free[0])
+                continue
             break
         Us.append(u)                                                 # (h)
         Vs.append(v)
@@ -123,3 +137,33 @@ def svd_eps_rank(X: np.ndarray, eps: float) -> int:
         if tail[k] <= eps * eps * tot:
             return k
     return len(s)
+
+
+def aca_full(X: np.ndarray, eps: float, kcap: int | None = None) -> ACAResult:
+    """Cross approximation with FULL pivoting (the paper's variant, eq:aca) and the exact
+    Frobenius residual as stop test (eq:erel, reading R5): pivot = largest |residual| entry (row-major
+    order, lowest index on ties); stop as soon as ||R||_F <= eps ||X||_F.  Reaching kcap returns rank kcap
+    with no factors (the caller stores the block dense)."""
+    X = np.asarray(X, dtype=np.float64)
+    m, n = X.shape
+    if kcap is None:
+        kcap = min(m, n)
+    R = X.copy()
+    thr = eps * eps * float(np.sum(X * X))
+    R2 = float(np.sum(R * R))
+    Us, Vs = [], []
+    while R2 > thr:
+        if len(Us) == kcap:
+            return ACAResult(np.zeros((m, kcap)), np.zeros((n, kcap)), 0.0, None, None)
+        a = int(np.argmax(np.abs(R)))
+        i, j = divmod(a, n)
+        u = R[:, j].copy()
+        v = R[i, :] / R[i, j]
+        R = R - np.outer(u, v)
+        R2 = float(np.sum(R * R))
+        Us.append(u)
+        Vs.append(v)
+    k = len(Us)
+    U = np.stack(Us, axis=1) if k else np.zeros((m, 0))
+    V = np.stack(Vs, axis=1) if k else np.zeros((n, 0))
+    return ACAResult(U, V, 0.0, None, None)

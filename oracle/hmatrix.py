@@ -90,7 +90,7 @@ class HMatrix:
 
 
 def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True,
-             adm_mode: int = 0, k_max: int = 48) -> HMatrix:
+             adm_mode: int = 0, k_max: int = 48, probes: int = 3, pivoting: str = "partial") -> HMatrix:
     """Trees (Alg. 1, 2), dense near field, partial-pivot ACA far field, then row sums
     and closed-cavity scaling of the row factors (U and dense rows)."""
     tr = _tree.build_cluster_tree(facets.centroid, n_min, facets.aabb, adm_mode)
@@ -107,10 +107,15 @@ def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True
         hb = HBlock(blk.level, r0, r1, c0, c1, blk.admissible, KIND_DENSE, 0)
         if blk.admissible:
             kcap = _aca.storage_cap(m, n, k_max)
-            res = _aca.aca_partial(
-                lambda i: _vf.entry_pairs(c, nrm, A, np.full(n, r0 + i), cols),
-                lambda j: _vf.entry_pairs(c, nrm, A, rows, np.full(m, c0 + j)),
-                m, n, eps_aca, kcap)
+            if pivoting == "full":   # the paper's variant on the explicit block
+                I, J = np.meshgrid(rows, cols, indexing="ij")
+                Xb = _vf.entry_pairs(c, nrm, A, I.ravel(), J.ravel()).reshape(m, n)
+                res = _aca.aca_full(Xb, eps_aca, kcap)
+            else:
+                res = _aca.aca_partial(
+                    lambda i: _vf.entry_pairs(c, nrm, A, np.full(n, r0 + i), cols),
+                    lambda j: _vf.entry_pairs(c, nrm, A, rows, np.full(m, c0 + j)),
+                    m, n, eps_aca, kcap, probes)
             hb.margin = res.margin
             k = res.rank
             if k >= kcap:

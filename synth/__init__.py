@@ -96,14 +96,16 @@ class Facets:
         return int(self.area.shape[0])
 
 
-def _facets_from_tris(V: np.ndarray, T: np.ndarray, interior=(0.0, 0.0, 0.0), name="") -> Facets:
+def _facets_from_tris(V: np.ndarray, T: np.ndarray, interior=(0.0, 0.0, 0.0), name="", outward=None) -> Facets:
     v0, v1, v2 = V[T[:, 0]], V[T[:, 1]], V[T[:, 2]]
     cen = (v0 + v1 + v2) / 3.0
     cr = np.cross(v1 - v0, v2 - v0)
     ln = np.sqrt((cr * cr).sum(axis=1))
     nrm = cr / ln[:, None]
-    # orient into the cavity: towards an interior point of the convex cavity
-    s = ((np.asarray(interior)[None, :] - cen) * nrm).sum(axis=1)
+    # orient into the cavity: towards an interior point of a convex cavity, or (outward = per-facet body
+    # centres) away from the body a facet bounds, for a cavity exterior to several bodies
+    ref = np.asarray(interior)[None, :] if outward is None else 2.0 * cen - outward
+    s = ((ref - cen) * nrm).sum(axis=1)
     nrm = np.where(s[:, None] < 0, -nrm, nrm)
     area = 0.5 * ln
     tri = np.stack([v0, v1, v2], axis=1)
@@ -184,6 +186,55 @@ def cylinder(n_theta: int = 1000, n_z: int = 40, R: float = 1.0, L: float = 4.0)
     for m in range(n_theta):
         tris.append((ct, top + m, top + (m + 1) % n_theta))
     return _facets_from_tris(V, np.array(tris, dtype=np.int64), name=f"cylinder{n_theta}x{n_z}")
+
+
+def fibonacci_centers(radius_unit: float = 1.0) -> np.ndarray:
+    """Centres of the 13 spheres of PAPER.md:831 (reading R29): sphere 1 at the origin; spheres
+    2, 3, 5, 7, 9, 11, 13 offset from the previous one of that list by (+-a_n, +-a_n), a_n the n-th
+    Fibonacci number, the sign pairs turning counter-clockwise ((+,+), (-,+), (-,-), (+,-), ...); spheres 4,
+    6, 8, 10, 12 at the midpoints of the quarter-circular arcs joining their neighbours (arc centre: the
+    corner of the axis-aligned square the two points span that keeps the spiral counter-clockwise).
+    Planar spiral in z = 0, lengths in units of a_1."""
+    fib = [1, 1, 2, 3, 5, 8, 13]
+    signs = [(1, 1), (-1, 1), (-1, -1), (1, -1)]
+    main = [np.zeros(2)]
+    for k in range(7):
+        sx, sy = signs[k % 4]
+        main.append(main[-1] + fib[k] * np.array([sx, sy], dtype=float))
+    # main[0..7] are spheres 1, 2, 3, 5, 7, 9, 11, 13
+    centers = {1: main[0], 2: main[1], 3: main[2], 5: main[3], 7: main[4], 9: main[5], 11: main[6], 13: main[7]}
+    for mid, (a, b) in zip((4, 6, 8, 10, 12), ((3, 5), (5, 7), (7, 9), (9, 11), (11, 13))):
+        pa, pb = centers[a], centers[b]
+        # quarter circle from pa to pb turning counter-clockwise: its centre is the square corner c with
+        # |c - pa| = |c - pb| = |dx| = |dy| and (pa - c) x (pb - c) > 0
+        for c in (np.array([pa[0], pb[1]]), np.array([pb[0], pa[1]])):
+            u, v = pa - c, pb - c
+            if u[0] * v[1] - u[1] * v[0] > 0:
+                r = np.linalg.norm(u)
+                w = (u + v) / np.linalg.norm(u + v)
+                centers[mid] = c + r * w
+                break
+    out = np.zeros((13, 3))
+    for i in range(13):
+        out[i, :2] = centers[i + 1] * radius_unit
+    return out
+
+
+def fibonacci_spheres(sub: int = 2, radius: float = 0.4) -> Facets:
+    """NEXT-2 stand-in for the paper's workload: 13 equal spheres (icosphere
+    subdivision `sub`, radius `radius`, watertight) on the Fibonacci spiral of fibonacci_centers; the cavity
+    is the region outside the spheres, so normals point out of each sphere.  Facet order: sphere-major."""
+    Vs, Ts, Cs = [], [], []
+    V0, T0 = icosphere_mesh(sub)
+    off = 0
+    for c in fibonacci_centers():
+        Vs.append(V0 * radius + c[None, :])
+        Ts.append(T0 + off)
+        Cs.append(np.repeat(c[None, :], T0.shape[0], axis=0))
+        off += V0.shape[0]
+    f = _facets_from_tris(np.concatenate(Vs), np.concatenate(Ts), name=f"fibonacci13-sub{sub}",
+                          outward=np.concatenate(Cs))
+    return f
 
 
 def line_facets(n: int) -> Facets:
@@ -270,13 +321,18 @@ def make_config(cfg: int, *, exact: bool = False, geometry: Facets | None = None
     elif cfg == 5:
         f = geometry or icosphere(8, exact)
         n_min, eps_aca = 128, 1e-5
+    elif cfg == 6:   # NEXT-2: the paper's workload shape (13 spheres on a Fibonacci spiral), reading R29
+        f = geometry or fibonacci_spheres(3)
+        n_min, eps_aca = 64, 1e-6
     else:
         raise ValueError(cfg)
     n = f.n
-    eps = np.full(n, 0.8) if cfg == 1 else emissivities(seed, n)
+    eps = np.full(n, 0.8) if cfg in (1, 6) else emissivities(seed, n)
     r = nrhs if nrhs is not None else (64 if cfg == 5 else 1)
     T = temperatures(seed, n, r)
-    return Config(cfg, f"C{cfg}:{f.name}", f, eps, T, n_min, 1.0, eps_aca, seed)
+    c = Config(cfg, f"C{cfg}:{f.name}", f, eps, T, n_min, 1.0, eps_aca, seed)
+    c.extra["closed"] = cfg != 6   # the spiral is an open cavity: no eqn:F_closed scaling
+    return c
 
 
 def step_perturbation(cfg_seed: int, step: int, n: int) -> np.ndarray:

@@ -365,3 +365,44 @@ def test_sampled_rows_match_dense(cfg1):
     Z = vf.solve(C, X)
     r = vf.sampled_residual(f.centroid, f.normal, f.area, cfg1.emissivity, rows, Z, X)
     assert np.abs(r).max() <= 1e-12 * np.abs(X).max()
+
+
+# ---------------------------------------------------------------- NEXT-2: the paper's workload shape
+def test_fibonacci_spiral_rule_and_isolated_facets():
+    """sphere 1 at the origin, spheres 2, 3, 5, ... offset by (+-a_n, +-a_n) turning
+    counter-clockwise; the remaining five on quarter-arc midpoints.  PAPER.md:845: about 7 % of the facets
+    see no other facet (zero rows of F); the back-face clamp (R3) is active between spheres."""
+    c = synth.fibonacci_centers()
+    assert np.allclose(c[[0, 1, 2, 4], :2], [[0, 0], [1, 1], [0, 2], [-2, 0]])        # spheres 1, 2, 3, 5
+    assert np.allclose(np.linalg.norm(c[3, :2]), 2.0)                                   # sphere 4 on the r=2 arc
+    for a, m, b in ((3, 4, 5), (5, 6, 7), (7, 8, 9), (9, 10, 11), (11, 12, 13)):
+        pa, pm, pb = c[a - 1, :2], c[m - 1, :2], c[b - 1, :2]
+        assert np.isclose(np.linalg.norm(pm - pa), np.linalg.norm(pm - pb))             # arc midpoint
+    f = synth.fibonacci_spheres(2)
+    assert f.n == 13 * 320
+    F = vf.dense_F(f.centroid, f.normal, f.area)
+    iso = (F.sum(axis=1) == 0.0).mean()
+    assert 0.05 < iso < 0.10
+    assert (F >= 0).all() and np.array_equal(F, F.T)
+    assert (F.sum(axis=1) / f.area).max() < 1.0                                          # open cavity
+
+
+def test_aca_full_pivot_textbook_and_error_bound():
+    """Full-pivot cross approximation (the paper's ACA): exact ranks on rank-r matrices, the
+    Frobenius error bound eq:erel holds exactly (exact residual stop), rank >= SVD eps-rank."""
+    rng = np.random.default_rng(3)
+    for r in (1, 3, 6):
+        X = rng.standard_normal((30, r)) @ rng.standard_normal((r, 25))
+        res = aca.aca_full(X, 1e-12)
+        assert res.rank == r
+        assert np.linalg.norm(X - res.U @ res.V.T) <= 1e-12 * np.linalg.norm(X)
+    assert aca.aca_full(np.zeros((5, 4)), 1e-6).rank == 0
+    cfg = synth.make_config(2, geometry=synth.icosphere(3))
+    H = hmatrix.assemble(cfg.facets, 64, 1.0, 1e-6, pivoting="full")
+    f = cfg.facets
+    for b in [b for b in H.blocks if b.kind == 1][:40]:
+        rows, cols = H.perm[b.r0:b.r1], H.perm[b.c0:b.c1]
+        I, J = np.meshgrid(rows, cols, indexing="ij")
+        Xb = vf.entry_pairs(f.centroid, f.normal, f.area, I.ravel(), J.ravel()).reshape(len(rows), len(cols))
+        assert np.linalg.norm(Xb - b.U @ b.V.T) <= 1e-6 * np.linalg.norm(Xb) * (1 + 1e-9)
+        assert b.rank >= aca.svd_eps_rank(Xb, 1e-6)
