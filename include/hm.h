@@ -76,6 +76,15 @@ typedef struct {
     double eps_aca;        /* eq:erel relative tolerance of the partial-pivot ACA stop test     */
     int32_t k_max;         /* rank cap (<= 64; blocks reaching it are stored dense); 0 = 48     */
     int32_t closed_cavity; /* 1: eq:rowsum / eq:clamped_rowsum / eqn:F_closed row scaling       */
+    int32_t probes;        /* 0..16: when the partial-pivot stop test fires, first try this many rows
+                              spread over the block as pivots (reading R30: catches parts of
+                              a block the pivot path missed, e.g. on multi-body geometries); 0 = off,
+                              the Python binding passes 3                                        */
+    int32_t pivoting;      /* 0: partial pivoting (default); 1: full pivoting,
+                              the paper's variant (NEXT-3): each admissible block is
+                              evaluated densely and cross-approximated with full pivoting and the exact
+                              Frobenius residual as stop test, so every block meets eq:erel; costs all
+                              m n entries of the admissible blocks (moderate n only)                  */
 } hm_aca_params;
 
 /* H-LU parameters. */

@@ -273,6 +273,8 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         if (!(params->eps_aca > 0.0) || params->eps_aca >= 1.0)
             throw Error(HM_ERR_INVALID_ARG, "eps_aca must be in (0, 1)");
         if (params->k_max < 0 || params->k_max > 64) throw Error(HM_ERR_INVALID_ARG, "k_max must be in [0, 64]");
+        if (params->probes < 0 || params->probes > 16) throw Error(HM_ERR_INVALID_ARG, "probes must be in [0, 16]");
+        if (params->pivoting != 0 && params->pivoting != 1) throw Error(HM_ERR_INVALID_ARG, "pivoting must be 0 or 1");
         const Geom& g = geom->g;
         const cudaStream_t s = c->stream;
         const int64_t n = g.n;
@@ -297,7 +299,83 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         err.alloc(c, 4, "err");
         HM_CUDA(cudaMemsetAsync(err.p, 0, 4 * sizeof(int32_t), s));
         size_t b = 0;
-        while (b < nb) {
+        while (params->pivoting == 1 && b < nb) {
+            // full pivoting (the paper's ACA variant, NEXT-3): evaluate the admissible
+            // blocks of a batch densely (row-major X[i][j] = F(r0+i, c0+j), filled through the bitwise
+            // symmetry of the unscaled entry, reading R3), then cross approximation with full pivoting
+            // and the exact Frobenius residual as stop test (eq:erel): ||X - U V^T||_F <= eps ||X||_F
+            std::vector<int64_t> hblk, hfill;
+            std::vector<int32_t> hkcap;
+            std::vector<size_t> ids;
+            int64_t cur = 0, fac = 0;
+            for (; b < nb; ++b) {
+                const Blk& B = g.blocks[b];
+                if (!B.adm) continue;
+                const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+                const int64_t klim = (m * nn + m + nn - 1) / (m + nn);
+                const int kc = (int)std::min<int64_t>(KMAX, klim);
+                const int64_t need = m * nn + ((m * kc + 1) & ~1LL) + ((nn * kc + 1) & ~1LL);
+                if (!ids.empty() && (cur + fac + need > budget || ids.size() >= 1000000)) break;
+                hfill.insert(hfill.end(), {cur, B.c0, nn, B.r0, m, nn});   // X^T column-major = X row-major
+                hblk.insert(hblk.end(), {0, m, cur, nn, 0, 0, nn});        // X = T + cur, row stride nn
+                hkcap.push_back(kc);
+                ids.push_back(b);
+                cur += m * nn;
+                fac += ((m * kc + 1) & ~1LL) + ((nn * kc + 1) & ~1LL);
+            }
+            if (ids.empty()) break;
+            int64_t fo = 0;
+            for (size_t q = 0; q < ids.size(); ++q) {   // factor slots after the dense blocks
+                const Blk& B = g.blocks[ids[q]];
+                const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0, kc = hkcap[q];
+                hblk[7 * q + 4] = cur + fo;
+                fo += (m * kc + 1) & ~1LL;
+                hblk[7 * q + 5] = cur + fo;
+                fo += (nn * kc + 1) & ~1LL;
+            }
+            DBuf<double> scratch;
+            scratch.alloc(c, (size_t)std::max<int64_t>(cur + fo, 2), "full-pivot ACA scratch");
+            DBuf<int64_t> dfill, dblk;
+            DBuf<int32_t> dkcap, drank;
+            dfill.upload(c, hfill, "fp-aca fill", s);
+            dblk.upload(c, hblk, "fp-aca blocks", s);
+            dkcap.upload(c, hkcap, "fp-aca kcap", s);
+            drank.alloc(c, ids.size(), "fp-aca ranks");
+            k::fill_entries(g.d_geo.p, n, dfill.p, (int)ids.size(), scratch.p, err.p, s);
+            k::cpaca_batch(scratch.p, 1, dblk.p, dkcap.p, (int)ids.size(), params->eps_aca, scratch.p, drank.p, s);
+            std::vector<int32_t> hrank(ids.size());
+            HM_CUDA(cudaMemcpyAsync(hrank.data(), drank.p, ids.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            HM_CUDA(cudaStreamSynchronize(s));
+            std::vector<int64_t> ctasks;
+            int64_t ctot = 0;
+            for (size_t q = 0; q < ids.size(); ++q) {
+                const size_t bb = ids[q];
+                const Blk& B = g.blocks[bb];
+                const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+                const int kq = hrank[q];
+                F.blk_rank[bb] = kq < 0 ? hkcap[q] : kq;
+                F.blk_kind[bb] = kq < 0 ? KIND_ADM_DENSE : KIND_LR;
+                if (F.blk_kind[bb] != KIND_LR) continue;
+                const int64_t uo = ctot, vo = ctot + ((m * kq + 1) & ~1LL);
+                ctot = vo + ((nn * kq + 1) & ~1LL);
+                if (kq > 0) {
+                    ctasks.insert(ctasks.end(), {uo, (int64_t)(uintptr_t)(scratch.p + hblk[7 * q + 4]), m * kq, 1, 1, 0, m * kq});
+                    ctasks.insert(ctasks.end(), {vo, (int64_t)(uintptr_t)(scratch.p + hblk[7 * q + 5]), nn * kq, 1, 1, 0, nn * kq});
+                }
+                rec[bb] = AcaRec{(int)batches.size(), uo, vo, hkcap[q]};
+            }
+            DBuf<double> compact;
+            compact.alloc(c, (size_t)std::max<int64_t>(ctot, 2), "ACA factors");
+            if (!ctasks.empty()) {
+                DBuf<int64_t> dct;
+                dct.upload(c, ctasks, "compaction tasks", s);
+                k::pack(dct.p, (int)(ctasks.size() / 7), compact.p, s);
+                HM_CUDA(cudaStreamSynchronize(s));
+            }
+            scratch.reset();
+            batches.push_back(std::move(compact));
+        }
+        while (params->pivoting == 0 && b < nb) {
             std::vector<int64_t> hblk, huoff, hvoff;
             std::vector<int32_t> hkcap;
             std::vector<size_t> ids;
@@ -331,7 +409,7 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             drank.alloc(c, ids.size(), "aca ranks");
             dmargin.alloc(c, ids.size(), "aca margins");
             scratch.alloc(c, (size_t)std::max<int64_t>(cur, 2), "aca scratch");
-            k::aca_batch(g.d_geo.p, n, dblk.p, duoff.p, dvoff.p, dkcap.p, (int)ids.size(), params->eps_aca, scratch.p,
+            k::aca_batch(g.d_geo.p, n, dblk.p, duoff.p, dvoff.p, params->probes, dkcap.p, (int)ids.size(), params->eps_aca, scratch.p,
                          drank.p, dmargin.p, err.p, s, max_m, max_n);
             std::vector<int32_t> hrank(ids.size());
             HM_CUDA(cudaMemcpyAsync(hrank.data(), drank.p, ids.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));

@@ -116,7 +116,7 @@ struct Factorizer {
             tot += (m * kc + 1) & ~1LL;
             const int64_t vo = tot;
             tot += (nn * kc + 1) & ~1LL;
-            blk.insert(blk.end(), {B.r0 - row0, m, B.c0 - col0, nn, uo, vo});
+            blk.insert(blk.end(), {B.r0 - row0, m, B.c0 - col0, nn, uo, vo, 0});
             kcap.push_back(kc);
             which.push_back(b);
         }
@@ -141,9 +141,9 @@ struct Factorizer {
             S.r0 = B.r0; S.m = m; S.c0 = B.c0; S.n = nn;
             S.kind = KIND_LR;
             S.k = rk[q];
-            S.U = fac.p + blk[6 * q + 4];
+            S.U = fac.p + blk[7 * q + 4];
             S.u_ld = m;
-            S.V = fac.p + blk[6 * q + 5];
+            S.V = fac.p + blk[7 * q + 5];
             S.v_ld = nn;
             out.push_back(S);
         }

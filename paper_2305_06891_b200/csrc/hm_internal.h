@@ -470,7 +470,7 @@ struct HLU {
 namespace k {
 // assembly
 void aca_batch(const double* geo, int64_t n, const int64_t* blk /*[nb][4] r0,m,c0,n*/,
-               const int64_t* uoff, const int64_t* voff, const int32_t* kcap, int nb, double eps,
+               const int64_t* uoff, const int64_t* voff, int probes, const int32_t* kcap, int nb, double eps,
                double* scratch, int32_t* rank_out, double* margin_out, int32_t* err, cudaStream_t s,
                int64_t max_m, int64_t max_n);
 void fill_entries(const double* geo, int64_t n, const int64_t* tasks /*[nt][6] dst,r0,rows,c0,cols,dld*/,
@@ -503,7 +503,7 @@ void leaf_lu_inv(double* M, double* Minv, int64_t ld, int n, int32_t* err, cudaS
 void extract_tri(const double* Minv, int64_t ld, int64_t r0, int64_t m, int mode, double* dst, cudaStream_t s);
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
             cudaStream_t s);
-void cpaca_batch(double* T, int64_t ldt, const int64_t* blk /*[nb][6] i0,m,j0,n,uoff,voff*/,
+void cpaca_batch(double* T, int64_t ldt, const int64_t* blk /*[nb][7] i0,m,j0,n,uoff,voff,ld (<=0: ldt)*/,
                  const int32_t* kcap, int nb, double eps, double* fac, int32_t* rank_out,
                  cudaStream_t s);
 }  // namespace k

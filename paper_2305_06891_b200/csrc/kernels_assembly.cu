@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(kAcaThreads)
 aca_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restrict__ blk,
            const int64_t* __restrict__ uoff, const int64_t* __restrict__ voff,
            const int32_t* __restrict__ kcap_arr, double eps, double* __restrict__ scratch,
-           int32_t* __restrict__ rank_out, double* __restrict__ margin_out, int32_t* err) {
+           int32_t* __restrict__ rank_out, double* __restrict__ margin_out, int32_t* err, int probes) {
+    __shared__ int64_t s_probe;
     extern __shared__ uint32_t smem_bits[];
     __shared__ ArgMax s_am[kAcaWarps];
     __shared__ double s_red[kAcaWarps * 8];
@@ -121,6 +122,7 @@ aca_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restri
     int k = 0;
     int64_t istar = 0;
     int64_t n_used_r = 0;
+    int probe_q = 0;
     while (true) {
         // (a) row residual r_j = X(i*,j) - sum_{l<k} U[i*,l] V[j,l] into V slot k
         if (tid < k) s_urow[tid] = U[(int64_t)tid * m + istar];
@@ -189,7 +191,30 @@ aca_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restri
         const double S2n = (S2 + nu2 * nv2) + 2.0 * X2;
         const double lhs = nu2 * nv2, rhs = eps2 * S2n;
         if (rhs > 0.0) margin = fmin(margin, fabs(lhs / rhs - 1.0));
-        if (lhs <= rhs) break;  // (g) stop, discard this cross
+        if (lhs <= rhs) {  // (g) stop, discard this cross
+            if (probe_q < probes) {
+                // R30: before stopping, probe the smallest unused row at or after m (q+1)/(probes+1)
+                // (wrapping to the smallest unused row) as the next pivot row
+                const int64_t pos = (m * (probe_q + 1)) / (probes + 1);
+                ++probe_q;
+                __syncthreads();
+                if (tid == 0) {
+                    int64_t p = -1, first = -1;
+                    for (int64_t i = 0; i < m; ++i) {
+                        if (bit_get(used_r, i)) continue;
+                        if (first < 0) first = i;
+                        if (i >= pos) { p = i; break; }
+                    }
+                    s_probe = p >= 0 ? p : first;
+                }
+                __syncthreads();
+                if (s_probe < 0) break;
+                istar = s_probe;
+                __syncthreads();
+                continue;
+            }
+            break;
+        }
         // (h) append
         ++k;
         S2 = S2n;
@@ -249,7 +274,7 @@ __global__ void scale_rows_kernel(const int64_t* __restrict__ tasks, double* __r
 
 namespace k {
 
-void aca_batch(const double* geo, int64_t n, const int64_t* blk, const int64_t* uoff, const int64_t* voff,
+void aca_batch(const double* geo, int64_t n, const int64_t* blk, const int64_t* uoff, const int64_t* voff, int probes,
                const int32_t* kcap, int nb, double eps, double* scratch, int32_t* rank_out, double* margin_out,
                int32_t* err, cudaStream_t s, int64_t max_m, int64_t max_n) {
     if (nb == 0) return;
@@ -257,7 +282,7 @@ void aca_batch(const double* geo, int64_t n, const int64_t* blk, const int64_t* 
     if (smem > 48 * 1024)
         HM_CUDA(cudaFuncSetAttribute(aca_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     aca_kernel<<<nb, kAcaThreads, smem, s>>>(geo, n, blk, uoff, voff, kcap, eps, scratch, rank_out, margin_out,
-                                             err);
+                                             err, probes);
     HM_CUDA(cudaGetLastError());
     debug_sync(s, "aca_kernel");
 }

@@ -252,8 +252,9 @@ cpaca_kernel(double* __restrict__ T, int64_t ldt, const int64_t* __restrict__ bl
              double eps, double* __restrict__ fac, int32_t* __restrict__ rank_out) {
     __shared__ double sd[kCT / 32];
     __shared__ AM sa[kCT / 32];
-    const int64_t* bb = blk + 6 * blockIdx.x;
+    const int64_t* bb = blk + 7 * blockIdx.x;
     const int64_t i0 = bb[0], m = bb[1], j0 = bb[2], n = bb[3];
+    ldt = bb[6] > 0 ? bb[6] : ldt;   // per-block row stride (packed blocks) or the batch's
     double* U = fac + bb[4];
     double* V = fac + bb[5];
     double* X = T + i0 * ldt + j0;

@@ -69,17 +69,30 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const dou
         bcol[i] = nt * 8 + ar;
     }
     const int nfull = ncols & ~3;
-    for (int k4 = 0; k4 < nfull; k4 += 4) {
-        const double* Ak = Ap + (k4 + ak) * ld;
-        const double* Xk = Xp + (k4 + ak) * kXStride;
-        double a[TM], b[TM];
+    if (8 % N8 == 0) {   // N8 in {1, 2, 4, 8}: nt = (cw + 8 i) mod N8 = cw mod N8 for every tile of the warp
+        const int bc = bcol[0];
+        for (int k4 = 0; k4 < nfull; k4 += 4) {
+            const double* Ak = Ap + (k4 + ak) * ld;
+            double a[TM];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) {
-            a[i] = Ak[arow[i]];
-            b[i] = Xk[bcol[i]];
+            for (int i = 0; i < TM; ++i) a[i] = Ak[arow[i]];
+            const double b = Xp[(k4 + ak) * kXStride + bc];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) dmma(acc[i], a[i], b);
         }
+    } else {
+        for (int k4 = 0; k4 < nfull; k4 += 4) {
+            const double* Ak = Ap + (k4 + ak) * ld;
+            const double* Xk = Xp + (k4 + ak) * kXStride;
+            double a[TM], b[TM];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) dmma(acc[i], a[i], b[i]);
+            for (int i = 0; i < TM; ++i) {
+                a[i] = Ak[arow[i]];
+                b[i] = Xk[bcol[i]];
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i) dmma(acc[i], a[i], b[i]);
+        }
     }
     if (nfull < ncols) {
         const int kk = nfull + ak;

@@ -37,9 +37,9 @@ def rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
 
 
-def build(hm, ctx, f, n_min, eps, closed=True, adm_mode=0, eta=1.0):
+def build(hm, ctx, f, n_min, eps, closed=True, adm_mode=0, eta=1.0, pivoting="partial"):
     g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=n_min, eta=eta, adm_mode=adm_mode)
-    F = hm.hm_assemble_aca(ctx, g, eps_aca=eps, closed_cavity=closed)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=eps, closed_cavity=closed, pivoting=pivoting)
     return g, F
 
 
@@ -416,3 +416,67 @@ def test_level_form_repeatable_bitwise(hm, ctx):
     torch.cuda.synchronize()
     assert np.array_equal(z.cpu().numpy(), z0)
     assert np.array_equal(q.cpu().numpy(), q0)
+
+
+# ---------------------------------------------------------------- NEXT-2: paper-shaped workload
+@pytest.mark.parametrize("sub", [2, 3])
+def test_fibonacci_spiral_open_cavity(hm, ctx, sub):
+    """13 spheres on the Fibonacci spiral (reading R29; open cavity, ~8 % isolated facets
+    with zero rows, back-face clamp active, admissible blocks from tree level 3).
+    Partial pivoting (+ R30 probes): exact partition and ACA ranks vs the oracle and F x equal to the oracle
+    H-matrix (1e-13) -- but on this geometry the partial-pivot stop can miss parts of a block, so the dense
+    bound is only checked for
+    full pivoting (the paper's ACA, NEXT-3): F x, solve and flux (both solve forms) vs the dense oracle
+    within 10 eps, ranks within +-1 of the oracle's own full-pivot ACA."""
+    import torch
+    cfg = synth.make_config(6, geometry=synth.fibonacci_spheres(sub))
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca, closed=False)
+    H = ohm.assemble(f, cfg.n_min, 1.0, cfg.eps_aca, closed=False)
+    assert (hm.hm_export_perm(g) == H.perm).all()
+    P, Q = hm.hm_export_partition(g, F), H.partition()
+    assert (P == Q).all()
+    x = cfg.rhs()[:, 0]
+    y = np.empty(f.n)
+    hm.hm_apply_F(ctx, F, x, y)
+    assert rel(y, H.apply(x)) <= TOL_EXACT
+    # full pivoting
+    g2, F2 = build(hm, ctx, f, cfg.n_min, cfg.eps_aca, closed=False, pivoting="full")
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity, closed=False)
+    hm.hm_apply_F(ctx, F2, x, y)
+    assert rel(y, Fd @ x) <= 10 * cfg.eps_aca
+    if sub == 2:
+        H2 = ohm.assemble(f, cfg.n_min, 1.0, cfg.eps_aca, closed=False, pivoting="full")
+        P2, Q2 = hm.hm_export_partition(g2, F2), H2.partition()
+        assert (P2[:, :6] == Q2[:, :6]).all()
+        lr = Q2[:, 5] == 1
+        assert np.abs(P2[lr, 7] - Q2[lr, 7]).max() <= 1
+        assert (P2[lr, 7] != Q2[lr, 7]).mean() <= 0.02
+    qo = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]
+    zo = vf.solve(C, x)
+    for cut in (-1, 99):
+        LU = hm.hm_factor_hlu(ctx, F2, cfg.emissivity, cut_level=cut)
+        z = np.empty(f.n)
+        hm.hm_solve_C(ctx, LU, x, z)
+        assert rel(z, zo) <= 10 * cfg.eps_aca
+        T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+        q = torch.empty_like(T)
+        hm.hm_radiative_flux(ctx, F2, LU, T, q)
+        torch.cuda.synchronize()
+        assert rel(q.cpu().numpy(), qo) <= 10 * cfg.eps_aca
+
+
+@pytest.mark.parametrize("case_name", ["C1", "ico4-rand-eps"])
+def test_full_pivot_aca_matches_dense(hm, ctx, case_name):
+    """NEXT-3 full-pivot ACA on the BASELINE geometries: F x within 10 eps of dense, fewer or equal stored
+    bytes than partial pivoting (ranks close to the SVD eps-ranks)."""
+    cfg, n_min = CASES[case_name]()
+    f = cfg.facets
+    g1, F1 = build(hm, ctx, f, n_min, cfg.eps_aca)
+    g2, F2 = build(hm, ctx, f, n_min, cfg.eps_aca, pivoting="full")
+    x = cfg.rhs()[:, 0]
+    y = np.empty(f.n)
+    hm.hm_apply_F(ctx, F2, x, y)
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
+    assert rel(y, Fd @ x) <= 10 * cfg.eps_aca
+    assert hm.hm_storage_report(F2)["bytes_F"] <= hm.hm_storage_report(F1)["bytes_F"]
