@@ -78,8 +78,8 @@ typedef struct {
     int32_t closed_cavity; /* 1: eq:rowsum / eq:clamped_rowsum / eqn:F_closed row scaling       */
     int32_t probes;        /* 0..16: when the partial-pivot stop test fires, first try this many rows
                               spread over the block as pivots (reading R30: catches parts of
-                              a block the pivot path missed, e.g. on multi-body geometries); 0 = off,
-                              the Python binding passes 3                                        */
+                              a block the pivot path missed, e.g. on multi-body geometries); 0 = off
+                              (plain step 10, the default; adds ~1.6 % stored bytes on C2)       */
     int32_t pivoting;      /* 0: partial pivoting (default); 1: full pivoting,
                               the paper's variant (NEXT-3): each admissible block is
                               evaluated densely and cross-approximated with full pivoting and the exact

@@ -90,7 +90,7 @@ class HMatrix:
 
 
 def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True,
-             adm_mode: int = 0, k_max: int = 48, probes: int = 3, pivoting: str = "partial") -> HMatrix:
+             adm_mode: int = 0, k_max: int = 48, probes: int = 0, pivoting: str = "partial") -> HMatrix:
     """Trees (Alg. 1, 2), dense near field, partial-pivot ACA far field, then row sums
     and closed-cavity scaling of the row factors (U and dense rows)."""
     tr = _tree.build_cluster_tree(facets.centroid, n_min, facets.aabb, adm_mode)

@@ -250,7 +250,7 @@ def hm_build_geometry(ctx: Context, centroid, normal, area, facet_aabb=None, n_m
     return Geometry(ctx, h, a.shape[0])
 
 
-def hm_assemble_aca(ctx: Context, geom: Geometry, eps_aca=1e-6, k_max=0, closed_cavity=True, probes=3,
+def hm_assemble_aca(ctx: Context, geom: Geometry, eps_aca=1e-6, k_max=0, closed_cavity=True, probes=0,
                     pivoting="partial") -> HMatrix:
     p = hm_aca_params(float(eps_aca), int(k_max), int(bool(closed_cavity)), int(probes),
                       {"partial": 0, "full": 1}[pivoting])

@@ -138,17 +138,31 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
         };
         const bool xonly = task_xonly[i] != 0;
         if (kind == DEP_BARRIER) {
+            // HM_DIAG_DEPS (timing experiments only, results are wrong): "none" drops every wait,
+            // "intra" the phase-1 -> phase-2 waits, "cross" the operator-to-operator waits
+            static const char* diagb = getenv("HM_DIAG_DEPS");
+            const char* diag = diagb;
             const int xd = pass_xdep[t.pass];
+            if (diag && diag[0] == 'n') continue;
+            if (diag && diag[0] == 'i' && xd != -2) { wait(xd); continue; }
+            if (diag && diag[0] == 'c' && (xonly || xd == -2 || pass_xdep[t.pass] == t.pass - 1)) {
+                if (!xonly && xd != -2) wait(t.pass - 1);
+                continue;
+            }
             wait(xonly && xd != -2 ? xd : t.pass - 1);
             continue;
         }
         if (!g || node < 0) throw Error(HM_ERR_INVALID_ARG, "tree-dependency pass without tree nodes");
         const int sw = sweep_of(kind);
+        static const char* diag = getenv("HM_DIAG_DEPS");
+        if (diag && diag[0] == 'n') continue;
         int par = g->nodes[node].parent;
         while (par >= 0 && cnt[c_all(sw, par)] == 0) par = g->nodes[par].parent;
-        if (par >= 0) wait(c_all(sw, par));
-        else wait(sweep_dep[sw]);
-        if ((kind == DEP_FWD_P2 || kind == DEP_BWD_P2) && !xonly) wait(c_p1(sw, node));
+        if (!(diag && diag[0] == 'c')) {
+            if (par >= 0) wait(c_all(sw, par));
+            else wait(sweep_dep[sw]);
+        }
+        if ((kind == DEP_FWD_P2 || kind == DEP_BWD_P2) && !xonly && !(diag && diag[0] == 'i')) wait(c_p1(sw, node));
     }
     for (size_t i = 0; i < h_tasks.size(); ++i) {   // per-chunk copies of the task's dependency record
         const Task& t = h_tasks[i];
@@ -226,13 +240,6 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
                 "compute %.1f task-end %.1f | retire wait %.1f work %.1f | producer wait-pempty %.1f total %.1f | consumer wait-gathered %.1f\n",
                 h_passes.size(), h_units.size(), grid, h[0] / G / 1e3, h[1] / G / 1e3, h[2] / G, h[3] / G / 1e3,
                 h[4] / G / 1e3, h[5] / G / 1e3, h[6] / G / 1e3, h[7] / G / 1e3, h[8] / G / 1e3, h[9] / G / 1e3, h[10] / G / 1e3, h[11] / G / 1e3, h[12] / G / 1e3, h[13] / G / 1e3);
-        if (!mrhs)
-            for (size_t p = 0; p < h_passes.size() && p < 16; ++p) {
-                const unsigned long long* q = h + 16 + 4 * p;
-                fprintf(stderr, "   pass %zu: chunks/CTA %.1f | consumer kcycles/CTA: wait-gathered %.1f wait-payload %.1f "
-                        "compute %.1f (%.0f cycles/chunk)\n", p, q[3] / G, q[0] / G / 1e3, q[1] / G / 1e3, q[2] / G / 1e3,
-                        q[3] ? (double)q[2] / q[3] : 0.0);
-            }
     }
 }
 

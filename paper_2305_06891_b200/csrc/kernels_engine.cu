@@ -2,19 +2,20 @@
 // (SURVEY.md §8(a) rows a1-a7): flux prologue / permute, the level-scheduled forward and backward
 // substitution sweeps, the leaf inverses, both phases of the F apply and the flux epilogue.
 //
-// One CTA per SM (co-resident by cooperative launch), warp-specialised, through a kStages-deep
-// shared-memory ring of 32 KB chunks:
-//   warp 0 (producer): grabs tasks (a panel, or a piece of a big panel) from a monotone queue
-//          counter in topological order and streams their chunks with 1-D TMA bulk copies
-//          (cp.async.bulk, mbarrier transaction counts): payload + 16-byte aligned column sources;
-//   warps 1-2 (gatherers; warp w owns the stages s = w-1 mod 2, so two gathers are in flight and
-//          each warp still visits every phase of its barriers in order): before gathering for a
-//          task, wait for the task's dependencies (per-pass or per-tree-node counters), then load
-//          the chunk's inputs from L2 (ld.cg: written by other SMs) into the stage;
-//   warps 3-7 (consumers): multiply from shared memory and accumulate the task in registers;
-//          release each stage as soon as it is read; at the task's last chunk reduce in fixed
-//          order, emit once (pieces of a split panel combine deterministically), retire the task
-//          (cumulative fence, then the pass / node counters).
+// One CTA per SM (co-resident by cooperative launch), warp-specialised, 19 warps:
+//   warp 0 (producer, one thread): grabs tasks (a panel, or a piece of a big panel) from a monotone
+//          queue counter in topological order; per chunk it TMA-copies the chunk descriptor into a
+//          header/gather slot (12-slot ring) and, kLookahead chunks later, the chunk's payload into a
+//          32 KB payload stage (4-stage ring), both with 1-D bulk copies and mbarrier transaction counts;
+//   warps 1-4 (gatherers; warp w owns the header slots k = w-1 mod 4): before gathering for a task,
+//          wait for the task's dependencies (per-pass or per-tree-node counters), then load the
+//          chunk's inputs from L2 (ld.cg: written by other SMs) into the slot;
+//   warps 5-12 (consumers): multiply from shared memory and accumulate the task in registers;
+//          release each stage as soon as it is read; at the task's last chunk hand the per-thread
+//          partials to a retire slot;
+//   warps 13-18 (retire; warp w takes task ends k = w mod 6): reduce the partials in fixed order,
+//          emit once (pieces of a split panel combine deterministically), publish the task (release
+//          atomics on the pass / node counters).
 //
 // Deadlock freedom: tasks are grabbed in increasing (topological) order and every wait refers to
 // lower-numbered tasks, so the lowest unfinished task can always proceed.  Counters are monotone
@@ -35,9 +36,9 @@ constexpr int kGatherers = 4;                       // warps 1..4 (gatherer w ow
 constexpr int kConsumerWarps = 8;                   // warps 5..12
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kConsumer0 = 32 * (1 + kGatherers);
-constexpr int kRetireWarp = 1 + kGatherers + kConsumerWarps;   // warps 13..14
-constexpr int kRetireWarps = 2;
-constexpr int kThreads = 32 * (kRetireWarp + kRetireWarps);  // 480
+constexpr int kRetireWarp = 1 + kGatherers + kConsumerWarps;   // warps 13..18
+constexpr int kRetireWarps = 6;   // 2 -> 6: the retire (emit + release) was the C2 bottleneck
+constexpr int kThreads = 32 * (kRetireWarp + kRetireWarps);  // 608
 
 // Two rings: payload stages (TMA of the factor bytes) and header/gather slots (chunk descriptor +
 // gathered inputs).  The producer posts a chunk's header kLookahead chunks before it issues its
@@ -45,7 +46,7 @@ constexpr int kThreads = 32 * (kRetireWarp + kRetireWarps);  // 480
 constexpr int kPStages = 4;
 constexpr int kGSlots = 12;
 constexpr int kLookahead = kGSlots - kPStages;
-constexpr int kRetireSlots = 4;    // task-end handoff buffers (consumers -> retire warps)
+constexpr int kRetireSlots = 8;    // task-end handoff buffers (consumers -> retire warps)
 constexpr int kMaxCols = 512;      // per chunk; payload <= 32 KB
 constexpr int kMaxPasses = 96;     // pass table held in shared memory
 static_assert(kGSlots % kGatherers == 0, "slot ownership");
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
         // partial sums in fixed order, emit (split panels: publish the partial, the last-finishing piece
         // adds all partials in piece order), then publish the task (release fence, dependency counters)
         unsigned long long st_rwait = 0, st_rwork = 0;
-        for (int64_t k = warp - kRetireWarp;; k += kRetireWarps) {   // retire warp w: slots k = w (mod 2)
+        for (int64_t k = warp - kRetireWarp;; k += kRetireWarps) {   // retire warp w: task ends k = w (mod kRetireWarps)
             const int r = (int)(k % kRetireSlots);
             long long c0 = clock64();
             mbar_wait(&S.rfull[r], (uint32_t)((k / kRetireSlots) & 1));

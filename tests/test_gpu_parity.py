@@ -37,9 +37,9 @@ def rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
 
 
-def build(hm, ctx, f, n_min, eps, closed=True, adm_mode=0, eta=1.0, pivoting="partial"):
+def build(hm, ctx, f, n_min, eps, closed=True, adm_mode=0, eta=1.0, pivoting="partial", probes=0):
     g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=n_min, eta=eta, adm_mode=adm_mode)
-    F = hm.hm_assemble_aca(ctx, g, eps_aca=eps, closed_cavity=closed, pivoting=pivoting)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=eps, closed_cavity=closed, pivoting=pivoting, probes=probes)
     return g, F
 
 
@@ -431,8 +431,8 @@ def test_fibonacci_spiral_open_cavity(hm, ctx, sub):
     import torch
     cfg = synth.make_config(6, geometry=synth.fibonacci_spheres(sub))
     f = cfg.facets
-    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca, closed=False)
-    H = ohm.assemble(f, cfg.n_min, 1.0, cfg.eps_aca, closed=False)
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca, closed=False, probes=3)
+    H = ohm.assemble(f, cfg.n_min, 1.0, cfg.eps_aca, closed=False, probes=3)
     assert (hm.hm_export_perm(g) == H.perm).all()
     P, Q = hm.hm_export_partition(g, F), H.partition()
     assert (P == Q).all()
