@@ -8,8 +8,8 @@
 //   colsrc[c] = index into XT = [x (n) | t (sum k)] of the input multiplying column c.
 // Panels have <= 128 rows and are cut into work units of <= 32 KB contiguous payload.
 #include <algorithm>
+#include <cstdlib>
 #include <map>
-#include <algorithm>
 
 #include "hm_internal.h"
 
@@ -30,13 +30,16 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
     P.unit_xonly.clear();
     int64_t part = 0;
     int32_t grp = 0;
-    // piece size adapted to the pass: ~4 tasks per SM (small passes still spread over the chip),
-    // between four chunks and kPieceDoubles, so the tail of a pass (the dependency barrier of the
-    // next one) is short
+    // piece size adapted to the pass: ~2 tasks per SM (small passes still spread over the chip),
+    // between four chunks and kPieceDoubles (measured on C2: 2 per SM 193 us, 4 per SM 197 us,
+    // 8 per SM 209 us -- fewer split-K partials beat a shorter pass tail); HM_PIECE_DIV /
+    // HM_PIECE_MIN override for experiments
     int64_t pass_doubles = 0;
     for (const Panel& pn : P.panels) pass_doubles += (int64_t)pn.ncols * pn.ld;
-    const int64_t piece = std::max<int64_t>(4 * kUnitPayloadDoubles,
-                                            std::min<int64_t>(kPieceDoubles, pass_doubles / (4 * 148)));
+    static const int piece_div = getenv("HM_PIECE_DIV") ? atoi(getenv("HM_PIECE_DIV")) : 2;
+    static const int piece_min = getenv("HM_PIECE_MIN") ? atoi(getenv("HM_PIECE_MIN")) : 4;
+    const int64_t piece = std::max<int64_t>(piece_min * kUnitPayloadDoubles,
+                                            std::min<int64_t>(kPieceDoubles, pass_doubles / (piece_div * 148)));
     struct Piece { std::vector<Unit> u; std::vector<int32_t> cs; int32_t panel; int64_t doubles; uint8_t xonly; };
     std::vector<Piece> pieces;
     for (size_t pi = 0; pi < P.panels.size(); ++pi) {

@@ -27,24 +27,44 @@ constexpr int kMGatherers = 2;
 constexpr int kMConsumerWarps = 8;
 constexpr int kMConsumers = 32 * kMConsumerWarps;
 constexpr int kMConsumer0 = 32 * (1 + kMGatherers);
-constexpr int kMThreads = 32 * (1 + kMGatherers + kMConsumerWarps);   // 352
+constexpr int kMPubWarp = 1 + kMGatherers + kMConsumerWarps;          // warp 11: publisher
+constexpr int kMThreads = 32 * (kMPubWarp + 1);                        // 384
+constexpr int kPubSlots = 8;          // task-end descriptors in flight (consumers -> publisher)
 constexpr int kMStages = 3;
-constexpr int kXStride = 72;          // X tile row stride (doubles): conflict-free B fragments
+// Shared-memory strides for conflict-free fragment loads: an 8-byte fragment load by a half-warp
+// (lanes g = 0..3 row, t = 0..3 k) reads words t * stride + g; the 16 words fall into distinct bank
+// pairs iff stride = 4 or 12 (mod 16).
+constexpr int kXStride = 68;          // X tile row stride (doubles)
+__host__ __device__ constexpr int padded_ld(int ld) {   // smem column stride of a chunk with ld rows
+    return ld + ((ld & 15) <= 4 ? 4 - (ld & 15) : (ld & 15) <= 12 ? 12 - (ld & 15) : 20 - (ld & 15));
+}
+// payload columns land at stride padded_ld(ld) (one bulk copy per column): at most
+// kUnitPayloadDoubles + 6 * kMrhsMaxCols doubles
+constexpr int kMPayload = kUnitPayloadDoubles + 6 * kMrhsMaxCols;
 constexpr int kMaxPassesM = 96;
 constexpr int kMaxTiles = 16;         // 8x8 accumulator tiles per consumer warp (128 rows x 64 cols / 8 warps)
 
 struct __align__(16) MStage {
     Unit hdr;
-    double payload[kUnitPayloadDoubles];
+    double payload[kMPayload];
     double X[kMrhsMaxCols * kXStride];
+};
+
+struct PubDesc {        // what the publisher needs of a finished task
+    int32_t type, pass, inc0, inc1;
 };
 
 struct MSmem {
     MStage st[kMStages];
     Pass passes[kMaxPassesM];
+    PubDesc pub[kPubSlots];
     unsigned long long posted[kMStages], full[kMStages], gathered[kMStages], empty[kMStages];
+    unsigned long long pfull[kPubSlots], pempty[kPubSlots];
     int last;
 };
+
+static_assert(sizeof(MSmem) + 128 <= 232448, "multi-RHS engine shared memory exceeds 227 KB");
+static_assert(padded_ld(40) == 44 && padded_ld(80) == 84 && padded_ld(126) == 132 && padded_ld(2) == 4, "padded_ld");
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -141,6 +161,10 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             mbar_init(&S.gathered[s], kMGatherers);
             mbar_init(&S.empty[s], kMConsumerWarps);
         }
+        for (int r = 0; r < kPubSlots; ++r) {
+            mbar_init(&S.pfull[r], kMConsumerWarps);
+            mbar_init(&S.pempty[r], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < A.n_passes; i += kMThreads) S.passes[i] = A.passes[i];
@@ -175,8 +199,13 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                     if (k >= kMStages && lane == 0) mbar_wait(&S.empty[s], (uint32_t)(((k / kMStages) - 1) & 1));
                     __syncwarp();
                     st_e += clock64() - c0;
+                    MStage& St = S.st[s];
+                    const int utype = __shfl_sync(0xffffffffu, mine.type, c);
+                    const int uncols = __shfl_sync(0xffffffffu, mine.ncols, c);
+                    const int uld = __shfl_sync(0xffffffffu, mine.ld, c);
+                    const int upass = __shfl_sync(0xffffffffu, mine.pass, c);
+                    const long long uoff = __shfl_sync(0xffffffffu, (long long)mine.a_off, c);
                     if (lane == c) {
-                        MStage& St = S.st[s];
                         if (end) {
                             St.hdr.type = -1;
                             mbar_arrive(&S.posted[s]);
@@ -184,14 +213,18 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                         } else {
                             St.hdr = mine;
                             mbar_arrive(&S.posted[s]);
-                            if (mine.type == UNIT_STREAM) {
-                                const uint32_t pb = (uint32_t)mine.ncols * (uint32_t)mine.ld * 8u;
-                                mbar_expect_tx(&S.full[s], pb);
-                                tma_load_1d(St.payload, S.passes[mine.pass].arena + mine.a_off, pb, &S.full[s]);
-                            } else {
+                            if (mine.type == UNIT_STREAM)
+                                mbar_expect_tx(&S.full[s], (uint32_t)mine.ncols * (uint32_t)mine.ld * 8u);
+                            else
                                 mbar_arrive(&S.full[s]);
-                            }
                         }
+                    }
+                    __syncwarp();
+                    if (!end && utype == UNIT_STREAM) {   // column j -> payload + j * padded_ld(ld)
+                        const double* src = S.passes[upass].arena + uoff;
+                        const int ldp = padded_ld(uld);
+                        for (int j = lane; j < uncols; j += 32)
+                            tma_load_1d(St.payload + j * ldp, src + (int64_t)j * uld, (uint32_t)uld * 8u, &S.full[s]);
                     }
                 }
                 nxt = __shfl_sync(0xffffffffu, nxt, 0);
@@ -302,6 +335,30 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
         }
         return;
     }
+    if (warp == kMPubWarp) {
+        // ------------------------------------------------ publisher: per finished task, make its outputs
+        // (written by the consumers before their mbarrier arrival) visible GPU-wide, then move the
+        // dependency counters -- off the consumers' critical path
+        unsigned long long st_pw = 0;
+        for (int64_t j = 0;; ++j) {
+            const int r = (int)(j % kPubSlots);
+            const long long c0 = clock64();
+            mbar_wait(&S.pfull[r], (uint32_t)((j / kPubSlots) & 1));
+            st_pw += clock64() - c0;
+            const PubDesc d = S.pub[r];
+            if (d.type < 0) break;
+            if (lane == 0) {
+                __threadfence();
+                atomicAdd(A.done + d.pass, 1ull);
+                if (d.inc0 >= 0) atomicAdd(A.done + d.inc0, 1ull);
+                if (d.inc1 >= 0) atomicAdd(A.done + d.inc1, 1ull);
+                mbar_arrive(&S.pempty[r]);
+            }
+            __syncwarp();
+        }
+        if (A.stats && lane == 0) atomicAdd(A.stats + 9, st_pw);
+        return;
+    }
     // ---------------------------------------------------- consumers: DMMA, task accumulators in registers
     const int cw = warp - 1 - kMGatherers;   // consumer warp 0..7
     const int ct = tid - kMConsumer0;
@@ -310,6 +367,17 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
     for (int i = 0; i < kMaxTiles; ++i) acc[i][0] = acc[i][1] = 0.0;
     const int ar = lane >> 2, ak = lane & 3;     // fragment coordinates
     unsigned long long st_wg = 0, st_wf = 0, st_c = 0, st_t = 0;
+    int64_t ntask = 0;     // tasks handed to the publisher
+    // task-end handoff: every consumer warp waits for the slot's previous use to be published, warp 0
+    // lane 0 writes the descriptor, every warp arrives after its own output stores
+    auto hand_off = [&](int type, int pass, int32_t inc0, int32_t inc1) {
+        const int r = (int)(ntask % kPubSlots);
+        if (lane == 0 && ntask >= kPubSlots) mbar_wait(&S.pempty[r], (uint32_t)(((ntask / kPubSlots) - 1) & 1));
+        if (ct == 0) S.pub[r] = PubDesc{type, pass, inc0, inc1};
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.pfull[r]);
+        ++ntask;
+    };
     long long c0 = clock64();
     for (int64_t k = 0;; ++k) {
         const int s = (int)(k % kMStages);
@@ -318,7 +386,10 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
         st_wg += c1 - c0;
         MStage& St = S.st[s];
         const int type = St.hdr.type;
-        if (type < 0) break;
+        if (type < 0) {
+            hand_off(-1, 0, -1, -1);
+            break;
+        }
         mbar_wait(&S.full[s], (uint32_t)((k / kMStages) & 1));
         long long c2 = clock64();
         st_wf += c2 - c1;
@@ -337,6 +408,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             }
             const double* Ap = St.payload;
             const double* Xp = St.X;
+            const int ldp = padded_ld(ld);
             // this warp's tiles t = cw + 8 i (row tiles mt, column tile nt); the k loop is
             // specialised on the tile count so the fragments of a k-step are loaded as a batch into
             // distinct registers and then feed back-to-back DMMAs
@@ -346,7 +418,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 if (cw + 8 * i < ntile) nmine = i + 1;
             switch (nmine) {
 #define HM_MMA_CASE(TM) \
-    case TM: mma_chunk<TM>(acc, Ap, Xp, ld, ncols, cw, N8, ar, ak); break;
+    case TM: mma_chunk<TM>(acc, Ap, Xp, ldp, ncols, cw, N8, ar, ak); break;
                 HM_MMA_CASE(1) HM_MMA_CASE(2) HM_MMA_CASE(3) HM_MMA_CASE(4)
                 HM_MMA_CASE(5) HM_MMA_CASE(6) HM_MMA_CASE(7) HM_MMA_CASE(8)
                 HM_MMA_CASE(9) HM_MMA_CASE(10) HM_MMA_CASE(11) HM_MMA_CASE(12)
@@ -461,13 +533,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 }
             }
         }
-        cons_sync();
-        if (ct == 0) {
-            __threadfence();
-            atomicAdd(A.done + pass, 1ull);
-            if (inc0 >= 0) atomicAdd(A.done + inc0, 1ull);
-            if (inc1 >= 0) atomicAdd(A.done + inc1, 1ull);
-        }
+        hand_off(type, pass, inc0, inc1);
         const long long c3 = clock64();
         st_t += c3 - c0;
         c0 = c3;

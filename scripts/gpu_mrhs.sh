@@ -1,0 +1,4 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null || exit 1
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q --tb=short -k "multi_rhs or host_pointers" 2>&1 | tail -3
+timeout 300 python scripts/mrhs_bench.py 2>&1 | tail -8
+HM_ENGINE_STATS=1 timeout 300 python scripts/mrhs_stats.py 2>&1 | grep "engine stats" | awk 'NR%2==0'
