@@ -285,6 +285,19 @@ def main():
                       "bytes_C": rep_lf["bytes_C"],
                       "solve_hbm_gbs": rep_lf["bytes_C"] / (lf_ms["solve_C"] * 1e-3) / 1e9}
         del LU_lf
+    # NEXT-3: the same flux step with recompressed ACA factors (hm_aca_params.recompress, reading R32)
+    recompressed = None
+    if not args.no_level_form and world == 1:
+        F_rc = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca, recompress=True)
+        LU_rc = hm.hm_factor_hlu(ctx, F_rc, cfg.emissivity)
+        rep_rc = hm.hm_storage_report(F_rc, LU_rc)
+        rc_ms, _ = hm.hm_profile_flux(ctx, F_rc, LU_rc, T, q, args.profile_iters, stream=stream.cuda_stream)
+        b_rc = rep_rc["bytes_F"] + rep_rc["bytes_C"]
+        recompressed = {"flux_ms": rc_ms["flux"], "applies_per_s": 1e3 / rc_ms["flux"], "bytes_F": rep_rc["bytes_F"],
+                        "bytes_C": rep_rc["bytes_C"], "ranks_F_mean": rep_rc["rank_mean"],
+                        "flux_hbm_gbs": b_rc / (rc_ms["flux"] * 1e-3) / 1e9,
+                        "setup_recompress_s": rep_rc["setup_seconds"].get("aca")}
+        del LU_rc, F_rc
     # NEXT-1: the cavity Jacobian action J^cav x = 4 P^T Rbar P (T^3 o x) (eq:Jcav) GMRES applies, on the
     # same operators (one projection + the flux program + one transpose projection)
     jcav = None
@@ -332,7 +345,8 @@ def main():
                        "ranks_C": {"mean": rep["rank_mean_C"], "max": rep["rank_max_C"]},
                        "setup_s": dict(rep["setup_seconds"], wall=setup_wall),
                        "solve_form": "inverse factors (cut level 0, DESIGN.md R27)",
-                       "level_form": level_form, "cavity_jacobian_action": jcav},
+                       "level_form": level_form, "recompressed": recompressed,
+                       "cavity_jacobian_action": jcav},
             "roofline": {"bound": "hbm", "kernel": "engine_kernel (flux program)" + (" + NCCL allgathers, rank 0" if world > 1 else ""),
                          "achieved": achieved,
                          "peak": peak, "unit": "GB/s",

@@ -85,6 +85,10 @@ typedef struct {
                               evaluated densely and cross-approximated with full pivoting and the exact
                               Frobenius residual as stop test, so every block meets eq:erel; costs all
                               m n entries of the admissible blocks (moderate n only)                  */
+    int32_t recompress;    /* 1: recompress every low-rank block (rank >= 2) after the ACA to its best
+                              rank-k' approximation at eps_aca (QR + SVD truncation, Frobenius tail;
+                              PAPER.md:642, reading R32): fewer stored bytes, ranks no longer
+                              the raw ACA ranks; 0: off (default)                                    */
 } hm_aca_params;
 
 /* H-LU parameters. */

@@ -167,3 +167,33 @@ def aca_full(X: np.ndarray, eps: float, kcap: int | None = None) -> ACAResult:
     U = np.stack(Us, axis=1) if k else np.zeros((m, 0))
     V = np.stack(Vs, axis=1) if k else np.zeros((n, 0))
     return ACAResult(U, V, 0.0, None, None)
+
+
+def recompress(U: np.ndarray, V: np.ndarray, eps: float):
+    """QR + SVD recompression of a low-rank factor pair (the ACA output "may be further
+    postprocessed (or truncated)"; reading R32).  Written out step by step:
+
+      U = Q_U R_U, V = Q_V R_V                     (reduced QR)
+      R_U R_V^T = X diag(s) Y^T                     (SVD of the k x k core)
+      k' = smallest k' with sqrt(sum_{i >= k'} s_i^2) <= eps sqrt(sum_i s_i^2)   (Frobenius tail, reading A5)
+      U' = Q_U X[:, :k'] diag(s[:k']),  V' = Q_V Y[:, :k']
+
+    so U' V'^T is the best rank-k' approximation of U V^T (Eckart-Young) and
+    ||U V^T - U' V'^T||_F <= eps ||U V^T||_F.  Returns (U', V')."""
+    U = np.asarray(U, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    k = U.shape[1]
+    if k == 0:
+        return U.copy(), V.copy()
+    Qu, Ru = np.linalg.qr(U)
+    Qv, Rv = np.linalg.qr(V)
+    X, s, Yt = np.linalg.svd(Ru @ Rv.T)
+    tail = np.sqrt(np.cumsum((s * s)[::-1])[::-1])          # tail[i] = sqrt(sum_{j >= i} s_j^2)
+    total = tail[0]
+    kk = k
+    for i in range(k + 1):
+        t = tail[i] if i < k else 0.0
+        if t <= eps * total:
+            kk = i
+            break
+    return Qu @ (X[:, :kk] * s[:kk]), Qv @ Yt[:kk].T

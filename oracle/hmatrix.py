@@ -90,9 +90,11 @@ class HMatrix:
 
 
 def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True,
-             adm_mode: int = 0, k_max: int = 48, probes: int = 0, pivoting: str = "partial") -> HMatrix:
-    """Trees (Alg. 1, 2), dense near field, partial-pivot ACA far field, then row sums
-    and closed-cavity scaling of the row factors (U and dense rows)."""
+             adm_mode: int = 0, k_max: int = 48, probes: int = 0, pivoting: str = "partial",
+             recompress: bool = False) -> HMatrix:
+    """Trees (Alg. 1, 2), dense near field, partial-pivot ACA far field (optionally recompressed,
+    aca.recompress at eps_aca), then row sums and closed-cavity scaling of the row factors (U and
+    dense rows)."""
     tr = _tree.build_cluster_tree(facets.centroid, n_min, facets.aabb, adm_mode)
     perm = tr.perm
     c = facets.centroid[perm]
@@ -121,7 +123,8 @@ def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True
             if k >= kcap:
                 hb.kind, hb.rank = KIND_ADM_DENSE, k
             else:
-                hb.kind, hb.rank, hb.U, hb.V = KIND_LR, k, res.U, res.V
+                U, V = (_aca.recompress(res.U, res.V, eps_aca) if recompress and k > 1 else (res.U, res.V))
+                hb.kind, hb.rank, hb.U, hb.V = KIND_LR, U.shape[1], U, V
         if hb.kind != KIND_LR:
             I, J = np.meshgrid(rows, cols, indexing="ij")
             hb.D = _vf.entry_pairs(c, nrm, A, I.ravel(), J.ravel()).reshape(m, n)

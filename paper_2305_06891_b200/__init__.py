@@ -38,7 +38,7 @@ class hm_tree_params(C.Structure):
 
 class hm_aca_params(C.Structure):
     _fields_ = [("eps_aca", C.c_double), ("k_max", C.c_int32), ("closed_cavity", C.c_int32),
-                ("probes", C.c_int32), ("pivoting", C.c_int32)]
+                ("probes", C.c_int32), ("pivoting", C.c_int32), ("recompress", C.c_int32)]
 
 
 class hm_lu_params(C.Structure):
@@ -251,9 +251,9 @@ def hm_build_geometry(ctx: Context, centroid, normal, area, facet_aabb=None, n_m
 
 
 def hm_assemble_aca(ctx: Context, geom: Geometry, eps_aca=1e-6, k_max=0, closed_cavity=True, probes=0,
-                    pivoting="partial") -> HMatrix:
+                    pivoting="partial", recompress=False) -> HMatrix:
     p = hm_aca_params(float(eps_aca), int(k_max), int(bool(closed_cavity)), int(probes),
-                      {"partial": 0, "full": 1}[pivoting])
+                      {"partial": 0, "full": 1}[pivoting], int(bool(recompress)))
     h = C.c_void_p()
     ctx.check(ctx.lib.hm_assemble_aca(ctx.h, geom.h, C.byref(p), C.byref(h)), "hm_assemble_aca")
     return HMatrix(ctx, h, geom)

@@ -20,7 +20,7 @@ COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=o
           "-I", os.path.join(os.path.dirname(HERE), "include")]
 SOURCES = ["tree.cpp", "hop.cpp", "api.cpp", "hlu.cpp", "engine.cpp", "shard.cpp",
            "kernels_assembly.cu", "kernels_apply.cu", "kernels_dense.cu", "kernels_engine.cu",
-           "kernels_mrhs.cu"]
+           "kernels_mrhs.cu", "kernels_recompress.cu"]
 
 
 def _digest() -> str:

@@ -275,6 +275,7 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         if (params->k_max < 0 || params->k_max > 64) throw Error(HM_ERR_INVALID_ARG, "k_max must be in [0, 64]");
         if (params->probes < 0 || params->probes > 16) throw Error(HM_ERR_INVALID_ARG, "probes must be in [0, 16]");
         if (params->pivoting != 0 && params->pivoting != 1) throw Error(HM_ERR_INVALID_ARG, "pivoting must be 0 or 1");
+        if (params->recompress != 0 && params->recompress != 1) throw Error(HM_ERR_INVALID_ARG, "recompress must be 0 or 1");
         const Geom& g = geom->g;
         const cudaStream_t s = c->stream;
         const int64_t n = g.n;
@@ -443,6 +444,31 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             }
             scratch.reset();
             batches.push_back(std::move(compact));
+        }
+        // ---- optional recompression of the low-rank factors (reading R32): per batch, in place
+        if (params->recompress) {
+            for (size_t bi = 0; bi < batches.size(); ++bi) {
+                std::vector<int64_t> hb;
+                std::vector<size_t> ids;
+                for (size_t q = 0; q < nb; ++q) {
+                    if (F.blk_kind[q] != KIND_LR || rec[q].batch != (int)bi || F.blk_rank[q] < 2) continue;
+                    const Blk& B = g.blocks[q];
+                    hb.insert(hb.end(), {rec[q].uoff, B.r1 - B.r0, rec[q].voff, B.c1 - B.c0, (int64_t)F.blk_rank[q]});
+                    ids.push_back(q);
+                }
+                if (ids.empty()) continue;
+                DBuf<int64_t> dblk;
+                DBuf<int32_t> drank;
+                dblk.upload(c, hb, "recompression blocks", s);
+                drank.alloc(c, ids.size(), "recompressed ranks");
+                for (size_t q0 = 0; q0 < ids.size(); q0 += 1000000)
+                    k::recompress_batch(batches[bi].p, dblk.p + 5 * q0, (int)std::min<size_t>(1000000, ids.size() - q0),
+                                        params->eps_aca, drank.p + q0, s);
+                std::vector<int32_t> hr(ids.size());
+                HM_CUDA(cudaMemcpyAsync(hr.data(), drank.p, ids.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                HM_CUDA(cudaStreamSynchronize(s));
+                for (size_t q = 0; q < ids.size(); ++q) F.blk_rank[ids[q]] = hr[q];
+            }
         }
         int32_t herr[4];
         HM_CUDA(cudaMemcpy(herr, err.p, sizeof(herr), cudaMemcpyDeviceToHost));

@@ -503,6 +503,8 @@ void leaf_lu_inv(double* M, double* Minv, int64_t ld, int n, int32_t* err, cudaS
 void extract_tri(const double* Minv, int64_t ld, int64_t r0, int64_t m, int mode, double* dst, cudaStream_t s);
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
             cudaStream_t s);
+// ACA factor recompression (kernels_recompress.cu): blk[5 q + 0..4] = uoff, m, voff, n, k (k in [2, 64])
+void recompress_batch(double* base, const int64_t* blk, int nb, double eps, int32_t* new_rank, cudaStream_t s);
 void cpaca_batch(double* T, int64_t ldt, const int64_t* blk /*[nb][7] i0,m,j0,n,uoff,voff,ld (<=0: ldt)*/,
                  const int32_t* kcap, int nb, double eps, double* fac, int32_t* rank_out,
                  cudaStream_t s);

@@ -84,7 +84,7 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const dou
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const int t = cw + 8 * i;
-        const int mt = t / N8, nt = t - mt * N8;
+        const int mt = N8 == 8 ? i : t / N8, nt = N8 == 8 ? cw : t - mt * N8;   // 64 RHS: no division
         arow[i] = mt * 8 + ar;
         bcol[i] = nt * 8 + ar;
     }

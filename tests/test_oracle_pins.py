@@ -406,3 +406,52 @@ def test_aca_full_pivot_textbook_and_error_bound():
         Xb = vf.entry_pairs(f.centroid, f.normal, f.area, I.ravel(), J.ravel()).reshape(len(rows), len(cols))
         assert np.linalg.norm(Xb - b.U @ b.V.T) <= 1e-6 * np.linalg.norm(Xb) * (1 + 1e-9)
         assert b.rank >= aca.svd_eps_rank(Xb, 1e-6)
+
+
+def test_recompression_is_optimal_truncation():
+    """oracle.aca.recompress (reading R32) against an independent route: the SVD of the explicit
+    product U V^T (Eckart-Young: the best rank-k' approximation has error sqrt(sum_{i >= k'} s_i^2));
+    redundant factors collapse to the true rank; the error bound eps holds."""
+    from oracle import aca as oaca
+    rng = np.random.default_rng(11)
+    m, n, k = 60, 50, 12
+    U = rng.standard_normal((m, k)) * (10.0 ** -np.arange(k))[None, :]
+    V = rng.standard_normal((n, k))
+    X = U @ V.T
+    s = np.linalg.svd(X, compute_uv=False)
+    for eps in (1e-2, 1e-4, 1e-6):
+        U2, V2 = oaca.recompress(U, V, eps)
+        kk = U2.shape[1]
+        tail = np.sqrt(np.cumsum((s * s)[::-1])[::-1])
+        kref = int(np.argmax(np.append(tail, 0.0) <= eps * np.linalg.norm(X)))
+        assert kk == kref
+        err = np.linalg.norm(X - U2 @ V2.T)
+        assert err <= eps * np.linalg.norm(X)
+        assert abs(err - (tail[kk] if kk < len(tail) else 0.0)) <= 1e-12 * np.linalg.norm(X)
+    # redundant factors: rank 3 written with 9 columns
+    A = rng.standard_normal((m, 3))
+    B = rng.standard_normal((n, 3))
+    C = rng.standard_normal((3, 9))
+    U, V = A @ C, B @ np.linalg.pinv(C).T
+    U2, V2 = oaca.recompress(U, V, 1e-10)
+    assert U2.shape[1] == 3
+    assert np.linalg.norm(U @ V.T - U2 @ V2.T) <= 1e-13 * np.linalg.norm(U @ V.T)
+    # zero pair -> rank 0
+    U2, V2 = oaca.recompress(np.zeros((5, 2)), np.zeros((4, 2)), 1e-6)
+    assert U2.shape[1] == 0
+
+
+def test_recompressed_hmatrix_c1():
+    """C1 with recompressed ACA factors: every block's rank <= its ACA rank, fewer stored doubles, same
+    partition, F x within 10 eps of the dense F."""
+    cfg = synth.make_config(1)
+    f = cfg.facets
+    H0 = hmatrix.assemble(f, cfg.n_min, 1.0, cfg.eps_aca)
+    H1 = hmatrix.assemble(f, cfg.n_min, 1.0, cfg.eps_aca, recompress=True)
+    P0, P1 = H0.partition(), H1.partition()
+    assert (P0[:, :6] == P1[:, :6]).all()
+    assert (P1[:, 7] <= P0[:, 7]).all() and (P1[:, 7] < P0[:, 7]).any()
+    assert H1.stored_doubles() < H0.stored_doubles()
+    Fd, _, _ = vf.dense_operators(f, cfg.emissivity)
+    x = cfg.rhs()[:, 0]
+    assert np.linalg.norm(H1.apply(x) - Fd @ x) <= 10 * cfg.eps_aca * np.linalg.norm(Fd @ x)
