@@ -497,6 +497,7 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
                 S.fill_entries = true;
             }
         }
+        F.op.p1_by_key = true;   // phase 1 in cluster order (row-group links of the flux program)
         build_hop(c, g, src, F.op, s);
         if (g.shard.sharded()) build_hop(c, g, src, F.op_loc, s, &g.shard);   // this rank's block rows
         batches.clear();

@@ -11,6 +11,7 @@
 #include "engine.h"
 
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 
 namespace hm {
@@ -48,6 +49,8 @@ int add_stream_impl(Program& P, const StreamPass& sp, const HOp& op, const doubl
             P.task_kind.push_back(kind);
             P.task_node.push_back(panel_node ? (*panel_node)[sp.unit_panel[q]] : -1);
             P.task_xonly.push_back(sp.unit_xonly[q]);
+            P.task_key.push_back(sp.panels[sp.unit_panel[q]].key);
+            P.task_span.push_back(sp.panels[sp.unit_panel[q]].ncols);
             ++p.n_tasks;
         }
         P.h_units.push_back(u);
@@ -91,6 +94,8 @@ void Program::add_elementwise(int type, int64_t n, double* out, int rows_per_uni
         task_kind.push_back(DEP_BARRIER);
         task_node.push_back(-1);
         task_xonly.push_back(0);
+        task_key.push_back(r);
+        task_span.push_back(0);
         h_units.push_back(u);
     }
     p.n_units = (int64_t)h_units.size() - p.first_unit;
@@ -107,7 +112,33 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
     const int64_t P = (int64_t)h_passes.size();
     if (P > engine_max_passes()) throw Error(HM_ERR_UNSUPPORTED, "program has more passes than the engine's pass table");
     const int64_t nn = g ? (int64_t)g->nodes.size() : 0;
-    n_counters = P + 4 * nn;
+    // row groups for link_rows: the tree nodes of level depth - 4 (leaves above it are groups too)
+    std::vector<int32_t> groups;           // node ids, in row order
+    if (g && !row_links.empty()) {
+        int depth = 0;
+        for (const Node& N : g->nodes) depth = std::max(depth, (int)N.level);
+        const int lg = std::max(0, depth - 4);
+        std::vector<int32_t> st{0};
+        while (!st.empty()) {
+            const int id = st.back();
+            st.pop_back();
+            const Node& N = g->nodes[id];
+            if (N.level == lg || N.is_leaf()) { groups.push_back(id); continue; }
+            st.push_back(N.child[1]);
+            st.push_back(N.child[0]);
+        }
+    }
+    const int64_t ng = (int64_t)groups.size();
+    auto group_of = [&](int64_t row) {   // index of the group containing row (groups are in row order)
+        int64_t lo = 0, hi = ng - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (g->nodes[groups[mid]].begin <= row) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    };
+    const int64_t c_rows0 = P + 4 * nn;
+    n_counters = c_rows0 + (int64_t)row_links.size() * ng;
     auto c_p1 = [&](int sw, int node) { return (int32_t)(P + sw * 2 * nn + node); };
     auto c_all = [&](int sw, int node) { return (int32_t)(P + sw * 2 * nn + nn + node); };
     std::vector<int64_t> cnt(n_counters, 0);  // tasks that increment each counter
@@ -121,6 +152,12 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
             t.inc_id[1] = c_all(sweep_of(kind), node);
         } else if (kind == DEP_FWD_P2 || kind == DEP_BWD_P2) {
             t.inc_id[0] = c_all(sweep_of(kind), node);
+        }
+        for (int li = 0; li < (int)row_links.size(); ++li) {   // phase-2 tasks feed their row group
+            if (t.pass != row_links[li].first) continue;
+            const int slot = t.inc_id[0] < 0 ? 0 : t.inc_id[1] < 0 ? 1 : -1;
+            if (slot < 0) throw Error(HM_ERR_UNSUPPORTED, "no free counter slot for a row-group link");
+            t.inc_id[slot] = (int32_t)(c_rows0 + li * ng + group_of(task_key[i]));
         }
         for (int q = 0; q < 2; ++q)
             if (t.inc_id[q] >= 0) cnt[t.inc_id[q]]++;
@@ -163,6 +200,24 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
             else wait(sweep_dep[sw]);
         }
         if ((kind == DEP_FWD_P2 || kind == DEP_BWD_P2) && !xonly && !(diag && diag[0] == 'i')) wait(c_p1(sw, node));
+    }
+    // row-group links: a phase-1 task whose cluster [key, key + span) lies in one group waits for that
+    // group's phase-2 tasks of the linked pass instead of for the whole pass (its only input)
+    for (int li = 0; li < (int)row_links.size(); ++li) {
+        const int32_t p2 = row_links[li].first, p1 = row_links[li].second;
+        for (size_t i = 0; i < h_tasks.size(); ++i) {
+            Task& t = h_tasks[i];
+            if (t.pass != p1) continue;
+            const int64_t gi = group_of(task_key[i]);
+            const Node& G = g->nodes[groups[gi]];
+            if (task_key[i] + task_span[i] > G.end) continue;   // spans several groups: whole pass
+            const int32_t id = (int32_t)(c_rows0 + li * ng + gi);
+            for (int q = 0; q < 2; ++q)
+                if (t.wait_id[q] == p2) {
+                    t.wait_id[q] = cnt[id] > 0 ? id : -1;
+                    t.wait_cnt[q] = (int32_t)cnt[id];
+                }
+        }
     }
     for (size_t i = 0; i < h_tasks.size(); ++i) {   // per-chunk copies of the task's dependency record
         const Task& t = h_tasks[i];

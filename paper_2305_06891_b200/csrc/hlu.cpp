@@ -379,6 +379,10 @@ void factor_hlu(HLU& L, const double* emissivity) {
         tA += L.fwd[lv].n_t;
         tB += L.bwd[lv].n_t;
     }
+    if (Lc == 0) {   // inverse-factor form: L^-1 -> U^-1 -> F chained group by group (Program::link_rows)
+        L.leafL.p2_by_row = true;
+        L.leafU.p1_by_key = L.leafU.p2_by_row = true;
+    }
     build_hop(c, g, srcL, L.leafL, s, nullptr, tA);
     build_hop(c, g, srcU, L.leafU, s, nullptr, tB);
     tA += L.leafL.n_t;
@@ -450,14 +454,23 @@ void factor_hlu(HLU& L, const double* emissivity) {
             P.add_stream(op.p1, op, L.xtB.p, L.xtB.p, OUT_ASSIGN, DEP_BWD_P1, &m1);
             P.add_stream(op.p2, op, L.xtB.p, L.xtB.p, OUT_SUB, DEP_BWD_P2, &m2);
         }
+        const size_t np_before = P.h_passes.size();
         P.add_stream(L.leafU.p1, L.leafU, L.xtB.p, L.xtB.p, OUT_ASSIGN, DEP_BWD_P1, &mU1);
+        if (Lc == 0 && P.h_passes.size() > np_before && P.sweep_dep[1] < (int32_t)np_before && !L.leafL.p2.empty())
+            P.link_rows(P.sweep_dep[1], (int32_t)np_before);
     };
     solve_passes(L.prog_solve, IN_PERM);
     L.prog_solve.add_stream(L.leafU.p2, L.leafU, L.xtB.p, nullptr, OUT_PERM, DEP_BWD_P2, &mU2);
     L.prog_solve.finalize(c, s, &g);
     solve_passes(L.prog_flux, IN_FLUX);
-    L.prog_flux.add_stream(L.leafU.p2, L.leafU, L.xtB.p, Fm.xt.p, OUT_ASSIGN, DEP_BWD_P2, &mU2);
-    L.prog_flux.add_stream(F.op.p1, F.op, Fm.xt.p, Fm.xt.p, OUT_ASSIGN);
+    auto add_U2_F1 = [&](Program& P) {   // U^-1 phase 2 -> F phase 1, linked group by group (cut level 0)
+        const size_t a = P.h_passes.size();
+        P.add_stream(L.leafU.p2, L.leafU, L.xtB.p, Fm.xt.p, OUT_ASSIGN, DEP_BWD_P2, &mU2);
+        const size_t b = P.h_passes.size();
+        P.add_stream(F.op.p1, F.op, Fm.xt.p, Fm.xt.p, OUT_ASSIGN);
+        if (Lc == 0 && b == a + 1 && P.h_passes.size() == b + 1) P.link_rows((int32_t)a, (int32_t)b);
+    };
+    add_U2_F1(L.prog_flux);
     // x-only (near-field) tasks of phase 2 wait for z, not for phase 1
     L.prog_flux.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN,
                            (int)L.prog_flux.h_passes.size() - 2);
@@ -469,8 +482,7 @@ void factor_hlu(HLU& L, const double* emissivity) {
     {
         Program pg;
         solve_passes(pg, IN_PERM);
-        pg.add_stream(L.leafU.p2, L.leafU, L.xtB.p, Fm.xt.p, OUT_ASSIGN, DEP_BWD_P2, &mU2);
-        pg.add_stream(F.op.p1, F.op, Fm.xt.p, Fm.xt.p, OUT_ASSIGN);
+        add_U2_F1(pg);
         pg.add_stream(F.op.p2, F.op, Fm.xt.p, L.g_int.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
                       (int)pg.h_passes.size() - 2);
         pg.finalize(c, s, &g);

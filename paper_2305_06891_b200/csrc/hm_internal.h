@@ -272,6 +272,10 @@ struct HOp {
     int64_t n_lr = 0, n_dense = 0;
     int64_t rank_sum = 0;
     int rank_max = 0;
+    // task order (set before build_hop): phase-1 pieces by cluster start (they wait on row groups of
+    // the previous operator, Program::link_rows), phase-2 t-reading pieces by row (they feed the next
+    // operator's phase 1 group by group); default: largest first
+    bool p1_by_key = false, p2_by_row = false;
     int64_t p1_doubles() const { return p1.doubles; }
     int64_t p2_doubles() const { return p2.doubles; }
     bool empty() const { return p1.empty() && p2.empty(); }
@@ -352,6 +356,9 @@ struct Program {
     bool mrhs = false;   // multi-RHS program (engine_mrhs_kernel, kMrhsMax columns per launch)
     int64_t n_x = 0;     // x-region size of the programs' XT buffers (fused-prologue gathers)
     std::vector<int32_t> task_kind, task_node;   // dependency kind / tree node of each task
+    std::vector<int64_t> task_key;               // panel key (phase 1: cluster start, phase 2: row start)
+    std::vector<int32_t> task_span;              // phase 1: cluster size
+    std::vector<std::pair<int32_t, int32_t>> row_links;   // (phase-2 pass, next operator's phase-1 pass)
     std::vector<uint8_t> task_xonly;             // task reads only the x region of its input
     std::vector<int32_t> pass_xdep;              // per pass: see add_stream
     int32_t sweep_dep[2] = {-1, -1};             // pass the root of the fwd / bwd sweep waits for
@@ -366,6 +373,9 @@ struct Program {
                     int xdep = -2);
     void add_elementwise(int type, int64_t n, double* out, int rows_per_unit = 1024, const double* in = nullptr,
                          int mode = 0 /* OUT_ASSIGN */);
+    // the phase-1 tasks of pass p1 whose cluster lies inside one row group (a tree node of level
+    // depth - 4) wait for the phase-2 tasks of pass p2 on that group's rows instead of for all of p2
+    void link_rows(int32_t p2, int32_t p1) { row_links.emplace_back(p2, p1); }
     void finalize(Ctx* ctx, cudaStream_t s, const Geom* g = nullptr);
     void launch(ProgArgs a, cudaStream_t s);
 };

@@ -23,7 +23,8 @@ static inline int64_t align2(int64_t x) { return (x + 1) & ~int64_t(1); }
 // max_cols: columns per chunk (single vector: kUnitMaxCols; multi-RHS: kMrhsMaxCols); part_scale:
 // partial-sum doubles per panel row (1, or kMrhsMax for the multi-RHS units)
 static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs, std::vector<int32_t>& ucs,
-                       cudaStream_t s, int max_cols = kUnitMaxCols, int part_scale = 1, bool split_xonly = true) {
+                       cudaStream_t s, int max_cols = kUnitMaxCols, int part_scale = 1, bool split_xonly = true,
+                       int order = 0 /* 0: largest first; 1: all pieces by key; 2: t-reading pieces by key */) {
     std::vector<Unit>& units = P.h_units;
     units.clear();
     P.unit_panel.clear();
@@ -40,7 +41,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
     static const int piece_min = getenv("HM_PIECE_MIN") ? atoi(getenv("HM_PIECE_MIN")) : 4;
     const int64_t piece = std::max<int64_t>(piece_min * kUnitPayloadDoubles,
                                             std::min<int64_t>(kPieceDoubles, pass_doubles / (piece_div * 148)));
-    struct Piece { std::vector<Unit> u; std::vector<int32_t> cs; int32_t panel; int64_t doubles; uint8_t xonly; };
+    struct Piece { std::vector<Unit> u; std::vector<int32_t> cs; int32_t panel; int64_t doubles; uint8_t xonly; int64_t key; };
     std::vector<Piece> pieces;
     for (size_t pi = 0; pi < P.panels.size(); ++pi) {
         const Panel& pn = P.panels[pi];
@@ -73,6 +74,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
                 C = (p1 - p0 + nch - 1) / nch;
                 Piece PC;
                 PC.panel = (int32_t)pi;
+                PC.key = pn.key;
                 PC.doubles = (p1 - p0) * pn.ld;
                 PC.xonly = p1 <= pn.ndense ? 1 : 0;   // reads only x (no t)
                 for (int32_t ch = 0; ch < nch; ++ch) {
@@ -122,8 +124,11 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
     }
     // x-only pieces first, then largest first (tasks are taken in order: a pass starts with work that
     // needs no t values and ends on small tasks)
-    std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& a, const Piece& b) {
+    // (order 1 / 2: all pieces / the t-reading pieces in panel-key order instead, so the row groups of
+    // Program::link_rows become ready, or complete, one after another)
+    std::stable_sort(pieces.begin(), pieces.end(), [order](const Piece& a, const Piece& b) {
         if (a.xonly != b.xonly) return a.xonly > b.xonly;
+        if ((order == 1 || (order == 2 && !a.xonly)) && a.key != b.key) return a.key < b.key;
         return a.doubles > b.doubles;
     });
     for (Piece& PC : pieces) {
@@ -271,8 +276,8 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     op.arena.alloc(ctx, (size_t)std::max<int64_t>(off, 2), "operator arena");
     HM_CUDA(cudaMemsetAsync(op.arena.p, 0, sizeof(double) * (size_t)std::max<int64_t>(off, 2), s));
     std::vector<int32_t> ucs;
-    make_units(ctx, op.p1, colsrc, ucs, s);
-    make_units(ctx, op.p2, colsrc, ucs, s);
+    make_units(ctx, op.p1, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p1_by_key ? 1 : 0);
+    make_units(ctx, op.p2, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p2_by_row ? 2 : 0);
     if (!shd) {   // multi-RHS chunking of the same panels (<= kMrhsMaxCols columns: X tile in smem)
         op.p1m.panels = op.p1.panels;
         op.p2m.panels = op.p2.panels;
