@@ -237,6 +237,26 @@ def fibonacci_spheres(sub: int = 2, radius: float = 0.4) -> Facets:
     return f
 
 
+def parallel_plates(m: int, L: float = 1.0, gap: float = 1.0) -> Facets:
+    """NEXT-4: the paper's second example: two parallel L x L plates a distance `gap`
+    apart, each an m x m grid of square facets (m = 40, 64, 106 give the paper's 3,200 / 8,192 / 22,472
+    facets); normals face the other plate; an open cavity.  Facet order: plate z = 0 row-major, then
+    plate z = gap."""
+    h = L / m
+    xs = (np.arange(m) + 0.5) * h
+    X, Y = np.meshgrid(xs, xs, indexing="ij")
+    cx, cy = X.ravel(), Y.ravel()
+    cen, nrm, box = [], [], []
+    for z, nz in ((0.0, 1.0), (gap, -1.0)):
+        c = np.stack([cx, cy, np.full(cx.shape, z)], axis=1)
+        cen.append(c)
+        nrm.append(np.tile([0.0, 0.0, nz], (c.shape[0], 1)))
+        box.append(np.concatenate([c - [0.5 * h, 0.5 * h, 0.0], c + [0.5 * h, 0.5 * h, 0.0]], axis=1))
+    cen, nrm, box = np.concatenate(cen), np.concatenate(nrm), np.concatenate(box)
+    return Facets(np.ascontiguousarray(cen), np.ascontiguousarray(nrm), np.full(cen.shape[0], h * h),
+                  np.ascontiguousarray(box), None, f"plates{m}x{m}")
+
+
 def line_facets(n: int) -> Facets:
     """PAPER.md:368-370 Example 1: n equidistant facets on a straight line; facet i is the
     interval [i-1/2, i+1/2] on the x axis (the facet-extent boxes that reproduce Fig. 1)."""
@@ -324,6 +344,9 @@ def make_config(cfg: int, *, exact: bool = False, geometry: Facets | None = None
     elif cfg == 6:   # NEXT-2: the paper's workload shape (13 spheres on a Fibonacci spiral), reading R29
         f = geometry or fibonacci_spheres(3)
         n_min, eps_aca = 64, 1e-6
+    elif cfg == 7:   # NEXT-4: the paper's parallel plates, leaf size 128
+        f = geometry or parallel_plates(40)
+        n_min, eps_aca = 128, 1e-6
     else:
         raise ValueError(cfg)
     n = f.n
@@ -331,7 +354,7 @@ def make_config(cfg: int, *, exact: bool = False, geometry: Facets | None = None
     r = nrhs if nrhs is not None else (64 if cfg == 5 else 1)
     T = temperatures(seed, n, r)
     c = Config(cfg, f"C{cfg}:{f.name}", f, eps, T, n_min, 1.0, eps_aca, seed)
-    c.extra["closed"] = cfg != 6   # the spiral is an open cavity: no eqn:F_closed scaling
+    c.extra["closed"] = cfg not in (6, 7)   # spiral and plates are open cavities: no eqn:F_closed scaling
     return c
 
 

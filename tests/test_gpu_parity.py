@@ -517,3 +517,35 @@ def test_recompressed_aca_matches_oracle_and_dense(hm, ctx, case_name):
     torch.cuda.synchronize()
     qo = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]
     assert rel(q.cpu().numpy(), qo) <= 10 * cfg.eps_aca
+
+
+@pytest.mark.parametrize("m", [40, 64])
+def test_parallel_plates_open_cavity(hm, ctx, m):
+    """NEXT-4: the paper's parallel plates (2 m^2 facets, leaf size 128, open cavity):
+    same-plate blocks are exactly zero (ACA rank 0), partition and ranks equal the oracle's, F x equals
+    the oracle H-matrix (1e-13) and the dense F within 10 eps; C^-1 b and the flux within 10 eps."""
+    import torch
+    cfg = synth.make_config(7, geometry=synth.parallel_plates(m))
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca, closed=False)
+    H = ohm.assemble(f, cfg.n_min, 1.0, cfg.eps_aca, closed=False)
+    assert (hm.hm_export_perm(g) == H.perm).all()
+    P, Q = hm.hm_export_partition(g, F), H.partition()
+    assert (P == Q).all()
+    assert ((Q[:, 5] == 1) & (Q[:, 7] == 0)).any()          # zero same-plate admissible blocks
+    x = cfg.rhs()[:, 0]
+    y = np.empty(f.n)
+    hm.hm_apply_F(ctx, F, x, y)
+    assert rel(y, H.apply(x)) <= TOL_EXACT
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity, closed=False)
+    assert rel(y, Fd @ x) <= 10 * cfg.eps_aca
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, x, z)
+    assert rel(z, vf.solve(C, x)) <= 10 * cfg.eps_aca
+    T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+    q = torch.empty_like(T)
+    hm.hm_radiative_flux(ctx, F, LU, T, q)
+    torch.cuda.synchronize()
+    qo = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]
+    assert rel(q.cpu().numpy(), qo) <= 10 * cfg.eps_aca

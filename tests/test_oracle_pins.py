@@ -455,3 +455,33 @@ def test_recompressed_hmatrix_c1():
     Fd, _, _ = vf.dense_operators(f, cfg.emissivity)
     x = cfg.rhs()[:, 0]
     assert np.linalg.norm(H1.apply(x) - Fd @ x) <= 10 * cfg.eps_aca * np.linalg.norm(Fd @ x)
+
+
+def _howell_parallel_squares(X, Y):
+    """View factor between directly opposed parallel rectangles a x b at distance c, X = a/c, Y = b/c
+    (textbook closed form, e.g. Howell's catalogue C-11)."""
+    return 2.0 / (math.pi * X * Y) * (
+        math.log(math.sqrt((1 + X * X) * (1 + Y * Y) / (1 + X * X + Y * Y)))
+        + X * math.sqrt(1 + Y * Y) * math.atan(X / math.sqrt(1 + Y * Y))
+        + Y * math.sqrt(1 + X * X) * math.atan(Y / math.sqrt(1 + X * X))
+        - X * math.atan(X) - Y * math.atan(Y))
+
+
+def test_parallel_plates_view_factor_converges_to_closed_form():
+    """NEXT-4 plates: the plate-to-plate view factor of the one-point F,
+    sum_{i in P1, j in P2} F_ij / A_P1, converges to the analytic value 0.19982 for unit squares a unit
+    apart at O(h^2) (midpoint rule of a smooth kernel); same-plate entries vanish exactly (coplanar,
+    reading A3); F is symmetric."""
+    ex = _howell_parallel_squares(1.0, 1.0)
+    assert abs(ex - 0.19982489569838746) < 1e-15
+    errs = []
+    for m in (10, 20, 40):
+        f = synth.parallel_plates(m)
+        F, _, _ = vf.dense_operators(f, np.full(f.n, 0.8), closed=False)
+        h = m * m
+        errs.append(F[:h, h:].sum() / 1.0 - ex)
+        assert np.abs(F[:h, :h]).max() == 0.0 and np.abs(F[h:, h:]).max() == 0.0
+        assert np.array_equal(F, F.T)
+    assert abs(errs[-1]) <= 2.5e-4 * ex
+    for a, b in zip(errs, errs[1:]):
+        assert 3.8 <= a / b <= 4.2
