@@ -555,6 +555,15 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             P.add_stream(F.op_loc.p1, F.op_loc, F.xt_loc.p, F.xt_loc.p, OUT_ASSIGN);
             P.add_stream(F.op_loc.p2, F.op_loc, F.xt_loc.p, nullptr, OUT_LOCAL, DEP_BARRIER, nullptr, IN_PLAIN, -1);
             F.sp_apply.finalize(c, s, &g);
+            // multi-RHS (C5's sharded 64-RHS apply): allgather of the n_pad x 64 block, DMMA engine
+            F.xt_loc_m.alloc(c, (size_t)(S.n_pad() + F.op_loc.n_t) * kMrhsMax, "F xt (local, multi-RHS)");
+            F.sp_apply_m.mrhs = true;
+            Program& Pm = F.sp_apply_m.add(F.xt_loc_m.p, true);
+            Pm.mrhs = true;
+            Pm.n_x = S.n_pad();
+            Pm.add_stream(F.op_loc.p1m, F.op_loc, F.xt_loc_m.p, F.xt_loc_m.p, OUT_ASSIGN);
+            Pm.add_stream(F.op_loc.p2m, F.op_loc, F.xt_loc_m.p, nullptr, OUT_LOCAL, DEP_BARRIER, nullptr, IN_PLAIN, -1);
+            F.sp_apply_m.finalize(c, s, &g);
         }
         F.s_ext.resize(n);
         F.c_ext.resize(n);
@@ -617,6 +626,12 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
                 ProgArgs a = base_args(*F.geom, xd + c0, yd + c0, nrhs, 0);
                 a.nrhs = std::min(kMrhsMax, nrhs - c0);
                 F.prog_apply_m.launch(a, s);
+            }
+        } else if (nrhs >= 2 && !F.sp_apply_m.empty()) {   // sharded multi-RHS: allgather + DMMA engine
+            for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
+                ProgArgs a = base_args(*F.geom, xd, yd + c0, nrhs, c0);
+                a.nrhs = std::min(kMrhsMax, nrhs - c0);
+                F.sp_apply_m.launch(c, *F.geom, a, s);
             }
         } else {
             for (int col = 0; col < nrhs; ++col) launch_apply(c, F, xd, yd, nrhs, col, s);

@@ -302,15 +302,16 @@ void SegProgram::launch(Ctx* ctx, const Geom& g, ProgArgs a, cudaStream_t s) {
     const Shard& S = g.shard;
     for (size_t i = 0; i < segs.size(); ++i) {
         if (pre[i]) {
-            if (pre_user[i]) {   // this rank's slice (column a.col of the caller's n_loc x ld array)
+            if (pre_user[i]) {   // this rank's slice (columns a.col.. of the caller's n_loc x ld array)
                 const int64_t nl = S.le() - S.lb();
+                const size_t w = mrhs ? (size_t)a.nrhs : 1, dst_pitch = mrhs ? kMrhsMax : 1;
                 if (nl > 0)
-                    HM_CUDA(cudaMemcpy2DAsync(pre[i] + S.base(), sizeof(double), a.user_in + a.col,
-                                              sizeof(double) * (size_t)(a.ld ? a.ld : 1), sizeof(double), (size_t)nl,
+                    HM_CUDA(cudaMemcpy2DAsync(pre[i] + S.base() * dst_pitch, sizeof(double) * dst_pitch, a.user_in + a.col,
+                                              sizeof(double) * (size_t)(a.ld ? a.ld : 1), sizeof(double) * w, (size_t)nl,
                                               cudaMemcpyDeviceToDevice, s));
             }
             if (!ctx->ex) throw Error(HM_ERR_NOT_READY, "sharded program without an exchanger");
-            ctx->ex->allgather(pre[i], S.maxc, s);
+            ctx->ex->allgather(pre[i], S.maxc * (mrhs ? kMrhsMax : 1), s);
             debug_sync(s, "allgather");
         }
         segs[i]->launch(a, s);

@@ -387,6 +387,8 @@ struct SegProgram {
     std::vector<std::unique_ptr<Program>> segs;
     std::vector<double*> pre;
     std::vector<uint8_t> pre_user;
+    bool mrhs = false;   // vectors row-major n_pad x kMrhsMax: the user slice is a.nrhs columns from
+                         // column a.col, the allgather moves maxc x kMrhsMax doubles per rank
     Program& add(double* exch_buf, bool user_slice) {
         segs.emplace_back(new Program());
         pre.push_back(exch_buf);
@@ -439,6 +441,8 @@ struct HMat {
     HOp op_loc;
     DBuf<double> xt_loc;  // [x_pad | t]
     SegProgram sp_apply;  // allgather x -> phase 1 -> phase 2
+    SegProgram sp_apply_m;   // the same for up to kMrhsMax columns (DMMA engine)
+    DBuf<double> xt_loc_m;
     // multi-RHS hot path (world == 1): blocks of kMrhsMax columns, row-major n x kMrhsMax vectors
     DBuf<double> xt_m;
     Program prog_apply_m;

@@ -278,7 +278,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     std::vector<int32_t> ucs;
     make_units(ctx, op.p1, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p1_by_key ? 1 : 0);
     make_units(ctx, op.p2, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p2_by_row ? 2 : 0);
-    if (!shd) {   // multi-RHS chunking of the same panels (<= kMrhsMaxCols columns: X tile in smem)
+    {   // multi-RHS chunking of the same panels (<= kMrhsMaxCols columns: X tile in smem)
         op.p1m.panels = op.p1.panels;
         op.p2m.panels = op.p2.panels;
         op.p1m.doubles = op.p1.doubles;

@@ -139,6 +139,7 @@ __device__ __forceinline__ void emit_m(const ProgArgs& A, const Pass& P, int64_t
         case OUT_ASSIGN: P.out[row * kMrhsMax + col] = s; break;
         case OUT_SUB: P.out[row * kMrhsMax + col] = __ldcg(P.out + row * kMrhsMax + col) - s; break;
         case OUT_PERM: A.user_out[(int64_t)A.perm[row] * A.ld + col] = s; break;
+        case OUT_LOCAL: A.user_out[(row - A.local0) * A.ld + col] = s; break;   // sharded: this rank's rows
         default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form)
             const int64_t e = A.perm[row];
             const double eta = pow4(A.user_in[e * A.ld + col]);

@@ -139,3 +139,53 @@ def test_virtual_shards_level_form(world, cut):
     Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
     assert rel(Z, vf.solve(C, x)) <= 10 * cfg.eps_aca
     assert rel(Q, vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]) <= 10 * cfg.eps_aca
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_virtual_shards_multi_rhs_apply(world):
+    """Sharded 64-RHS F apply (config 5's shape: row-cluster shards, allgather of the n x 64 block, DMMA
+    engine per rank): every column equals the world = 1 multi-RHS apply (1e-13) and the dense oracle
+    within 10 eps."""
+    import paper_2305_06891_b200 as hm
+    cfg = synth.make_config(2, geometry=synth.icosphere(4), nrhs=64)
+    f = cfg.facets
+    X = np.ascontiguousarray(cfg.rhs())
+    out, errs = {}, []
+
+    def run(rank):
+        try:
+            ctx = hm.hm_init(0, rank, world, 700 + world, hm.HM_FLAG_LOCAL_GROUP)
+            g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
+            F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+            perm = hm.hm_export_perm(g)
+            b, e = hm.hm_local_range(g, rank, world)
+            rows = perm[b:e]
+            x = np.ascontiguousarray(X[rows])
+            y = np.empty_like(x)
+            for _ in range(2):
+                hm.hm_apply_F(ctx, F, x, y)
+            out[rank] = dict(rows=rows, y=y)
+            del F, g
+            ctx.close()
+        except Exception as ex:                             # noqa: BLE001
+            errs.append(f"rank {rank}: {ex!r}")
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    Y = np.empty_like(X)
+    for r in range(world):
+        Y[out[r]["rows"]] = out[r]["y"]
+    ctx = hm.hm_init(0)
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+    Y1 = np.empty_like(X)
+    hm.hm_apply_F(ctx, F, X, Y1)
+    assert rel(Y, Y1) <= 1e-13
+    Fd, _, _ = vf.dense_operators(f, cfg.emissivity)
+    Yd = Fd @ X
+    for c in (0, 17, 63):
+        assert rel(Y[:, c], Yd[:, c]) <= 10 * cfg.eps_aca
