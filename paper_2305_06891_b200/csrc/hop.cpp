@@ -39,8 +39,14 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
     for (const Panel& pn : P.panels) pass_doubles += (int64_t)pn.ncols * pn.ld;
     static const int piece_div = getenv("HM_PIECE_DIV") ? atoi(getenv("HM_PIECE_DIV")) : 2;
     static const int piece_min = getenv("HM_PIECE_MIN") ? atoi(getenv("HM_PIECE_MIN")) : 4;
-    const int64_t piece = std::max<int64_t>(piece_min * kUnitPayloadDoubles,
-                                            std::min<int64_t>(kPieceDoubles, pass_doubles / (piece_div * 148)));
+    static const int mrhs_min = getenv("HM_MRHS_PIECE_MIN") ? atoi(getenv("HM_MRHS_PIECE_MIN")) : 64;   // measured C2 flux: 4 -> 1.46, 64 -> 1.35 ms
+    // multi-RHS units (part_scale > 1): compute-bound, and every split piece costs a rows x 64 partial
+    // write + combine, so only panels above mrhs_min chunks (HM_MRHS_PIECE_MIN) are split
+    const int64_t piece = part_scale > 1
+        ? std::max<int64_t>((int64_t)mrhs_min * kUnitPayloadDoubles,
+                            std::min<int64_t>(kPieceDoubles, pass_doubles / (piece_div * 148)))
+        : std::max<int64_t>(piece_min * kUnitPayloadDoubles,
+                            std::min<int64_t>(kPieceDoubles, pass_doubles / (piece_div * 148)));
     struct Piece { std::vector<Unit> u; std::vector<int32_t> cs; int32_t panel; int64_t doubles; uint8_t xonly; int64_t key; };
     std::vector<Piece> pieces;
     for (size_t pi = 0; pi < P.panels.size(); ++pi) {
@@ -57,7 +63,10 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
         for (Seg& sg : segs) {
             const int64_t w = sg.c1 - sg.c0;
             if (w <= 0) continue;
-            sg.np = (int32_t)std::min<int64_t>(w, (w * pn.ld + piece - 1) / piece);
+            // t-reading segments of split passes (phase 2) end the pass: optionally finer pieces there
+            static const int tdiv = getenv("HM_PIECE_TDIV") ? atoi(getenv("HM_PIECE_TDIV")) : 2;   // measured: 1 -> 184.7, 2 -> 183.4 us
+            const int64_t pc_sz = (&sg == &segs[1] && nd > 0) ? std::max<int64_t>(2 * kUnitPayloadDoubles, piece / tdiv) : piece;
+            sg.np = (int32_t)std::min<int64_t>(w, (w * pn.ld + pc_sz - 1) / pc_sz);
             npieces += sg.np;
         }
         const int32_t g = npieces > 1 ? grp++ : -1;
