@@ -662,6 +662,12 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
                 a.nrhs = std::min(kMrhsMax, nrhs - c0);
                 L.prog_solve_m.launch(a, s);
             }
+        } else if (nrhs >= 2 && !L.sp_solve_m.empty()) {   // sharded multi-RHS
+            for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
+                ProgArgs a = base_args(*L.F->geom, bd, zd + c0, nrhs, c0);
+                a.nrhs = std::min(kMrhsMax, nrhs - c0);
+                L.sp_solve_m.launch(c, *L.F->geom, a, s);
+            }
         } else {
             for (int col = 0; col < nrhs; ++col) launch_solve(c, L, bd, zd, nrhs, col, s);
         }
@@ -762,6 +768,18 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
         }
         if (nrhs >= 2 && L.prog_flux_m.ready) {
             for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) launch_flux_m(L, Td + c0, qd + c0, nrhs, std::min(kMrhsMax, nrhs - c0), s);
+        } else if (nrhs >= 2 && !L.sp_flux_m.empty()) {   // sharded multi-RHS flux
+            const Geom& g = *L.F->geom;
+            for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
+                ProgArgs a = base_args(g, Td, qd + c0, nrhs, c0);
+                a.nrhs = std::min(kMrhsMax, nrhs - c0);
+                a.sigma = 5.670374419e-8;   // DESIGN.md reading R2
+                a.eps_int = L.eps_pad.p;
+                a.area_int = L.area_pad.p;
+                a.g_int = L.g_pad.p;
+                a.T_pad = L.T_loc_m.p;
+                L.sp_flux_m.launch(c, g, a, s);
+            }
         } else {
             for (int col = 0; col < nrhs; ++col) launch_flux(c, L, Td, qd, nrhs, col, s);
         }

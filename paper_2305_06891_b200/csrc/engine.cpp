@@ -65,7 +65,8 @@ void Program::add_stream(const StreamPass& sp, const HOp& op, const double* in, 
     add_stream_impl(*this, sp, op, in, out, mode, kind, panel_node, in_mode, xdep);
 }
 
-void Program::add_elementwise(int type, int64_t n, double* out, int rows_per_unit, const double* in, int mode) {
+void Program::add_elementwise(int type, int64_t n, double* out, int rows_per_unit, const double* in, int mode,
+                              int64_t row0) {
     Pass p{};
     p.type = type;
     p.dep = (int32_t)h_passes.size() - 1;
@@ -74,10 +75,10 @@ void Program::add_elementwise(int type, int64_t n, double* out, int rows_per_uni
     p.out = out;
     p.in = in;
     const int32_t idx = (int32_t)h_passes.size();
-    for (int64_t r = 0; r < n; r += rows_per_unit) {
+    for (int64_t r = row0; r < row0 + n; r += rows_per_unit) {
         Unit u{};
         u.out0 = r;
-        u.nrows = (int32_t)std::min<int64_t>(rows_per_unit, n - r);
+        u.nrows = (int32_t)std::min<int64_t>(rows_per_unit, row0 + n - r);
         u.grp = -1;
         u.nseg = 1;
         u.pass = idx;

@@ -607,6 +607,42 @@ void factor_hlu(HLU& L, const double* emissivity) {
             P.add_stream(F.op_loc.p2, F.op_loc, Fm.xt_loc.p, nullptr, OUT_FLUX_LOCAL, DEP_BARRIER, nullptr, IN_PLAIN, -1);
         }
         L.sp_flux.finalize(c, s, &g);
+        if (Lc == 0) {   // sharded multi-RHS solve / flux (kMrhsMax columns per launch, DMMA engine)
+            const int64_t nl = S.le() - S.lb();
+            L.xtA_loc_m.alloc(c, (size_t)(np + tA_loc) * kMrhsMax, "solve xtA (local, multi-RHS)");
+            L.xtB_loc_m.alloc(c, (size_t)(np + tB_loc) * kMrhsMax, "solve xtB (local, multi-RHS)");
+            L.T_loc_m.alloc(c, (size_t)np * kMrhsMax, "T (padded, multi-RHS)");
+            L.y_loc_m.alloc(c, (size_t)np * kMrhsMax, "F y (local, multi-RHS)");
+            auto sweeps_m = [&](SegProgram& SP, bool flux, double* out_u, int mode_u) {
+                SP.mrhs = true;
+                Program* P = &SP.add(flux ? L.T_loc_m.p : L.xtA_loc_m.p, true);
+                P->mrhs = true;
+                P->n_x = np;
+                if (flux) P->add_elementwise(UNIT_PROLOGUE_INT, np, L.xtA_loc_m.p, 128, L.T_loc_m.p);
+                P->add_stream(L.leafL_loc.p1m, L.leafL_loc, L.xtA_loc_m.p, L.xtA_loc_m.p, OUT_ASSIGN);
+                P->add_stream(L.leafL_loc.p2m, L.leafL_loc, L.xtA_loc_m.p, L.xtB_loc_m.p, OUT_ASSIGN, DEP_BARRIER,
+                              nullptr, IN_PLAIN, -1);
+                P = &SP.add(L.xtB_loc_m.p, false);   // allgather y -> U^-1
+                P->mrhs = true;
+                P->n_x = np;
+                P->add_stream(L.leafU_loc.p1m, L.leafU_loc, L.xtB_loc_m.p, L.xtB_loc_m.p, OUT_ASSIGN);
+                P->add_stream(L.leafU_loc.p2m, L.leafU_loc, L.xtB_loc_m.p, out_u, mode_u, DEP_BARRIER, nullptr,
+                              IN_PLAIN, -1);
+            };
+            sweeps_m(L.sp_solve_m, false, nullptr, OUT_LOCAL);
+            L.sp_solve_m.finalize(c, s, &g);
+            sweeps_m(L.sp_flux_m, true, Fm.xt_loc_m.p, OUT_ASSIGN);
+            {
+                Program& P = L.sp_flux_m.add(Fm.xt_loc_m.p, false);   // allgather z -> F -> flux epilogue
+                P.mrhs = true;
+                P.n_x = np;
+                P.add_stream(F.op_loc.p1m, F.op_loc, Fm.xt_loc_m.p, Fm.xt_loc_m.p, OUT_ASSIGN);
+                P.add_stream(F.op_loc.p2m, F.op_loc, Fm.xt_loc_m.p, L.y_loc_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr,
+                             IN_PLAIN, -1);
+                P.add_elementwise(UNIT_EPILOGUE, nl, nullptr, 128, L.y_loc_m.p, OUT_FLUX_LOCAL, S.base());
+            }
+            L.sp_flux_m.finalize(c, s, &g);
+        }
         HM_CUDA(cudaStreamSynchronize(s));
     }
 }

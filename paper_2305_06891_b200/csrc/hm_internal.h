@@ -372,7 +372,7 @@ struct Program {
                     int kind = DEP_BARRIER, const std::vector<int32_t>* panel_node = nullptr, int in_mode = IN_PLAIN,
                     int xdep = -2);
     void add_elementwise(int type, int64_t n, double* out, int rows_per_unit = 1024, const double* in = nullptr,
-                         int mode = 0 /* OUT_ASSIGN */);
+                         int mode = 0 /* OUT_ASSIGN */, int64_t row0 = 0 /* rows [row0, row0 + n) */);
     // the phase-1 tasks of pass p1 whose cluster lies inside one row group (a tree node of level
     // depth - 4) wait for the phase-2 tasks of pass p2 on that group's rows instead of for all of p2
     void link_rows(int32_t p2, int32_t p1) { row_links.emplace_back(p2, p1); }
@@ -475,6 +475,9 @@ struct HLU {
     DBuf<double> eps_pad, area_pad, g_pad;
     SegProgram sp_solve;  // AG b -> L^-1 -> AG y -> U^-1
     SegProgram sp_flux;   // AG T -> L^-1 (w = eps T^4 fused) -> AG y -> U^-1 -> AG z -> F + flux epilogue
+    // sharded multi-RHS (cut level 0): the same exchanges on n_pad x 64 blocks, DMMA engine
+    SegProgram sp_solve_m, sp_flux_m;
+    DBuf<double> xtA_loc_m, xtB_loc_m, T_loc_m, y_loc_m;
     // multi-RHS hot path (world == 1, inverse-factor form)
     DBuf<double> xtA_m, xtB_m;
     Program prog_solve_m, prog_flux_m;

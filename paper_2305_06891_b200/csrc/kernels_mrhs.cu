@@ -140,6 +140,12 @@ __device__ __forceinline__ void emit_m(const ProgArgs& A, const Pass& P, int64_t
         case OUT_SUB: P.out[row * kMrhsMax + col] = __ldcg(P.out + row * kMrhsMax + col) - s; break;
         case OUT_PERM: A.user_out[(int64_t)A.perm[row] * A.ld + col] = s; break;
         case OUT_LOCAL: A.user_out[(row - A.local0) * A.ld + col] = s; break;   // sharded: this rank's rows
+        case OUT_FLUX_LOCAL: {   // sharded flux epilogue: T (padded rows x 64) and eps / A / g padded
+            const double eta = pow4(__ldcg(A.T_pad + row * kMrhsMax + col));
+            A.user_out[(row - A.local0) * A.ld + col] =
+                A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row]);
+            break;
+        }
         default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form)
             const int64_t e = A.perm[row];
             const double eta = pow4(A.user_in[e * A.ld + col]);
@@ -443,6 +449,14 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                     const int e = e0 + u * kMConsumers;
                     if (e < tot) emit_m(A, P, out0 + e / R, e % R, v[u]);
                 }
+            }
+        } else if (type == UNIT_PROLOGUE_INT) {
+            // sharded flux prologue: w = eps T^4 over padded rows, from the gathered T block
+            const int tot = nrows * R;
+            for (int e = ct; e < tot; e += kMConsumers) {
+                const int64_t row = out0 + e / R;
+                const int col = e % R;
+                P.out[row * kMrhsMax + col] = __ldg(A.eps_int + row) * pow4(__ldcg(P.in + row * kMrhsMax + col));
             }
         } else {
             // element-wise prologue: rows x R of the caller's external-order array permuted into the

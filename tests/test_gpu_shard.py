@@ -142,10 +142,10 @@ def test_virtual_shards_level_form(world, cut):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_virtual_shards_multi_rhs_apply(world):
-    """Sharded 64-RHS F apply (config 5's shape: row-cluster shards, allgather of the n x 64 block, DMMA
-    engine per rank): every column equals the world = 1 multi-RHS apply (1e-13) and the dense oracle
-    within 10 eps."""
+def test_virtual_shards_multi_rhs(world):
+    """Sharded 64-RHS F apply, C^-1 solve and flux (config 5's shape: row-cluster shards, allgathers of
+    n x 64 blocks, DMMA engine per rank): every column equals the world = 1 multi-RHS path (1e-13 /
+    1e-12) and the dense oracle within 10 eps."""
     import paper_2305_06891_b200 as hm
     cfg = synth.make_config(2, geometry=synth.icosphere(4), nrhs=64)
     f = cfg.facets
@@ -164,8 +164,14 @@ def test_virtual_shards_multi_rhs_apply(world):
             y = np.empty_like(x)
             for _ in range(2):
                 hm.hm_apply_F(ctx, F, x, y)
-            out[rank] = dict(rows=rows, y=y)
-            del F, g
+            LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+            z, q = np.empty_like(x), np.empty_like(x)
+            hm.hm_solve_C(ctx, LU, x, z)
+            Tl = np.ascontiguousarray(cfg.T[rows])
+            for _ in range(2):
+                hm.hm_radiative_flux(ctx, F, LU, Tl, q)
+            out[rank] = dict(rows=rows, y=y, z=z, q=q)
+            del LU, F, g
             ctx.close()
         except Exception as ex:                             # noqa: BLE001
             errs.append(f"rank {rank}: {ex!r}")
@@ -176,16 +182,26 @@ def test_virtual_shards_multi_rhs_apply(world):
     for t in th:
         t.join(timeout=600)
     assert not errs, errs
-    Y = np.empty_like(X)
+    Y, Z, Q = np.empty_like(X), np.empty_like(X), np.empty_like(X)
     for r in range(world):
-        Y[out[r]["rows"]] = out[r]["y"]
+        o = out[r]
+        Y[o["rows"]], Z[o["rows"]], Q[o["rows"]] = o["y"], o["z"], o["q"]
     ctx = hm.hm_init(0)
     g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
     F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
-    Y1 = np.empty_like(X)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    Y1, Z1, Q1 = np.empty_like(X), np.empty_like(X), np.empty_like(X)
     hm.hm_apply_F(ctx, F, X, Y1)
+    hm.hm_solve_C(ctx, LU, X, Z1)
+    hm.hm_radiative_flux(ctx, F, LU, np.ascontiguousarray(cfg.T), Q1)
     assert rel(Y, Y1) <= 1e-13
-    Fd, _, _ = vf.dense_operators(f, cfg.emissivity)
+    assert rel(Z, Z1) <= 1e-13
+    assert rel(Q, Q1) <= 1e-12
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
     Yd = Fd @ X
+    Zd = vf.solve(C, X)
+    Qd = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T)
     for c in (0, 17, 63):
         assert rel(Y[:, c], Yd[:, c]) <= 10 * cfg.eps_aca
+        assert rel(Z[:, c], Zd[:, c]) <= 10 * cfg.eps_aca
+        assert rel(Q[:, c], Qd[:, c]) <= 10 * cfg.eps_aca
