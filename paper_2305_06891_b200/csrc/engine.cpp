@@ -293,9 +293,10 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
         fprintf(stderr,
                 "[engine stats] passes %zu units %zu grid %d | per CTA (kcycles): producer wait-empty %.1f meta %.1f "
                 "chunks %.0f | gatherer(sum of warps) wait-full %.1f dep %.1f gather %.1f | consumer wait %.1f "
-                "compute %.1f task-end %.1f | retire wait %.1f work %.1f | producer wait-pempty %.1f total %.1f | consumer wait-gathered %.1f\n",
+                "compute %.1f task-end %.1f | retire wait %.1f work %.1f | producer wait-pempty %.1f total %.1f | consumer wait-gathered %.1f | handoff %.1f split-tasks %.0f\n",
                 h_passes.size(), h_units.size(), grid, h[0] / G / 1e3, h[1] / G / 1e3, h[2] / G, h[3] / G / 1e3,
-                h[4] / G / 1e3, h[5] / G / 1e3, h[6] / G / 1e3, h[7] / G / 1e3, h[8] / G / 1e3, h[9] / G / 1e3, h[10] / G / 1e3, h[11] / G / 1e3, h[12] / G / 1e3, h[13] / G / 1e3);
+                h[4] / G / 1e3, h[5] / G / 1e3, h[6] / G / 1e3, h[7] / G / 1e3, h[8] / G / 1e3, h[9] / G / 1e3, h[10] / G / 1e3, h[11] / G / 1e3, h[12] / G / 1e3, h[13] / G / 1e3,
+                h[14] / G / 1e3, (double)h[15]);
     }
 }
 

@@ -130,6 +130,63 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const dou
     }
 }
 
+// Warp tiling.  N8 == 8 (> 56 columns, the usual 64-RHS block): "2-D" -- consumer warp cw owns the
+// column-tile pair {2 (cw & 3), 2 (cw & 3) + 1} and the row tiles mt = (cw >> 2) + 2 j, so each A
+// fragment feeds two DMMAs and shared-memory fragment traffic per DMMA drops from (TM + 1) / TM to
+// (TM / 2 + 2) / TM (shared memory is the co-bottleneck with the TMA writes).  Otherwise tiles
+// t = cw + 8 i, (mt, nt) = (t / N8, t mod N8).  Tile i of the warp -> (mt, nt); false past the last.
+__device__ __forceinline__ bool warp_tile(int i, int cw, int M8, int N8, int& mt, int& nt) {
+    if (N8 == 8) {
+        mt = (cw >> 2) + 2 * (i >> 1);
+        nt = 2 * (cw & 3) + (i & 1);
+        return mt < M8;
+    }
+    const int t = cw + 8 * i;
+    mt = t / N8;
+    nt = t - mt * N8;
+    return t < M8 * N8;
+}
+
+// 2-D tiling (N8 == 8): RM row tiles x 2 column tiles, acc[2 j + c]
+template <int RM>
+__device__ __forceinline__ void mma_chunk2d(double (&acc)[kMaxTiles][2], const double* __restrict__ Ap,
+                                            const double* __restrict__ Xp, int ld, int ncols, int cw, int ar,
+                                            int ak) {
+    int arow[RM];
+#pragma unroll
+    for (int j = 0; j < RM; ++j) arow[j] = ((cw >> 2) + 2 * j) * 8 + ar;
+    const int bc = 2 * (cw & 3) * 8 + ar;
+    const int nfull = ncols & ~3;
+    for (int k4 = 0; k4 < nfull; k4 += 4) {
+        const double* Ak = Ap + (k4 + ak) * ld;
+        const double* Xk = Xp + (k4 + ak) * kXStride + bc;
+        double a[RM];
+#pragma unroll
+        for (int j = 0; j < RM; ++j) a[j] = Ak[arow[j]];
+        const double b0 = Xk[0], b1 = Xk[8];
+#pragma unroll
+        for (int j = 0; j < RM; ++j) {
+            dmma(acc[2 * j], a[j], b0);
+            dmma(acc[2 * j + 1], a[j], b1);
+        }
+    }
+    if (nfull < ncols) {   // k tail: zero A past ncols (stale A could be NaN; X rows there are zero)
+        const int kk = nfull + ak;
+        const bool kv = kk < ncols;
+        const double* Ak = Ap + kk * ld;
+        const double* Xk = Xp + kk * kXStride + bc;
+        double a[RM];
+#pragma unroll
+        for (int j = 0; j < RM; ++j) a[j] = kv ? Ak[arow[j]] : 0.0;
+        const double b0 = Xk[0], b1 = Xk[8];
+#pragma unroll
+        for (int j = 0; j < RM; ++j) {
+            dmma(acc[2 * j], a[j], b0);
+            dmma(acc[2 * j + 1], a[j], b1);
+        }
+    }
+}
+
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kMConsumers) : "memory"); }
 
 // out[row, col] for the program's output mode; vectors inside the library are row-major with
@@ -419,6 +476,16 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             // this warp's tiles t = cw + 8 i (row tiles mt, column tile nt); the k loop is
             // specialised on the tile count so the fragments of a k-step are loaded as a batch into
             // distinct registers and then feed back-to-back DMMAs
+            if (N8 == 8) {
+                switch ((M8 - (cw >> 2) + 1) >> 1) {   // this warp's row tiles
+#define HM_MMA2_CASE(RM) \
+    case RM: mma_chunk2d<RM>(acc, Ap, Xp, ldp, ncols, cw, ar, ak); break;
+                    HM_MMA2_CASE(1) HM_MMA2_CASE(2) HM_MMA2_CASE(3) HM_MMA2_CASE(4)
+                    HM_MMA2_CASE(5) HM_MMA2_CASE(6) HM_MMA2_CASE(7) HM_MMA2_CASE(8)
+#undef HM_MMA2_CASE
+                    default: break;
+                }
+            } else {
             int nmine = 0;
 #pragma unroll
             for (int i = 0; i < kMaxTiles; ++i)
@@ -432,6 +499,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 HM_MMA_CASE(13) HM_MMA_CASE(14) HM_MMA_CASE(15) HM_MMA_CASE(16)
 #undef HM_MMA_CASE
                 default: break;
+            }
             }
         } else if (type == UNIT_EPILOGUE) {
             // rows x R of the internal result through the pass's output mode (permute-out / flux
@@ -494,9 +562,8 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             if (grp < 0) {
 #pragma unroll
                 for (int i = 0; i < kMaxTiles; ++i) {
-                    const int t = cw + 8 * i;
-                    if (t >= ntile) break;
-                    const int mt = t / N8, nt = t - (t / N8) * N8;
+                    int mt, nt;
+                    if (!warp_tile(i, cw, M8, N8, mt, nt)) break;
                     const int row = mt * 8 + ar;
                     const int col = nt * 8 + 2 * ak;
                     if (row < nrows) {
@@ -508,9 +575,8 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 double* part = P.part + part_off;
 #pragma unroll
                 for (int i = 0; i < kMaxTiles; ++i) {
-                    const int t = cw + 8 * i;
-                    if (t >= ntile) break;
-                    const int mt = t / N8, nt = t - (t / N8) * N8;
+                    int mt, nt;
+                    if (!warp_tile(i, cw, M8, N8, mt, nt)) break;
                     const int row = mt * 8 + ar;
                     const int col = nt * 8 + 2 * ak;
                     if (row < nrows) {
