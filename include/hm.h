@@ -186,7 +186,7 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LU, int32_t nrhs, const double* 
 hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, int32_t nrhs,
                             const double* T, double* q, void* stream);
 
-/* ---- cavity operator around the hot path (world == 1) ---------- */
+/* ---- cavity operator around the hot path ------------------------ */
 /* Facet <- node projection P (n_facets x n_nodes, PAPER.md:175-183 eqn:projection_operator,
    P_iM = (1/A_i) int_{Gamma_i} phi_M dS) as host CSR arrays in EXTERNAL facet order: row_ptr[n+1]
    (int64, row_ptr[0] = 0), col[nnz] node ids in [0, n_nodes), val[nnz].  The library copies them. */
@@ -197,7 +197,9 @@ void hm_destroy_projection(hm_proj* P);
    eq:Rdef / eq:Rbardef): Q_N = sum_i q_i A_i P_iN with q of eq:qi_new_location at eta = P T^4 -- one
    projection, one C^-1 solve, one F apply, one transpose projection.  T_nodes, Q_nodes: n_nodes x nrhs
    (device or host, as for hm_radiative_flux).  LU must have been factored from F, P built on F's
-   geometry. */
+   geometry.  world > 1: nodal arrays are NOT sharded -- every rank passes all n_nodes values and
+   receives the full Q (each rank reduces over its own facets; the node partials are allgathered and
+   summed in rank order). */
 hm_status hm_cavity_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, hm_proj* P, int32_t nrhs,
                          const double* T_nodes, double* Q_nodes, void* stream);
 /* y = J^cav x = 4 S (T^3 o x) (eq:Jcav): the action GMRES needs,

@@ -931,6 +931,30 @@ void cavity_column(Ctx* c, HLU& L, Proj& P, const double* Tn, const double* xn, 
     k::proj_nodes(P.tp.p, P.ti.p, P.tv.p, P.rbar.p, ld, col, Qn, P.n_nodes, s);
 }
 
+// Sharded (world > 1): node vectors are replicated on every rank; each rank projects onto its own facets,
+// runs the sharded flux program with the eta-input / Rbar-output modes on its slice, projects back onto
+// the nodes its facets touch, and the per-rank node partials are allgathered and summed in rank order.
+void cavity_column_sharded(Ctx* c, HLU& L, Proj& P, const double* Tn, const double* xn, int mode, int ld, int col,
+                           double* Qn, cudaStream_t s) {
+    const Geom& g = *L.F->geom;
+    const Shard& S = g.shard;
+    k::proj_facets(P.rp_loc.p, P.ci_loc.p, P.cv_loc.p, Tn, xn, mode, ld, col, P.eta_loc.p, P.n_loc, s);
+    ProgArgs a = base_args(g, P.eta_loc.p, P.rbar_loc.p, 1, 0);
+    a.sigma = 5.670374419e-8;  // DESIGN.md reading R2
+    a.eps_int = L.eps_pad.p;
+    a.area_int = L.area_pad.p;
+    a.g_int = L.g_pad.p;
+    a.T_pad = L.T_pad;
+    a.eta_in = 1;
+    a.rbar_out = 1;
+    L.sp_flux.launch(c, g, a, s);
+    k::proj_nodes(P.tp_loc.p, P.ti_loc.p, P.tv_loc.p, P.rbar_loc.p, 1, 0, P.qpart.p + (int64_t)S.rank * P.qcount,
+                  P.n_nodes, s);
+    if (!c->ex) throw Error(HM_ERR_NOT_READY, "sharded cavity operator without an exchanger");
+    c->ex->allgather(P.qpart.p, P.qcount, s);
+    k::sum_segments(P.qpart.p, S.world, P.qcount, P.n_nodes, ld, col, Qn, s);
+}
+
 hm_status cavity_call(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, hm_proj* Ph, int32_t nrhs, const double* T,
                       const double* x, double* out, void* stream, int mode) {
     if (!ctx || !Fh || !LUh || !Ph || !T || !out || nrhs < 1 || (mode == 1 && !x)) return HM_ERR_INVALID_ARG;
@@ -940,8 +964,6 @@ hm_status cavity_call(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, hm_proj
     }
     Ctx* c = &ctx->c;
     return guarded(c, [&] {
-        if (Fh->h.geom->shard.sharded())
-            throw Error(HM_ERR_UNSUPPORTED, "cavity operator: world == 1 only in this build");
         HLU& L = const_cast<HLU&>(LUh->h);
         Proj& P = Ph->p;
         const size_t cnt = (size_t)P.n_nodes * nrhs;
@@ -955,7 +977,11 @@ hm_status cavity_call(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, hm_proj
             if (P.host_out.n < cnt) P.host_out.alloc(c, cnt, "host staging (out)");
             od = P.host_out.p;
         }
-        for (int col = 0; col < nrhs; ++col) cavity_column(c, L, P, Td, xd, mode, nrhs, col, od, s);
+        const bool sharded = Fh->h.geom->shard.sharded();
+        for (int col = 0; col < nrhs; ++col) {
+            if (sharded) cavity_column_sharded(c, L, P, Td, xd, mode, nrhs, col, od, s);
+            else cavity_column(c, L, P, Td, xd, mode, nrhs, col, od, s);
+        }
         if (hout) HM_CUDA(cudaMemcpyAsync(out, od, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (h1 || h2 || hout) HM_CUDA(cudaStreamSynchronize(s));
     });
@@ -1010,6 +1036,44 @@ hm_status hm_projection_create(hm_ctx* ctx, const hm_geom* geom, int64_t n_nodes
         P.tv.upload(c, tv, "P^T val", s);
         P.eta.alloc(c, (size_t)n, "cavity eta");
         P.rbar.alloc(c, (size_t)n, "cavity Rbar eta");
+        const Shard& S = geom->g.shard;
+        if (S.sharded()) {   // this rank's facets in local internal order (the sharded flux's slice)
+            const int64_t lb = S.lb(), nl = S.le() - S.lb();
+            std::vector<int64_t> rl(nl + 1, 0);
+            std::vector<int32_t> cl;
+            std::vector<double> vl;
+            for (int64_t r = 0; r < nl; ++r) {
+                const int64_t i = geom->g.perm[lb + r];
+                for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; ++q) {
+                    cl.push_back(col[q]);
+                    vl.push_back(val[q]);
+                }
+                rl[r + 1] = (int64_t)cl.size();
+            }
+            std::vector<int64_t> tl(n_nodes + 1, 0);
+            for (int32_t m : cl) ++tl[m + 1];
+            for (int64_t m = 0; m < n_nodes; ++m) tl[m + 1] += tl[m];
+            std::vector<int32_t> til(cl.size());
+            std::vector<double> tvl(cl.size());
+            std::vector<int64_t> fl(tl.begin(), tl.end() - 1);
+            for (int64_t r = 0; r < nl; ++r)
+                for (int64_t q = rl[r]; q < rl[r + 1]; ++q) {
+                    const int64_t d = fl[cl[q]]++;
+                    til[d] = (int32_t)r;
+                    tvl[d] = vl[q];
+                }
+            P.n_loc = nl;
+            P.qcount = (n_nodes + 1) & ~int64_t(1);
+            P.rp_loc.upload(c, rl, "P row_ptr (local)", s);
+            P.ci_loc.upload(c, cl.empty() ? std::vector<int32_t>{0} : cl, "P col (local)", s);
+            P.cv_loc.upload(c, vl.empty() ? std::vector<double>{0.0} : vl, "P val (local)", s);
+            P.tp_loc.upload(c, tl, "P^T row_ptr (local)", s);
+            P.ti_loc.upload(c, til.empty() ? std::vector<int32_t>{0} : til, "P^T facets (local)", s);
+            P.tv_loc.upload(c, tvl.empty() ? std::vector<double>{0.0} : tvl, "P^T val (local)", s);
+            P.eta_loc.alloc(c, (size_t)std::max<int64_t>(nl, 1), "cavity eta (local)");
+            P.rbar_loc.alloc(c, (size_t)std::max<int64_t>(nl, 1), "cavity Rbar eta (local)");
+            P.qpart.alloc(c, (size_t)(S.world * P.qcount), "cavity node partials");
+        }
         HM_CUDA(cudaStreamSynchronize(s));
         *out = guard.release();
     });

@@ -505,6 +505,8 @@ void flux_prologue(const double* T_ext, int ld, int col, const int32_t* perm, co
 void fill_value(double* p, int64_t n, double v, cudaStream_t s);
 void proj_facets(const int64_t* rp, const int32_t* col_idx, const double* val, const double* T, const double* x,
                  int mode, int ld, int col, double* eta, int64_t n, cudaStream_t s);
+// out[N * ld + col] = sum_{r < world} buf[r * count + N] in rank order (sharded node reduction)
+void sum_segments(const double* buf, int world, int64_t count, int64_t n, int ld, int col, double* out, cudaStream_t s);
 void proj_nodes(const int64_t* tp, const int32_t* tidx, const double* tval, const double* y, int ld, int col, double* Q,
                 int64_t n_nodes, cudaStream_t s);
 void row_sums_clamp(const double* y, const double* area, double* sv, double* c, double* cdiv,
@@ -556,6 +558,12 @@ struct Proj {
     DBuf<double> cv, tv;
     DBuf<double> eta, rbar;     // facet workspaces (external order)
     DBuf<double> host_in, host_in2, host_out;
+    // sharded (world > 1): this rank's facets (internal rows [lb, le)) as CSR rows in local order, the
+    // transpose restricted to them, and the allgather buffer of per-rank node partials (qcount each)
+    DBuf<int64_t> rp_loc, tp_loc;
+    DBuf<int32_t> ci_loc, ti_loc;
+    DBuf<double> cv_loc, tv_loc, eta_loc, rbar_loc, qpart;
+    int64_t n_loc = 0, qcount = 0;
 };
 }  // namespace hm
 struct hm_proj { hm::Proj p; };

@@ -85,11 +85,26 @@ __global__ void proj_nodes_kernel(const int64_t* __restrict__ tp, const int32_t*
     Q[M * ld + col] = s;
 }
 
+__global__ void sum_segments_kernel(const double* __restrict__ buf, int world, int64_t count, int64_t n, int ld,
+                                    int col, double* __restrict__ out) {
+    const int64_t N = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (N >= n) return;
+    double s = 0.0;
+    for (int r = 0; r < world; ++r) s += buf[(int64_t)r * count + N];
+    out[N * ld + col] = s;
+}
+
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
 
 namespace k {
+
+void sum_segments(const double* buf, int world, int64_t count, int64_t n, int ld, int col, double* out, cudaStream_t s) {
+    sum_segments_kernel<<<nblk(n, 256), 256, 0, s>>>(buf, world, count, n, ld, col, out);
+    HM_CUDA(cudaGetLastError());
+    debug_sync(s, "sum_segments");
+}
 
 void permute_in(const double* x_ext, int ld, int col, const int32_t* perm, double* x_int, int64_t n, cudaStream_t s) {
     permute_in_kernel<<<nblk(n, 256), 256, 0, s>>>(x_ext, ld, col, perm, x_int, n);

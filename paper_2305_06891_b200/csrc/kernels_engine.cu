@@ -91,10 +91,11 @@ __device__ __forceinline__ void emit(const ProgArgs& A, const Pass& P, int64_t r
         case OUT_SUB: P.out[row] = __ldcg(P.out + row) - s; break;
         case OUT_PERM: A.user_out[(int64_t)A.perm[row] * A.ld + A.col] = s; break;
         case OUT_LOCAL: A.user_out[(row - A.local0) * A.ld + A.col] = s; break;
-        case OUT_FLUX_LOCAL: {
-            const double eta = pow4(__ldcg(A.T_pad + row));
-            A.user_out[(row - A.local0) * A.ld + A.col] =
-                A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row]);
+        case OUT_FLUX_LOCAL: {   // sharded; eta_in / rbar_out as in OUT_FLUX (sharded cavity operator)
+            const double t = __ldcg(A.T_pad + row);
+            const double eta = A.eta_in ? t : pow4(t);
+            const double sc = A.rbar_out ? A.eps_int[row] : A.eps_int[row] / A.area_int[row];
+            A.user_out[(row - A.local0) * A.ld + A.col] = A.sigma * sc * (s - eta * A.g_int[row]);
             break;
         }
         default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form);
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                         if (im == IN_FLUXI) {   // sharded flux prologue: w_j = eps_j T_j^4 (x region)
 #pragma unroll
                             for (int q = 0; q < kPer; ++q)
-                                if (idx[q] >= 0 && idx[q] < A.n_x) v[q] = __ldg(A.eps_int + idx[q]) * pow4(v[q]);
+                                if (idx[q] >= 0 && idx[q] < A.n_x) v[q] = __ldg(A.eps_int + idx[q]) * (A.eta_in ? v[q] : pow4(v[q]));
                         }
                     } else if (im == IN_PLAIN || im == IN_FLUXI) {
                         int32_t idx[kPer];
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                         if (im == IN_FLUXI) {
 #pragma unroll
                             for (int q = 0; q < kPer; ++q)
-                                if (idx[q] >= 0 && idx[q] < A.n_x) v[q] = __ldg(A.eps_int + idx[q]) * pow4(v[q]);
+                                if (idx[q] >= 0 && idx[q] < A.n_x) v[q] = __ldg(A.eps_int + idx[q]) * (A.eta_in ? v[q] : pow4(v[q]));
                         }
                     } else {
                         // fused prologue: x-region inputs come straight from the caller's external-order
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             if (u.type == UNIT_PROLOGUE_INT) {   // sharded: w = eps T^4 in place on padded internal rows
                 for (int i = ct; i < u.nrows; i += kConsumers) {
                     const int64_t row = u.out0 + i;
-                    P.out[row] = A.eps_int[row] * pow4(P.in[row]);
+                    P.out[row] = A.eps_int[row] * (A.eta_in ? P.in[row] : pow4(P.in[row]));
                 }
             } else {
                 for (int i = ct; i < u.nrows; i += kConsumers) {   // element-wise: rows [out0, out0 + nrows)

@@ -205,3 +205,59 @@ def test_virtual_shards_multi_rhs(world):
         assert rel(Y[:, c], Yd[:, c]) <= 10 * cfg.eps_aca
         assert rel(Z[:, c], Zd[:, c]) <= 10 * cfg.eps_aca
         assert rel(Q[:, c], Qd[:, c]) <= 10 * cfg.eps_aca
+
+
+@pytest.mark.parametrize("world,cut", [(2, -1), (4, -1), (4, 99)])
+def test_virtual_shards_cavity_operator(world, cut):
+    """Sharded cavity operator (NEXT-1 on G ranks): nodal T / x replicated, each rank projects onto its own
+    facets, runs the sharded flux program (eta input, Rbar output) and projects back; the per-rank node
+    partials are allgathered and summed in rank order.  Q and J^cav x equal world = 1 within 1e-12 and the
+    dense oracle within 10 eps on every rank."""
+    import paper_2305_06891_b200 as hm
+    from oracle import cavity as ocav
+    cfg = synth.make_config(2, geometry=synth.icosphere(3))
+    f = cfg.facets
+    csr = synth.projection_csr(f)
+    Tn = synth.node_temperatures(cfg.seed, f.n_nodes)
+    xn = synth.uniform(5, f.n_nodes) - 0.5
+    out, errs = {}, []
+
+    def run(rank):
+        try:
+            ctx = hm.hm_init(0, rank, world, 900 + 10 * world + (cut > 0), hm.HM_FLAG_LOCAL_GROUP)
+            g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
+            F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+            LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=cut)
+            P = hm.hm_projection_create(ctx, g, f.n_nodes, *csr)
+            Q, y = np.empty(f.n_nodes), np.empty(f.n_nodes)
+            for _ in range(2):
+                hm.hm_cavity_flux(ctx, F, LU, P, Tn, Q)
+                hm.hm_cavity_jacobian(ctx, F, LU, P, Tn, xn, y)
+            out[rank] = (Q, y)
+            del P, LU, F, g
+            ctx.close()
+        except Exception as ex:                             # noqa: BLE001
+            errs.append(f"rank {rank}: {ex!r}")
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    ctx = hm.hm_init(0)
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=cut)
+    P = hm.hm_projection_create(ctx, g, f.n_nodes, *csr)
+    Q1, y1 = np.empty(f.n_nodes), np.empty(f.n_nodes)
+    hm.hm_cavity_flux(ctx, F, LU, P, Tn, Q1)
+    hm.hm_cavity_jacobian(ctx, F, LU, P, Tn, xn, y1)
+    Pd = ocav.dense_projection(f.n, f.n_nodes, *csr)
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
+    S = ocav.S_matrix(ocav.Rbar_matrix(ocav.R_matrix(Fd, C, cfg.emissivity)), Pd)
+    for r in range(world):
+        Q, y = out[r]
+        assert rel(Q, Q1) <= 1e-12 and rel(y, y1) <= 1e-12
+        assert rel(Q, ocav.flux_residual(S, Tn)) <= 10 * cfg.eps_aca
+        assert rel(y, ocav.jacobian_apply(S, Tn, xn)) <= 10 * cfg.eps_aca
