@@ -164,10 +164,13 @@ hm_status hm_build_geometry(hm_ctx* ctx, int64_t n, const double* xyz, const dou
 hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params* params,
                           hm_hmat** F_out);
 /* One-time factorisation of C = I - Lambda F (Lambda_ii = (1-eps_i)/A_i) in the block
-   structure of F, stored in LEVEL FORM for the level-scheduled solve
-   (DESIGN.md §solve): per internal node t, W^L_t = L21 L11^-1 and W^U_t = U12 U22^-1
-   compressed to eps_lu in the block partition of F, plus dense leaf inverses.
-   emissivity: host array, n, external order, 0 < eps_i <= 1. */
+   structure of F, stored for the solve form chosen by params->cut_level
+   (reading R27): per internal node t above the cut, W^L_t = L21 L11^-1 and
+   W^U_t = U12 U22^-1, and the inverse factors of the cut-level diagonal blocks, all compressed
+   to eps_lu in the block partition of F (cut 0, the default: L^-1 and U^-1 as two H-matrices;
+   cut >= depth: the pure level form with dense leaf inverses).
+   emissivity: host array, n, external order, 0 < eps_i <= 1.  The factorisation is dense on
+   the GPU (stage A, R28): HM_ERR_UNSUPPORTED when it does not fit (n above ~1e5). */
 hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
                         const hm_lu_params* params, hm_hlu** out);
 
@@ -176,7 +179,8 @@ hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
    1/A_i, reading R1).  x, y: n x nrhs, external order; x and y must not overlap. */
 hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* F, int32_t nrhs, const double* x, double* y,
                      void* stream);
-/* z ~= C^-1 b by level-scheduled forward then backward substitution. */
+/* z ~= C^-1 b by forward then backward substitution with the factors: level-
+   scheduled W updates above the cut, then the cut-level inverse factors (R27). */
 hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LU, int32_t nrhs, const double* b, double* z,
                      void* stream);
 /* q = sigma (eps/A) o (F C^-1 (eps o eta) - eta o g), eta = T^4, g = F C^-1 eps (cached at
