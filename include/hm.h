@@ -175,8 +175,8 @@ hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
                         const hm_lu_params* params, hm_hlu** out);
 
 /* ---- hot path ------------------------------------------------------------------------- */
-/* y = F x (F is the stored, closed-cavity-scaled H-matrix; the paper's convention without
-   1/A_i, reading R1).  x, y: n x nrhs, external order; x and y must not overlap. */
+/* y = F x, the H-matrix-vector product of PAPER.md:782 (F of eq:Fdef_new_location, PAPER.md:150-153,
+   as stored: closed-cavity-scaled, the paper's convention without 1/A_i, reading R1).  x, y: n x nrhs, external order; x and y must not overlap. */
 hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* F, int32_t nrhs, const double* x, double* y,
                      void* stream);
 /* z ~= C^-1 b by forward then backward substitution with the factors: level-
