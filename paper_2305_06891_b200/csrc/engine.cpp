@@ -257,7 +257,12 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
     queue.alloc(ctx, 1, "engine task queue");
     HM_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(unsigned long long), s));
     grid = mrhs ? engine_mrhs_grid() : engine_grid();
-    epoch = 0;
+    {
+        const unsigned long long e0[2] = {1ull, 0ull};
+        epoch_dev.alloc(ctx, 2, "engine epoch");
+        HM_CUDA(cudaMemcpyAsync(epoch_dev.p, e0, sizeof(e0), cudaMemcpyHostToDevice, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+    }
     ready = true;
 }
 
@@ -271,11 +276,10 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
     a.n_tasks = (int64_t)h_tasks.size();
     a.queue = queue.p;
     // every CTA's producer takes exactly one index past the end: the counter advances by
-    // n_tasks + grid per launch
-    a.queue_base = epoch * (unsigned long long)(h_tasks.size() + grid);
+    // n_tasks + grid per launch (the kernel derives its base from the device epoch)
     a.n_units = (int64_t)h_units.size();
     a.done = done.p;
-    a.epoch = ++epoch;
+    a.epoch_dev = epoch_dev.p;
     if (a.ld == 0) a.ld = 1;
     static const bool want_stats = [] { const char* e = getenv("HM_ENGINE_STATS"); return e && e[0] == '1'; }();
     if (want_stats) {

@@ -73,8 +73,19 @@ __device__ __forceinline__ double pow4(double T) {
     return t2 * t2;
 }
 
-__device__ __forceinline__ void wait_counter(const ProgArgs& A, int id, int cnt) {
-    const unsigned long long target = A.epoch * (unsigned long long)cnt;
+// This launch's epoch (program launch number, 1-based) into *out_smem by thread 0 before the CTA
+// barrier that follows; the last CTA to start advances the device epoch for the next launch.
+__device__ __forceinline__ void read_epoch(const ProgArgs& A, unsigned long long* out_smem) {
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(A.epoch_dev);
+    *out_smem = e;
+    if (atomicAdd(A.epoch_dev + 1, 1ull) == e * gridDim.x - 1) {   // every CTA of this launch has read e
+        *reinterpret_cast<volatile unsigned long long*>(A.epoch_dev) = e + 1;
+        __threadfence();
+    }
+}
+
+__device__ __forceinline__ void wait_counter(const ProgArgs& A, unsigned long long epoch, int id, int cnt) {
+    const unsigned long long target = epoch * (unsigned long long)cnt;
     const unsigned long long* d = A.done + id;
     unsigned ns = 20;
     while (true) {

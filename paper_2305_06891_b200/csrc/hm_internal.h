@@ -312,13 +312,15 @@ struct ProgArgs {
     const Unit* units;
     const Task* tasks;
     int64_t n_tasks;
-    unsigned long long* queue;  // monotone task counter
-    unsigned long long queue_base;  // counter value at the start of this launch
+    unsigned long long* queue;  // monotone task counter: advances by n_tasks + grid per launch
     int64_t n_units;
     unsigned long long* done;   // dependency counters (passes, then per-node), monotone over launches
     unsigned long long* trace;  // optional: per pass [first gather, last retire] (%globaltimer ns)
     unsigned long long* stats;  // optional: per-role SM cycle counters (diagnostics, HM_ENGINE_STATS=1)
-    unsigned long long epoch;   // launch number of this program (1-based)
+    // [0] launch number of this program (1-based), [1] CTA starts so far.  Read by every CTA at its
+    // start; the last CTA to start advances [0] -- so the epoch lives on the device and a launch
+    // captured in a CUDA graph is replayable (no host-side launch counter baked into the arguments)
+    unsigned long long* epoch_dev;
     const int32_t* perm;
     const double* user_in;      // x / b / T (external order, ld x ncol)
     int64_t n_x;                // size of the x region of XT (IN_PERM / IN_FLUX apply below it)
@@ -350,7 +352,7 @@ struct Program {
     DBuf<Task> tasks;
     DBuf<unsigned long long> queue;   // monotone task counter (epoch * n_tasks at the end of a launch)
     DBuf<unsigned long long> done;
-    unsigned long long epoch = 0;
+    DBuf<unsigned long long> epoch_dev;   // see ProgArgs::epoch_dev
     int grid = 0;
     bool ready = false;
     bool mrhs = false;   // multi-RHS program (engine_mrhs_kernel, kMrhsMax columns per launch)

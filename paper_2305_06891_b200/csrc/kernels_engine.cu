@@ -83,6 +83,7 @@ struct EngineSmem {
     unsigned long long gready[kGSlots], gathered[kGSlots], gempty[kGSlots];
     unsigned long long full[kPStages], pempty[kPStages];
     unsigned long long rfull[kRetireSlots], rempty[kRetireSlots];
+    unsigned long long epoch;   // this launch's epoch (read_epoch)
 };
 
 __device__ __forceinline__ void emit(const ProgArgs& A, const Pass& P, int64_t row, double s) {
@@ -129,9 +130,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             mbar_init(&S.rempty[r], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        read_epoch(A, &S.epoch);
     }
     for (int i = tid; i < A.n_passes; i += kThreads) S.passes[i] = A.passes[i];
     __syncthreads();
+    const unsigned long long epoch = S.epoch;
+    const unsigned long long queue_base = (epoch - 1) * (unsigned long long)(A.n_tasks + gridDim.x);
 
     if (warp == 0) {
         // ------------------------------------------------ producer (one thread): grab tasks; per chunk,
@@ -167,12 +171,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             st_empty += clock64() - c0;
             return g;
         };
-        unsigned long long t = atomicAdd(A.queue, 1ull) - A.queue_base;
+        unsigned long long t = atomicAdd(A.queue, 1ull) - queue_base;
         bool have_t = t < (unsigned long long)A.n_tasks;
         unsigned long long tn = ~0ull;   // pending grab of the next task index
         Task task{};
         if (have_t) {
-            tn = atomicAdd(A.queue, 1ull) - A.queue_base;
+            tn = atomicAdd(A.queue, 1ull) - queue_base;
             task = A.tasks[t];
         }
         while (have_t) {
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             unsigned long long tnn = ~0ull;
             if (have_n) {
                 task_n = A.tasks[tn];
-                tnn = atomicAdd(A.queue, 1ull) - A.queue_base;
+                tnn = atomicAdd(A.queue, 1ull) - queue_base;
             }
             st_meta += clock64() - c0;
             const int nch = task.n_units;
@@ -240,10 +244,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                         for (int q = 0; q < 2; ++q) {
                             const int id = H.wait_id[q];
                             if (id < 0) continue;
-                            const unsigned long long tgt = A.epoch * (unsigned long long)H.wait_cnt[q];
+                            const unsigned long long tgt = epoch * (unsigned long long)H.wait_cnt[q];
                             if (id == sat_id[0] && tgt <= sat_tgt[0]) continue;
                             if (id == sat_id[1] && tgt <= sat_tgt[1]) continue;
-                            wait_counter(A, id, H.wait_cnt[q]);
+                            wait_counter(A, epoch, id, H.wait_cnt[q]);
                             sat_id[1] = sat_id[0]; sat_tgt[1] = sat_tgt[0];
                             sat_id[0] = id; sat_tgt[0] = tgt;
                         }

@@ -58,6 +58,7 @@ struct MSmem {
     MStage st[kMStages];
     Pass passes[kMaxPassesM];
     PubDesc pub[kPubSlots];
+    unsigned long long epoch;   // this launch's epoch (read_epoch)
     unsigned long long posted[kMStages], full[kMStages], gathered[kMStages], empty[kMStages];
     unsigned long long pfull[kPubSlots], pempty[kPubSlots];
     int last;
@@ -230,15 +231,18 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             mbar_init(&S.pempty[r], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        read_epoch(A, &S.epoch);
     }
     for (int i = tid; i < A.n_passes; i += kMThreads) S.passes[i] = A.passes[i];
     __syncthreads();
+    const unsigned long long epoch = S.epoch;
+    const unsigned long long queue_base = (epoch - 1) * (unsigned long long)(A.n_tasks + gridDim.x);
 
     if (warp == 0) {
         // ------------------------------------------------ producer
         unsigned long long nxt = 0, st_e = 0, st_m = 0;
         const long long t0 = clock64();
-        if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - A.queue_base;
+        if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - queue_base;
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
         int64_t k = 0;
         while (true) {
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             Task task{};
             if (!end) {
                 task = A.tasks[t];
-                if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - A.queue_base;
+                if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - queue_base;
             }
             const int nch = end ? 1 : task.n_units;
             for (int base = 0; base < nch; base += 32) {
@@ -319,8 +323,8 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             const int type = H.type;
             if (type >= 0 && H.task != verified) {
                 if (lane == 0) {
-                    if (H.wait_id[0] >= 0) wait_counter(A, H.wait_id[0], H.wait_cnt[0]);
-                    if (H.wait_id[1] >= 0) wait_counter(A, H.wait_id[1], H.wait_cnt[1]);
+                    if (H.wait_id[0] >= 0) wait_counter(A, epoch, H.wait_id[0], H.wait_cnt[0]);
+                    if (H.wait_id[1] >= 0) wait_counter(A, epoch, H.wait_id[1], H.wait_cnt[1]);
                 }
                 __syncwarp();
                 fence_proxy_async_global();

@@ -604,3 +604,36 @@ def test_parallel_plates_open_cavity(hm, ctx, m):
     torch.cuda.synchronize()
     qo = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]
     assert rel(q.cpu().numpy(), qo) <= 10 * cfg.eps_aca
+
+
+def test_flux_cuda_graph_replay(hm, ctx):
+    """The hot path is graph-capturable and REPLAYABLE: the engine's launch epoch lives on the device,
+    so a captured hm_radiative_flux replayed with new temperatures in the captured input buffer gives
+    the eager results bitwise (fixed-order reductions), for the single-vector and the 64-RHS engine."""
+    import torch
+    cfg = synth.make_config(2, geometry=synth.icosphere(4), nrhs=64)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    for cols in (1, 64):
+        T = torch.from_numpy(np.ascontiguousarray(cfg.T[:, :cols])).cuda()
+        q = torch.empty_like(T)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            hm.hm_radiative_flux(ctx, F, LU, T, q, stream=side.cuda_stream)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            hm.hm_radiative_flux(ctx, F, LU, T, q, stream=torch.cuda.current_stream().cuda_stream)
+        for trial in range(3):
+            Tn = cfg.T[:, :cols] + 10.0 * (trial + 1)
+            T.copy_(torch.from_numpy(np.ascontiguousarray(Tn)))
+            graph.replay()
+            torch.cuda.synchronize()
+            qg = q.cpu().numpy().copy()
+            qe = torch.empty_like(T)
+            hm.hm_radiative_flux(ctx, F, LU, T, qe)
+            torch.cuda.synchronize()
+            assert np.array_equal(qg, qe.cpu().numpy()), (cols, trial)
