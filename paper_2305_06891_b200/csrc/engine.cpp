@@ -178,7 +178,11 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
         if (kind == DEP_BARRIER) {
             // HM_DIAG_DEPS (timing experiments only, results are wrong): "none" drops every wait,
             // "intra" the phase-1 -> phase-2 waits, "cross" the operator-to-operator waits
-            static const char* diagb = getenv("HM_DIAG_DEPS");
+            static const char* diagb = [] {
+                const char* e = getenv("HM_DIAG_DEPS");
+                if (e) fprintf(stderr, "[hm] HM_DIAG_DEPS=%s: dependency waits dropped -- timing experiment, results are WRONG\n", e);
+                return e;
+            }();
             const char* diag = diagb;
             const int xd = pass_xdep[t.pass];
             if (diag && diag[0] == 'n') continue;

@@ -17,6 +17,14 @@ namespace hm {
 
 static inline int64_t align2(int64_t x) { return (x + 1) & ~int64_t(1); }
 
+// experiment knobs (piece sizing): positive integers only, else the default
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    if (!e) return dflt;
+    const int v = atoi(e);
+    return v >= 1 && v <= 1 << 20 ? v : dflt;
+}
+
 // Cut panels into pieces (only panels above 512 KB are split, for load balance) and pieces into
 // chunks of <= 32 KB contiguous payload (<= 512 columns), each chunk with its own 16-byte
 // aligned column-source segment (so the engine can TMA both).
@@ -37,9 +45,9 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
     // HM_PIECE_MIN override for experiments
     int64_t pass_doubles = 0;
     for (const Panel& pn : P.panels) pass_doubles += (int64_t)pn.ncols * pn.ld;
-    static const int piece_div = getenv("HM_PIECE_DIV") ? atoi(getenv("HM_PIECE_DIV")) : 2;
-    static const int piece_min = getenv("HM_PIECE_MIN") ? atoi(getenv("HM_PIECE_MIN")) : 4;
-    static const int mrhs_min = getenv("HM_MRHS_PIECE_MIN") ? atoi(getenv("HM_MRHS_PIECE_MIN")) : 64;   // measured C2 flux: 4 -> 1.46, 64 -> 1.35 ms
+    static const int piece_div = env_int("HM_PIECE_DIV", 2);
+    static const int piece_min = env_int("HM_PIECE_MIN", 4);
+    static const int mrhs_min = env_int("HM_MRHS_PIECE_MIN", 64);   // measured C2 64-RHS flux: 4 -> 1.46, 64 -> 1.35 ms
     // multi-RHS units (part_scale > 1): compute-bound, and every split piece costs a rows x 64 partial
     // write + combine, so only panels above mrhs_min chunks (HM_MRHS_PIECE_MIN) are split
     const int64_t piece = part_scale > 1
@@ -64,7 +72,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
             const int64_t w = sg.c1 - sg.c0;
             if (w <= 0) continue;
             // t-reading segments of split passes (phase 2) end the pass: optionally finer pieces there
-            static const int tdiv = getenv("HM_PIECE_TDIV") ? atoi(getenv("HM_PIECE_TDIV")) : 2;   // measured: 1 -> 184.7, 2 -> 183.4 us
+            static const int tdiv = env_int("HM_PIECE_TDIV", 2);   // measured: 1 -> 184.7, 2 -> 183.4 us
             const int64_t pc_sz = (&sg == &segs[1] && nd > 0) ? std::max<int64_t>(2 * kUnitPayloadDoubles, piece / tdiv) : piece;
             sg.np = (int32_t)std::min<int64_t>(w, (w * pn.ld + pc_sz - 1) / pc_sz);
             npieces += sg.np;
