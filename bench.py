@@ -298,6 +298,24 @@ def main():
                         "flux_hbm_gbs": b_rc / (rc_ms["flux"] * 1e-3) / 1e9,
                         "setup_recompress_s": rep_rc["setup_seconds"].get("aca")}
         del LU_rc, F_rc
+    # multi-RHS: 64 temperature columns per call through the DMMA engine
+    multi_rhs = None
+    if not args.no_level_form and world == 1:
+        Tm = torch.from_numpy(np.ascontiguousarray(synth.make_config(args.config, nrhs=64).T)).cuda()
+        qm = torch.empty_like(Tm)
+        for _ in range(3):
+            hm.hm_radiative_flux(ctx, F, LU, Tm, qm, stream=stream.cuda_stream)
+        em0, em1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        em0.record(stream)
+        for _ in range(args.profile_iters):
+            hm.hm_radiative_flux(ctx, F, LU, Tm, qm, stream=stream.cuda_stream)
+        em1.record(stream)
+        torch.cuda.synchronize()
+        mms = em0.elapsed_time(em1) / args.profile_iters
+        flop = 2.0 * 64 * (rep["bytes_F"] + rep["bytes_C"]) / 8
+        multi_rhs = {"nrhs": 64, "flux_ms": mms, "column_applies_per_s": 64 / (mms * 1e-3),
+                     "fp64_tflops": flop / (mms * 1e-3) / 1e12, "engine": "engine_mrhs_kernel (DMMA)"}
+        del Tm, qm
     # NEXT-1: the cavity Jacobian action J^cav x = 4 P^T Rbar P (T^3 o x) (eq:Jcav) GMRES applies, on the
     # same operators (one projection + the flux program + one transpose projection)
     jcav = None
@@ -345,7 +363,7 @@ def main():
                        "ranks_C": {"mean": rep["rank_mean_C"], "max": rep["rank_max_C"]},
                        "setup_s": dict(rep["setup_seconds"], wall=setup_wall),
                        "solve_form": "inverse factors (cut level 0, DESIGN.md R27)",
-                       "level_form": level_form, "recompressed": recompressed,
+                       "level_form": level_form, "recompressed": recompressed, "multi_rhs": multi_rhs,
                        "cavity_jacobian_action": jcav},
             "roofline": {"bound": "hbm", "kernel": "engine_kernel (flux program)" + (" + NCCL allgathers, rank 0" if world > 1 else ""),
                          "achieved": achieved,
