@@ -121,15 +121,24 @@ def header_symbols(header: str = HEADER) -> list:
 
 
 # ----------------------------------------------------------------------------- marshalling
-def _ptr(a):
-    """(pointer, keepalive) for a numpy array or torch tensor (float64/int32, contiguous)."""
+def _ptr(a, out=False):
+    """(pointer, keepalive) for a float64 numpy array or torch tensor.  Inputs are converted to a
+    C-contiguous float64 copy if needed; outputs (out=True) must already be C-contiguous float64 (a
+    converted copy would silently drop the results)."""
     if a is None:
         return None, None
     if hasattr(a, "data_ptr"):           # torch.Tensor
+        import torch
+        if a.dtype != torch.float64:
+            raise TypeError(f"tensor must be float64, got {a.dtype}")
         if not a.is_contiguous():
             raise ValueError("tensor must be contiguous")
         return a.data_ptr(), a
-    arr = np.ascontiguousarray(a)
+    if out:
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise TypeError("output array must be a C-contiguous float64 numpy array")
+        return a.ctypes.data, a
+    arr = np.ascontiguousarray(a, dtype=np.float64)
     return arr.ctypes.data, arr
 
 
@@ -285,14 +294,14 @@ def _nrhs(x, n):
 def hm_apply_F(ctx: Context, F: HMatrix, x, y, stream=None):
     """y = F x; x, y: (n,) or (n, nrhs) float64, device tensors or host arrays."""
     px, kx = _ptr(x)
-    py, ky = _ptr(y)
+    py, ky = _ptr(y, out=True)
     ctx.check(ctx.lib.hm_apply_F(ctx.h, F.h, _nrhs(x, _rows(F, F.geom)), px, py, _stream(stream, x, y)), "hm_apply_F")
     return y
 
 
 def hm_solve_C(ctx: Context, LU: HLU, b, z, stream=None):
     pb, kb = _ptr(b)
-    pz, kz = _ptr(z)
+    pz, kz = _ptr(z, out=True)
     ctx.check(ctx.lib.hm_solve_C(ctx.h, LU.h, _nrhs(b, _rows(LU, LU.F.geom)), pb, pz, _stream(stream, b, z)),
               "hm_solve_C")
     return z
@@ -300,7 +309,7 @@ def hm_solve_C(ctx: Context, LU: HLU, b, z, stream=None):
 
 def hm_radiative_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, stream=None):
     pT, kT = _ptr(T)
-    pq, kq = _ptr(q)
+    pq, kq = _ptr(q, out=True)
     ctx.check(ctx.lib.hm_radiative_flux(ctx.h, F.h, LU.h, _nrhs(T, _rows(F, F.geom)), pT, pq, _stream(stream, T, q)),
               "hm_radiative_flux")
     return q
@@ -345,7 +354,7 @@ def hm_profile_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, iters: int, stream=
     ms = (C.c_double * 6)()
     la = (C.c_int64 * 6)()
     pT, kT = _ptr(T)
-    pq, kq = _ptr(q)
+    pq, kq = _ptr(q, out=True)
     ctx.check(ctx.lib.hm_profile_flux(ctx.h, F.h, LU.h, pT, pq, int(iters), ms, la, _stream(stream, T, q)),
               "hm_profile_flux")
     ms_d = {"flux": ms[0], "apply_F": ms[1], "solve_C": ms[2]}
@@ -360,7 +369,7 @@ def hm_trace_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, max_passes: int = 256
     e = np.zeros(max_passes)
     by = np.zeros(max_passes, dtype=np.int64)
     pT, kT = _ptr(T)
-    pq, kq = _ptr(q)
+    pq, kq = _ptr(q, out=True)
     ctx.check(ctx.lib.hm_trace_flux(ctx.h, F.h, LU.h, pT, pq, max_passes, C.byref(npass), b.ctypes.data,
                                     e.ctypes.data, by.ctypes.data, _stream(stream, T, q)), "hm_trace_flux")
     m = min(npass.value, max_passes)
@@ -389,7 +398,7 @@ def hm_projection_create(ctx: Context, geom: Geometry, n_nodes: int, row_ptr, co
 
 def hm_cavity_flux(ctx: Context, F: HMatrix, LU: HLU, P: Projection, T_nodes, Q_nodes, stream=None):
     pT, kT = _ptr(T_nodes)
-    pQ, kQ = _ptr(Q_nodes)
+    pQ, kQ = _ptr(Q_nodes, out=True)
     ctx.check(ctx.lib.hm_cavity_flux(ctx.h, F.h, LU.h, P.h, _nrhs(T_nodes, P.n_nodes), pT, pQ,
                                      _stream(stream, T_nodes, Q_nodes)), "hm_cavity_flux")
     return Q_nodes
@@ -398,7 +407,7 @@ def hm_cavity_flux(ctx: Context, F: HMatrix, LU: HLU, P: Projection, T_nodes, Q_
 def hm_cavity_jacobian(ctx: Context, F: HMatrix, LU: HLU, P: Projection, T_nodes, x_nodes, y_nodes, stream=None):
     pT, kT = _ptr(T_nodes)
     px, kx = _ptr(x_nodes)
-    py, ky = _ptr(y_nodes)
+    py, ky = _ptr(y_nodes, out=True)
     ctx.check(ctx.lib.hm_cavity_jacobian(ctx.h, F.h, LU.h, P.h, _nrhs(T_nodes, P.n_nodes), pT, px, py,
                                          _stream(stream, T_nodes, y_nodes)), "hm_cavity_jacobian")
     return y_nodes

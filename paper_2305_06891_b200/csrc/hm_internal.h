@@ -201,7 +201,7 @@ enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2, 
 constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage
 constexpr int kMrhsMax = 64;                // multi-RHS block width (columns of X per program launch)
 constexpr int kMrhsMaxCols = 64;            // multi-RHS chunk: <= 64 panel columns (X tile 64 x 64)
-constexpr int kUnitMaxCols = 512;
+constexpr int kUnitMaxCols = 256;
 constexpr int64_t kPieceDoubles = 65536;    // panels above 512 KB are split into pieces
 
 // A task waits until counter[wait_id[i]] >= epoch * wait_cnt[i] (i < 2, id -1 = none) before its

@@ -4,6 +4,7 @@ the oracle."""
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -67,3 +68,14 @@ def test_header_documents_every_entry_point():
     for s in ["hm_apply_F", "hm_solve_C", "hm_radiative_flux", "hm_factor_hlu", "hm_assemble_aca"]:
         i = txt.index(s + "(")
         assert "PAPER.md:" in txt[max(0, i - 900):i], s
+
+
+def test_binding_rejects_unsafe_output_arrays():
+    """Outputs must be C-contiguous float64: a silently converted copy would drop the results."""
+    import paper_2305_06891_b200 as hm
+    with pytest.raises(TypeError):
+        hm._ptr(np.empty(4, dtype=np.float32), out=True)
+    with pytest.raises(TypeError):
+        hm._ptr(np.empty((4, 2))[:, 0], out=True)
+    p, keep = hm._ptr(np.arange(4), out=False)          # inputs are converted
+    assert keep.dtype == np.float64 and p == keep.ctypes.data
