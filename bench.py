@@ -356,6 +356,7 @@ def main():
                        "stored_bytes_per_step": bytes_step, "bytes_F": rep["bytes_F"], "bytes_C": rep["bytes_C"],
                        "step_hbm_gbs": bytes_step / (ms_step * 1e-3) / 1e9,
                        "step_frac_of_peak": bytes_step / (ms_step * 1e-3) / 1e9 / peak,
+                       "engine_frac_of_8000_spec": achieved / 8000.0,   # north-star target >= 0.6
                        "engine_ms": eng_ms, "engine": eng_info,
                        "apply_F_hbm_gbs": rep["bytes_F"] / (eng_ms["apply_F"] * 1e-3) / 1e9,
                        "solve_C_hbm_gbs": rep["bytes_C"] / (eng_ms["solve_C"] * 1e-3) / 1e9,
