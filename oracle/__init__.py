@@ -14,7 +14,10 @@ Plain, slow, obviously-correct numpy (fp64) written from PAPER.md:
                     (eq:qi_new_location), sampled-row (matrix-free) variants.
   tree.py        -- Alg. 1 BuildIndexTree, Alg. 2 BuildBlockTree + admissibility.
   aca.py         -- adaptive cross approximation with partial pivoting (eq:aca, eq:erel)
-                    following DESIGN.md reading R10 step by step.
+                    following DESIGN.md reading R10 step by step (probe rows: R30), full
+                    pivoting (R31) and QR + SVD recompression (R32).
+  cavity.py      -- the cavity operator around the hot path: R, Rbar, S = P^T Rbar P, the flux
+                    residual and J^cav (PAPER.md:163-260, NEXT-1).
   hmatrix.py     -- the oracle's own H-matrix (dense near field + ACA far field) and its
                     block-recursive matrix-vector product.
 
