@@ -137,7 +137,7 @@ def test_host_pointers_and_multiple_rhs(hm, case):
         assert rel(Yh[:, c], case["H"].apply(X[:, c])) <= TOL_EXACT
 
 
-@pytest.mark.parametrize("nrhs", [8, 64, 70])
+@pytest.mark.parametrize("nrhs", [8, 13, 37, 64, 70])
 def test_multi_rhs_dmma_matches_single_columns_and_oracle(hm, case, nrhs):
     """blocks of 64 right-hand sides through the DMMA engine (apply, solve, flux)
     equal the single-vector path column by column (summation order differs: 1e-12) and the dense
