@@ -192,6 +192,33 @@ def hm_init(device: int = 0, rank: int = 0, world: int = 1, comm_id=None, flags:
     return Context(device, rank, world, comm_id, flags)
 
 
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+def hm_set_allocator(ctx: Context, alloc=None, free=None):
+    """Route the library's device allocations through Python callables alloc(bytes, stream) -> int
+    pointer and free(pointer, stream) (e.g. torch's caching allocator, see use_torch_allocator);
+    alloc=None restores cudaMalloc.  Set it before building handles: a buffer is freed through the
+    hook that was active when it was allocated only if the hook is still set."""
+    if alloc is None:
+        ctx._alloc_cbs = None
+        ctx.check(ctx.lib.hm_set_allocator(ctx.h, None, None, None), "hm_set_allocator")
+        return
+    a = _ALLOC_FN(lambda nbytes, stream, user: alloc(int(nbytes), stream) or None)
+    f = _FREE_FN(lambda ptr, stream, user: free(ptr, stream))
+    ctx._alloc_cbs = (a, f)   # keep the ctypes thunks alive as long as the context uses them
+    ctx.check(ctx.lib.hm_set_allocator(ctx.h, C.cast(a, C.c_void_p), C.cast(f, C.c_void_p), None),
+              "hm_set_allocator")
+
+
+def use_torch_allocator(ctx: Context, device: int = 0):
+    """Device memory of this context from torch's caching allocator (shares torch's pool)."""
+    import torch
+    hm_set_allocator(ctx, lambda n, stream: torch.cuda.caching_allocator_alloc(n, device, stream),
+                     lambda ptr, stream: torch.cuda.caching_allocator_delete(ptr))
+
+
 def hm_nccl_unique_id() -> bytes:
     lib = load_library()
     buf = C.create_string_buffer(128)

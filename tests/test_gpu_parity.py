@@ -637,3 +637,43 @@ def test_flux_cuda_graph_replay(hm, ctx):
             hm.hm_radiative_flux(ctx, F, LU, T, qe)
             torch.cuda.synchronize()
             assert np.array_equal(qg, qe.cpu().numpy()), (cols, trial)
+
+
+def test_allocator_hook_routes_device_memory(hm):
+    """hm_set_allocator: every device allocation of a context goes through the hook (here torch's
+    caching allocator), every one is freed through it when the handles are destroyed, and results are
+    bitwise those of the default cudaMalloc context."""
+    import torch
+    cfg = synth.make_config(1)
+    f = cfg.facets
+    counts = {"alloc": 0, "free": 0}
+    live = set()
+
+    def alloc(n, stream):
+        p = torch.cuda.caching_allocator_alloc(n, 0, stream)
+        counts["alloc"] += 1
+        live.add(p)
+        return p
+
+    def free(p, stream):
+        counts["free"] += 1
+        live.discard(p)
+        torch.cuda.caching_allocator_delete(p)
+
+    outs = []
+    for hooked in (False, True):
+        ctx = hm.hm_init(0)
+        if hooked:
+            hm.hm_set_allocator(ctx, alloc, free)
+        g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min)
+        F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+        LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+        T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+        q = torch.empty_like(T)
+        hm.hm_radiative_flux(ctx, F, LU, T, q)
+        torch.cuda.synchronize()
+        outs.append(q.cpu().numpy())
+        del LU, F, g
+        ctx.close()
+    assert counts["alloc"] > 10 and counts["free"] == counts["alloc"] and not live
+    assert np.array_equal(outs[0], outs[1])
