@@ -677,3 +677,29 @@ def test_allocator_hook_routes_device_memory(hm):
         ctx.close()
     assert counts["alloc"] > 10 and counts["free"] == counts["alloc"] and not live
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_high_rank_cap_and_tight_tolerance(hm, ctx):
+    """Maximum rank cap k_max = 64 with eps_ACA = 1e-12 (ranks far above the default runs; stacked
+    phase-1 panels reach the 128-row limit): exact partition and ranks vs the oracle, F x equal to the
+    oracle H-matrix, and the 64-RHS DMMA apply (16 row tiles per panel) equal to single columns."""
+    import torch
+    cfg = synth.make_config(2, geometry=synth.icosphere(4))
+    f = cfg.facets
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=1e-12, k_max=64)
+    H = ohm.assemble(f, cfg.n_min, 1.0, 1e-12, k_max=64)
+    P, Q = hm.hm_export_partition(g, F), H.partition()
+    assert (P == Q).all()
+    assert Q[Q[:, 6] == 1, 7].max() >= 48
+    x = cfg.rhs()[:, 0]
+    y = np.empty(f.n)
+    hm.hm_apply_F(ctx, F, x, y)
+    assert rel(y, H.apply(x)) <= TOL_EXACT
+    X = torch.from_numpy(np.ascontiguousarray(synth.make_config(2, geometry=synth.icosphere(4), nrhs=64).rhs())).cuda()
+    Y = torch.empty_like(X)
+    hm.hm_apply_F(ctx, F, X, Y)
+    y1 = torch.empty(f.n, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, X[:, 5].contiguous(), y1)
+    torch.cuda.synchronize()
+    assert rel(Y[:, 5].cpu().numpy(), y1.cpu().numpy()) <= 1e-13
