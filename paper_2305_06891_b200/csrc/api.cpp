@@ -90,6 +90,29 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Output target of a hot-path call: device memory as is; pinned host memory through its device alias,
+// so the kernels' emits write it directly (no staging buffer, no device-to-host copy after the
+// program); pageable host memory through a staging buffer and a copy.  kind: 0 device, 1 pinned host,
+// 2 staged.
+double* out_target(Ctx* ctx, DBuf<double>& stage, double* p, size_t count, int& kind) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        a.type = cudaMemoryTypeUnregistered;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+        kind = 0;
+        return p;
+    }
+    if (a.type == cudaMemoryTypeHost && a.devicePointer) {
+        kind = 1;
+        return static_cast<double*>(a.devicePointer);
+    }
+    kind = 2;
+    if (stage.n < count) stage.alloc(ctx, count, "host staging (out)");
+    return stage.p;
+}
+
 // Stage host arrays through device buffers; returns the device pointer to use.
 const double* stage_in(Ctx* ctx, DBuf<double>& buf, const double* p, size_t count, cudaStream_t s, bool& host) {
     host = !is_device_ptr(p);
@@ -615,12 +638,9 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
         cudaStream_t s = (cudaStream_t)stream;
         bool hin = false;
         const double* xd = stage_in(c, F.host_stage_in, x, cnt, s, hin);
-        const bool hout = !is_device_ptr(y);
-        double* yd = y;
-        if (hout) {
-            if (F.host_stage_out.n < cnt) F.host_stage_out.alloc(c, cnt, "host staging (out)");
-            yd = F.host_stage_out.p;
-        }
+        int ok_ = 0;
+        double* yd = out_target(c, F.host_stage_out, y, cnt, ok_);
+        const bool hout = ok_ == 2, hsync = ok_ != 0;
         if (nrhs >= 2 && F.prog_apply_m.ready) {   // multi-RHS engine, kMrhsMax columns per launch
             for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
                 ProgArgs a = base_args(*F.geom, xd + c0, yd + c0, nrhs, 0);
@@ -637,7 +657,7 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
             for (int col = 0; col < nrhs; ++col) launch_apply(c, F, xd, yd, nrhs, col, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
+        if (hin || hsync) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
 
@@ -650,12 +670,9 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
         cudaStream_t s = (cudaStream_t)stream;
         bool hin = false;
         const double* bd = stage_in(c, L.host_stage_in, b, cnt, s, hin);
-        const bool hout = !is_device_ptr(z);
-        double* zd = z;
-        if (hout) {
-            if (L.host_stage_out.n < cnt) L.host_stage_out.alloc(c, cnt, "host staging (out)");
-            zd = L.host_stage_out.p;
-        }
+        int ok_ = 0;
+        double* zd = out_target(c, L.host_stage_out, z, cnt, ok_);
+        const bool hout = ok_ == 2, hsync = ok_ != 0;
         if (nrhs >= 2 && L.prog_solve_m.ready) {
             for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
                 ProgArgs a = base_args(*L.F->geom, bd + c0, zd + c0, nrhs, 0);
@@ -672,7 +689,7 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
             for (int col = 0; col < nrhs; ++col) launch_solve(c, L, bd, zd, nrhs, col, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
+        if (hin || hsync) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
 
@@ -760,12 +777,9 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
         cudaStream_t s = (cudaStream_t)stream;
         bool hin = false;
         const double* Td = stage_in(c, L.host_stage_in, T, cnt, s, hin);
-        const bool hout = !is_device_ptr(q);
-        double* qd = q;
-        if (hout) {
-            if (L.host_stage_out.n < cnt) L.host_stage_out.alloc(c, cnt, "host staging (out)");
-            qd = L.host_stage_out.p;
-        }
+        int ok_ = 0;
+        double* qd = out_target(c, L.host_stage_out, q, cnt, ok_);
+        const bool hout = ok_ == 2, hsync = ok_ != 0;
         if (nrhs >= 2 && L.prog_flux_m.ready) {
             for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) launch_flux_m(L, Td + c0, qd + c0, nrhs, std::min(kMrhsMax, nrhs - c0), s);
         } else if (nrhs >= 2 && !L.sp_flux_m.empty()) {   // sharded multi-RHS flux
@@ -784,7 +798,7 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
             for (int col = 0; col < nrhs; ++col) launch_flux(c, L, Td, qd, nrhs, col, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (hin || hout) HM_CUDA(cudaStreamSynchronize(s));
+        if (hin || hsync) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
 

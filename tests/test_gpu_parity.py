@@ -703,3 +703,31 @@ def test_high_rank_cap_and_tight_tolerance(hm, ctx):
     hm.hm_apply_F(ctx, F, X[:, 5].contiguous(), y1)
     torch.cuda.synchronize()
     assert rel(Y[:, 5].cpu().numpy(), y1.cpu().numpy()) <= 1e-13
+
+
+def test_pinned_host_outputs_written_directly(hm, ctx):
+    """Pinned host outputs are written by the kernels through their device alias (no staging copy):
+    apply / solve / flux into pinned host memory equal the device-output results bitwise, for 1 and 64
+    columns; pageable outputs still go through staging (same values)."""
+    import torch
+    cfg = synth.make_config(2, geometry=synth.icosphere(4), nrhs=64)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    for cols in (1, 64):
+        X = np.ascontiguousarray(cfg.rhs()[:, :cols]) if cols > 1 else cfg.rhs()[:, 0].copy()
+        T = np.ascontiguousarray(cfg.T[:, :cols]) if cols > 1 else cfg.T[:, 0].copy()
+        Xd, Td = torch.from_numpy(X).cuda(), torch.from_numpy(T).cuda()
+        for name, fn, inp, inpd in (("apply", lambda a, o: hm.hm_apply_F(ctx, F, a, o), X, Xd),
+                                    ("solve", lambda a, o: hm.hm_solve_C(ctx, LU, a, o), X, Xd),
+                                    ("flux", lambda a, o: hm.hm_radiative_flux(ctx, F, LU, a, o), T, Td)):
+            od = torch.empty_like(inpd)
+            fn(inpd, od)
+            torch.cuda.synchronize()
+            ref = od.cpu().numpy()
+            op = torch.empty(inp.shape, dtype=torch.float64).pin_memory()
+            fn(inp, op)
+            assert np.array_equal(op.numpy(), ref), (name, cols)
+            opg = np.empty_like(inp)
+            fn(inp, opg)
+            assert np.array_equal(opg, ref), (name, cols, "pageable")
