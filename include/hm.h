@@ -179,9 +179,10 @@ hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
    as stored: closed-cavity-scaled, the paper's convention without 1/A_i, reading R1).  x, y: n x nrhs, external order; x and y must not overlap. */
 hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* F, int32_t nrhs, const double* x, double* y,
                      void* stream);
-/* Host buffers (all hot-path calls): inputs are copied to the device on `stream`; outputs in PINNED
-   host memory are written by the kernels directly (device alias), pageable outputs are staged and
-   copied back; with any host buffer the call synchronises `stream` before returning. */
+/* Host buffers (all hot-path calls): inputs are copied to the device on `stream` (a PINNED
+   single-vector hm_radiative_flux input is read by the program's own copy-in pass instead); outputs in
+   PINNED host memory are written by the kernels directly (device alias), pageable outputs are staged
+   and copied back; with any host buffer the call synchronises `stream` before returning. */
 /* z ~= C^-1 b by forward then backward substitution with the factors: level-
    scheduled W updates above the cut, then the cut-level inverse factors (R27). */
 hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LU, int32_t nrhs, const double* b, double* z,

@@ -775,11 +775,34 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
         HLU& L = const_cast<HLU&>(LUh->h);
         const size_t cnt = (size_t)vec_rows(*L.F->geom) * nrhs;
         cudaStream_t s = (cudaStream_t)stream;
-        bool hin = false;
-        const double* Td = stage_in(c, L.host_stage_in, T, cnt, s, hin);
         int ok_ = 0;
         double* qd = out_target(c, L.host_stage_out, q, cnt, ok_);
         const bool hout = ok_ == 2, hsync = ok_ != 0;
+        // single vector, pinned host T: the program's copy-in pass reads it (no separate H2D copy
+        // before the kernel: the payload stream starts while T crosses the bus)
+        if (nrhs == 1 && L.prog_flux_h.ready && !L.F->geom->shard.sharded()) {
+            cudaPointerAttributes pa;
+            if (cudaPointerGetAttributes(&pa, T) != cudaSuccess) {
+                cudaGetLastError();
+                pa.type = cudaMemoryTypeUnregistered;
+            }
+            if (pa.type == cudaMemoryTypeHost && pa.devicePointer) {
+                const Geom& g = *L.F->geom;
+                ProgArgs a = base_args(g, L.T_dev.p, qd, 1, 0);
+                a.host_in = static_cast<const double*>(pa.devicePointer);
+                a.sigma = 5.670374419e-8;   // DESIGN.md reading R2
+                a.eps_int = L.eps_int.p;
+                a.eps_ext = L.eps_ext.p;
+                a.area_int = g.d_geo.p + 6 * g.n;
+                a.g_int = L.g_int.p;
+                L.prog_flux_h.launch(a, s);
+                if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
+                HM_CUDA(cudaStreamSynchronize(s));
+                return;
+            }
+        }
+        bool hin = false;
+        const double* Td = stage_in(c, L.host_stage_in, T, cnt, s, hin);
         if (nrhs >= 2 && L.prog_flux_m.ready) {
             for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) launch_flux_m(L, Td + c0, qd + c0, nrhs, std::min(kMrhsMax, nrhs - c0), s);
         } else if (nrhs >= 2 && !L.sp_flux_m.empty()) {   // sharded multi-RHS flux

@@ -432,13 +432,16 @@ void factor_hlu(HLU& L, const double* emissivity) {
     // With Lc == 0 nothing updates b in place, so the prologue (permute-in, or eta = T^4 and
     // w = eps eta for the flux) is fused into the gathers of the first operator's passes (in_mode);
     // otherwise an element-wise pass materialises b first.
-    auto solve_passes = [&](Program& P, int in_mode) {
+    auto solve_passes = [&](Program& P, int in_mode, double* copy_in = nullptr) {
         P.n_x = n;
+        // pinned host input: an element-wise pass copies it into copy_in first (the payload stream
+        // starts meanwhile; every reader of the input waits for the pass)
+        if (copy_in) P.add_elementwise(UNIT_COPYIN, n, copy_in, 1024);
         if (Lc > 0) {
             P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA.p);
             in_mode = IN_PLAIN;
         }
-        P.sweep_dep[0] = (int32_t)P.h_passes.size() - 1;  // the prologue / permute pass (-1: fused)
+        P.sweep_dep[0] = (int32_t)P.h_passes.size() - 1;  // the copy-in / prologue / permute pass (-1: none)
         for (int lv = 0; lv < Lc; ++lv) {
             HOp& op = L.fwd[lv];
             const auto m1 = node_map(op.p1, lv), m2 = node_map(op.p2, lv);
@@ -475,6 +478,13 @@ void factor_hlu(HLU& L, const double* emissivity) {
     L.prog_flux.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN,
                            (int)L.prog_flux.h_passes.size() - 2);
     L.prog_flux.finalize(c, s, &g);
+    // the same flux program behind a copy-in pass, for a pinned host T (single vector, world == 1)
+    L.T_dev.alloc(c, (size_t)n, "flux T (pinned host copy-in)");
+    solve_passes(L.prog_flux_h, IN_FLUX, L.T_dev.p);
+    add_U2_F1(L.prog_flux_h);
+    L.prog_flux_h.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN,
+                             (int)L.prog_flux_h.h_passes.size() - 2);
+    L.prog_flux_h.finalize(c, s, &g);
 
     // ---- flux constant g = F C^-1 eps, with a setup program
     t0 = now_seconds();

@@ -197,7 +197,9 @@ static_assert(sizeof(Unit) % 16 == 0, "Unit is TMA-copied");
 // UNIT_EPILOGUE (multi-RHS): rows of an internal n x kMrhsMax result emitted through the pass's output
 // mode (permute-out / flux epilogue) by element-wise units, coalesced and fully parallel
 // UNIT_PROLOGUE_INT (sharded level form): out[row] = eps[row] * in[row]^4 on padded internal rows
-enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2, UNIT_EPILOGUE = 3, UNIT_PROLOGUE_INT = 4 };
+// UNIT_COPYIN (pinned host input): out[row * ld + col] = host_in[row * ld + col], rows in external order
+enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2, UNIT_EPILOGUE = 3, UNIT_PROLOGUE_INT = 4,
+                          UNIT_COPYIN = 5 };
 constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage
 constexpr int kMrhsMax = 64;                // multi-RHS block width (columns of X per program launch)
 constexpr int kMrhsMaxCols = 64;            // multi-RHS chunk: <= 64 panel columns (X tile 64 x 64)
@@ -323,6 +325,7 @@ struct ProgArgs {
     unsigned long long* epoch_dev;
     const int32_t* perm;
     const double* user_in;      // x / b / T (external order, ld x ncol)
+    const double* host_in;      // UNIT_COPYIN: device alias of the caller's pinned host input
     int64_t n_x;                // size of the x region of XT (IN_PERM / IN_FLUX apply below it)
     double* user_out;           // y / z / q (external order)
     int ld, col;
@@ -468,6 +471,8 @@ struct HLU {
     int rank_max = 0;
     Program prog_solve;   // permute-in -> forward levels -> leaf L^-1 -> backward levels -> leaf U^-1
     Program prog_flux;    // prologue -> solve passes -> F phase 1 -> F phase 2 + flux epilogue
+    Program prog_flux_h;  // the same behind a copy-in pass for a pinned host T (single vector)
+    DBuf<double> T_dev;   // its device copy of T
     // sharded hot path (world > 1, inverse-factor form): this rank's rows of L^-1, U^-1
     HOp leafL_loc, leafU_loc;
     std::vector<HOp> fwd_loc, bwd_loc;   // level-form W operators, this rank's rows

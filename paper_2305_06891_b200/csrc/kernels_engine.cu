@@ -505,7 +505,12 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                 }
             }
         } else {
-            if (u.type == UNIT_PROLOGUE_INT) {   // sharded: w = eps T^4 in place on padded internal rows
+            if (u.type == UNIT_COPYIN) {   // pinned host input -> device copy (overlaps the payload stream)
+                for (int i = ct; i < u.nrows; i += kConsumers) {
+                    const int64_t row = u.out0 + i;
+                    P.out[row * A.ld + A.col] = A.host_in[row * A.ld + A.col];
+                }
+            } else if (u.type == UNIT_PROLOGUE_INT) {   // sharded: w = eps T^4 in place on padded internal rows
                 for (int i = ct; i < u.nrows; i += kConsumers) {
                     const int64_t row = u.out0 + i;
                     P.out[row] = A.eps_int[row] * (A.eta_in ? P.in[row] : pow4(P.in[row]));

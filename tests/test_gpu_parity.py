@@ -706,9 +706,9 @@ def test_high_rank_cap_and_tight_tolerance(hm, ctx):
 
 
 def test_pinned_host_outputs_written_directly(hm, ctx):
-    """Pinned host outputs are written by the kernels through their device alias (no staging copy):
-    apply / solve / flux into pinned host memory equal the device-output results bitwise, for 1 and 64
-    columns; pageable outputs still go through staging (same values)."""
+    """Pinned host outputs are written by the kernels through their device alias (no staging copy), and
+    a pinned single-vector flux input is read by the program's copy-in pass: apply / solve / flux with
+    pinned or pageable host buffers equal the device-buffer results bitwise, for 1 and 64 columns."""
     import torch
     cfg = synth.make_config(2, geometry=synth.icosphere(4), nrhs=64)
     f = cfg.facets
@@ -731,3 +731,7 @@ def test_pinned_host_outputs_written_directly(hm, ctx):
             opg = np.empty_like(inp)
             fn(inp, opg)
             assert np.array_equal(opg, ref), (name, cols, "pageable")
+            ip = torch.from_numpy(inp).pin_memory()       # pinned input (flux: the copy-in program)
+            op2 = torch.empty(inp.shape, dtype=torch.float64).pin_memory()
+            fn(ip, op2)
+            assert np.array_equal(op2.numpy(), ref), (name, cols, "pinned input")
