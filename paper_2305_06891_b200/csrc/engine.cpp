@@ -291,8 +291,34 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
         HM_CUDA(cudaMemsetAsync(stats.p, 0, (16 + 64) * sizeof(unsigned long long), s));
         a.stats = stats.p;
     }
+    // HM_TRACE_MRHS=1 (diagnostics): per-pass [first gather, last publish] of multi-RHS launches
+    static const bool want_trace_m = [] { const char* e = getenv("HM_TRACE_MRHS"); return e && e[0] == '1'; }();
+    std::vector<unsigned long long> tr_init;
+    if (mrhs && want_trace_m && !a.trace) {
+        const size_t np = h_passes.size();
+        if (trace.n < 2 * np) trace.alloc(nullptr, 2 * np, "engine trace");
+        tr_init.assign(2 * np, 0ull);
+        for (size_t i = 0; i < np; ++i) tr_init[2 * i] = ~0ull;
+        HM_CUDA(cudaMemcpyAsync(trace.p, tr_init.data(), 2 * np * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+        a.trace = trace.p;
+    }
     if (mrhs) engine_mrhs_launch(a, grid, s);
     else engine_launch(a, grid, s);
+    if (!tr_init.empty()) {
+        const size_t np = h_passes.size();
+        std::vector<unsigned long long> tr(2 * np);
+        HM_CUDA(cudaMemcpyAsync(tr.data(), trace.p, 2 * np * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        unsigned long long t0 = ~0ull;
+        for (size_t i = 0; i < np; ++i) t0 = std::min(t0, tr[2 * i]);
+        for (size_t i = 0; i < np; ++i) {
+            double mb = 0;
+            for (int64_t u = h_passes[i].first_unit; u < h_passes[i].first_unit + h_passes[i].n_units; ++u)
+                mb += h_units[u].type == UNIT_STREAM ? 8e-6 * h_units[u].ncols * h_units[u].ld : 0.0;
+            fprintf(stderr, "[mrhs trace] pass %zu type %d: %.1f -> %.1f us (%.1f MB)\n", i, h_passes[i].type,
+                    tr[2 * i] == ~0ull ? -1.0 : (tr[2 * i] - t0) * 1e-3, (tr[2 * i + 1] - t0) * 1e-3, mb);
+        }
+    }
     if (want_stats) {
         unsigned long long h[16 + 64];
         HM_CUDA(cudaMemcpyAsync(h, stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));

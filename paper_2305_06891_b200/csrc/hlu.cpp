@@ -515,7 +515,7 @@ void factor_hlu(HLU& L, const double* emissivity) {
             P.n_x = n;
             // prologue: b (or w = eps T^4) into the internal n x 64 layout, then every gather is a
             // 512-byte TMA row copy
-            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, 128);
+            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, 32);
             P.add_stream(L.leafL.p1m, L.leafL, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN);
             P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
                          (int)P.h_passes.size() - 2);
@@ -526,13 +526,13 @@ void factor_hlu(HLU& L, const double* emissivity) {
         // final results go to an internal n x 64 buffer, then an element-wise epilogue pass emits them
         // (permute-out / flux epilogue) coalesced and fully parallel
         mprog(L.prog_solve_m, IN_PERM, Fm.y_m.p, OUT_ASSIGN);
-        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 128, Fm.y_m.p, OUT_PERM);
+        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_PERM);
         L.prog_solve_m.finalize(c, s, &g);
         mprog(L.prog_flux_m, IN_FLUX, Fm.xt_m.p, OUT_ASSIGN);
         L.prog_flux_m.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
         L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
                                  (int)L.prog_flux_m.h_passes.size() - 2);
-        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 128, Fm.y_m.p, OUT_FLUX);
+        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_FLUX);
         L.prog_flux_m.finalize(c, s, &g);
     }
 

@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 if (lane == 0) {
                     if (H.wait_id[0] >= 0) wait_counter(A, epoch, H.wait_id[0], H.wait_cnt[0]);
                     if (H.wait_id[1] >= 0) wait_counter(A, epoch, H.wait_id[1], H.wait_cnt[1]);
+                    if (A.trace && H.chunk == 0) atomicMin(A.trace + 2 * H.pass, gtimer());
                 }
                 __syncwarp();
                 fence_proxy_async_global();
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             if (d.type < 0) break;
             if (lane == 0) {
                 __threadfence();
+                if (A.trace) atomicMax(A.trace + 2 * d.pass + 1, gtimer());
                 atomicAdd(A.done + d.pass, 1ull);
                 if (d.inc0 >= 0) atomicAdd(A.done + d.inc0, 1ull);
                 if (d.inc1 >= 0) atomicAdd(A.done + d.inc1, 1ull);
@@ -506,20 +508,55 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             }
             }
         } else if (type == UNIT_EPILOGUE) {
-            // rows x R of the internal result through the pass's output mode (permute-out / flux
-            // epilogue); 4 independent elements per thread in flight
-            const int tot = nrows * R;
-            for (int e0 = ct; e0 < tot; e0 += 4 * kMConsumers) {
-                double v[4];
+            // rows x R of the internal result through the pass's output mode: row-wise, warp cw takes
+            // rows cw, cw + 8, ..., four rows in flight, lanes take the columns (coalesced); the per-row
+            // scalars (perm, eps, A, g) are loaded once per row
+            if (P.mode == OUT_PERM || P.mode == OUT_FLUX) {
+                const bool flux = P.mode == OUT_FLUX;
+                for (int r0 = cw; r0 < nrows; r0 += 4 * kMConsumerWarps) {
+                    int64_t e[4];
+                    double sc[4], gg[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = e0 + u * kMConsumers;
-                    v[u] = e < tot ? __ldcg(P.in + (out0 + e / R) * kMrhsMax + (e % R)) : 0.0;
+                    for (int u = 0; u < 4; ++u) {
+                        const int r = r0 + u * kMConsumerWarps;
+                        const int64_t row = out0 + (r < nrows ? r : 0);
+                        e[u] = __ldg(A.perm + row);
+                        sc[u] = flux ? A.sigma * (__ldg(A.eps_int + row) / __ldg(A.area_int + row)) : 0.0;
+                        gg[u] = flux ? __ldg(A.g_int + row) : 0.0;
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = lane + 32 * h;
+                        double v[4], t[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int r = r0 + u * kMConsumerWarps;
+                            const bool ok = r < nrows && col < R;
+                            v[u] = ok ? __ldcg(P.in + (out0 + r) * kMrhsMax + col) : 0.0;
+                            t[u] = ok && flux ? __ldg(A.user_in + e[u] * A.ld + col) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int r = r0 + u * kMConsumerWarps;
+                            if (r < nrows && col < R)
+                                A.user_out[e[u] * A.ld + col] = flux ? sc[u] * (v[u] - pow4(t[u]) * gg[u]) : v[u];
+                        }
+                    }
                 }
+            } else {   // other modes (sharded): element by element, 4 in flight
+                const int tot = nrows * R;
+                for (int e0 = ct; e0 < tot; e0 += 4 * kMConsumers) {
+                    double v[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = e0 + u * kMConsumers;
-                    if (e < tot) emit_m(A, P, out0 + e / R, e % R, v[u]);
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = e0 + u * kMConsumers;
+                        v[u] = e < tot ? __ldcg(P.in + (out0 + e / R) * kMrhsMax + (e % R)) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = e0 + u * kMConsumers;
+                        if (e < tot) emit_m(A, P, out0 + e / R, e % R, v[u]);
+                    }
                 }
             }
         } else if (type == UNIT_PROLOGUE_INT) {
@@ -532,25 +569,32 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             }
         } else {
             // element-wise prologue: rows x R of the caller's external-order array permuted into the
-            // internal n x 64 layout (UNIT_PROLOGUE: w = eps T^4); coalesced, 4 elements in flight
-            const int tot = nrows * R;
-            for (int e0 = ct; e0 < tot; e0 += 4 * kMConsumers) {
-                double v[4];
+            // internal n x 64 layout (UNIT_PROLOGUE: w = eps T^4); row-wise as the epilogue (perm and eps
+            // once per row, lanes over the columns, four rows in flight per warp)
+            for (int r0 = cw; r0 < nrows; r0 += 4 * kMConsumerWarps) {
+                int64_t e[4];
+                double ep[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int e = e0 + u * kMConsumers;
-                    v[u] = 0.0;
-                    if (e < tot) {
-                        const int64_t row = out0 + e / R;
-                        v[u] = __ldg(A.user_in + (int64_t)__ldg(A.perm + row) * A.ld + (e % R));
-                    }
+                    const int r = r0 + u * kMConsumerWarps;
+                    const int64_t row = out0 + (r < nrows ? r : 0);
+                    e[u] = __ldg(A.perm + row);
+                    ep[u] = type == UNIT_PROLOGUE ? __ldg(A.eps_int + row) : 1.0;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = e0 + u * kMConsumers;
-                    if (e < tot) {
-                        const int64_t row = out0 + e / R;
-                        P.out[row * kMrhsMax + (e % R)] = type == UNIT_PROLOGUE ? __ldg(A.eps_int + row) * pow4(v[u]) : v[u];
+                for (int h = 0; h < 2; ++h) {
+                    const int col = lane + 32 * h;
+                    double v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int r = r0 + u * kMConsumerWarps;
+                        v[u] = (r < nrows && col < R) ? __ldg(A.user_in + e[u] * A.ld + col) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int r = r0 + u * kMConsumerWarps;
+                        if (r < nrows && col < R)
+                            P.out[(out0 + r) * kMrhsMax + col] = type == UNIT_PROLOGUE ? ep[u] * pow4(v[u]) : v[u];
                     }
                 }
             }
