@@ -180,7 +180,8 @@ hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
 hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* F, int32_t nrhs, const double* x, double* y,
                      void* stream);
 /* Host buffers (all hot-path calls): inputs are copied to the device on `stream` (a PINNED
-   single-vector hm_radiative_flux input is read by the program's own copy-in pass instead); outputs in
+   single-vector input of hm_apply_F / hm_solve_C / hm_radiative_flux is read by the program's own
+   copy-in pass instead, world == 1); outputs in
    PINNED host memory are written by the kernels directly (device alias), pageable outputs are staged
    and copied back; with any host buffer the call synchronises `stream` before returning. */
 /* z ~= C^-1 b by forward then backward substitution with the factors: level-

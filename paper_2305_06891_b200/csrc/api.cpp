@@ -113,6 +113,16 @@ double* out_target(Ctx* ctx, DBuf<double>& stage, double* p, size_t count, int& 
     return stage.p;
 }
 
+// Device alias of a pinned host input (nullptr for device, managed or pageable memory).
+const double* pinned_alias(const double* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? static_cast<const double*>(a.devicePointer) : nullptr;
+}
+
 // Stage host arrays through device buffers; returns the device pointer to use.
 const double* stage_in(Ctx* ctx, DBuf<double>& buf, const double* p, size_t count, cudaStream_t s, bool& host) {
     host = !is_device_ptr(p);
@@ -600,6 +610,15 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         F.prog_apply.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PERM);
         F.prog_apply.add_stream(F.op.p2, F.op, F.xt.p, nullptr, OUT_PERM, DEP_BARRIER, nullptr, IN_PERM, -1);
         F.prog_apply.finalize(c, s);
+        {   // pinned host x: copy-in pass first; phase 1 and the x-only phase-2 pieces wait for it
+            F.x_dev.alloc(c, (size_t)n, "apply x (pinned host copy-in)");
+            Program& P = F.prog_apply_h;
+            P.n_x = n;
+            P.add_elementwise(UNIT_COPYIN, n, F.x_dev.p, 1024);
+            P.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PERM);
+            P.add_stream(F.op.p2, F.op, F.xt.p, nullptr, OUT_PERM, DEP_BARRIER, nullptr, IN_PERM, 0);
+            P.finalize(c, s);
+        }
         if (!g.shard.sharded()) {   // multi-RHS program: blocks of kMrhsMax columns, DMMA engine
             F.xt_m.alloc(c, (size_t)(n + F.op.n_t) * kMrhsMax, "F xt (multi-RHS)");
             F.y_m.alloc(c, (size_t)n * kMrhsMax, "F y (multi-RHS)");
@@ -636,11 +655,21 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
         HMat& F = const_cast<HMat&>(Fh->h);
         const size_t cnt = (size_t)vec_rows(*F.geom) * nrhs;
         cudaStream_t s = (cudaStream_t)stream;
-        bool hin = false;
-        const double* xd = stage_in(c, F.host_stage_in, x, cnt, s, hin);
         int ok_ = 0;
         double* yd = out_target(c, F.host_stage_out, y, cnt, ok_);
         const bool hout = ok_ == 2, hsync = ok_ != 0;
+        if (nrhs == 1 && F.prog_apply_h.ready && !F.geom->shard.sharded()) {
+            if (const double* xa = pinned_alias(x)) {   // pinned host x: the program's copy-in pass
+                ProgArgs a = base_args(*F.geom, F.x_dev.p, yd, 1, 0);
+                a.host_in = xa;
+                F.prog_apply_h.launch(a, s);
+                if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
+                HM_CUDA(cudaStreamSynchronize(s));
+                return;
+            }
+        }
+        bool hin = false;
+        const double* xd = stage_in(c, F.host_stage_in, x, cnt, s, hin);
         if (nrhs >= 2 && F.prog_apply_m.ready) {   // multi-RHS engine, kMrhsMax columns per launch
             for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
                 ProgArgs a = base_args(*F.geom, xd + c0, yd + c0, nrhs, 0);
@@ -668,11 +697,21 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
         HLU& L = const_cast<HLU&>(LUh->h);
         const size_t cnt = (size_t)vec_rows(*L.F->geom) * nrhs;
         cudaStream_t s = (cudaStream_t)stream;
-        bool hin = false;
-        const double* bd = stage_in(c, L.host_stage_in, b, cnt, s, hin);
         int ok_ = 0;
         double* zd = out_target(c, L.host_stage_out, z, cnt, ok_);
         const bool hout = ok_ == 2, hsync = ok_ != 0;
+        if (nrhs == 1 && L.prog_solve_h.ready && !L.F->geom->shard.sharded()) {
+            if (const double* ba = pinned_alias(b)) {   // pinned host b: the program's copy-in pass
+                ProgArgs a = base_args(*L.F->geom, L.T_dev.p, zd, 1, 0);
+                a.host_in = ba;
+                L.prog_solve_h.launch(a, s);
+                if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
+                HM_CUDA(cudaStreamSynchronize(s));
+                return;
+            }
+        }
+        bool hin = false;
+        const double* bd = stage_in(c, L.host_stage_in, b, cnt, s, hin);
         if (nrhs >= 2 && L.prog_solve_m.ready) {
             for (int c0 = 0; c0 < nrhs; c0 += kMrhsMax) {
                 ProgArgs a = base_args(*L.F->geom, bd + c0, zd + c0, nrhs, 0);

@@ -465,6 +465,10 @@ void factor_hlu(HLU& L, const double* emissivity) {
     solve_passes(L.prog_solve, IN_PERM);
     L.prog_solve.add_stream(L.leafU.p2, L.leafU, L.xtB.p, nullptr, OUT_PERM, DEP_BWD_P2, &mU2);
     L.prog_solve.finalize(c, s, &g);
+    L.T_dev.alloc(c, (size_t)n, "pinned host copy-in (solve b / flux T)");
+    solve_passes(L.prog_solve_h, IN_PERM, L.T_dev.p);
+    L.prog_solve_h.add_stream(L.leafU.p2, L.leafU, L.xtB.p, nullptr, OUT_PERM, DEP_BWD_P2, &mU2);
+    L.prog_solve_h.finalize(c, s, &g);
     solve_passes(L.prog_flux, IN_FLUX);
     auto add_U2_F1 = [&](Program& P) {   // U^-1 phase 2 -> F phase 1, linked group by group (cut level 0)
         const size_t a = P.h_passes.size();
@@ -479,7 +483,6 @@ void factor_hlu(HLU& L, const double* emissivity) {
                            (int)L.prog_flux.h_passes.size() - 2);
     L.prog_flux.finalize(c, s, &g);
     // the same flux program behind a copy-in pass, for a pinned host T (single vector, world == 1)
-    L.T_dev.alloc(c, (size_t)n, "flux T (pinned host copy-in)");
     solve_passes(L.prog_flux_h, IN_FLUX, L.T_dev.p);
     add_U2_F1(L.prog_flux_h);
     L.prog_flux_h.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN,

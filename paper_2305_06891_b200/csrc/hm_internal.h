@@ -442,6 +442,8 @@ struct HMat {
     DBuf<double> y;    // internal-order output
     DBuf<double> host_stage_in, host_stage_out;
     Program prog_apply;   // permute-in -> F phase 1 -> F phase 2 (+ permute-out)
+    Program prog_apply_h; // the same behind a copy-in pass for a pinned host x (single vector)
+    DBuf<double> x_dev;   // its device copy of x
     // sharded hot path (world > 1): this rank's block rows, padded vectors
     HOp op_loc;
     DBuf<double> xt_loc;  // [x_pad | t]
@@ -470,6 +472,7 @@ struct HLU {
     int64_t bytes = 0, bytes_leaf = 0, n_blocks = 0, n_lr = 0, rank_sum = 0;
     int rank_max = 0;
     Program prog_solve;   // permute-in -> forward levels -> leaf L^-1 -> backward levels -> leaf U^-1
+    Program prog_solve_h; // the same behind a copy-in pass for a pinned host b (single vector)
     Program prog_flux;    // prologue -> solve passes -> F phase 1 -> F phase 2 + flux epilogue
     Program prog_flux_h;  // the same behind a copy-in pass for a pinned host T (single vector)
     DBuf<double> T_dev;   // its device copy of T
