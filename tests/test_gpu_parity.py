@@ -338,6 +338,16 @@ def test_config2_full_size(hm, ctx):
     torch.cuda.synchronize()
     sig = vf.SIGMA_SB * 700.0 ** 4
     assert np.abs(q.cpu().numpy()).max() <= 10 * cfg.eps_aca * sig
+    # the recompressed variant bench.py reports beside the headline (R32): same sampled-row bounds
+    Fr = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca, recompress=True)
+    yr = np.empty(f.n)
+    hm.hm_apply_F(ctx, Fr, x, yr)
+    assert rel(yr[rows], ys) <= 10 * cfg.eps_aca
+    LUr = hm.hm_factor_hlu(ctx, Fr, cfg.emissivity)
+    zr = np.empty(f.n)
+    hm.hm_solve_C(ctx, LUr, x, zr)
+    rr = vf.sampled_residual(f.centroid, f.normal, f.area, cfg.emissivity, rows, zr[:, None], x[:, None])[:, 0]
+    assert np.linalg.norm(rr) / np.linalg.norm(x[rows]) <= 10 * cfg.eps_aca
 
 
 # ---------------------------------------------------------------- BASELINE configs[2] (C3, 82,000 facets)
