@@ -537,6 +537,46 @@ void factor_hlu(HLU& L, const double* emissivity) {
                                  (int)L.prog_flux_m.h_passes.size() - 2);
         L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_FLUX);
         L.prog_flux_m.finalize(c, s, &g);
+    } else if (!g.shard.sharded()) {
+        // level form (cut level > 0) with 64 columns: the same tree-scheduled sweeps as the single-vector
+        // solve, on the multi-RHS units (W updates b_t2 -= W b_t1 in place, OUT_SUB), prologue and
+        // epilogue as element-wise passes
+        L.xtA_m.alloc(c, (size_t)(n + tA) * kMrhsMax, "solve xtA (multi-RHS, level form)");
+        L.xtB_m.alloc(c, (size_t)(n + tB) * kMrhsMax, "solve xtB (multi-RHS, level form)");
+        auto mprog_lf = [&](Program& P, int in_mode, double* out_u) {
+            P.mrhs = true;
+            P.n_x = n;
+            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, 32);
+            P.sweep_dep[0] = (int32_t)P.h_passes.size() - 1;
+            for (int lv = 0; lv < Lc; ++lv) {
+                HOp& op = L.fwd[lv];
+                const auto m1 = node_map(op.p1m, lv), m2 = node_map(op.p2m, lv);
+                P.add_stream(op.p1m, op, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN, DEP_FWD_P1, &m1);
+                P.add_stream(op.p2m, op, L.xtA_m.p, L.xtA_m.p, OUT_SUB, DEP_FWD_P2, &m2);
+            }
+            const auto l1 = node_map(L.leafL.p1m, Lc), l2 = node_map(L.leafL.p2m, Lc);
+            P.add_stream(L.leafL.p1m, L.leafL, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN, DEP_FWD_P1, &l1);
+            P.sweep_dep[1] = (int32_t)P.h_passes.size();
+            P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_FWD_P2, &l2);
+            for (int lv = 0; lv < Lc; ++lv) {
+                HOp& op = L.bwd[lv];
+                const auto m1 = node_map(op.p1m, lv), m2 = node_map(op.p2m, lv);
+                P.add_stream(op.p1m, op, L.xtB_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BWD_P1, &m1);
+                P.add_stream(op.p2m, op, L.xtB_m.p, L.xtB_m.p, OUT_SUB, DEP_BWD_P2, &m2);
+            }
+            const auto u1 = node_map(L.leafU.p1m, Lc), u2 = node_map(L.leafU.p2m, Lc);
+            P.add_stream(L.leafU.p1m, L.leafU, L.xtB_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BWD_P1, &u1);
+            P.add_stream(L.leafU.p2m, L.leafU, L.xtB_m.p, out_u, OUT_ASSIGN, DEP_BWD_P2, &u2);
+        };
+        mprog_lf(L.prog_solve_m, IN_PERM, Fm.y_m.p);
+        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_PERM);
+        L.prog_solve_m.finalize(c, s, &g);
+        mprog_lf(L.prog_flux_m, IN_FLUX, Fm.xt_m.p);
+        L.prog_flux_m.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
+        L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
+                                 (int)L.prog_flux_m.h_passes.size() - 2);
+        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_FLUX);
+        L.prog_flux_m.finalize(c, s, &g);
     }
 
     // ---- sharded hot path (world > 1): exchange steps between the engine programs

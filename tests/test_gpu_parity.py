@@ -745,3 +745,33 @@ def test_pinned_host_outputs_written_directly(hm, ctx):
             op2 = torch.empty(inp.shape, dtype=torch.float64).pin_memory()
             fn(ip, op2)
             assert np.array_equal(op2.numpy(), ref), (name, cols, "pinned input")
+
+
+@pytest.mark.parametrize("cut", [2, 99])
+def test_multi_rhs_level_form(hm, ctx, cut):
+    """The level-scheduled solve (cut level > 0, W updates in place) on the DMMA engine with 64 columns:
+    solve and flux equal the single-vector level form column by column and the dense oracle."""
+    import torch
+    cfg = synth.make_config(2, geometry=synth.icosphere(4), nrhs=64)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=cut)
+    X = torch.from_numpy(np.ascontiguousarray(cfg.rhs())).cuda()
+    T = torch.from_numpy(np.ascontiguousarray(cfg.T)).cuda()
+    Z, Q = torch.empty_like(X), torch.empty_like(T)
+    hm.hm_solve_C(ctx, LU, X, Z)
+    hm.hm_radiative_flux(ctx, F, LU, T, Q)
+    torch.cuda.synchronize()
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
+    Zd = vf.solve(C, cfg.rhs())
+    Qd = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T)
+    for col in (0, 31, 63):
+        z1 = torch.empty(f.n, dtype=torch.float64, device="cuda")
+        q1 = torch.empty_like(z1)
+        hm.hm_solve_C(ctx, LU, X[:, col].contiguous(), z1)
+        hm.hm_radiative_flux(ctx, F, LU, T[:, col].contiguous(), q1)
+        torch.cuda.synchronize()
+        assert rel(Z[:, col].cpu().numpy(), z1.cpu().numpy()) <= 1e-13
+        assert rel(Q[:, col].cpu().numpy(), q1.cpu().numpy()) <= 1e-12
+        assert rel(Z[:, col].cpu().numpy(), Zd[:, col]) <= 10 * cfg.eps_aca
+        assert rel(Q[:, col].cpu().numpy(), Qd[:, col]) <= 10 * cfg.eps_aca
