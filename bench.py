@@ -313,8 +313,11 @@ def main():
         torch.cuda.synchronize()
         mms = em0.elapsed_time(em1) / args.profile_iters
         flop = 2.0 * 64 * (rep["bytes_F"] + rep["bytes_C"]) / 8
+        tf = flop / (mms * 1e-3) / 1e12
         multi_rhs = {"nrhs": 64, "flux_ms": mms, "column_applies_per_s": 64 / (mms * 1e-3),
-                     "fp64_tflops": flop / (mms * 1e-3) / 1e12, "engine": "engine_mrhs_kernel (DMMA)"}
+                     "fp64_tflops": tf, "engine": "engine_mrhs_kernel (DMMA)",
+                     "frac_of_dmma_peak": tf / 37.1,
+                     "dmma_peak_source": "37.1 FP64 TFLOP/s measured with scripts/ubench_fp64.cu (DMMA.8x8x4)"}
         del Tm, qm
     # NEXT-1: the cavity Jacobian action J^cav x = 4 P^T Rbar P (T^3 o x) (eq:Jcav) GMRES applies, on the
     # same operators (one projection + the flux program + one transpose projection)
