@@ -435,6 +435,33 @@ def test_config4_apply_sampled(hm, ctx):
 
 
 @pytest.mark.slow
+def test_config5_flat_apply_sampled(hm, ctx):
+    """C5 at its BASELINE parameters (icosphere sub 8, 1,310,720 flat facets, eps_ACA = 1e-5, leaf 128,
+    64 right-hand sides T ~ U[300,1000] K as sigma T^4): F X through the DMMA engine and the single-vector
+    engine vs 200 sampled dense rows of the oracle within 10 eps_ACA (A25: 1e-4).
+    The 64-column result's first column equals the single-vector apply to rounding."""
+    import torch
+    cfg = synth.make_config(5)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    rows = synth.sample_rows(synth.stream_seed(cfg.seed, 999), f.n, 200)
+    X = cfg.rhs()
+    assert X.shape == (f.n, 64)
+    Y = torch.empty(f.n, 64, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, torch.from_numpy(X).cuda(), Y)
+    y1 = torch.empty(f.n, dtype=torch.float64, device="cuda")
+    hm.hm_apply_F(ctx, F, torch.from_numpy(X[:, 0].copy()).cuda(), y1)
+    torch.cuda.synchronize()
+    Yh = Y.cpu().numpy()
+    y1h = y1.cpu().numpy()
+    del Y, y1
+    Ys = vf.sampled_apply(f.centroid, f.normal, f.area, rows, X)
+    assert max(rel(Yh[rows, c], Ys[:, c]) for c in range(64)) <= 10 * cfg.eps_aca
+    assert rel(y1h[rows], Ys[:, 0]) <= 10 * cfg.eps_aca
+    assert rel(Yh[:, 0], y1h) <= 1e-12
+
+
+@pytest.mark.slow
 def test_config5_sphere_exact_rank_one_and_closed_form(hm, ctx):
     """C5 geometry (icosphere sub 8, 1,310,720 facets, eps_ACA = 1e-5) in sphere-exact mode: every admissible
     block is exactly rank 1 (A_sigma A_tau^T / 4 pi) -- an integer pin at a size no dense oracle reaches --
