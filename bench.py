@@ -345,6 +345,16 @@ def main():
     if os.path.exists(tp) and world == 1 and args.config == 2:
         traffic = json.load(open(tp)).get("engine_kernel_flux_c2")
     launches = eng_info["launches_per_call"]
+    shard = None
+    if world > 1:   # SURVEY.md §8(e) report: per-GPU GB/s and load imbalance (max/mean per-rank stored bytes)
+        bl = torch.tensor([float(bytes_local)], device="cuda")
+        allb = [torch.zeros_like(bl) for _ in range(world)]
+        dist.all_gather(allb, bl)
+        per_rank = [float(v.item()) for v in allb]
+        shard = {"bytes_per_rank": per_rank, "imbalance_max_over_mean": max(per_rank) / (sum(per_rank) / world),
+                 "per_gpu_hbm_gbs_max_rank": max(per_rank) / (ms_step * 1e-3) / 1e9,
+                 "exchanges_per_step": "3 in-place ncclAllGather of the padded vector (T, y, z)",
+                 "comm_share": (1.0 - eng_ms["flux_no_exchange"] / eng_ms["flux"]) if "flux_no_exchange" in eng_ms else None}
 
     if rank == 0:
         out = {
@@ -368,7 +378,7 @@ def main():
                        "setup_s": dict(rep["setup_seconds"], wall=setup_wall),
                        "solve_form": "inverse factors (cut level 0, DESIGN.md R27)",
                        "level_form": level_form, "recompressed": recompressed, "multi_rhs": multi_rhs,
-                       "cavity_jacobian_action": jcav},
+                       "cavity_jacobian_action": jcav, "shard": shard},
             "roofline": {"bound": "hbm", "kernel": "engine_kernel (flux program)" + (" + NCCL allgathers, rank 0" if world > 1 else ""),
                          "achieved": achieved,
                          "peak": peak, "unit": "GB/s",

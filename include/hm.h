@@ -238,8 +238,11 @@ hm_status hm_shard_plan(const hm_geom* geom, int world, int64_t* begin, int64_t*
 /* ---- measurement support (bench.py) ---------------------------------------------------- */
 /* Times the hot-path programs with CUDA events on `stream` (device pointers T, q; nrhs = 1) over
    `iters` calls each: ms_out[0] = hm_radiative_flux, ms_out[1] = hm_apply_F, ms_out[2] =
-   hm_solve_C (per call; each call is ONE launch of the persistent stream engine); ms_out[3..5]
-   = 0.  launches_out[0..2] = kernel launches per call (1); launches_out[3] = passes of the flux
+   hm_solve_C (per call; ONE launch of the persistent stream engine at world 1, one launch per
+   segment plus the allgathers between them when sharded); ms_out[3] = sharded only: the flux
+   segments with their allgathers skipped (compute-only time for the communication share; the
+   results of those calls are not valid), else 0; ms_out[4..5] = 0.  launches_out[0..2] = kernel
+   launches per call (1, or the segment count when sharded); launches_out[3] = passes of the flux
    program, [4] = its work units, [5] = its grid size. */
 hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, const double* T,
                           double* q, int32_t iters, double* ms_out, int64_t* launches_out,

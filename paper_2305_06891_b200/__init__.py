@@ -385,6 +385,8 @@ def hm_profile_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, iters: int, stream=
     ctx.check(ctx.lib.hm_profile_flux(ctx.h, F.h, LU.h, pT, pq, int(iters), ms, la, _stream(stream, T, q)),
               "hm_profile_flux")
     ms_d = {"flux": ms[0], "apply_F": ms[1], "solve_C": ms[2]}
+    if ms[3] > 0:   # sharded: the flux segments with their allgathers skipped (compute-only; results invalid)
+        ms_d["flux_no_exchange"] = ms[3]
     info = {"launches_per_call": int(la[0]), "passes": int(la[3]), "units": int(la[4]), "grid": int(la[5])}
     return ms_d, info
 

@@ -889,6 +889,16 @@ hm_status hm_profile_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, con
         ms_out[1] = timeit([&] { launch_apply(c, F, T, q, 1, 0, s); });
         ms_out[2] = timeit([&] { launch_solve(c, L, T, q, 1, 0, s); });
         for (int i = 3; i < 6; ++i) ms_out[i] = 0.0;
+        if (F.geom->shard.sharded()) {   // the same segments with their allgathers skipped: comm share
+            c->skip_exchange = true;
+            try {
+                ms_out[3] = timeit([&] { launch_flux(c, L, T, q, 1, 0, s); });
+            } catch (...) {
+                c->skip_exchange = false;
+                throw;
+            }
+            c->skip_exchange = false;
+        }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (launches_out) {

@@ -337,7 +337,7 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
 void SegProgram::launch(Ctx* ctx, const Geom& g, ProgArgs a, cudaStream_t s) {
     const Shard& S = g.shard;
     for (size_t i = 0; i < segs.size(); ++i) {
-        if (pre[i]) {
+        if (pre[i]) {   // (ctx->skip_exchange: compute-only timing of the segments, results not valid)
             if (pre_user[i]) {   // this rank's slice (columns a.col.. of the caller's n_loc x ld array)
                 const int64_t nl = S.le() - S.lb();
                 const size_t w = mrhs ? (size_t)a.nrhs : 1, dst_pitch = mrhs ? kMrhsMax : 1;
@@ -347,7 +347,7 @@ void SegProgram::launch(Ctx* ctx, const Geom& g, ProgArgs a, cudaStream_t s) {
                                               cudaMemcpyDeviceToDevice, s));
             }
             if (!ctx->ex) throw Error(HM_ERR_NOT_READY, "sharded program without an exchanger");
-            ctx->ex->allgather(pre[i], S.maxc * (mrhs ? kMrhsMax : 1), s);
+            if (!ctx->skip_exchange) ctx->ex->allgather(pre[i], S.maxc * (mrhs ? kMrhsMax : 1), s);
             debug_sync(s, "allgather");
         }
         segs[i]->launch(a, s);

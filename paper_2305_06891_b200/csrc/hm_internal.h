@@ -68,6 +68,7 @@ struct Ctx {
     int device = 0, rank = 0, world = 1;
     bool host_only = false;            // device < 0: trees / shard plan only (no CUDA)
     Exchanger* ex = nullptr;           // world > 1 (owned)
+    bool skip_exchange = false;        // measurement only (hm_profile_flux): sharded programs skip their allgathers
     uint32_t flags = 0;
     cudaStream_t stream = nullptr;  // setup stream
     std::string last_error;

@@ -36,9 +36,13 @@ def _run_rank(hm, rank, world, key, cfg, out, errs):
         hm.hm_apply_F(ctx, F, x, y)
         hm.hm_solve_C(ctx, LU, x, z)
         hm.hm_radiative_flux(ctx, F, LU, T, q)
+        import torch
+        Td = torch.from_numpy(T[:, 0].copy()).cuda()
+        qd = torch.empty_like(Td)
+        ms, info = hm.hm_profile_flux(ctx, F, LU, Td, qd, 3)   # bench.py's comm-share timing path
         for _ in range(3):                                  # repeated calls: exchange state reuse
             hm.hm_radiative_flux(ctx, F, LU, T, q)
-        out[rank] = dict(rows=rows, y=y[:, 0], z=z[:, 0], q=q[:, 0])
+        out[rank] = dict(rows=rows, y=y[:, 0], z=z[:, 0], q=q[:, 0], ms=ms, info=info)
         del LU, F, g
         ctx.close()
     except Exception as ex:                                 # noqa: BLE001 -- reported by the test
@@ -57,6 +61,9 @@ def test_virtual_shards_match_single_rank_and_oracle(world):
     for t in th:
         t.join(timeout=600)
     assert not errs, errs
+    for r in range(world):   # sharded profile: segment count and the compute-only (no-exchange) timing
+        assert out[r]["info"]["launches_per_call"] == 3
+        assert out[r]["ms"]["flux"] > 0 and out[r]["ms"]["flux_no_exchange"] > 0
     n = f.n
     Y, Z, Q = np.empty(n), np.empty(n), np.empty(n)
     for r in range(world):
