@@ -142,6 +142,11 @@ hm_status hm_init(int device, int rank, int world, const void* comm_id, uint32_t
                   hm_ctx** ctx);
 /* 128-byte ncclUniqueId into id_out (rank 0 of a world > 1 job). */
 hm_status hm_nccl_unique_id(void* id_out);
+/* Self-test of the NCCL exchanger on one device: a one-rank communicator and the in-place
+   ncclAllGather the sharded hot path issues, on `count` doubles, checked exactly.  HM_OK, or
+   HM_ERR_NCCL (library missing, communicator or collective failed, data mismatch), HM_ERR_CUDA,
+   HM_ERR_OOM, HM_ERR_INVALID_ARG (count < 1). */
+hm_status hm_nccl_selftest(int device, int64_t count);
 void hm_finalize(hm_ctx* ctx);
 const char* hm_status_string(hm_status s);
 const char* hm_last_error(const hm_ctx* ctx);

@@ -96,6 +96,7 @@ def load_library(path: str = LIB_PATH):
         "hm_profile_flux": (C.c_int, [P, P, P, P, P, I32, P, P, P]),
         "hm_trace_flux": (C.c_int, [P, P, P, P, P, I32, C.POINTER(I32), P, P, P, P]),
         "hm_nccl_unique_id": (C.c_int, [P]),
+        "hm_nccl_selftest": (C.c_int, [C.c_int, C.c_int64]),
         "hm_projection_create": (C.c_int, [P, P, I64, P, P, P, C.POINTER(P)]),
         "hm_destroy_projection": (None, [P]),
         "hm_cavity_flux": (C.c_int, [P, P, P, P, I32, P, P, P]),
@@ -226,6 +227,14 @@ def hm_nccl_unique_id() -> bytes:
     if st != 0:
         raise HMError(st, "hm_nccl_unique_id failed")
     return buf.raw
+
+
+def hm_nccl_selftest(device: int = 0, count: int = 4096) -> None:
+    """One-rank NCCL communicator + the sharded path's in-place allgather, checked (raises HMError)."""
+    lib = load_library()
+    st = lib.hm_nccl_selftest(int(device), C.c_int64(int(count)))
+    if st != 0:
+        raise HMError(st, "hm_nccl_selftest failed")
 
 
 def hm_shard_plan(geom, world: int):

@@ -243,6 +243,44 @@ hm_status hm_nccl_unique_id(void* id_out) {
     }
 }
 
+// One-rank communicator on `device`, then the exact in-place allgather call the sharded hot path
+// issues (NcclExchanger::allgather) on a device buffer of `count` doubles, checked element by
+// element.  A one-GPU box cannot run world > 1 over NCCL (duplicate device), so this is how the
+// dlopen'd symbols, the unique-id handoff and the call form are exercised on real hardware.
+hm_status hm_nccl_selftest(int device, int64_t count) {
+    if (count < 1) return HM_ERR_INVALID_ARG;
+    double* d = nullptr;
+    try {
+        if (cudaSetDevice(device) != cudaSuccess) return HM_ERR_CUDA;
+        char id[128];
+        const hm_status st = hm_nccl_unique_id(id);
+        if (st != HM_OK) return st;
+        NcclExchanger ex(id, 0, 1);
+        std::vector<double> h((size_t)count), back((size_t)count);
+        for (int64_t i = 0; i < count; ++i) h[(size_t)i] = 0.5 + (double)i;
+        if (cudaMalloc(&d, sizeof(double) * (size_t)count) != cudaSuccess) return HM_ERR_OOM;
+        cudaStream_t s;
+        if (cudaStreamCreate(&s) != cudaSuccess) { cudaFree(d); return HM_ERR_CUDA; }
+        cudaMemcpyAsync(d, h.data(), sizeof(double) * (size_t)count, cudaMemcpyHostToDevice, s);
+        ex.allgather(d, count, s);
+        cudaMemcpyAsync(back.data(), d, sizeof(double) * (size_t)count, cudaMemcpyDeviceToHost, s);
+        const cudaError_t ce = cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+        cudaFree(d);
+        d = nullptr;
+        if (ce != cudaSuccess) return HM_ERR_CUDA;
+        ncclResult_t ar = ncclSuccess;
+        nccl_check(nccl().CommGetAsyncError(ex.comm, &ar), "ncclCommGetAsyncError");
+        nccl_check(ar, "ncclAllGather (async)");
+        for (int64_t i = 0; i < count; ++i)
+            if (back[(size_t)i] != h[(size_t)i]) return HM_ERR_NCCL;
+        return HM_OK;
+    } catch (const Error& e) {
+        if (d) cudaFree(d);
+        return e.code;
+    }
+}
+
 hm_status hm_shard_plan(const hm_geom* geom, int world, int64_t* begin, int64_t* end, int64_t* maxc,
                         int64_t* block_owner) {
     if (!geom || world < 1 || (world & (world - 1)) || !begin || !end || !maxc) return HM_ERR_INVALID_ARG;

@@ -268,3 +268,14 @@ def test_virtual_shards_cavity_operator(world, cut):
         assert rel(Q, Q1) <= 1e-12 and rel(y, y1) <= 1e-12
         assert rel(Q, ocav.flux_residual(S, Tn)) <= 10 * cfg.eps_aca
         assert rel(y, ocav.jacobian_apply(S, Tn, xn)) <= 10 * cfg.eps_aca
+
+
+def test_nccl_exchanger_selftest():
+    """The NCCL exchanger of the multi-GPU path on real hardware: libnccl.so.2 dlopen'd (torch's copy),
+    a one-rank communicator from hm_nccl_unique_id, and the in-place ncclAllGather call the sharded
+    programs issue, checked exactly (world > 1 over NCCL needs one GPU per rank)."""
+    import torch  # noqa: F401 -- loads torch's libnccl.so.2 first, as bench.py does
+    import paper_2305_06891_b200 as hm
+    hm.hm_nccl_selftest(0, 1 << 16)
+    with pytest.raises(hm.HMError):
+        hm.hm_nccl_selftest(0, 0)
