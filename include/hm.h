@@ -56,6 +56,11 @@ typedef enum {
 #define HM_FLAG_LOCAL_GROUP 0x1u   /* world > 1 inside ONE process: comm_id points to an int64 group
                                       key shared by the ranks (one host thread per rank); the exchange
                                       is done with device copies (tests of the sharded path on one GPU) */
+#define HM_FLAG_ASYNC_PINNED 0x2u  /* hot-path calls whose output is PINNED host memory (written in place
+                                      by the kernels through its device alias) return without
+                                      synchronizing, stream-ordered like cudaMemcpyAsync: the caller
+                                      synchronizes the stream before reading the output or rewriting a
+                                      pinned input.  Pageable host buffers stay synchronous. */
 
 typedef struct hm_ctx hm_ctx;
 typedef struct hm_geom hm_geom;
@@ -150,6 +155,9 @@ hm_status hm_nccl_selftest(int device, int64_t count);
 void hm_finalize(hm_ctx* ctx);
 const char* hm_status_string(hm_status s);
 const char* hm_last_error(const hm_ctx* ctx);
+/* Change the call-mode flag HM_FLAG_ASYNC_PINNED after hm_init (0 clears it).  Any other bit:
+   HM_ERR_INVALID_ARG (HM_FLAG_LOCAL_GROUP is fixed at hm_init). */
+hm_status hm_set_flags(hm_ctx* ctx, uint32_t flags);
 /* Optional device allocator hook (e.g. torch's caching allocator); NULL restores cudaMalloc. */
 hm_status hm_set_allocator(hm_ctx* ctx, void* (*alloc_fn)(size_t bytes, void* stream, void* user),
                            void (*free_fn)(void* ptr, void* stream, void* user), void* user);

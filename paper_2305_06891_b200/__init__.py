@@ -82,6 +82,7 @@ def load_library(path: str = LIB_PATH):
         "hm_status_string": (C.c_char_p, [C.c_int]),
         "hm_last_error": (C.c_char_p, [P]),
         "hm_set_allocator": (C.c_int, [P, P, P, P]),
+        "hm_set_flags": (C.c_int, [P, C.c_uint32]),
         "hm_build_geometry": (C.c_int, [P, I64, P, P, P, P, C.POINTER(hm_tree_params), C.POINTER(P)]),
         "hm_assemble_aca": (C.c_int, [P, P, C.POINTER(hm_aca_params), C.POINTER(P)]),
         "hm_factor_hlu": (C.c_int, [P, P, P, C.POINTER(hm_lu_params), C.POINTER(P)]),
@@ -154,6 +155,7 @@ def _stream(stream, *arrays):
 
 
 HM_FLAG_LOCAL_GROUP = 0x1
+HM_FLAG_ASYNC_PINNED = 0x2   # pinned host outputs: calls return without a sync (caller syncs the stream)
 
 
 class Context:
@@ -191,6 +193,11 @@ class Context:
 
 def hm_init(device: int = 0, rank: int = 0, world: int = 1, comm_id=None, flags: int = 0) -> Context:
     return Context(device, rank, world, comm_id, flags)
+
+
+def hm_set_flags(ctx: Context, flags: int) -> None:
+    """Set the call-mode flag (HM_FLAG_ASYNC_PINNED or 0) of an existing context."""
+    ctx.check(ctx.lib.hm_set_flags(ctx.h, int(flags)), "hm_set_flags")
 
 
 _ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)

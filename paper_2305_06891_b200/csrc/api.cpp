@@ -197,6 +197,12 @@ void hm_finalize(hm_ctx* ctx) {
     delete ctx;
 }
 
+hm_status hm_set_flags(hm_ctx* ctx, uint32_t flags) {
+    if (!ctx || (flags & ~HM_FLAG_ASYNC_PINNED)) return HM_ERR_INVALID_ARG;   // only the call-mode flag changes
+    ctx->c.flags = (ctx->c.flags & ~HM_FLAG_ASYNC_PINNED) | flags;
+    return HM_OK;
+}
+
 hm_status hm_set_allocator(hm_ctx* ctx, void* (*alloc_fn)(size_t, void*, void*), void (*free_fn)(void*, void*, void*),
                            void* user) {
     if (!ctx || (!alloc_fn) != (!free_fn)) return HM_ERR_INVALID_ARG;
@@ -658,13 +664,15 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
         int ok_ = 0;
         double* yd = out_target(c, F.host_stage_out, y, cnt, ok_);
         const bool hout = ok_ == 2, hsync = ok_ != 0;
+        // HM_FLAG_ASYNC_PINNED: a pinned host output written in place by the program needs no sync
+        const bool async_ok = ok_ == 1 && (c->flags & HM_FLAG_ASYNC_PINNED);
         if (nrhs == 1 && F.prog_apply_h.ready && !F.geom->shard.sharded()) {
             if (const double* xa = pinned_alias(x)) {   // pinned host x: the program's copy-in pass
                 ProgArgs a = base_args(*F.geom, F.x_dev.p, yd, 1, 0);
                 a.host_in = xa;
                 F.prog_apply_h.launch(a, s);
                 if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-                HM_CUDA(cudaStreamSynchronize(s));
+                if (!async_ok) HM_CUDA(cudaStreamSynchronize(s));
                 return;
             }
         }
@@ -686,7 +694,7 @@ hm_status hm_apply_F(hm_ctx* ctx, const hm_hmat* Fh, int32_t nrhs, const double*
             for (int col = 0; col < nrhs; ++col) launch_apply(c, F, xd, yd, nrhs, col, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(y, yd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (hin || hsync) HM_CUDA(cudaStreamSynchronize(s));
+        if (hin || (hsync && !async_ok)) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
 
@@ -700,13 +708,15 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
         int ok_ = 0;
         double* zd = out_target(c, L.host_stage_out, z, cnt, ok_);
         const bool hout = ok_ == 2, hsync = ok_ != 0;
+        // HM_FLAG_ASYNC_PINNED: a pinned host output written in place by the program needs no sync
+        const bool async_ok = ok_ == 1 && (c->flags & HM_FLAG_ASYNC_PINNED);
         if (nrhs == 1 && L.prog_solve_h.ready && !L.F->geom->shard.sharded()) {
             if (const double* ba = pinned_alias(b)) {   // pinned host b: the program's copy-in pass
                 ProgArgs a = base_args(*L.F->geom, L.T_dev.p, zd, 1, 0);
                 a.host_in = ba;
                 L.prog_solve_h.launch(a, s);
                 if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-                HM_CUDA(cudaStreamSynchronize(s));
+                if (!async_ok) HM_CUDA(cudaStreamSynchronize(s));
                 return;
             }
         }
@@ -728,7 +738,7 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LUh, int32_t nrhs, const double*
             for (int col = 0; col < nrhs; ++col) launch_solve(c, L, bd, zd, nrhs, col, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(z, zd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (hin || hsync) HM_CUDA(cudaStreamSynchronize(s));
+        if (hin || (hsync && !async_ok)) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
 
@@ -817,6 +827,8 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
         int ok_ = 0;
         double* qd = out_target(c, L.host_stage_out, q, cnt, ok_);
         const bool hout = ok_ == 2, hsync = ok_ != 0;
+        // HM_FLAG_ASYNC_PINNED: a pinned host output written in place by the program needs no sync
+        const bool async_ok = ok_ == 1 && (c->flags & HM_FLAG_ASYNC_PINNED);
         // single vector, pinned host T: the program's copy-in pass reads it (no separate H2D copy
         // before the kernel: the payload stream starts while T crosses the bus)
         if (nrhs == 1 && L.prog_flux_h.ready && !L.F->geom->shard.sharded()) {
@@ -836,7 +848,7 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
                 a.g_int = L.g_int.p;
                 L.prog_flux_h.launch(a, s);
                 if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-                HM_CUDA(cudaStreamSynchronize(s));
+                if (!async_ok) HM_CUDA(cudaStreamSynchronize(s));
                 return;
             }
         }
@@ -860,7 +872,7 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
             for (int col = 0; col < nrhs; ++col) launch_flux(c, L, Td, qd, nrhs, col, s);
         }
         if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (hin || hsync) HM_CUDA(cudaStreamSynchronize(s));
+        if (hin || (hsync && !async_ok)) HM_CUDA(cudaStreamSynchronize(s));
     });
 }
 

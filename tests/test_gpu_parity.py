@@ -772,6 +772,18 @@ def test_pinned_host_outputs_written_directly(hm, ctx):
             op2 = torch.empty(inp.shape, dtype=torch.float64).pin_memory()
             fn(ip, op2)
             assert np.array_equal(op2.numpy(), ref), (name, cols, "pinned input")
+            # HM_FLAG_ASYNC_PINNED: pinned outputs, no sync inside the call; the caller syncs the stream
+            op3 = torch.full(inp.shape, float("nan"), dtype=torch.float64).pin_memory()
+            hm.hm_set_flags(ctx, hm.HM_FLAG_ASYNC_PINNED)
+            try:
+                for _ in range(3):
+                    fn(ip, op3)
+                torch.cuda.synchronize()
+            finally:
+                hm.hm_set_flags(ctx, 0)
+            assert np.array_equal(op3.numpy(), ref), (name, cols, "async pinned")
+    with pytest.raises(hm.HMError):
+        hm.hm_set_flags(ctx, hm.HM_FLAG_LOCAL_GROUP)
 
 
 @pytest.mark.parametrize("cut", [2, 99])
