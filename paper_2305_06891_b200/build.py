@@ -18,6 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", CSRC,
           "-I", os.path.join(os.path.dirname(HERE), "include")]
+# experiment-only engine geometry overrides (e.g. HM_BUILD_DEFINES="HM_PSTAGES=4 HM_STAGE_DOUBLES=5120")
+COMMON += ["-D" + d for d in os.environ.get("HM_BUILD_DEFINES", "").split()]
 SOURCES = ["tree.cpp", "hop.cpp", "api.cpp", "hlu.cpp", "engine.cpp", "shard.cpp",
            "kernels_assembly.cu", "kernels_apply.cu", "kernels_dense.cu", "kernels_engine.cu",
            "kernels_mrhs.cu", "kernels_recompress.cu"]

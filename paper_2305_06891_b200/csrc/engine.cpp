@@ -108,7 +108,7 @@ void Program::add_elementwise(int type, int64_t n, double* out, int rows_per_uni
 void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
     for (const Unit& u : h_units)
         if (u.type == UNIT_STREAM && (u.ncols > (mrhs ? kMrhsMaxCols : kUnitMaxCols) || u.ld > 128 ||
-                                      (int64_t)u.ncols * u.ld > kUnitPayloadDoubles))
+                                      (int64_t)u.ncols * u.ld > (mrhs ? kUnitPayloadDoubles : kStageDoubles)))
             throw Error(HM_ERR_UNSUPPORTED, "work unit exceeds the engine stage size");
     const int64_t P = (int64_t)h_passes.size();
     if (P > engine_max_passes()) throw Error(HM_ERR_UNSUPPORTED, "program has more passes than the engine's pass table");

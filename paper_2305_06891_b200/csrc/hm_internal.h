@@ -201,7 +201,11 @@ static_assert(sizeof(Unit) % 16 == 0, "Unit is TMA-copied");
 // UNIT_COPYIN (pinned host input): out[row * ld + col] = host_in[row * ld + col], rows in external order
 enum UnitType : int32_t { UNIT_STREAM = 0, UNIT_PROLOGUE = 1, UNIT_PERMUTE = 2, UNIT_EPILOGUE = 3, UNIT_PROLOGUE_INT = 4,
                           UNIT_COPYIN = 5 };
-constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage
+constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage (multi-RHS engine)
+#ifndef HM_STAGE_DOUBLES
+#define HM_STAGE_DOUBLES 7240
+#endif
+constexpr int kStageDoubles = HM_STAGE_DOUBLES;   // single-vector engine payload stage (doubles): 56.6 KB
 constexpr int kMrhsMax = 64;                // multi-RHS block width (columns of X per program launch)
 constexpr int kMrhsMaxCols = 64;            // multi-RHS chunk: <= 64 panel columns (X tile 64 x 64)
 constexpr int kUnitMaxCols = 256;

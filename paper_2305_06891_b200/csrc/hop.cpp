@@ -6,7 +6,8 @@
 //           [ phase-2 panels: per leaf row r, the leaf-row slices of every dense block and U
 //             factor covering r: column-major, ld = m_r (even), in block order              ]
 //   colsrc[c] = index into XT = [x (n) | t (sum k)] of the input multiplying column c.
-// Panels have <= 128 rows and are cut into work units of <= 32 KB contiguous payload.
+// Panels have <= 128 rows and are cut into work units of <= kStageDoubles (single vector, 56.6 KB)
+// or kUnitPayloadDoubles (multi-RHS, 32 KB) of contiguous payload.
 #include <algorithm>
 #include <cstdlib>
 #include <map>
@@ -26,7 +27,7 @@ static int env_int(const char* name, int dflt) {
 }
 
 // Cut panels into pieces (only panels above 512 KB are split, for load balance) and pieces into
-// chunks of <= 32 KB contiguous payload (<= 512 columns), each chunk with its own 16-byte
+// chunks of <= one engine stage of contiguous payload (<= 256 columns), each chunk with its own 16-byte
 // aligned column-source segment (so the engine can TMA both).
 // max_cols: columns per chunk (single vector: kUnitMaxCols; multi-RHS: kMrhsMaxCols); part_scale:
 // partial-sum doubles per panel row (1, or kMrhsMax for the multi-RHS units)
@@ -86,7 +87,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
             for (int32_t q = 0; q < sg.np; ++q, ++pc) {
                 const int64_t p0 = sg.c0 + q * Cp, p1 = std::min<int64_t>(sg.c1, p0 + Cp);
                 if (p1 <= p0) { --pc; continue; }
-                int64_t C = std::min<int64_t>(max_cols, kUnitPayloadDoubles / pn.ld);
+                int64_t C = std::min<int64_t>(max_cols, (part_scale > 1 ? kUnitPayloadDoubles : kStageDoubles) / pn.ld);
                 const int32_t nch = (int32_t)((p1 - p0 + C - 1) / C);
                 C = (p1 - p0 + nch - 1) / nch;
                 Piece PC;

@@ -5,8 +5,8 @@
 // One CTA per SM (co-resident by cooperative launch), warp-specialised, 19 warps:
 //   warp 0 (producer, one thread): grabs tasks (a panel, or a piece of a big panel) from a monotone
 //          queue counter in topological order; per chunk it TMA-copies the chunk descriptor into a
-//          header/gather slot (12-slot ring) and, kLookahead = 7 chunks later, the chunk's payload into
-//          a 32 KB payload stage (5-stage ring), both with 1-D bulk copies and mbarrier transaction counts;
+//          header/gather slot (12-slot ring) and, kLookahead = 9 chunks later, the chunk's payload into
+//          a 56.6 KB payload stage (3-stage ring), both with 1-D bulk copies and mbarrier transaction counts;
 //   warps 1-4 (gatherers; warp w owns the header slots k = w-1 mod 4): before gathering for a task,
 //          wait for the task's dependencies (per-pass or per-tree-node counters), then load the
 //          chunk's inputs from L2 (ld.cg: written by other SMs) into the slot;
@@ -43,16 +43,29 @@ constexpr int kThreads = 32 * (kRetireWarp + kRetireWarps);  // 608
 // Two rings: payload stages (TMA of the factor bytes) and header/gather slots (chunk descriptor +
 // gathered inputs).  The producer posts a chunk's header kLookahead chunks before it issues its
 // payload, so the input gather (an L2 round trip) is finished by the time the payload lands.
-constexpr int kPStages = 5;      // 4 -> 5 (with 256-column chunks and 6 retire slots to fit 227 KB): C2 184.9 -> 183.0 us
-constexpr int kGSlots = 12;
+#ifndef HM_PSTAGES
+#define HM_PSTAGES 3
+#endif
+#ifndef HM_GSLOTS
+#define HM_GSLOTS 12
+#endif
+#ifndef HM_RSLOTS
+#define HM_RSLOTS 6
+#endif
+// Stage geometry (160 -> 170 KB of payload stages): 5 x 32 KB -> 3 x 56.6 KB chunks
+// (HM_STAGE_DOUBLES = 7240): each CTA's pipe is bound by a per-chunk cost, so fewer, larger chunks
+// win -- C2 flux 182.4 -> 171.5 us, C3 flux 0.910 -> 0.822 ms, C4 apply 2.011 -> 1.954 ms
+// (scripts/gpu_stage_sweep*.sh; 4 x 42 KB is within 1 % of this)
+constexpr int kPStages = HM_PSTAGES;
+constexpr int kGSlots = HM_GSLOTS;
 constexpr int kLookahead = kGSlots - kPStages;
-constexpr int kRetireSlots = 6;    // task-end handoff buffers (consumers -> retire warps)
-constexpr int kMaxCols = 256;      // per chunk; payload <= 32 KB
+constexpr int kRetireSlots = HM_RSLOTS;    // task-end handoff buffers (consumers -> retire warps)
+constexpr int kMaxCols = 256;      // per chunk; payload <= kStageDoubles
 constexpr int kMaxPasses = 64;     // pass table held in shared memory
 static_assert(kGSlots % kGatherers == 0, "slot ownership");
 
 struct __align__(16) PStage {
-    double payload[kUnitPayloadDoubles];
+    double payload[kStageDoubles];
 };
 
 // Header/gather slot: the chunk's descriptor (TMA-copied by the producer: everything the gatherers
