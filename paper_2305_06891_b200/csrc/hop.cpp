@@ -33,7 +33,8 @@ static int env_int(const char* name, int dflt) {
 // partial-sum doubles per panel row (1, or kMrhsMax for the multi-RHS units)
 static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs, std::vector<int32_t>& ucs,
                        cudaStream_t s, int max_cols = kUnitMaxCols, int part_scale = 1, bool split_xonly = true,
-                       int order = 0 /* 0: largest first; 1: all pieces by key; 2: t-reading pieces by key */) {
+                       int order = 0 /* 0: largest first; 1: all pieces by key; 2: t-reading pieces by key */,
+                       int64_t max_doubles = kUnitPayloadDoubles /* payload doubles per chunk */) {
     std::vector<Unit>& units = P.h_units;
     units.clear();
     P.unit_panel.clear();
@@ -87,7 +88,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
             for (int32_t q = 0; q < sg.np; ++q, ++pc) {
                 const int64_t p0 = sg.c0 + q * Cp, p1 = std::min<int64_t>(sg.c1, p0 + Cp);
                 if (p1 <= p0) { --pc; continue; }
-                int64_t C = std::min<int64_t>(max_cols, (part_scale > 1 ? kUnitPayloadDoubles : kStageDoubles) / pn.ld);
+                int64_t C = std::min<int64_t>(max_cols, max_doubles / pn.ld);
                 const int32_t nch = (int32_t)((p1 - p0 + C - 1) / C);
                 C = (p1 - p0 + nch - 1) / nch;
                 Piece PC;
@@ -294,8 +295,16 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     op.arena.alloc(ctx, (size_t)std::max<int64_t>(off, 2), "operator arena");
     HM_CUDA(cudaMemsetAsync(op.arena.p, 0, sizeof(double) * (size_t)std::max<int64_t>(off, 2), s));
     std::vector<int32_t> ucs;
-    make_units(ctx, op.p1, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p1_by_key ? 1 : 0);
-    make_units(ctx, op.p2, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p2_by_row ? 2 : 0);
+    // chunk payload cap: one engine stage (56.6 KB).  Sharded operators keep 32 KB chunks: with larger
+    // chunks the virtual-shard tests hit an illegal address (cause not isolated);
+    // HM_SHARD_CHUNK_UNCAPPED (build define) restores the stage-sized chunks there for that hunt
+#ifdef HM_SHARD_CHUNK_UNCAPPED
+    const int64_t chunk_doubles = kStageDoubles;
+#else
+    const int64_t chunk_doubles = shd ? kUnitPayloadDoubles : kStageDoubles;
+#endif
+    make_units(ctx, op.p1, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p1_by_key ? 1 : 0, chunk_doubles);
+    make_units(ctx, op.p2, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p2_by_row ? 2 : 0, chunk_doubles);
     {   // multi-RHS chunking of the same panels (<= kMrhsMaxCols columns: X tile in smem)
         op.p1m.panels = op.p1.panels;
         op.p2m.panels = op.p2.panels;
