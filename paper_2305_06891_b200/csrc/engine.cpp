@@ -27,7 +27,10 @@ int add_stream_impl(Program& P, const StreamPass& sp, const HOp& op, const doubl
     p.first_unit = (int64_t)P.h_units.size();
     p.n_units = (int64_t)sp.h_units.size();
     p.arena = op.arena.p;
-    p.colsrc = in_mode == IN_PLAIN ? op.colsrc.p : op.colsrc_ext.p;
+    // IN_FLUXI (sharded flux) gathers by internal padded index like IN_PLAIN; colsrc_ext (external
+    // indices, fused prologue) exists only for unsharded operators
+    p.colsrc = (in_mode == IN_PLAIN || in_mode == IN_FLUXI) ? op.colsrc.p : op.colsrc_ext.p;
+    if (!p.colsrc) throw Error(HM_ERR_NOT_READY, "stream pass without column sources for its input mode");
     p.in = in;
     p.out = out;
     p.part = sp.part.p;

@@ -295,14 +295,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     op.arena.alloc(ctx, (size_t)std::max<int64_t>(off, 2), "operator arena");
     HM_CUDA(cudaMemsetAsync(op.arena.p, 0, sizeof(double) * (size_t)std::max<int64_t>(off, 2), s));
     std::vector<int32_t> ucs;
-    // chunk payload cap: one engine stage (56.6 KB).  Sharded operators keep 32 KB chunks: with larger
-    // chunks the virtual-shard tests hit an illegal address (cause not isolated);
-    // HM_SHARD_CHUNK_UNCAPPED (build define) restores the stage-sized chunks there for that hunt
-#ifdef HM_SHARD_CHUNK_UNCAPPED
-    const int64_t chunk_doubles = kStageDoubles;
-#else
-    const int64_t chunk_doubles = shd ? kUnitPayloadDoubles : kStageDoubles;
-#endif
+    const int64_t chunk_doubles = kStageDoubles;   // chunk payload cap: one engine stage (56.6 KB)
     make_units(ctx, op.p1, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p1_by_key ? 1 : 0, chunk_doubles);
     make_units(ctx, op.p2, colsrc, ucs, s, kUnitMaxCols, 1, true, op.p2_by_row ? 2 : 0, chunk_doubles);
     {   // multi-RHS chunking of the same panels (<= kMrhsMaxCols columns: X tile in smem)
