@@ -106,6 +106,13 @@ typedef struct {
                               of the cut_level diagonal blocks, compressed in F's partition.
                               < 0 (default) -> 0: C^-1 b = U^-1 (L^-1 b) as two H-matrix products;
                               >= depth: pure level form (leaf inverses only).                  */
+    int32_t method;        /* 0 (default): hierarchical arithmetic ("stage B", reading R33):
+                              the 4-step recursion of PAPER.md:770-775 on the blocks of C in F's
+                              partition, recursive substitutions and block products, every low-rank
+                              sum truncated at eps_lu; memory O(stored blocks), any
+                              n.  1: dense tiles on the GPU ("stage A", reading R28), then truncation
+                              block by block; needs ~18 n^2 bytes of device memory (n up to ~1e5);
+                              kept as a cross-check.                                             */
 } hm_lu_params;
 
 /* Storage / traffic accounting (bytes are fp64 payload bytes actually stored in HBM). */
@@ -176,14 +183,16 @@ hm_status hm_build_geometry(hm_ctx* ctx, int64_t n, const double* xyz, const dou
    clamp and row scaling. */
 hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params* params,
                           hm_hmat** F_out);
-/* One-time factorisation of C = I - Lambda F (Lambda_ii = (1-eps_i)/A_i) in the block
-   structure of F, stored for the solve form chosen by params->cut_level
-   (reading R27): per internal node t above the cut, W^L_t = L21 L11^-1 and
-   W^U_t = U12 U22^-1, and the inverse factors of the cut-level diagonal blocks, all compressed
-   to eps_lu in the block partition of F (cut 0, the default: L^-1 and U^-1 as two H-matrices;
-   cut >= depth: the pure level form with dense leaf inverses).
-   emissivity: host array, n, external order, 0 < eps_i <= 1.  The factorisation is dense on
-   the GPU (stage A, R28): HM_ERR_UNSUPPORTED when it does not fit (n above ~1e5). */
+/* One-time factorisation of C = I - Lambda F (Lambda_ii = (1-eps_i)/A_i, eq:reflection_matrix)
+   in the block structure of F, stored for the solve form of params->cut_level (R27):
+   W^L_t = L21 L11^-1, W^U_t = U12 U22^-1 per tree node t above the cut, and the inverse factors
+   of the cut-level diagonal blocks (cut 0, default: L^-1 and U^-1), compressed to eps_lu in F's
+   partition.  emissivity: host array, n, external order, 0 < eps_i <= 1.  params->method:
+   hierarchical arithmetic (default, any n; host recursion, OpenMP tasks over independent blocks)
+   or dense GPU tiles (HM_ERR_UNSUPPORTED above n ~ 1e5).  HM_ERR_SINGULAR on a leaf pivot below
+   1e-14 of its block's largest entry.  Host-only contexts factor an F from hm_hmat_from_host and
+   keep the factors for hm_export_factors.  The 4-step recursion, substitutions and truncation
+   policy are PAPER.md:751-779. */
 hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
                         const hm_lu_params* params, hm_hlu** out);
 
@@ -237,6 +246,31 @@ hm_status hm_export_perm(const hm_geom* geom, int32_t* perm /* n: perm[internal]
    (then stored_kind = !admissible ? 0 : 1 and rank = 0). */
 hm_status hm_export_partition(const hm_geom* geom, const hm_hmat* F, int64_t* n_blocks,
                               int64_t* rows);
+/* The stored blocks of one hot-path operator (host buffers), e.g. for the "apply is exact" check of
+   PAPER.md:782.  op: HM_OP_F = F as stored (closed-cavity scaled); HM_OP_LINV / HM_OP_UINV = the
+   inverse factors of the cut-level diagonal blocks (cut level 0: L^-1 and U^-1 of C, R27);
+   HM_OP_WL(l) / HM_OP_WU(l) = the level-form blocks W^L_t / W^U_t of the tree nodes t of level l
+   (l < cut level).  The operator is the SUM of the exported items (leaf-row slices of blocks on the
+   GPU, whole blocks on a host-only context); rows and columns in internal order (hm_export_perm).
+   Call with meta == NULL to get *n_items and *n_doubles, then with meta[6 n_items] =
+   (row0, m, col0, n, kind, k) and data[n_doubles]: kind 0 = dense m x n column-major, kind 1 = U
+   (m x k) followed by V (n x k), column-major (item = U V^T).  F or LU may be NULL when op does not
+   need it.  HM_ERR_INVALID_ARG for an op the handles do not hold. */
+#define HM_OP_F 0
+#define HM_OP_LINV 1
+#define HM_OP_UINV 2
+#define HM_OP_WL(l) (3 + 2 * (l))
+#define HM_OP_WU(l) (4 + 2 * (l))
+hm_status hm_export_factors(const hm_hmat* F, const hm_hlu* LU, int32_t op, int64_t* n_items,
+                            int64_t* n_doubles, int64_t* meta, double* data);
+/* An F given by the caller in the block partition of geom (host-only contexts, device < 0): one entry
+   per block of hm_export_partition's order, kind[b] = 0 dense (m x n column-major at data + offset[b])
+   or 1 low rank (U m x k then V n x k column-major at data + offset[b], k = rank[b]), internal order,
+   already closed-cavity scaled.  The library copies the payload.  It exists so the hierarchical H-LU
+   can be driven and checked without a GPU (tests/test_hlu_host.py).  HM_ERR_UNSUPPORTED on a
+   device context, HM_ERR_INVALID_ARG on a kind/rank/size mismatch. */
+hm_status hm_hmat_from_host(hm_ctx* ctx, const hm_geom* geom, const int32_t* kind, const int32_t* rank,
+                            const int64_t* offset, const double* data, hm_hmat** F_out);
 /* Row sums s_i = (F_H 1)_i / A_i before scaling and clamped c_i (external order, n each). */
 hm_status hm_export_row_sums(const hm_hmat* F, double* s, double* c);
 hm_status hm_storage_report(const hm_hmat* F, const hm_hlu* LU, hm_storage* out);

@@ -42,7 +42,7 @@ class hm_aca_params(C.Structure):
 
 
 class hm_lu_params(C.Structure):
-    _fields_ = [("eps_lu", C.c_double), ("cut_level", C.c_int32)]
+    _fields_ = [("eps_lu", C.c_double), ("cut_level", C.c_int32), ("method", C.c_int32)]
 
 
 class hm_storage(C.Structure):
@@ -103,6 +103,8 @@ def load_library(path: str = LIB_PATH):
         "hm_cavity_flux": (C.c_int, [P, P, P, P, I32, P, P, P]),
         "hm_cavity_jacobian": (C.c_int, [P, P, P, P, I32, P, P, P, P]),
         "hm_shard_plan": (C.c_int, [P, C.c_int, P, P, C.POINTER(I64), P]),
+        "hm_export_factors": (C.c_int, [P, P, I32, C.POINTER(I64), C.POINTER(I64), P, P]),
+        "hm_hmat_from_host": (C.c_int, [P, P, P, P, P, P, C.POINTER(P)]),
         "hm_destroy_geom": (None, [P]),
         "hm_destroy_hmat": (None, [P]),
         "hm_destroy_hlu": (None, [P]),
@@ -311,9 +313,12 @@ def hm_assemble_aca(ctx: Context, geom: Geometry, eps_aca=1e-6, k_max=0, closed_
     return HMatrix(ctx, h, geom)
 
 
-def hm_factor_hlu(ctx: Context, F: HMatrix, emissivity, eps_lu=0.0, cut_level=-1) -> HLU:
+HM_LU_HIERARCHICAL, HM_LU_DENSE = 0, 1   # hm_lu_params.method: stage B (default) / stage A
+
+
+def hm_factor_hlu(ctx: Context, F: HMatrix, emissivity, eps_lu=0.0, cut_level=-1, method="hierarchical") -> HLU:
     e = np.ascontiguousarray(emissivity, dtype=np.float64)
-    p = hm_lu_params(float(eps_lu), int(cut_level))
+    p = hm_lu_params(float(eps_lu), int(cut_level), {"hierarchical": 0, "dense": 1}[method])
     h = C.c_void_p()
     ctx.check(ctx.lib.hm_factor_hlu(ctx.h, F.h, e.ctypes.data, C.byref(p), C.byref(h)), "hm_factor_hlu")
     return HLU(ctx, h, F)
@@ -327,10 +332,18 @@ def _rows(F_or_geom_ctx, geom):
     return geom.n
 
 
-def _nrhs(x, n):
+def _nrhs(x, n, out=None):
+    """Column count of an (n,) or (n, nrhs) input; the output must have the input's shape (and, for
+    tensors, its device): the library writes n * nrhs doubles through the output pointer."""
     shp = tuple(x.shape)
-    if shp[0] != n or len(shp) > 2:
+    if len(shp) == 0 or shp[0] != n or len(shp) > 2:
         raise ValueError(f"expected ({n},) or ({n}, nrhs), got {shp}")
+    if out is not None:
+        if tuple(out.shape) != shp:
+            raise ValueError(f"output shape {tuple(out.shape)} differs from the input shape {shp}")
+        dx, do = getattr(x, "device", None), getattr(out, "device", None)
+        if hasattr(x, "data_ptr") and hasattr(out, "data_ptr") and dx != do:
+            raise ValueError(f"output on {do}, input on {dx}")
     return 1 if len(shp) == 1 else int(shp[1])
 
 
@@ -338,14 +351,14 @@ def hm_apply_F(ctx: Context, F: HMatrix, x, y, stream=None):
     """y = F x; x, y: (n,) or (n, nrhs) float64, device tensors or host arrays."""
     px, kx = _ptr(x)
     py, ky = _ptr(y, out=True)
-    ctx.check(ctx.lib.hm_apply_F(ctx.h, F.h, _nrhs(x, _rows(F, F.geom)), px, py, _stream(stream, x, y)), "hm_apply_F")
+    ctx.check(ctx.lib.hm_apply_F(ctx.h, F.h, _nrhs(x, _rows(F, F.geom), y), px, py, _stream(stream, x, y)), "hm_apply_F")
     return y
 
 
 def hm_solve_C(ctx: Context, LU: HLU, b, z, stream=None):
     pb, kb = _ptr(b)
     pz, kz = _ptr(z, out=True)
-    ctx.check(ctx.lib.hm_solve_C(ctx.h, LU.h, _nrhs(b, _rows(LU, LU.F.geom)), pb, pz, _stream(stream, b, z)),
+    ctx.check(ctx.lib.hm_solve_C(ctx.h, LU.h, _nrhs(b, _rows(LU, LU.F.geom), z), pb, pz, _stream(stream, b, z)),
               "hm_solve_C")
     return z
 
@@ -353,7 +366,7 @@ def hm_solve_C(ctx: Context, LU: HLU, b, z, stream=None):
 def hm_radiative_flux(ctx: Context, F: HMatrix, LU: HLU, T, q, stream=None):
     pT, kT = _ptr(T)
     pq, kq = _ptr(q, out=True)
-    ctx.check(ctx.lib.hm_radiative_flux(ctx.h, F.h, LU.h, _nrhs(T, _rows(F, F.geom)), pT, pq, _stream(stream, T, q)),
+    ctx.check(ctx.lib.hm_radiative_flux(ctx.h, F.h, LU.h, _nrhs(T, _rows(F, F.geom), q), pT, pq, _stream(stream, T, q)),
               "hm_radiative_flux")
     return q
 
@@ -372,6 +385,69 @@ def hm_export_partition(geom: Geometry, F: HMatrix | None = None) -> np.ndarray:
     geom.ctx.check(lib.hm_export_partition(geom.h, None if F is None else F.h, C.byref(nb), out.ctypes.data),
                    "partition")
     return out
+
+
+HM_OP_F, HM_OP_LINV, HM_OP_UINV = 0, 1, 2
+
+
+def HM_OP_WL(level):
+    return 3 + 2 * level
+
+
+def HM_OP_WU(level):
+    return 4 + 2 * level
+
+
+def hm_export_factors(op: int, F: HMatrix | None = None, LU: HLU | None = None):
+    """The stored items of one operator: list of (row0, m, col0, n, D) with D the dense m x n item,
+    or (row0, m, col0, n, (U, V)) for a low-rank item U V^T; internal order."""
+    ctx = (F or LU).ctx
+    ni, nd = C.c_int64(), C.c_int64()
+    fh, lh = (None if F is None else F.h), (None if LU is None else LU.h)
+    ctx.check(ctx.lib.hm_export_factors(fh, lh, int(op), C.byref(ni), C.byref(nd), None, None), "hm_export_factors")
+    meta = np.empty((ni.value, 6), dtype=np.int64)
+    data = np.empty(max(nd.value, 1))
+    ctx.check(ctx.lib.hm_export_factors(fh, lh, int(op), C.byref(ni), C.byref(nd), meta.ctypes.data,
+                                        data.ctypes.data), "hm_export_factors")
+    out, o = [], 0
+    for r0, m, c0, n, kind, k in meta.tolist():
+        if kind == 0:
+            out.append((r0, m, c0, n, data[o:o + m * n].reshape(n, m).T))
+            o += m * n
+        else:
+            U = data[o:o + m * k].reshape(k, m).T
+            V = data[o + m * k:o + (m + n) * k].reshape(k, n).T
+            out.append((r0, m, c0, n, (U, V)))
+            o += k * (m + n)
+    return out
+
+
+def hm_hmat_from_host(ctx: Context, geom: Geometry, blocks) -> HMatrix:
+    """F from the caller's blocks (host-only contexts): blocks in hm_export_partition order, each a
+    dense (m, n) array or a (U, V) pair (U m x k, V n x k), internal order."""
+    kinds, ranks, offs, parts, o = [], [], [], [], 0
+    for b in blocks:
+        offs.append(o)
+        if isinstance(b, tuple):
+            U, V = (np.asarray(b[0], dtype=np.float64), np.asarray(b[1], dtype=np.float64))
+            kinds.append(1)
+            ranks.append(U.shape[1])
+            parts += [U.T.ravel(), V.T.ravel()]
+            o += U.size + V.size
+        else:
+            D = np.asarray(b, dtype=np.float64)
+            kinds.append(0)
+            ranks.append(0)
+            parts.append(D.T.ravel())
+            o += D.size
+    data = np.ascontiguousarray(np.concatenate(parts) if parts else np.zeros(1))
+    k = np.asarray(kinds, dtype=np.int32)
+    r = np.asarray(ranks, dtype=np.int32)
+    of = np.asarray(offs, dtype=np.int64)
+    h = C.c_void_p()
+    ctx.check(ctx.lib.hm_hmat_from_host(ctx.h, geom.h, k.ctypes.data, r.ctypes.data, of.ctypes.data,
+                                        data.ctypes.data, C.byref(h)), "hm_hmat_from_host")
+    return HMatrix(ctx, h, geom)
 
 
 def hm_export_row_sums(F: HMatrix):
@@ -444,7 +520,7 @@ def hm_projection_create(ctx: Context, geom: Geometry, n_nodes: int, row_ptr, co
 def hm_cavity_flux(ctx: Context, F: HMatrix, LU: HLU, P: Projection, T_nodes, Q_nodes, stream=None):
     pT, kT = _ptr(T_nodes)
     pQ, kQ = _ptr(Q_nodes, out=True)
-    ctx.check(ctx.lib.hm_cavity_flux(ctx.h, F.h, LU.h, P.h, _nrhs(T_nodes, P.n_nodes), pT, pQ,
+    ctx.check(ctx.lib.hm_cavity_flux(ctx.h, F.h, LU.h, P.h, _nrhs(T_nodes, P.n_nodes, Q_nodes), pT, pQ,
                                      _stream(stream, T_nodes, Q_nodes)), "hm_cavity_flux")
     return Q_nodes
 
@@ -453,6 +529,6 @@ def hm_cavity_jacobian(ctx: Context, F: HMatrix, LU: HLU, P: Projection, T_nodes
     pT, kT = _ptr(T_nodes)
     px, kx = _ptr(x_nodes)
     py, ky = _ptr(y_nodes, out=True)
-    ctx.check(ctx.lib.hm_cavity_jacobian(ctx.h, F.h, LU.h, P.h, _nrhs(T_nodes, P.n_nodes), pT, px, py,
+    ctx.check(ctx.lib.hm_cavity_jacobian(ctx.h, F.h, LU.h, P.h, _nrhs(T_nodes, P.n_nodes, y_nodes), pT, px, py,
                                          _stream(stream, T_nodes, y_nodes)), "hm_cavity_jacobian")
     return y_nodes

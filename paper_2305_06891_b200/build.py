@@ -20,7 +20,10 @@ COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=o
           "-I", os.path.join(os.path.dirname(HERE), "include")]
 # experiment-only engine geometry overrides (e.g. HM_BUILD_DEFINES="HM_PSTAGES=4 HM_STAGE_DOUBLES=5120")
 COMMON += ["-D" + d for d in os.environ.get("HM_BUILD_DEFINES", "").split()]
-SOURCES = ["tree.cpp", "hop.cpp", "api.cpp", "hlu.cpp", "engine.cpp", "shard.cpp",
+# the host H-arithmetic (stage B) is vectorised, FMA-contracted and OpenMP-tasked; its results are
+# compared with tolerances, so contraction is allowed there (reading R22)
+EXTRA = {"hla.cpp": ["-Xcompiler", "-fopenmp,-ffp-contract=fast,-march=x86-64-v3,-mtune=sapphirerapids"]}
+SOURCES = ["tree.cpp", "hop.cpp", "api.cpp", "hlu.cpp", "hla.cpp", "engine.cpp", "shard.cpp",
            "kernels_assembly.cu", "kernels_apply.cu", "kernels_dense.cu", "kernels_engine.cu",
            "kernels_mrhs.cu", "kernels_recompress.cu"]
 
@@ -32,7 +35,7 @@ def _digest() -> str:
         if os.path.isfile(p):
             h.update(f.encode())
             h.update(open(p, "rb").read())
-    h.update(" ".join(ARCH + COMMON).encode())
+    h.update(" ".join(ARCH + COMMON + [str(EXTRA)]).encode())
     return h.hexdigest()
 
 
@@ -45,7 +48,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(BUILD, src + ".o")
-        cmd = [NVCC] + ARCH + COMMON + (["-Xptxas", "-v"] if verbose and src.endswith(".cu") else [])
+        cmd = [NVCC] + ARCH + COMMON + EXTRA.get(src, []) + (["-Xptxas", "-v"] if verbose and src.endswith(".cu") else [])
         if src.endswith(".cpp"):
             cmd += ["-x", "cu"] if False else []
         cmd += ["-c", os.path.join(CSRC, src), "-o", obj]
@@ -59,7 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-Xlinker", "--no-undefined", "-o", tmp] + objs + ["-ldl"]
+    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-Xlinker", "--no-undefined", "-o", tmp] + objs + ["-ldl", "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <memory>
 
+#include "hla.h"
 #include "hm_internal.h"
 
 namespace hm {
@@ -645,6 +646,176 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
 }
 
 void hm_destroy_hmat(hm_hmat* F) { delete F; }
+
+hm_status hm_hmat_from_host(hm_ctx* ctx, const hm_geom* geom, const int32_t* kind, const int32_t* rank,
+                            const int64_t* offset, const double* data, hm_hmat** F_out) {
+    if (!ctx || !geom || !kind || !rank || !offset || !data || !F_out) return HM_ERR_INVALID_ARG;
+    *F_out = nullptr;
+    Ctx* c = &ctx->c;
+    if (!c->host_only) {
+        c->last_error = "hm_hmat_from_host: host-only contexts (device < 0) only";
+        return HM_ERR_UNSUPPORTED;
+    }
+    return guarded(c, [&] {
+        const Geom& g = geom->g;
+        auto* H = new hm_hmat;
+        std::unique_ptr<hm_hmat> guard(H);
+        HMat& F = H->h;
+        F.ctx = c;
+        F.geom = &g;
+        F.params = hm_aca_params{};
+        const size_t nb = g.blocks.size();
+        F.blk_kind.assign(nb, KIND_DENSE);
+        F.blk_rank.assign(nb, 0);
+        F.host_blocks.resize(nb);
+        for (size_t b = 0; b < nb; ++b) {
+            const Blk& B = g.blocks[b];
+            const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+            HostBlock& Hb = F.host_blocks[b];
+            const double* p = data + offset[b];
+            if (kind[b] == 1) {
+                if (!B.adm || rank[b] < 0 || rank[b] > std::min<int64_t>(m, nn))
+                    throw Error(HM_ERR_INVALID_ARG, "block " + std::to_string(b) + ": low rank needs an admissible block and 0 <= k <= min(m, n)");
+                Hb.kind = KIND_LR;
+                Hb.k = rank[b];
+                Hb.U.assign(p, p + m * Hb.k);
+                Hb.V.assign(p + m * Hb.k, p + m * Hb.k + nn * Hb.k);
+                F.blk_kind[b] = KIND_LR;
+                F.blk_rank[b] = Hb.k;
+            } else if (kind[b] == 0) {
+                Hb.kind = KIND_DENSE;
+                Hb.D.assign(p, p + m * nn);
+                F.blk_kind[b] = B.adm ? KIND_ADM_DENSE : KIND_DENSE;
+            } else {
+                throw Error(HM_ERR_INVALID_ARG, "block " + std::to_string(b) + ": kind must be 0 or 1");
+            }
+        }
+        *F_out = guard.release();
+    });
+}
+
+hm_status hm_export_factors(const hm_hmat* Fh, const hm_hlu* LUh, int32_t op, int64_t* n_items, int64_t* n_doubles,
+                            int64_t* meta, double* data) {
+    if (!n_items || !n_doubles || op < 0 || (!Fh && !LUh)) return HM_ERR_INVALID_ARG;
+    Ctx* c = Fh ? Fh->h.ctx : LUh->h.ctx;
+    return guarded(c, [&] {
+        struct Item { int64_t r0, m, c0, n, kind, k; };
+        std::vector<Item> items;
+        const bool fill = meta != nullptr;
+        if (fill && !data) throw Error(HM_ERR_INVALID_ARG, "data is NULL");
+        int64_t nd = 0;
+        auto emit_meta = [&](const Item& it) {
+            if (fill) {
+                int64_t* r = meta + 6 * (int64_t)items.size();
+                r[0] = it.r0; r[1] = it.m; r[2] = it.c0; r[3] = it.n; r[4] = it.kind; r[5] = it.k;
+            }
+            items.push_back(it);
+        };
+        if (c->host_only) {
+            if (op == HM_OP_F) {
+                if (!Fh || Fh->h.host_blocks.empty()) throw Error(HM_ERR_INVALID_ARG, "F holds no host blocks");
+                const Geom& g = *Fh->h.geom;
+                for (size_t b = 0; b < g.blocks.size(); ++b) {
+                    const Blk& B = g.blocks[b];
+                    const HostBlock& H = Fh->h.host_blocks[b];
+                    const int64_t m = B.r1 - B.r0, nn = B.c1 - B.c0;
+                    const bool lr = H.kind == KIND_LR;
+                    emit_meta(Item{B.r0, m, B.c0, nn, lr ? 1 : 0, lr ? H.k : 0});
+                    if (fill) {
+                        if (lr) {
+                            std::copy(H.U.begin(), H.U.end(), data + nd);
+                            std::copy(H.V.begin(), H.V.end(), data + nd + m * H.k);
+                        } else {
+                            std::copy(H.D.begin(), H.D.end(), data + nd);
+                        }
+                    }
+                    nd += lr ? H.k * (m + nn) : m * nn;
+                }
+            } else {
+                if (!LUh || !LUh->h.host_factor) throw Error(HM_ERR_INVALID_ARG, "LU holds no host factors");
+                const HLU& L = LUh->h;
+                const Geom& g = *L.F->geom;
+                const int Lc = L.cut_level;
+                const int side_want = op == HM_OP_LINV ? 1 : op == HM_OP_UINV ? 2 : ((op - 3) % 2 == 0 ? 1 : 2);
+                const int lvl_want = op >= 3 ? (op - 3) / 2 : -1;
+                if (lvl_want >= Lc) throw Error(HM_ERR_INVALID_ARG, "no W blocks at that level (cut level " + std::to_string(Lc) + ")");
+                L.host_factor->visit([&](const hla::LeafView& v) {
+                    const hla::Mat& M = *v.M;
+                    if (v.side == 0) {
+                        if (lvl_want >= 0) return;
+                        const int64_t m = M.m;
+                        emit_meta(Item{M.r0, m, M.c0, m, 0, 0});
+                        if (fill)
+                            for (int64_t j = 0; j < m; ++j)
+                                for (int64_t i = 0; i < m; ++i) {
+                                    const double a = M.D[i + j * m];
+                                    double x = 0.0;
+                                    if (side_want == 1) x = i > j ? a : (i == j ? 1.0 : 0.0);
+                                    else x = i <= j ? a : 0.0;
+                                    data[nd + i + j * m] = x;
+                                }
+                        nd += m * m;
+                        return;
+                    }
+                    if (v.side != side_want) return;
+                    const int lvl = g.nodes[v.node].level;
+                    if (lvl_want >= 0 ? lvl != lvl_want : lvl < Lc) return;
+                    const bool lr = M.type == hla::T_LR;
+                    emit_meta(Item{M.r0, M.m, M.c0, M.n, lr ? 1 : 0, lr ? M.k : 0});
+                    if (fill) {
+                        if (lr) {
+                            std::copy(M.U.begin(), M.U.begin() + M.m * M.k, data + nd);
+                            std::copy(M.V.begin(), M.V.begin() + M.n * M.k, data + nd + M.m * M.k);
+                        } else {
+                            std::copy(M.D.begin(), M.D.end(), data + nd);
+                        }
+                    }
+                    nd += lr ? M.k * (M.m + M.n) : M.m * M.n;
+                });
+            }
+        } else {
+            const HOp* hop = nullptr;
+            if (op == HM_OP_F) {
+                if (!Fh) throw Error(HM_ERR_INVALID_ARG, "F is NULL");
+                hop = &Fh->h.op;
+            } else {
+                if (!LUh) throw Error(HM_ERR_INVALID_ARG, "LU is NULL");
+                const HLU& L = LUh->h;
+                if (op == HM_OP_LINV) hop = &L.leafL;
+                else if (op == HM_OP_UINV) hop = &L.leafU;
+                else {
+                    const int lv = (op - 3) / 2;
+                    if (lv >= L.cut_level) throw Error(HM_ERR_INVALID_ARG, "no W blocks at that level");
+                    hop = (op - 3) % 2 == 0 ? &L.fwd[lv] : &L.bwd[lv];
+                }
+            }
+            int64_t tot = 0;
+            std::vector<int64_t> at(hop->items.size());
+            for (size_t q = 0; q < hop->items.size(); ++q) {
+                const HOp::ItemRec& it = hop->items[q];
+                const bool lr = it.v_off >= 0;
+                emit_meta(Item{it.r0, it.m, it.c0, it.ncols, lr ? 1 : 0, lr ? it.k : 0});
+                at[q] = tot;
+                tot += lr ? it.k * (it.m + it.ncols) : it.m * it.ncols;
+            }
+            nd = tot;
+            if (fill)
+                read_items(c, *hop, [](size_t) { return true; }, [&](size_t q, const double* pay, const double* V) {
+                    const HOp::ItemRec& it = hop->items[q];
+                    const bool lr = it.v_off >= 0;
+                    double* dst = data + at[q];
+                    if (lr) {
+                        std::copy(pay, pay + it.m * it.k, dst);
+                        if (it.k > 0) std::copy(V, V + it.ncols * it.k, dst + it.m * it.k);
+                    } else {
+                        std::copy(pay, pay + it.m * it.ncols, dst);
+                    }
+                });
+        }
+        *n_items = (int64_t)items.size();
+        *n_doubles = nd;
+    });
+}
 
 hm_status hm_export_row_sums(const hm_hmat* F, double* s, double* c) {
     if (!F) return HM_ERR_INVALID_ARG;

@@ -1,15 +1,18 @@
 // One-time factorisation of C = I - Lambda F and the level-scheduled
 // substitution that applies C^-1, DESIGN.md §"Solve in level form".
 //
-// Factorisation ("stage A", n up to ~1e5 on one B200): C is expanded from the H-format F
-// (PAPER.md:747), then the paper's 4-step block LU recursion runs over the
-// cluster tree on the FP64 tensor pipe, carrying the triangular inverses along:
-//     L11 U11 = C11 (recursive); U12 = L11^-1 C12; L21 = C21 U11^-1; L22 U22 = C22 - L21 U12.
-// At every tree node t it forms the level-form blocks
+// Two factorisations produce the same factor set (the forms of reading R27):
+//  * stage B (default, hla.cpp, reading R33): hierarchical arithmetic on C's blocks in F's
+//    partition -- the paper's 4-step recursion with recursive substitutions and block products,
+//    every low-rank sum truncated at eps_LU; any n.  C's blocks are read back
+//    from F's arena (C = I - Lambda F block by block), factored on the host (OpenMP
+//    tasks over independent blocks) and the solve-form blocks uploaded for the packer.
+//  * stage A (method 1, n up to ~1e5): C expanded dense on the GPU, the same recursion on dense
+//    tiles with FP64 DMMA carrying the triangular inverses, then truncation block by block in F's
+//    partition by cross approximation with full pivoting.
+// Both give, per internal node t above the cut level,
 //     W^L_t = L21 L11^-1      W^U_t = U12 U22^-1
-// and truncates them to eps_LU block by block in the block partition of F, by
-// cross approximation with full pivoting and an exact Frobenius stop test.  Leaf blocks keep
-// dense L_rr^-1 and U_rr^-1.
+// and below it the inverse factors of the cut-level diagonal blocks (cut 0: L^-1 and U^-1).
 //
 // Solve: for levels top-down  b_t2 -= W^L_t b_t1   (one two-phase launch pair per level),
 //        leaves              y_r  = L_rr^-1 b_r,
@@ -19,9 +22,14 @@
 // all nodes of a level are independent.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
+#include <unordered_map>
+
+#include "hla.h"
 #include "hm_internal.h"
 
 namespace hm {
@@ -219,29 +227,18 @@ struct Factorizer {
     }
 };
 
-void account(HLU& L, const HOp& op) {
-    L.bytes += op.p1_doubles() + op.p2_doubles();
-    L.n_blocks += op.n_lr + op.n_dense;
-    L.n_lr += op.n_lr;
-    L.rank_sum += op.rank_sum;
-    L.rank_max = std::max(L.rank_max, op.rank_max);
-}
+// The blocks of the solve forms (reading R27), as sources for the operator builder.
+struct FactorSet {
+    std::vector<std::vector<SrcBlock>> fwd, bwd;   // W^L_t / W^U_t blocks per tree level < cut
+    std::vector<SrcBlock> srcL, srcU;              // inverse factors of the cut-level diagonal blocks
+    std::vector<DBuf<double>> staging;             // device payload the sources point into
+};
 
-}  // namespace
-
-void factor_hlu(HLU& L, const double* emissivity) {
-    const HMat& F = *L.F;
-    const Geom& g = *F.geom;
+// ---- stage A: dense tiles on the GPU (reading R28)
+void stage_a(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& lam, int Lc, FactorSet& out) {
     Ctx* c = L.ctx;
     const cudaStream_t s = c->stream;
     const int64_t n = g.n;
-    std::vector<double> eps_int(n), lam(n);
-    for (int64_t i = 0; i < n; ++i) {
-        const double e = emissivity[g.perm[i]];
-        if (!(e > 0.0 && e <= 1.0)) throw Error(HM_ERR_INVALID_ARG, "emissivity of facet " + std::to_string(g.perm[i]) + " not in (0, 1]");
-        eps_int[i] = e;
-        lam[i] = (1.0 - e) / g.area[i];  // Lambda_ii = (1 - eps_i) / A_i (eq:reflection_matrix)
-    }
     const int64_t half = (n + 1) / 2;
     const int64_t maxT = std::max<int64_t>(half * (n - half), 1);
     const double need = 8.0 * (2.0 * n * n + maxT) * 1.25;
@@ -250,8 +247,6 @@ void factor_hlu(HLU& L, const double* emissivity) {
     if (need > (double)freeb)
         throw Error(HM_ERR_UNSUPPORTED, "dense-stage H-LU needs ~" + std::to_string((int64_t)(need / 1e9)) +
                                             " GB of device memory (" + std::to_string((int64_t)(freeb / 1e9)) + " GB free)");
-    L.eps_int.upload(c, eps_int, "eps", s);
-    L.eps_ext.upload(c, std::vector<double>(emissivity, emissivity + n), "eps (external)", s);
     DBuf<double> dlam, dM, dMinv, dT;
     DBuf<int32_t> derr;
     dlam.upload(c, lam, "lambda", s);
@@ -285,13 +280,6 @@ void factor_hlu(HLU& L, const double* emissivity) {
     fz.T = dT.p;
     fz.err = derr.p;
     fz.collect();
-    const int D = g.depth;
-    // cut level: W-form updates for levels < Lc, then block-diagonal solves with the inverse
-    // factors of the level-Lc diagonal blocks (Lc = depth: leaf inverses only)
-    // cut level (reading R27): < 0 -> 0 (the default: U^-1 (L^-1 b) with the inverse factors
-    // in F's partition, fewest dependent passes, measured fastest on C2); >= depth -> pure level form
-    const int Lc = L.params.cut_level < 0 ? 0 : std::min(L.params.cut_level, D);
-    L.cut_level = Lc;
     fz.cut = Lc;
     fz.fwd_src.assign(std::max(Lc, 0), {});
     fz.bwd_src.assign(std::max(Lc, 0), {});
@@ -319,7 +307,6 @@ void factor_hlu(HLU& L, const double* emissivity) {
     DBuf<double> dLi, dUi;
     dLi.alloc(c, (size_t)leaf_tot, "leaf L^-1");
     dUi.alloc(c, (size_t)leaf_tot, "leaf U^-1");
-    std::vector<SrcBlock> srcL, srcU;
     int64_t off = 0;
     for (int l : g.leaves) {
         const Node& N = g.nodes[l];
@@ -332,9 +319,9 @@ void factor_hlu(HLU& L, const double* emissivity) {
         S.d_rs = m;
         S.d_cs = 1;
         S.dense = dLi.p + off;
-        srcL.push_back(S);
+        out.srcL.push_back(S);
         S.dense = dUi.p + off;
-        srcU.push_back(S);
+        out.srcU.push_back(S);
         off += m * m;
     }
     HM_CUDA(cudaStreamSynchronize(s));
@@ -348,22 +335,333 @@ void factor_hlu(HLU& L, const double* emissivity) {
             st.pop_back();
             const Node& N = g.nodes[t];
             if (N.is_leaf()) continue;
-            fz.stage_dense(fz.lower[t], 0, 0, n, srcL);
-            fz.stage_dense(fz.upper[t], 0, 0, n, srcU);
-            fz.compress(fz.lower[t], 0, 0, n, srcL);
-            fz.compress(fz.upper[t], 0, 0, n, srcU);
+            fz.stage_dense(fz.lower[t], 0, 0, n, out.srcL);
+            fz.stage_dense(fz.upper[t], 0, 0, n, out.srcU);
+            fz.compress(fz.lower[t], 0, 0, n, out.srcL);
+            fz.compress(fz.upper[t], 0, 0, n, out.srcU);
             st.push_back(N.child[0]);
             st.push_back(N.child[1]);
         }
     }
     HM_CUDA(cudaStreamSynchronize(s));
     L.setup_seconds[1] = now_seconds() - t0;
+    out.fwd = std::move(fz.fwd_src);
+    out.bwd = std::move(fz.bwd_src);
+    for (auto& b : fz.staging) out.staging.push_back(std::move(b));
+    out.staging.push_back(std::move(dLi));
+    out.staging.push_back(std::move(dUi));
+}
+
+}  // namespace
+
+// ---- reading an operator's payload back from its arena (stage B input, hm_export_factors)
+// For every phase-2 item (a leaf-row slice of a block): its payload (dense m x ncols, or the U slice
+// m x k, column-major) and, when want_v(item) is true and the item is low rank, the block's V
+// (ncols x k, column-major), staged through the device in batches of <= 64 Mi doubles.
+void read_items(Ctx* c, const HOp& op, const std::function<bool(size_t)>& want_v,
+                const std::function<void(size_t, const double*, const double*)>& fn) {
+    const cudaStream_t s = c->stream;
+    const int64_t budget = int64_t(1) << 26;
+    const size_t ni = op.items.size();
+    size_t i0 = 0;
+    DBuf<double> stage;
+    std::vector<double> host;
+    while (i0 < ni) {
+        std::vector<int64_t> tasks;
+        std::vector<int64_t> po, vo;
+        int64_t tot = 0;
+        size_t i1 = i0;
+        for (; i1 < ni; ++i1) {
+            const HOp::ItemRec& it = op.items[i1];
+            const bool lr = it.v_off >= 0;
+            const int64_t cols = lr ? it.k : it.ncols;
+            const bool wv = lr && it.k > 0 && want_v(i1);
+            const int64_t need = it.m * cols + (wv ? it.ncols * it.k : 0);
+            if (i1 > i0 && tot + need > budget) break;
+            po.push_back(tot);
+            if (it.m * cols > 0)
+                tasks.insert(tasks.end(), {tot, (int64_t)(uintptr_t)(op.arena.p + it.a_off), it.m, cols, 1, it.a_ld, it.m});
+            tot += it.m * cols;
+            vo.push_back(wv ? tot : -1);
+            if (wv) {
+                tasks.insert(tasks.end(), {tot, (int64_t)(uintptr_t)(op.arena.p + it.v_off), it.ncols, it.k, it.v_ld, 1, it.ncols});
+                tot += it.ncols * it.k;
+            }
+        }
+        if ((int64_t)stage.n < std::max<int64_t>(tot, 2)) stage.alloc(c, (size_t)std::max<int64_t>(tot, 2), "read-back staging");
+        if (!tasks.empty()) {
+            DBuf<int64_t> d;
+            d.upload(c, tasks, "read-back tasks", s);
+            k::pack(d.p, (int)(tasks.size() / 7), stage.p, s);
+        }
+        host.resize((size_t)std::max<int64_t>(tot, 1));
+        if (tot > 0) HM_CUDA(cudaMemcpyAsync(host.data(), stage.p, (size_t)tot * sizeof(double), cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        for (size_t q = i0; q < i1; ++q)
+            fn(q, host.data() + po[q - i0], vo[q - i0] >= 0 ? host.data() + vo[q - i0] : nullptr);
+        i0 = i1;
+    }
+}
+
+// geom block of every phase-2 item of an operator built in F's partition (block = the one whose
+// rows contain the item's rows and whose first column is the item's)
+std::vector<int> item_blocks(const Geom& g, const HOp& op) {
+    std::unordered_map<int64_t, int> key;
+    key.reserve(op.items.size() * 2);
+    for (size_t b = 0; b < g.blocks.size(); ++b) {
+        const Blk& B = g.blocks[b];
+        const int l0 = g.leaf_of(B.r0), l1 = g.leaf_of(B.r1 - 1);
+        for (int l = l0; l <= l1; ++l) key[((int64_t)l << 32) | B.c0] = (int)b;
+    }
+    std::vector<int> out(op.items.size(), -1);
+    for (size_t q = 0; q < op.items.size(); ++q) {
+        const HOp::ItemRec& it = op.items[q];
+        auto f = key.find(((int64_t)g.leaf_of(it.r0) << 32) | it.c0);
+        if (f == key.end()) throw Error(HM_ERR_CUDA, "operator item outside F's partition");
+        out[q] = f->second;
+    }
+    return out;
+}
+
+namespace {
+
+// ---- stage B: hierarchical arithmetic (reading R33)
+void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& lam, int Lc, FactorSet& out) {
+    Ctx* c = L.ctx;
+    const double eps = L.params.eps_lu;
+    double t0 = now_seconds();
+    std::vector<std::pair<int, int>> lb(g.blocks.size());
+    for (size_t b = 0; b < g.blocks.size(); ++b) lb[b] = {g.blocks[b].rnode, g.blocks[b].cnode};
+    auto hf = std::make_shared<hla::HFactor>(g.nodes, lb);
+    // C = I - Lambda F block by block: rows scaled by -lambda_i, identity on the
+    // diagonal leaves
+    auto to_C = [&](int b) {
+        const Blk& B = g.blocks[b];
+        hla::Mat& M = hf->leaf(b);
+        const int64_t m = M.m, nn = M.n;
+        if (M.type == hla::T_LR) {
+            for (int l = 0; l < M.k; ++l)
+                for (int64_t i = 0; i < m; ++i) M.U[i + l * m] *= -lam[B.r0 + i];
+        } else {
+            for (int64_t j = 0; j < nn; ++j)
+                for (int64_t i = 0; i < m; ++i) M.D[i + j * m] *= -lam[B.r0 + i];
+            if (B.rnode == B.cnode)
+                for (int64_t i = 0; i < m; ++i) M.D[i + i * m] += 1.0;
+        }
+    };
+    if (c->host_only) {
+        if (F.host_blocks.size() != g.blocks.size()) throw Error(HM_ERR_NOT_READY, "F holds no host blocks");
+        for (size_t b = 0; b < g.blocks.size(); ++b) {
+            const HostBlock& H = F.host_blocks[b];
+            hla::Mat& M = hf->leaf((int)b);
+            if (H.kind == KIND_LR) {
+                M.type = hla::T_LR;
+                M.k = H.k;
+                M.U = H.U;
+                M.V = H.V;
+            } else {
+                M.type = hla::T_DENSE;
+                M.D = H.D;
+            }
+            to_C((int)b);
+        }
+    } else {
+        const std::vector<int> ib = item_blocks(g, F.op);
+        for (size_t b = 0; b < g.blocks.size(); ++b) {
+            hla::Mat& M = hf->leaf((int)b);
+            if (F.blk_kind[b] == KIND_LR) {
+                M.type = hla::T_LR;
+                M.k = F.blk_rank[b];
+                M.U.assign((size_t)(M.m * M.k), 0.0);
+                M.V.assign((size_t)(M.n * M.k), 0.0);
+            } else {
+                M.type = hla::T_DENSE;
+                M.D.assign((size_t)(M.m * M.n), 0.0);
+            }
+        }
+        read_items(
+            c, F.op, [&](size_t q) { return F.op.items[q].r0 == g.blocks[ib[q]].r0; },
+            [&](size_t q, const double* pay, const double* V) {
+                const HOp::ItemRec& it = F.op.items[q];
+                const Blk& B = g.blocks[ib[q]];
+                hla::Mat& M = hf->leaf(ib[q]);
+                const int64_t ro = it.r0 - B.r0;
+                if (M.type == hla::T_LR) {
+                    for (int l = 0; l < M.k; ++l)
+                        std::copy(pay + l * it.m, pay + (l + 1) * it.m, M.U.begin() + l * M.m + ro);
+                    if (V) std::copy(V, V + M.n * M.k, M.V.begin());
+                } else {
+                    for (int64_t j = 0; j < M.n; ++j)
+                        std::copy(pay + j * it.m, pay + (j + 1) * it.m, M.D.begin() + j * M.m + ro);
+                }
+            });
+        for (size_t b = 0; b < g.blocks.size(); ++b) to_C((int)b);
+    }
+    L.setup_seconds[0] = now_seconds() - t0;
+
+    t0 = now_seconds();
+    hf->normalize(eps);
+    hf->factor(eps);
+    if (hf->singular())
+        throw Error(HM_ERR_SINGULAR, "near-zero pivot (|pivot| <= 1e-14 max|block|) in the leaf LU of C at internal " +
+                                         hf->singular_where());
+    hf->solve_form(Lc, eps);
+    if (getenv("HM_HLU_VERBOSE")) {
+        const hla::Stats& st = hf->stats();
+        fprintf(stderr, "[hm] stage-B H-LU n=%lld threads=%d: read %.3f s, lu %.3f s, form %.3f s, %lld truncations "
+                        "(mean rank in %.2f, out %.2f)\n",
+                (long long)g.n, hf->threads(), L.setup_seconds[0], st.seconds_lu, st.seconds_form,
+                (long long)st.truncations, st.truncations ? (double)st.trunc_rank_in / st.truncations : 0.0,
+                st.truncations ? (double)st.trunc_rank_out / st.truncations : 0.0);
+        hla::prof_dump();
+    }
+    L.hlu_truncations = hf->stats().truncations;
+    L.hlu_threads = hf->threads();
+    L.setup_seconds[1] = now_seconds() - t0;
+    if (c->host_only) {
+        L.host_factor = hf;
+        return;
+    }
+
+    // ---- upload the solve-form blocks (host chunks of <= 32 Mi doubles)
+    t0 = now_seconds();
+    out.fwd.assign(std::max(Lc, 0), {});
+    out.bwd.assign(std::max(Lc, 0), {});
+    int64_t total = 0;
+    auto dense_out = [](const hla::Mat& M) { return M.type != hla::T_LR || (int64_t)M.k * (M.m + M.n) >= M.m * M.n; };
+    hf->visit([&](const hla::LeafView& v) {
+        const hla::Mat& M = *v.M;
+        if (v.side == 0) total += 2 * M.m * M.m;
+        else if (dense_out(M)) total += M.m * M.n;
+        else total += M.k * (M.m + M.n);
+    });
+    DBuf<double> dev;
+    dev.alloc(c, (size_t)std::max<int64_t>(total, 2), "H-LU factor blocks");
+    const cudaStream_t s = c->stream;
+    const int64_t chunk = int64_t(1) << 25;
+    std::vector<double> hbuf;
+    hbuf.reserve((size_t)std::min<int64_t>(chunk, std::max<int64_t>(total, 1)));
+    int64_t flushed = 0;
+    auto flush = [&]() {
+        if (hbuf.empty()) return;
+        HM_CUDA(cudaMemcpy(dev.p + flushed, hbuf.data(), hbuf.size() * sizeof(double), cudaMemcpyHostToDevice));
+        flushed += (int64_t)hbuf.size();
+        hbuf.clear();
+    };
+    auto put = [&](const double* p, int64_t cnt) -> double* {   // device address of the copy
+        double* at = dev.p + flushed + (int64_t)hbuf.size();
+        if ((int64_t)hbuf.size() + cnt > chunk) {
+            flush();
+            at = dev.p + flushed;
+        }
+        if (cnt > chunk) {   // larger than a chunk: straight copy
+            HM_CUDA(cudaMemcpy(dev.p + flushed, p, (size_t)cnt * sizeof(double), cudaMemcpyHostToDevice));
+            flushed += cnt;
+            return at;
+        }
+        hbuf.insert(hbuf.end(), p, p + cnt);
+        return at;
+    };
+    hf->visit([&](const hla::LeafView& v) {
+        const hla::Mat& M = *v.M;
+        SrcBlock S;
+        S.r0 = M.r0; S.m = M.m; S.c0 = M.c0; S.n = M.n;
+        if (v.side == 0) {   // packed leaf inverses -> unit-lower L_rr^-1 and upper U_rr^-1, column-major
+            const int64_t m = M.m;
+            std::vector<double> Li((size_t)(m * m), 0.0), Ui((size_t)(m * m), 0.0);
+            for (int64_t j = 0; j < m; ++j)
+                for (int64_t i = 0; i < m; ++i) {
+                    const double a = M.D[i + j * m];
+                    if (i > j) Li[i + j * m] = a;
+                    else Ui[i + j * m] = a;
+                    if (i == j) Li[i + j * m] = 1.0;
+                }
+            S.kind = KIND_DENSE;
+            S.d_rs = 1;
+            S.d_cs = m;
+            S.dense = put(Li.data(), m * m);
+            out.srcL.push_back(S);
+            S.dense = put(Ui.data(), m * m);
+            out.srcU.push_back(S);
+            return;
+        }
+        if (dense_out(M)) {
+            S.kind = KIND_DENSE;
+            S.d_rs = 1;
+            S.d_cs = M.m;
+            if (M.type == hla::T_LR) {
+                std::vector<double> D((size_t)(M.m * M.n), 0.0);
+                for (int l = 0; l < M.k; ++l)
+                    for (int64_t j = 0; j < M.n; ++j) {
+                        const double vj = M.V[j + l * M.n];
+                        for (int64_t i = 0; i < M.m; ++i) D[i + j * M.m] += M.U[i + l * M.m] * vj;
+                    }
+                S.dense = put(D.data(), M.m * M.n);
+            } else {
+                S.dense = put(M.D.data(), M.m * M.n);
+            }
+        } else {
+            S.kind = KIND_LR;
+            S.k = M.k;
+            S.u_ld = M.m;
+            S.v_ld = M.n;
+            S.U = put(M.U.data(), M.m * M.k);
+            S.V = put(M.V.data(), M.n * M.k);
+        }
+        const int lvl = g.nodes[v.node].level;
+        if (lvl < Lc) (v.side == 1 ? out.fwd[lvl] : out.bwd[lvl]).push_back(S);
+        else (v.side == 1 ? out.srcL : out.srcU).push_back(S);
+    });
+    flush();
+    HM_CUDA(cudaStreamSynchronize(s));
+    out.staging.push_back(std::move(dev));
+    L.setup_seconds[2] = now_seconds() - t0;
+}
+
+void account(HLU& L, const HOp& op) {
+    L.bytes += op.p1_doubles() + op.p2_doubles();
+    L.n_blocks += op.n_lr + op.n_dense;
+    L.n_lr += op.n_lr;
+    L.rank_sum += op.rank_sum;
+    L.rank_max = std::max(L.rank_max, op.rank_max);
+}
+
+}  // namespace
+
+void factor_hlu(HLU& L, const double* emissivity) {
+    const HMat& F = *L.F;
+    const Geom& g = *F.geom;
+    Ctx* c = L.ctx;
+    const cudaStream_t s = c->stream;
+    const int64_t n = g.n;
+    std::vector<double> eps_int(n), lam(n);
+    for (int64_t i = 0; i < n; ++i) {
+        const double e = emissivity[g.perm[i]];
+        if (!(e > 0.0 && e <= 1.0)) throw Error(HM_ERR_INVALID_ARG, "emissivity of facet " + std::to_string(g.perm[i]) + " not in (0, 1]");
+        eps_int[i] = e;
+        lam[i] = (1.0 - e) / g.area[i];  // Lambda_ii = (1 - eps_i) / A_i (eq:reflection_matrix)
+    }
+    if (!(L.params.eps_lu > 0.0 && L.params.eps_lu < 1.0)) throw Error(HM_ERR_INVALID_ARG, "eps_lu must be in (0, 1)");
+    const int D = g.depth;
+    // cut level (reading R27): W-form updates for levels < Lc, then block-diagonal solves with
+    // the inverse factors of the level-Lc diagonal blocks.  < 0 -> 0 (the default: U^-1 (L^-1 b) with
+    // the inverse factors in F's partition, fewest dependent passes, measured fastest on C2);
+    // >= depth -> pure level form (leaf inverses only)
+    const int Lc = L.params.cut_level < 0 ? 0 : std::min(L.params.cut_level, D);
+    L.cut_level = Lc;
+    FactorSet fs;
+    if (L.params.method == 1) {
+        if (c->host_only) throw Error(HM_ERR_UNSUPPORTED, "the dense stage-A factorisation needs a device");
+        stage_a(L, F, g, lam, Lc, fs);
+    } else {
+        stage_b(L, F, g, lam, Lc, fs);
+    }
+    if (c->host_only) return;   // factors kept on the host for hm_export_factors
+    L.eps_int.upload(c, eps_int, "eps", s);
+    L.eps_ext.upload(c, std::vector<double>(emissivity, emissivity + n), "eps (external)", s);
 
     // ---- pack the level-form operators
-    t0 = now_seconds();
-    dM.reset();
-    dMinv.reset();
-    dT.reset();
+    double t0 = now_seconds();
     L.fwd.resize(std::max(Lc, 0));
     L.bwd.resize(std::max(Lc, 0));
     L.bytes = L.bytes_leaf = L.n_blocks = L.n_lr = L.rank_sum = 0;
@@ -372,8 +670,8 @@ void factor_hlu(HLU& L, const double* emissivity) {
     // backward levels then leafU)
     int64_t tA = 0, tB = 0;
     for (int lv = 0; lv < Lc; ++lv) {
-        build_hop(c, g, fz.fwd_src[lv], L.fwd[lv], s, nullptr, tA);
-        build_hop(c, g, fz.bwd_src[lv], L.bwd[lv], s, nullptr, tB);
+        build_hop(c, g, fs.fwd[lv], L.fwd[lv], s, nullptr, tA);
+        build_hop(c, g, fs.bwd[lv], L.bwd[lv], s, nullptr, tB);
         account(L, L.fwd[lv]);
         account(L, L.bwd[lv]);
         tA += L.fwd[lv].n_t;
@@ -383,8 +681,8 @@ void factor_hlu(HLU& L, const double* emissivity) {
         L.leafL.p2_by_row = true;
         L.leafU.p1_by_key = L.leafU.p2_by_row = true;
     }
-    build_hop(c, g, srcL, L.leafL, s, nullptr, tA);
-    build_hop(c, g, srcU, L.leafU, s, nullptr, tB);
+    build_hop(c, g, fs.srcL, L.leafL, s, nullptr, tA);
+    build_hop(c, g, fs.srcU, L.leafU, s, nullptr, tB);
     tA += L.leafL.n_t;
     tB += L.leafU.n_t;
     int64_t tA_loc = 0, tB_loc = 0;
@@ -392,24 +690,24 @@ void factor_hlu(HLU& L, const double* emissivity) {
         L.fwd_loc.resize(std::max(Lc, 0));
         L.bwd_loc.resize(std::max(Lc, 0));
         for (int lv = 0; lv < Lc; ++lv) {
-            build_hop(c, g, fz.fwd_src[lv], L.fwd_loc[lv], s, &g.shard, tA_loc);
-            build_hop(c, g, fz.bwd_src[lv], L.bwd_loc[lv], s, &g.shard, tB_loc);
+            build_hop(c, g, fs.fwd[lv], L.fwd_loc[lv], s, &g.shard, tA_loc);
+            build_hop(c, g, fs.bwd[lv], L.bwd_loc[lv], s, &g.shard, tB_loc);
             tA_loc += L.fwd_loc[lv].n_t;
             tB_loc += L.bwd_loc[lv].n_t;
         }
-        build_hop(c, g, srcL, L.leafL_loc, s, &g.shard, tA_loc);
-        build_hop(c, g, srcU, L.leafU_loc, s, &g.shard, tB_loc);
+        build_hop(c, g, fs.srcL, L.leafL_loc, s, &g.shard, tA_loc);
+        build_hop(c, g, fs.srcU, L.leafU_loc, s, &g.shard, tB_loc);
         tA_loc += L.leafL_loc.n_t;
         tB_loc += L.leafU_loc.n_t;
     }
     account(L, L.leafL);
     account(L, L.leafU);
     L.bytes_leaf = L.leafL.p1_doubles() + L.leafL.p2_doubles() + L.leafU.p1_doubles() + L.leafU.p2_doubles();
-    fz.staging.clear();
+    fs.staging.clear();
     L.xtA.alloc(c, (size_t)(n + tA), "solve xtA");
     L.xtB.alloc(c, (size_t)(n + tB), "solve xtB");
     L.z.alloc(c, (size_t)n, "solve z");
-    L.setup_seconds[2] = now_seconds() - t0;
+    L.setup_seconds[2] += now_seconds() - t0;
 
     // ---- hot-path programs for the persistent engine (tree dependencies within each sweep)
     HMat& Fm = const_cast<HMat&>(F);
@@ -718,6 +1016,8 @@ hm_status hm_factor_hlu(hm_ctx* ctx, const hm_hmat* F, const double* emissivity,
         H->h.F = &F->h;
         H->h.params.eps_lu = (params && params->eps_lu > 0.0) ? params->eps_lu : F->h.params.eps_aca;
         H->h.params.cut_level = params ? params->cut_level : -1;
+        H->h.params.method = params ? params->method : 0;
+        if (H->h.params.method != 0 && H->h.params.method != 1) throw Error(HM_ERR_INVALID_ARG, "method must be 0 or 1");
         factor_hlu(H->h, emissivity);
         *out = guard.release();
         return HM_OK;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -434,10 +435,20 @@ struct FluxEpi {  // OUT_FLUX: q_ext[perm[i]] = sigma * eps_i / A_i * (acc - eta
     int col;   // column of the external arrays
 };
 
+namespace hla { class HFactor; }
+
+// A block payload held on the host (host-only contexts: hm_hmat_from_host).
+struct HostBlock {
+    int kind = KIND_DENSE;   // KIND_DENSE: D column-major m x n; KIND_LR: U (m x k), V (n x k) column-major
+    int k = 0;
+    std::vector<double> D, U, V;
+};
+
 struct HMat {
     Ctx* ctx;
     const Geom* geom;
     hm_aca_params params;
+    std::vector<HostBlock> host_blocks;   // host-only contexts: the caller's F, per geom block
     HOp op;
     std::vector<double> s_ext, c_ext;  // row sums / clamped (external order)
     std::vector<int> blk_kind, blk_rank;  // per geom block
@@ -465,6 +476,9 @@ struct HLU {
     Ctx* ctx;
     const HMat* F;
     hm_lu_params params;
+    std::shared_ptr<hla::HFactor> host_factor;   // host-only contexts: the factors in solve form
+    int64_t hlu_truncations = 0;                 // stage B statistics (hm_storage_report)
+    double hlu_threads = 0;
     std::vector<HOp> fwd, bwd;   // per level above the cut (may be empty ops)
     HOp leafL, leafU;            // block-diagonal inverse factors of the cut-level diagonal blocks
     int cut_level = 0;
@@ -545,6 +559,14 @@ void cpaca_batch(double* T, int64_t ldt, const int64_t* blk /*[nb][7] i0,m,j0,n,
 }  // namespace k
 
 double now_seconds();
+
+// Read an operator's phase-2 items back from its arena (hlu.cpp): fn(item, payload, V) with the
+// item's payload (dense m x ncols or U slice m x k, column-major) and, for low-rank items with
+// want_v(item), the block's V (ncols x k column-major; else nullptr).  Synchronous.
+void read_items(Ctx* c, const HOp& op, const std::function<bool(size_t)>& want_v,
+                const std::function<void(size_t, const double*, const double*)>& fn);
+// geom block index of every phase-2 item of an operator built in F's partition
+std::vector<int> item_blocks(const Geom& g, const HOp& op);
 
 // hot-path launches for one column (api.cpp): world == 1 -> one engine program; sharded -> the
 // segmented program with its exchange steps
