@@ -46,35 +46,57 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle reasons sampled DURING the timed region (B200_PROFILING.md clocks line):
+    NVML polled every ~0.5 ms from a thread (the timed region can be a few ms), nvidia-smi -lms 50 if
+    NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []       # (t, sm_mhz, reason_bits)
+        self.max_mhz = None
+        self.window = [None, None]
+        self._stop = threading.Event()
+        self._nv = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-            t0 = time.time()
-            while not self.lines and time.time() - t0 < 10:   # sampler up before the timed region
-                time.sleep(0.01)
-        except Exception:
-            self.proc = None
-        self.window = [None, None]
-        return self
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
 
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append((time.time(), ln.strip()))
+            def poll():
+                while not self._stop.is_set():
+                    self.samples.append((time.time(), float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                         int(reasons(h))))
+                    time.sleep(0.0005)
+            self._nv = "nvml"
+        except Exception:
+            def poll():
+                proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                                         "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "50"],
+                                        stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                for ln in proc.stdout:
+                    if self._stop.is_set():
+                        break
+                    p = [x.strip() for x in ln.split(",")]
+                    try:
+                        self.max_mhz = float(p[1])
+                        self.samples.append((time.time(), float(p[0]), int(p[2], 16)))
+                    except (ValueError, IndexError):
+                        continue
+                proc.terminate()
+            self._nv = "nvidia-smi"
+        self.t = threading.Thread(target=poll, daemon=True)
+        self.t.start()
+        t0 = time.time()
+        while not self.samples and time.time() - t0 < 10:   # sampler up before the timed region
+            time.sleep(0.001)
+        return self
 
     def start(self):
         self.window[0] = time.time()
@@ -83,83 +105,124 @@ class Clocks:
         self.window[1] = time.time()
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         lo, hi = self.window
-        inside = [ln for t, ln in self.lines if lo is not None and hi is not None and lo <= t <= hi]
-        for ln in inside:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 6:
-                continue
-            try:
-                sm.append(float(p[0]))
-                mx = max(mx, float(p[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[2:6]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        inside = [(mhz, bits) for t, mhz, bits in self.samples if lo is not None and hi is not None and lo <= t <= hi]
+        reasons = sorted(nm for nm, bit in self.REASONS.items() if any(b & bit for _, b in inside))
+        sm = [mhz for mhz, _ in inside]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "source": self._nv}
 
 
-def cpu_baseline(cfg, budget_rows=256, sub_n=4096):
-    """The oracle as it stands on the host cores, on a bounded sample of the C2 step:
-    (i) oracle matrix-free F x (direct kernel summation) on `budget_rows` seeded rows, scaled
-    by n/rows; (ii) oracle C^-1 b (dense LAPACK gesv, as oracle.viewfactor.solve does every
-    call) on the leading sub_n x sub_n principal block of C, scaled by (n/sub_n)^3."""
-    import synth
+def host_info():
+    """CPU model, sockets, cores this process may use, RAM (record the host)."""
+    model, sockets = None, set()
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name") and model is None:
+                model = ln.split(":", 1)[1].strip()
+            if ln.startswith("physical id"):
+                sockets.add(ln.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    ram = None
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                ram = round(int(ln.split()[1]) / 1e6, 1)
+    except OSError:
+        pass
+    return {"cpu_model": model, "sockets": max(1, len(sockets)), "cores": len(os.sched_getaffinity(0)),
+            "ram_gb": ram}
+
+
+def cpu_dense_apply(cfg, steps, m=None, threads=None):
+    """The oracle as it stands on the host cores, SURVEY.md §8(d) CPU protocol: (i) dense F assembly
+    (oracle.viewfactor.dense_F / reflection_matrix), (iii) the dense LU once (lu_factor, LAPACK getrf),
+    then per apply (ii) the stored dense F x and (iv) the LU solve with the precomputed factors
+    (lu_factor_solve, getrs); (v) = (ii) + (iv) is one H-apply's dense counterpart.  m < n: the leading
+    m x m principal block stands in, and (ii), (iv) -- both stream n^2 doubles -- are scaled by (n/m)^2
+    (no cubic extrapolation; (i) and (iii) are reported for the sample as measured)."""
     from oracle import viewfactor as vf
     f = cfg.facets
     n = f.n
-    rows = synth.sample_rows(synth.stream_seed(cfg.seed, 999), n, budget_rows)
-    x = cfg.rhs()
-    t0 = time.perf_counter()
-    vf.sampled_apply(f.centroid, f.normal, f.area, rows, x)
-    t_fx = (time.perf_counter() - t0) * n / len(rows)
-    m = min(sub_n, n)
-    idx = np.arange(m)
-    I, J = np.meshgrid(idx, idx, indexing="ij")
-    Fs = vf.entry_pairs(f.centroid, f.normal, f.area, I.ravel(), J.ravel()).reshape(m, m)
-    Cs = vf.reflection_matrix(Fs, f.area[:m], cfg.emissivity[:m])
-    t0 = time.perf_counter()
-    vf.solve(Cs, x[:m, 0])
-    t_solve = (time.perf_counter() - t0) * (n / m) ** 3
-    step = t_fx + t_solve
-    return {"value": 1.0 / step, "unit": "applies/s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": (f"oracle F x by direct summation on {len(rows)} seeded rows (x n/{len(rows)}) + "
-                       f"oracle dense gesv C^-1 b on the leading {m}x{m} block of C (x (n/{m})^3); "
-                       f"per-step estimate {step:.2f} s")}
+    m = min(m or n, n)
+    ctl = None
+    if threads:
+        from threadpoolctl import threadpool_limits
+        ctl = threadpool_limits(threads)
+    try:
+        t0 = time.perf_counter()
+        Fd = vf.dense_F(f.centroid[:m], f.normal[:m], f.area[:m])
+        Cd = vf.reflection_matrix(Fd, f.area[:m], cfg.emissivity[:m])
+        t_asm = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        fac = vf.lu_factor(Cd)
+        t_lu = time.perf_counter() - t0
+        x = np.ascontiguousarray(cfg.rhs()[:m, 0])
+        y = Fd @ x          # untimed first touch
+        z = vf.lu_factor_solve(fac, x)
+        t_fx = t_sv = 0.0
+        per = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            y = Fd @ x
+            t1 = time.perf_counter()
+            z = vf.lu_factor_solve(fac, y)
+            t2 = time.perf_counter()
+            t_fx += t1 - t0
+            t_sv += t2 - t1
+            per.append(t2 - t0)
+        del Fd, Cd, fac, y, z
+    finally:
+        if ctl is not None:
+            ctl.unregister()
+    sc = (n / m) ** 2
+    step = (t_fx + t_sv) / steps * sc
+    return {"value": 1.0 / step, "unit": "applies/s", "kind": "oracle",
+            "cores": threads or len(os.sched_getaffinity(0)),
+            "per_apply_s": {"ii_dense_Fx": t_fx / steps * sc, "iv_lu_solve": t_sv / steps * sc, "v_total": step},
+            "setup_s": {"i_dense_F_assembly": t_asm, "iii_dense_lu": t_lu, "of_size": m},
+            "steps_s": [p * sc for p in per],
+            "sample": (f"dense oracle on the full {n}-facet operator" if m == n else
+                       f"dense oracle on the leading {m} x {m} block of C{cfg.cfg}; per-apply times (ii)+(iv) "
+                       f"measured over {steps} applies and scaled by (n/m)^2 = {sc:.2f} (both stream n^2 doubles)")}
+
+
+def cpu_baseline(cfg):
+    """Bounded inline baseline for this arm's JSON line (~10-20 s of CPU work on the box)."""
+    out = cpu_dense_apply(cfg, steps=10, m=8192)
+    out["host"] = host_info()
+    return out
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle as it stands."""
+    """--impl reference: the CPU oracle as it stands, on the FULL workload: dense F and
+    its LU once (reported as setup), then K timed applies (stored dense F x + LU solve with the
+    precomputed factors) after W warm-up applies; nothing extrapolated.  Plus the C1 protocol run on
+    one thread."""
     import synth
     if rank != 0:
         return
     cfg = synth.make_config(args.config)
-    cb = None
-    for _ in range(args.warmup):
-        cb = cpu_baseline(cfg, budget_rows=64, sub_n=1024)
-    vals = []
-    for _ in range(args.steps):
-        cb = cpu_baseline(cfg, budget_rows=128, sub_n=2048)
-        vals.append(1.0 / cb["value"])
-    step = float(np.mean(vals))
+    t0 = time.perf_counter()
+    r = cpu_dense_apply(cfg, steps=args.warmup + args.steps)
+    wall = time.perf_counter() - t0
+    per = r.pop("steps_s")[args.warmup:]
+    step = float(np.mean(per))
+    c1 = cpu_dense_apply(synth.make_config(1), steps=20, threads=1)
+    c1.pop("steps_s")
     out = {"impl": "reference", "metric": METRIC, "value": 1.0 / step, "unit": "applies/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": workload_desc(cfg), "n": cfg.n, "parallelism": "cpu-oracle"},
-           "cpu_baseline": {"kind": "oracle", "cores": os.cpu_count(), "sample": cb["sample"], "value": 1.0 / step,
-                            "unit": "applies/s"},
+           "config": {"workload": workload_desc(cfg), "n": cfg.n, "parallelism": "cpu-oracle",
+                      "median_ms": float(np.median(per)) * 1e3, "min_ms": float(np.min(per)) * 1e3,
+                      "wall_s": wall},
+           "cpu_baseline": dict(r, value=1.0 / step, host=host_info()),
+           "cpu_c1_one_thread": c1,
            "e2e": {"value": 1.0 / step, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -171,6 +234,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--side-config", type=int, default=3,
+                    help="a larger config timed beside the headline (0: off): per-rank work there exceeds the "
+                         "collective latency at 8 GPUs, so its sharded flux time is reported at every N")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=20)
     ap.add_argument("--no-level-form", action="store_true")
@@ -182,6 +248,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # setup: rank 0 runs the hierarchical H-LU and broadcasts the factors; the other
+        # ranks wait in the broadcast, so rank 0 may use the host's cores
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)) if rank == 0 else 1)
 
     import torch
     import torch.distributed as dist
@@ -288,6 +358,29 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e_async = float(t.item())
 
+    # ---- CUDA-graph replay of the step (SURVEY.md §8(d) timing protocol): one flux call captured,
+    # replayed with per-replay CUDA events; median and min per step
+    graph_replay = None
+    if world == 1:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            hm.hm_radiative_flux(ctx, F, LU, T, q, stream=gs.cuda_stream)
+        nrep = max(args.steps, 200 if n <= 25000 else 50)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nrep)]
+        with torch.cuda.stream(gs):
+            for _ in range(3):
+                graph.replay()
+            for a_, b_ in evs:
+                a_.record(gs)
+                graph.replay()
+                b_.record(gs)
+        torch.cuda.synchronize()
+        rt = np.array([a_.elapsed_time(b_) for a_, b_ in evs])
+        graph_replay = {"replays": nrep, "median_ms": float(np.median(rt)), "min_ms": float(rt.min()),
+                        "applies_per_s_median": 1e3 / float(np.median(rt))}
+        del graph
     # ---- the dominant (and only) kernel of a step: one persistent engine launch per call;
     # timed live with CUDA events on the launching stream, alongside F-only and solve-only calls
     eng_ms, eng_info = hm.hm_profile_flux(ctx, F, LU, T, q, args.profile_iters, stream=stream.cuda_stream)
@@ -353,6 +446,36 @@ def main():
         ej1.record(stream)
         torch.cuda.synchronize()
         jcav = {"ms": ej0.elapsed_time(ej1) / args.profile_iters, "n_nodes": f.n_nodes}
+    # a larger configuration beside the headline (C3 by default), same GPU count: setup once, the flux
+    # timed with hm_profile_flux (the engine launches, plus the allgathers when sharded)
+    side = None
+    if args.side_config and not args.no_level_form:
+        cfg3 = synth.make_config(args.side_config)
+        f3 = cfg3.facets
+        t0 = time.perf_counter()
+        g3 = hm.hm_build_geometry(ctx, f3.centroid, f3.normal, f3.area, f3.aabb, n_min=cfg3.n_min, eta=cfg3.eta)
+        F3 = hm.hm_assemble_aca(ctx, g3, eps_aca=cfg3.eps_aca)
+        LU3 = hm.hm_factor_hlu(ctx, F3, cfg3.emissivity)
+        setup3 = time.perf_counter() - t0
+        rep3 = hm.hm_storage_report(F3, LU3)
+        if world > 1:
+            p3 = hm.hm_export_perm(g3)
+            b3, e3_ = hm.hm_local_range(g3, rank, world)
+            T3 = torch.from_numpy(np.ascontiguousarray(cfg3.T[p3[b3:e3_], 0])).cuda()
+        else:
+            T3 = torch.from_numpy(np.ascontiguousarray(cfg3.T[:, 0])).cuda()
+        q3 = torch.empty_like(T3)
+        ms3, _ = hm.hm_profile_flux(ctx, F3, LU3, T3, q3, args.profile_iters, stream=stream.cuda_stream)
+        if world > 1:
+            t = torch.tensor([ms3["flux"]], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms3["flux"] = float(t.item())
+        b3tot = rep3["bytes_F"] + rep3["bytes_C"]
+        side = {"workload": workload_desc(cfg3), "n": f3.n, "flux_ms": ms3["flux"], "applies_per_s": 1e3 / ms3["flux"],
+                "stored_bytes_per_step": b3tot, "hbm_gbs_aggregate": b3tot / (ms3["flux"] * 1e-3) / 1e9,
+                "bytes_local": rep3["bytes_F_local"] + rep3["bytes_C_local"], "setup_s": setup3,
+                "comm_share": (1.0 - ms3["flux_no_exchange"] / ms3["flux"]) if "flux_no_exchange" in ms3 else None}
+        del LU3, F3, g3
     peak, peak_src = peaks()
     bytes_step = rep["bytes_F"] + rep["bytes_C"]
     bytes_local = rep["bytes_F_local"] + rep["bytes_C_local"]    # this rank's stored bytes (= bytes_step at N=1)
@@ -395,7 +518,8 @@ def main():
                        "setup_s": dict(rep["setup_seconds"], wall=setup_wall),
                        "solve_form": "inverse factors (cut level 0, DESIGN.md R27)",
                        "level_form": level_form, "recompressed": recompressed, "multi_rhs": multi_rhs,
-                       "cavity_jacobian_action": jcav, "shard": shard,
+                       "cavity_jacobian_action": jcav, "shard": shard, "graph_replay": graph_replay,
+                       "side_config": side,
                        "e2e_async_pinned": {"value": args.steps / (ms_e2e_async / 1e3), "unit": "applies/s",
                                             "mode": "HM_FLAG_ASYNC_PINNED: pinned T in / q out, no per-call sync"}},
             "roofline": {"bound": "hbm", "kernel": "engine_kernel (flux program)" + (" + NCCL allgathers, rank 0" if world > 1 else ""),

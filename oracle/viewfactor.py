@@ -118,6 +118,20 @@ def solve(C: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.linalg.solve(C, b)
 
 
+def lu_factor(C: np.ndarray):
+    """The dense LU of C with partial pivoting, by LAPACK getrf (scipy.linalg.lu_factor) as a library
+    step: the factorisation of the paper's 'Direct' comparison, computed once and
+    reused across solves (SURVEY.md §8(d) CPU protocol, items iii/iv)."""
+    import scipy.linalg as sla
+    return sla.lu_factor(C, check_finite=False)
+
+
+def lu_factor_solve(fac, b: np.ndarray) -> np.ndarray:
+    """z = C^-1 b by forward then backward substitution with the factors of lu_factor (LAPACK getrs)."""
+    import scipy.linalg as sla
+    return sla.lu_solve(fac, b, check_finite=False)
+
+
 def flux_from_dense(F: np.ndarray, C: np.ndarray, A: np.ndarray, eps: np.ndarray, T: np.ndarray) -> np.ndarray:
     """q = sigma (eps/A) o (F C^-1 (eps o eta) - eta o (F C^-1 eps)), eta = T^4.
 

@@ -114,7 +114,11 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
                                       (int64_t)u.ncols * u.ld > (mrhs ? kUnitPayloadDoubles : kStageDoubles)))
             throw Error(HM_ERR_UNSUPPORTED, "work unit exceeds the engine stage size");
     const int64_t P = (int64_t)h_passes.size();
-    if (P > engine_max_passes()) throw Error(HM_ERR_UNSUPPORTED, "program has more passes than the engine's pass table");
+    if (P > (mrhs ? engine_mrhs_max_passes() : engine_max_passes()))
+        throw Error(HM_ERR_UNSUPPORTED, "program has " + std::to_string(P) + " passes, more than the " +
+                                            (mrhs ? "multi-RHS" : "single-vector") + " engine's pass table (" +
+                                            std::to_string(mrhs ? engine_mrhs_max_passes() : engine_max_passes()) +
+                                            "; pure level form needs 7 + 4 depth)");
     const int64_t nn = g ? (int64_t)g->nodes.size() : 0;
     // row groups for link_rows: the tree nodes of level depth - 4 (leaves above it are groups too)
     std::vector<int32_t> groups;           // node ids, in row order

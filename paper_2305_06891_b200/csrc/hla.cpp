@@ -45,9 +45,13 @@ struct ProfT {
                            std::memory_order_relaxed);
     }
 };
+static std::atomic<int64_t> g_hist[5], g_histk[5];
 void prof_dump() {
+    for (int b = 0; b < 5; ++b)
+        if (g_hist[b]) fprintf(stderr, "  addlr-lr max(m,n) bucket %d: %lld calls, mean update rank %.1f\n", b,
+                               (long long)g_hist[b].load(), (double)g_histk[b].load() / g_hist[b].load());
     static const char* names[16] = {"trunc", "qr", "jacobi", "trunc-gemm", "addlr-lr", "agglom", "mm-lrlr", "mm-lrA",
-                                    "mm-lrB", "hmul-dense", "hmul-lr", "solve-dense", "lu-dense", "mm-dd", "mm-sub-lr", "x"};
+                                    "mm-lrB", "hmul-dense", "hmul-lr", "solve-dense", "lu-dense", "mm-dd", "addlr-subtop", "compress-dense"};
     for (int i = 0; i < 16; ++i)
         if (g_prof[i]) fprintf(stderr, "  %-12s %10lld calls %9.3f s\n", names[i], (long long)g_prof[i].load(), g_ns[i].load() * 1e-9);
 }
@@ -230,6 +234,53 @@ static void invert_packed(double* A, int64_t m) {
 // ---------------------------------------------------------------- QR (Householder) + Jacobi SVD
 // A (m x K column-major) = Q R, R kq x K upper (kq = min(m, K)); Q kept as Householder reflectors
 // (W below the diagonal, tau) and applied with apply_q (Q is never formed).
+// H = I - tau v v^T (v = [1; x[j+1..m)]) applied to rows j.. of the nc columns Y (ld m), four at a
+// time so every load of x feeds four dot products / updates
+static inline void reflect(const double* __restrict x, int j, int64_t m, double tj, double* Y, int64_t ldy, int nc) {
+    int c = 0;
+    for (; c + 4 <= nc; c += 4) {
+        double* __restrict y0 = Y + (int64_t)c * ldy;
+        double* __restrict y1 = y0 + ldy;
+        double* __restrict y2 = y1 + ldy;
+        double* __restrict y3 = y2 + ldy;
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma omp simd reduction(+ : s0, s1, s2, s3)
+        for (int64_t i = j + 1; i < m; ++i) {
+            const double xi = x[i];
+            s0 += xi * y0[i];
+            s1 += xi * y1[i];
+            s2 += xi * y2[i];
+            s3 += xi * y3[i];
+        }
+        s0 = (s0 + y0[j]) * tj;
+        s1 = (s1 + y1[j]) * tj;
+        s2 = (s2 + y2[j]) * tj;
+        s3 = (s3 + y3[j]) * tj;
+        y0[j] -= s0;
+        y1[j] -= s1;
+        y2[j] -= s2;
+        y3[j] -= s3;
+#pragma omp simd
+        for (int64_t i = j + 1; i < m; ++i) {
+            const double xi = x[i];
+            y0[i] -= s0 * xi;
+            y1[i] -= s1 * xi;
+            y2[i] -= s2 * xi;
+            y3[i] -= s3 * xi;
+        }
+    }
+    for (; c < nc; ++c) {
+        double* __restrict y = Y + (int64_t)c * ldy;
+        double s = 0.0;
+#pragma omp simd reduction(+ : s)
+        for (int64_t i = j + 1; i < m; ++i) s += x[i] * y[i];
+        s = (s + y[j]) * tj;
+        y[j] -= s;
+#pragma omp simd
+        for (int64_t i = j + 1; i < m; ++i) y[i] -= s * x[i];
+    }
+}
+
 struct QR {
     int64_t m = 0;
     int K = 0, kq = 0;
@@ -254,16 +305,7 @@ static void qr(int64_t m, int K, const double* A, QR& f) {
         for (int64_t i = j + 1; i < m; ++i) x[i] *= sc;
         const double tj = f.tau[j] = (beta - a0) / beta;
         x[j] = beta;
-        for (int c = j + 1; c < K; ++c) {
-            double* __restrict y = Wp + (int64_t)c * m;
-            double s = 0.0;
-#pragma omp simd reduction(+ : s)
-            for (int64_t i = j + 1; i < m; ++i) s += x[i] * y[i];
-            s = (s + y[j]) * tj;
-            y[j] -= s;
-#pragma omp simd
-            for (int64_t i = j + 1; i < m; ++i) y[i] -= s * x[i];
-        }
+        reflect(x, j, m, tj, Wp + (int64_t)(j + 1) * m, m, K - j - 1);
     }
     f.R.assign((size_t)kq * K, 0.0);
     for (int c = 0; c < K; ++c)
@@ -280,17 +322,7 @@ static void apply_q(const QR& f, const double* A, int c, double* out) {
     for (int j = kq - 1; j >= 0; --j) {
         const double tj = f.tau[j];
         if (tj == 0.0) continue;
-        const double* __restrict x = Wp + (int64_t)j * m;
-        for (int l = 0; l < c; ++l) {
-            double* __restrict y = out + (int64_t)l * m;
-            double s = 0.0;
-#pragma omp simd reduction(+ : s)
-            for (int64_t i = j + 1; i < m; ++i) s += x[i] * y[i];
-            s = (s + y[j]) * tj;
-            y[j] -= s;
-#pragma omp simd
-            for (int64_t i = j + 1; i < m; ++i) y[i] -= s * x[i];
-        }
+        reflect(Wp + (int64_t)j * m, j, m, tj, out, m, c);
     }
 }
 
@@ -424,6 +456,94 @@ int truncate(int64_t m, int64_t n, int K, Vec& U, Vec& V, double eps) {
     apply_q(fu, A.data(), kn, U.data());
     apply_q(fv, B.data(), kn, V.data());
     return kn;
+}
+
+// Best rank-k approximation of a dense m x n block D at eps (Frobenius tail, reading R5): Householder QR
+// with column pivoting stopped once the trailing columns hold <= (eps/2)^2 of ||D||_F^2, then the SVD
+// truncation of the small r x n factor at the remaining budget -- O(m n r) instead of a full SVD.
+int compress_dense(const double* D, int64_t m, int64_t n, double eps, Vec& U, Vec& V) {
+    ProfT _p(15);
+    QR f;
+    f.m = m;
+    f.K = (int)n;
+    f.W.assign(D, D + m * n);
+    const int kmax = (int)std::min<int64_t>(m, n);
+    f.tau.assign((size_t)kmax, 0.0);
+    std::vector<double> nrm((size_t)n), nrm0((size_t)n);
+    std::vector<int> perm((size_t)n);
+    double tot = 0.0;
+    for (int64_t c = 0; c < n; ++c) {
+        double a = 0.0;
+        for (int64_t i = 0; i < m; ++i) a += f.W[i + c * m] * f.W[i + c * m];
+        nrm[c] = nrm0[c] = a;
+        tot += a;
+        perm[c] = (int)c;
+    }
+    if (tot == 0.0) {
+        U.clear();
+        V.clear();
+        return 0;
+    }
+    const double lim = 0.25 * eps * eps * tot;
+    double* Wp = f.W.data();
+    int r = 0;
+    for (; r < kmax; ++r) {
+        double rem = 0.0;
+        int piv = r;
+        for (int64_t c = r; c < n; ++c) {
+            rem += nrm[c];
+            if (nrm[c] > nrm[piv]) piv = (int)c;
+        }
+        if (rem <= lim) break;
+        if (piv != r) {
+            std::swap_ranges(Wp + (int64_t)piv * m, Wp + (int64_t)(piv + 1) * m, Wp + (int64_t)r * m);
+            std::swap(nrm[piv], nrm[r]);
+            std::swap(nrm0[piv], nrm0[r]);
+            std::swap(perm[piv], perm[r]);
+        }
+        double* x = Wp + (int64_t)r * m;
+        double nn2 = 0.0;
+        for (int64_t i = r; i < m; ++i) nn2 += x[i] * x[i];
+        const double nv = std::sqrt(nn2);
+        if (nv == 0.0) break;
+        const double a0 = x[r];
+        const double beta = a0 >= 0.0 ? -nv : nv;
+        const double sc = 1.0 / (a0 - beta);
+        for (int64_t i = r + 1; i < m; ++i) x[i] *= sc;
+        const double tj = f.tau[r] = (beta - a0) / beta;
+        x[r] = beta;
+        reflect(x, r, m, tj, Wp + (int64_t)(r + 1) * m, m, (int)(n - r - 1));
+        for (int64_t c = r + 1; c < n; ++c) {   // downdate the trailing norms (recompute when they fade)
+            const double w = Wp[r + c * m];
+            nrm[c] -= w * w;
+            if (nrm[c] <= 1e-10 * nrm0[c]) {
+                double a = 0.0;
+                for (int64_t i = r + 1; i < m; ++i) a += Wp[i + c * m] * Wp[i + c * m];
+                nrm[c] = nrm0[c] = a;
+            }
+        }
+    }
+    f.kq = r;
+    if (r == 0) {
+        U.clear();
+        V.clear();
+        return 0;
+    }
+    // R~ = R P^T (r x n): SVD-truncate I_r R~ at the remaining budget (relative to ||R~|| ~ ||D||)
+    Vec Ui((size_t)r * r, 0.0), Vt((size_t)(n * r), 0.0);
+    for (int i = 0; i < r; ++i) Ui[i + (int64_t)i * r] = 1.0;
+    for (int64_t c = 0; c < n; ++c)
+        for (int i = 0; i <= std::min<int64_t>(c, r - 1); ++i) Vt[perm[c] + (int64_t)i * n] = Wp[i + c * m];
+    const int k = truncate(r, n, r, Ui, Vt, std::sqrt(0.75) * eps);
+    if (k == 0) {
+        U.clear();
+        V.clear();
+        return 0;
+    }
+    U.resize((size_t)(m * k));
+    apply_q(f, Ui.data(), k, U.data());
+    V.swap(Vt);
+    return k;
 }
 
 // ============================================================================ H-arithmetic
@@ -581,12 +701,21 @@ struct Impl {
     }
 
     // ---- C += alpha U V^T, U (C.m x k, ldu), V (C.n x k, ldv)
+    static thread_local int fan_depth;
     void addlr(Mat& C, const double* U, int64_t ldu, const double* V, int64_t ldv, int k, double alpha) {
         if (k <= 0) return;
+        if (C.type == T_SUB && fan_depth == 0) g_prof[14].fetch_add(1);
+        struct FD { bool on; FD(bool b) : on(b) { if (on) ++fan_depth; } ~FD() { if (on) --fan_depth; } } fd(C.type == T_SUB);
         if (C.type == T_DENSE) {
             gemm_nt(C.m, C.n, k, alpha, U, ldu, V, ldv, C.D.data(), C.m);
         } else if (C.type == T_LR) {
             ProfT _p(4);
+            {   // size histogram (diagnostics)
+                const int64_t mn = std::max(C.m, C.n);
+                int b = mn <= 64 ? 0 : mn <= 128 ? 1 : mn <= 256 ? 2 : mn <= 1024 ? 3 : 4;
+                g_hist[b].fetch_add(1, std::memory_order_relaxed);
+                g_histk[b].fetch_add(k, std::memory_order_relaxed);
+            }
             const int K = C.k + k;
             Vec Un((size_t)(C.m * K)), Vn((size_t)(C.n * K));
             std::copy(C.U.begin(), C.U.begin() + C.m * C.k, Un.begin());
@@ -620,6 +749,10 @@ struct Impl {
 
     // collapse a subdivided block whose leaves are all low rank into one low-rank block (truncated)
     void agglomerate(Mat& T, Vec& U, Vec& V, int& k) {
+        if (T.type == T_DENSE) {   // a dense leaf-pair accumulator: compress it on its own first
+            k = dense_to_lr(T.D.data(), T.m, T.n, U, V);
+            return;
+        }
         if (T.type == T_LR) {
             U = T.U;
             V = T.V;
@@ -679,7 +812,12 @@ struct Impl {
             c->c0 = cj.begin;
             c->m = ri.size();
             c->n = cj.size();
-            c->type = T_LR;
+            if (ri.is_leaf() && cj.is_leaf()) {   // leaf pair: accumulate dense (see densify_leaf_pairs)
+                c->type = T_DENSE;
+                c->D.assign((size_t)(c->m * c->n), 0.0);
+            } else {
+                c->type = T_LR;
+            }
             T->c[q] = std::move(c);
         }
         return T;
@@ -763,7 +901,6 @@ struct Impl {
                 addlr(C, Z.data(), A.m, I.data(), B.n, (int)B.n, alpha);
             } else {
                 // both subdivided: form the product in C's subdivision, collapse it, add it
-                g_prof[14].fetch_add(1);
                 auto T = lr_shape(C);
                 const bool par = big(C);
                 for (int q = 0; q < 4; ++q) {
@@ -859,26 +996,64 @@ struct Impl {
 #pragma omp taskwait
     }
 
+    // admissible blocks between two leaf clusters: dense while the factorisation runs (R33:
+    // most updates land on these small blocks; as dense targets they cost a GEMM each instead of a
+    // QR + SVD truncation), compressed once at the end at eps -- the same or a smaller error than
+    // truncating after every update
+    void densify_leaf_pairs(Mat& A) {
+        if (A.type == T_SUB) {
+            for (auto& c : A.c) densify_leaf_pairs(*c);
+            return;
+        }
+        if (A.type != T_LR || !nodes[A.rn].is_leaf() || !nodes[A.cn].is_leaf()) return;
+        A.D.assign((size_t)(A.m * A.n), 0.0);
+        gemm_nt(A.m, A.n, A.k, 1.0, A.U.data(), A.m, A.V.data(), A.n, A.D.data(), A.m);
+        A.U.clear();
+        A.V.clear();
+        A.U.shrink_to_fit();
+        A.V.shrink_to_fit();
+        A.k = 0;
+        A.type = T_DENSE;
+        A.acc = true;
+    }
+    void compress_acc(Mat& A) {
+        if (A.type == T_SUB) {
+            const bool par = big(A);
+            for (int q = 0; q < 4; ++q) {
+#pragma omp task default(shared) firstprivate(q) if (par)
+                compress_acc(*A.c[q]);
+            }
+#pragma omp taskwait
+            return;
+        }
+        if (!A.acc) return;
+        A.k = dense_to_lr(A.D.data(), A.m, A.n, A.U, A.V);
+        A.D.clear();
+        A.D.shrink_to_fit();
+        A.type = T_LR;
+        A.acc = false;
+    }
+    int dense_to_lr(const double* D, int64_t m, int64_t n, Vec& U, Vec& V) {
+        ntr.fetch_add(1, std::memory_order_relaxed);
+        rin.fetch_add(std::min(m, n), std::memory_order_relaxed);
+        const int k = compress_dense(D, m, n, eps, U, V);
+        rout.fetch_add(k, std::memory_order_relaxed);
+        return k;
+    }
+
     void normalize(Mat& A) {
         if (A.type == T_SUB) { for (auto& c : A.c) normalize(*c); return; }
         if (A.type != T_DENSE) return;
         if (nodes[A.rn].is_leaf() || nodes[A.cn].is_leaf()) return;   // a genuine near-field leaf
         // admissible block stored dense (rank cap reached in F): low-rank form, exact up to eps
-        if (A.n <= A.m) {
-            A.U = A.D;
-            A.V = identity(A.n);
-            A.k = (int)A.n;
-        } else {
-            A.U = identity(A.m);
-            A.V = transpose(A.D.data(), A.m, A.n, A.m);
-            A.k = (int)A.m;
-        }
+        A.k = dense_to_lr(A.D.data(), A.m, A.n, A.U, A.V);
         A.D.clear();
         A.D.shrink_to_fit();
         A.type = T_LR;
-        A.k = trunc(A, A.k);
     }
 };
+
+thread_local int Impl::fan_depth = 0;
 
 // ============================================================================ HFactor
 namespace {
@@ -929,6 +1104,12 @@ HFactor::~HFactor() = default;
 
 int HFactor::threads() const { return omp_get_max_threads(); }
 
+void HFactor::for_each_leaf(const std::function<void(int, Mat&)>& f) {
+    const int64_t nb = (int64_t)by_block_.size();
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t b = 0; b < nb; ++b) f((int)b, *by_block_[b]);
+}
+
 template <class F>
 static void run_tasks(Impl& I, F&& f) {
 #pragma omp parallel
@@ -949,6 +1130,7 @@ void HFactor::factor(double eps) {
     const auto t0 = std::chrono::steady_clock::now();
     Impl I{nodes_, eps};
     I.task_min = env_task_min();
+    if (!getenv("HM_HLU_NO_DENSE_LEAF_PAIRS")) run_tasks(I, [&](Impl& im) { im.densify_leaf_pairs(*root_); });
     run_tasks(I, [&](Impl& im) { im.lu(*root_); });
     singular_ = I.singular;
     singular_where_ = I.where;
@@ -962,7 +1144,10 @@ void HFactor::solve_form(int cut, double eps) {
     const auto t0 = std::chrono::steady_clock::now();
     Impl I{nodes_, eps};
     I.task_min = env_task_min();
-    run_tasks(I, [&](Impl& im) { im.form(*root_, cut); });
+    run_tasks(I, [&](Impl& im) {
+        im.form(*root_, cut);
+        im.compress_acc(*root_);
+    });
     stats_.truncations += I.ntr;
     stats_.trunc_rank_in += I.rin;
     stats_.trunc_rank_out += I.rout;

@@ -34,6 +34,8 @@ struct Mat {
     int k = 0;              // low rank: M = U V^T, U column-major m x k, V column-major n x k
     std::vector<double> U, V;
     std::unique_ptr<Mat> c[4];   // T_SUB: c[2 i + j] = (row child i, column child j)
+    bool acc = false;       // an admissible leaf-x-leaf block held dense while the factorisation runs
+                            // (its updates are GEMMs, not truncations); truncated once at the end
     Mat* ch(int i, int j) const { return c[2 * i + j].get(); }
 };
 
@@ -63,6 +65,8 @@ public:
     // V n x k column-major.  Admissible blocks stored dense in F ("adm-dense") may be given dense:
     // they are converted to the low-rank form by truncation (exact up to eps).
     Mat& leaf(int b) { return *by_block_[b]; }
+    // f(b, leaf(b)) for every partition block, OpenMP-parallel over blocks
+    void for_each_leaf(const std::function<void(int, Mat&)>& f);
     // Converts dense payloads of admissible-structure leaves (both clusters inner nodes) to low rank.
     void normalize(double eps);
     // In place H-LU without pivoting (reading R12): unit-lower L strictly below the

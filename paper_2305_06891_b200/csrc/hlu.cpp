@@ -365,7 +365,21 @@ void read_items(Ctx* c, const HOp& op, const std::function<bool(size_t)>& want_v
     const size_t ni = op.items.size();
     size_t i0 = 0;
     DBuf<double> stage;
-    std::vector<double> host;
+    // pinned host staging (one buffer for the whole read-back: several times the pageable bandwidth)
+    struct Pinned {
+        double* p = nullptr;
+        size_t n = 0;
+        ~Pinned() { if (p) cudaFreeHost(p); }
+        double* get(size_t want) {
+            if (want > n) {
+                if (p) cudaFreeHost(p);
+                p = nullptr;
+                if (cudaMallocHost(&p, want * sizeof(double)) != cudaSuccess) throw Error(HM_ERR_OOM, "pinned read-back staging");
+                n = want;
+            }
+            return p;
+        }
+    } host;
     while (i0 < ni) {
         std::vector<int64_t> tasks;
         std::vector<int64_t> po, vo;
@@ -394,11 +408,11 @@ void read_items(Ctx* c, const HOp& op, const std::function<bool(size_t)>& want_v
             d.upload(c, tasks, "read-back tasks", s);
             k::pack(d.p, (int)(tasks.size() / 7), stage.p, s);
         }
-        host.resize((size_t)std::max<int64_t>(tot, 1));
-        if (tot > 0) HM_CUDA(cudaMemcpyAsync(host.data(), stage.p, (size_t)tot * sizeof(double), cudaMemcpyDeviceToHost, s));
+        double* hp = host.get((size_t)std::max<int64_t>(tot, 1));
+        if (tot > 0) HM_CUDA(cudaMemcpyAsync(hp, stage.p, (size_t)tot * sizeof(double), cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaStreamSynchronize(s));
         for (size_t q = i0; q < i1; ++q)
-            fn(q, host.data() + po[q - i0], vo[q - i0] >= 0 ? host.data() + vo[q - i0] : nullptr);
+            fn(q, hp + po[q - i0], vo[q - i0] >= 0 ? hp + vo[q - i0] : nullptr);
         i0 = i1;
     }
 }
@@ -426,7 +440,7 @@ std::vector<int> item_blocks(const Geom& g, const HOp& op) {
 namespace {
 
 // ---- stage B: hierarchical arithmetic (reading R33)
-void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& lam, int Lc, FactorSet& out) {
+void stage_b_root(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& lam, int Lc, FactorSet& out) {
     Ctx* c = L.ctx;
     const double eps = L.params.eps_lu;
     double t0 = now_seconds();
@@ -451,9 +465,8 @@ void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& la
     };
     if (c->host_only) {
         if (F.host_blocks.size() != g.blocks.size()) throw Error(HM_ERR_NOT_READY, "F holds no host blocks");
-        for (size_t b = 0; b < g.blocks.size(); ++b) {
+        hf->for_each_leaf([&](int b, hla::Mat& M) {
             const HostBlock& H = F.host_blocks[b];
-            hla::Mat& M = hf->leaf((int)b);
             if (H.kind == KIND_LR) {
                 M.type = hla::T_LR;
                 M.k = H.k;
@@ -463,12 +476,11 @@ void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& la
                 M.type = hla::T_DENSE;
                 M.D = H.D;
             }
-            to_C((int)b);
-        }
+            to_C(b);
+        });
     } else {
         const std::vector<int> ib = item_blocks(g, F.op);
-        for (size_t b = 0; b < g.blocks.size(); ++b) {
-            hla::Mat& M = hf->leaf((int)b);
+        hf->for_each_leaf([&](int b, hla::Mat& M) {
             if (F.blk_kind[b] == KIND_LR) {
                 M.type = hla::T_LR;
                 M.k = F.blk_rank[b];
@@ -478,7 +490,7 @@ void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& la
                 M.type = hla::T_DENSE;
                 M.D.assign((size_t)(M.m * M.n), 0.0);
             }
-        }
+        });
         read_items(
             c, F.op, [&](size_t q) { return F.op.items[q].r0 == g.blocks[ib[q]].r0; },
             [&](size_t q, const double* pay, const double* V) {
@@ -495,7 +507,7 @@ void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& la
                         std::copy(pay + j * it.m, pay + (j + 1) * it.m, M.D.begin() + j * M.m + ro);
                 }
             });
-        for (size_t b = 0; b < g.blocks.size(); ++b) to_C((int)b);
+        hf->for_each_leaf([&](int b, hla::Mat&) { to_C(b); });
     }
     L.setup_seconds[0] = now_seconds() - t0;
 
@@ -538,28 +550,49 @@ void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& la
     DBuf<double> dev;
     dev.alloc(c, (size_t)std::max<int64_t>(total, 2), "H-LU factor blocks");
     const cudaStream_t s = c->stream;
+    // pinned double buffer of 32 Mi doubles: the copy of one half overlaps the filling of the other
     const int64_t chunk = int64_t(1) << 25;
-    std::vector<double> hbuf;
-    hbuf.reserve((size_t)std::min<int64_t>(chunk, std::max<int64_t>(total, 1)));
-    int64_t flushed = 0;
-    auto flush = [&]() {
-        if (hbuf.empty()) return;
-        HM_CUDA(cudaMemcpy(dev.p + flushed, hbuf.data(), hbuf.size() * sizeof(double), cudaMemcpyHostToDevice));
-        flushed += (int64_t)hbuf.size();
-        hbuf.clear();
-    };
-    auto put = [&](const double* p, int64_t cnt) -> double* {   // device address of the copy
-        double* at = dev.p + flushed + (int64_t)hbuf.size();
-        if ((int64_t)hbuf.size() + cnt > chunk) {
-            flush();
-            at = dev.p + flushed;
+    double* pin[2] = {nullptr, nullptr};
+    cudaEvent_t evs[2] = {nullptr, nullptr};
+    struct PinGuard {
+        double** p;
+        cudaEvent_t* e;
+        ~PinGuard() {
+            for (int i = 0; i < 2; ++i) {
+                if (p[i]) cudaFreeHost(p[i]);
+                if (e[i]) cudaEventDestroy(e[i]);
+            }
         }
-        if (cnt > chunk) {   // larger than a chunk: straight copy
+    } pg{pin, evs};
+    const int64_t cap = std::min<int64_t>(chunk, std::max<int64_t>(total, 1));
+    for (int i = 0; i < 2; ++i) {
+        if (cudaMallocHost(&pin[i], (size_t)cap * sizeof(double)) != cudaSuccess) throw Error(HM_ERR_OOM, "pinned upload staging");
+        HM_CUDA(cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming));
+    }
+    int cur = 0;
+    int64_t fill = 0, flushed = 0;
+    auto flush = [&]() {
+        if (fill == 0) return;
+        HM_CUDA(cudaMemcpyAsync(dev.p + flushed, pin[cur], (size_t)fill * sizeof(double), cudaMemcpyHostToDevice, s));
+        HM_CUDA(cudaEventRecord(evs[cur], s));
+        flushed += fill;
+        fill = 0;
+        cur ^= 1;
+        HM_CUDA(cudaEventSynchronize(evs[cur]));   // the other half is free again
+    };
+    HM_CUDA(cudaEventRecord(evs[0], s));
+    HM_CUDA(cudaEventRecord(evs[1], s));
+    auto put = [&](const double* p, int64_t cnt) -> double* {   // device address of the copy
+        if (fill + cnt > cap) flush();
+        double* at = dev.p + flushed + fill;
+        if (cnt > cap) {   // larger than a chunk: straight copy
+            HM_CUDA(cudaStreamSynchronize(s));
             HM_CUDA(cudaMemcpy(dev.p + flushed, p, (size_t)cnt * sizeof(double), cudaMemcpyHostToDevice));
             flushed += cnt;
             return at;
         }
-        hbuf.insert(hbuf.end(), p, p + cnt);
+        std::memcpy(pin[cur] + fill, p, (size_t)cnt * sizeof(double));
+        fill += cnt;
         return at;
     };
     hf->visit([&](const hla::LeafView& v) {
@@ -616,6 +649,99 @@ void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& la
     HM_CUDA(cudaStreamSynchronize(s));
     out.staging.push_back(std::move(dev));
     L.setup_seconds[2] = now_seconds() - t0;
+}
+
+// Sharded runs (world > 1): rank 0 factors (all host cores) and broadcasts the solve-form blocks over
+// the library's communicator (one header, the block records, the payload); every rank rebuilds the
+// same block lists on its own copy, keeps its rows when it packs (build_hop with the shard).  A
+// failure on rank 0 travels in the header, so no rank waits on a broadcast that never comes.
+void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& lam, int Lc, FactorSet& out) {
+    Ctx* c = L.ctx;
+    if (c->host_only || !g.shard.sharded() || !c->ex) {
+        stage_b_root(L, F, g, lam, Lc, out);
+        return;
+    }
+    const cudaStream_t s = c->stream;
+    const bool root = c->rank == 0;
+    int64_t head[4] = {0, 0, 0, 0};   // status, records, payload doubles, message length
+    std::string msg;
+    hm_status code = HM_OK;
+    std::vector<int64_t> rec;
+    const double* base = nullptr;
+    if (root) {
+        try {
+            stage_b_root(L, F, g, lam, Lc, out);
+        } catch (const Error& e) {
+            code = e.code;
+            msg = e.what();
+        }
+        if (code == HM_OK) {
+            base = out.staging.empty() ? nullptr : out.staging.back().p;
+            auto add = [&](int64_t list, const SrcBlock& S) {
+                const int64_t od = S.dense ? S.dense - base : -1, ou = S.U ? S.U - base : -1, ov = S.V ? S.V - base : -1;
+                rec.insert(rec.end(), {list, S.r0, S.m, S.c0, S.n, S.kind, S.k, S.d_rs, S.d_cs, od, S.u_ld, ou, S.v_ld, ov});
+            };
+            for (int lv = 0; lv < Lc; ++lv) {
+                for (const SrcBlock& S : out.fwd[lv]) add(2 * lv, S);
+                for (const SrcBlock& S : out.bwd[lv]) add(2 * lv + 1, S);
+            }
+            for (const SrcBlock& S : out.srcL) add(-1, S);
+            for (const SrcBlock& S : out.srcU) add(-2, S);
+            head[2] = out.staging.empty() ? 0 : (int64_t)out.staging.back().n;
+        }
+        head[0] = code;
+        head[1] = (int64_t)rec.size() / 14;
+        head[3] = (int64_t)msg.size();
+    }
+    DBuf<int64_t> dh;
+    dh.upload(c, std::vector<int64_t>(head, head + 4), "factor broadcast header", s);
+    c->ex->broadcast(dh.p, sizeof(head), 0, s);
+    HM_CUDA(cudaMemcpyAsync(head, dh.p, sizeof(head), cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    if (head[0] != HM_OK) {
+        std::vector<int64_t> m((size_t)(head[3] + 7) / 8 + 1, 0);
+        if (root) std::memcpy(m.data(), msg.data(), msg.size());
+        DBuf<int64_t> dm;
+        dm.upload(c, m, "factor broadcast message", s);
+        c->ex->broadcast(dm.p, m.size() * 8, 0, s);
+        HM_CUDA(cudaMemcpyAsync(m.data(), dm.p, m.size() * 8, cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaStreamSynchronize(s));
+        throw Error((hm_status)head[0], std::string((const char*)m.data(), (size_t)head[3]) + " (on rank 0)");
+    }
+    rec.resize((size_t)head[1] * 14);
+    DBuf<int64_t> dr;
+    dr.upload(c, rec, "factor broadcast records", s);
+    if (!root) {
+        out.staging.clear();
+        DBuf<double> pay;
+        pay.alloc(c, (size_t)std::max<int64_t>(head[2], 2), "H-LU factor blocks");
+        out.staging.push_back(std::move(pay));
+    }
+    if (!rec.empty()) c->ex->broadcast(dr.p, rec.size() * 8, 0, s);
+    if (head[2] > 0) c->ex->broadcast(out.staging.back().p, (size_t)head[2] * 8, 0, s);
+    if (!root && !rec.empty()) HM_CUDA(cudaMemcpyAsync(rec.data(), dr.p, rec.size() * 8, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    if (!root) {
+        const double* b = out.staging.back().p;
+        out.fwd.assign(std::max(Lc, 0), {});
+        out.bwd.assign(std::max(Lc, 0), {});
+        for (size_t q = 0; q < rec.size(); q += 14) {
+            const int64_t* r = &rec[q];
+            SrcBlock S;
+            S.r0 = r[1]; S.m = r[2]; S.c0 = r[3]; S.n = r[4];
+            S.kind = (int)r[5]; S.k = (int)r[6];
+            S.d_rs = r[7]; S.d_cs = r[8];
+            S.dense = r[9] >= 0 ? b + r[9] : nullptr;
+            S.u_ld = r[10];
+            S.U = r[11] >= 0 ? b + r[11] : nullptr;
+            S.v_ld = r[12];
+            S.V = r[13] >= 0 ? b + r[13] : nullptr;
+            const int64_t list = r[0];
+            if (list == -1) out.srcL.push_back(S);
+            else if (list == -2) out.srcU.push_back(S);
+            else (list % 2 == 0 ? out.fwd : out.bwd)[list / 2].push_back(S);
+        }
+    }
 }
 
 void account(HLU& L, const HOp& op) {

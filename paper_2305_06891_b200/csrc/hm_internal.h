@@ -62,6 +62,8 @@ struct DBuf {  // owning device buffer
 struct Exchanger {
     virtual ~Exchanger() = default;
     virtual void allgather(double* buf, int64_t count, cudaStream_t s) = 0;
+    // buf (bytes, device) of `root` to every rank, stream-ordered (setup: the H-LU factors)
+    virtual void broadcast(void* buf, size_t bytes, int root, cudaStream_t s) = 0;
     virtual const char* kind() const = 0;
 };
 
@@ -164,7 +166,8 @@ std::unique_ptr<Exchanger> make_exchanger(int device, int rank, int world, const
 // A panel is cut into work units (row tile <= 128 rows x column chunk of ~48 KB).  Units of the
 // same row tile ("group") write partial sums; the last-arriving unit adds them in segment order
 // (deterministic, no floating-point atomics).
-// A chunk: <= 32 KB of contiguous payload (ncols * ld doubles) + its column-source list; the unit
+// A chunk: <= one engine stage (kStageDoubles, 56.6 KB; 32 KB in the multi-RHS engine) of contiguous
+// payload (ncols * ld doubles) + its column-source list; the unit
 // of TMA transfer.  A task = consecutive chunks of one panel piece, processed by one CTA that
 // accumulates in registers and emits once.  Pieces of the same panel (only panels > 512 KB are
 // split) combine deterministically: the last-finishing piece adds the partials in piece order.
@@ -415,6 +418,7 @@ struct SegProgram {
 
 size_t engine_smem_bytes();
 int engine_mrhs_grid();
+int engine_mrhs_max_passes();
 void engine_mrhs_launch(const ProgArgs& A, int grid, cudaStream_t s);
 int engine_max_passes();
 int engine_grid();
@@ -525,12 +529,6 @@ void fill_entries(const double* geo, int64_t n, const int64_t* tasks /*[nt][6] d
 void pack(const int64_t* tasks /*[nt][7] dst,src,rows,cols,rs,cs,dld*/, int nt, double* arena, cudaStream_t s);
 void scale_rows(const int64_t* tasks /*[nt][5] a_off,ld,m,ncols,r0*/, int nt, double* arena, const double* cdiv,
                 cudaStream_t s);
-void permute_in(const double* x_ext, int ld, int col, const int32_t* perm, double* x_int, int64_t n,
-                cudaStream_t s);
-void permute_out(const double* y_int, const int32_t* perm, double* y_ext, int ld, int col, int64_t n,
-                 cudaStream_t s);
-void flux_prologue(const double* T_ext, int ld, int col, const int32_t* perm, const double* eps_int,
-                   double* w_int, int64_t n, cudaStream_t s);
 void fill_value(double* p, int64_t n, double v, cudaStream_t s);
 void proj_facets(const int64_t* rp, const int32_t* col_idx, const double* val, const double* T, const double* x,
                  int mode, int ld, int col, double* eta, int64_t n, cudaStream_t s);

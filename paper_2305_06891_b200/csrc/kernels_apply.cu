@@ -18,26 +18,7 @@ namespace hm {
 namespace {
 
 
-__device__ __forceinline__ double pow4(double T) {
-    const double t2 = T * T;
-    return t2 * t2;
-}
 
-__global__ void permute_in_kernel(const double* __restrict__ x_ext, int ld, int col, const int32_t* __restrict__ perm,
-                                  double* __restrict__ x_int, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) x_int[i] = x_ext[(int64_t)perm[i] * ld + col];
-}
-__global__ void permute_out_kernel(const double* __restrict__ y_int, const int32_t* __restrict__ perm,
-                                   double* __restrict__ y_ext, int ld, int col, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) y_ext[(int64_t)perm[i] * ld + col] = y_int[i];
-}
-__global__ void flux_prologue_kernel(const double* __restrict__ T_ext, int ld, int col, const int32_t* __restrict__ perm,
-                                     const double* __restrict__ eps_int, double* __restrict__ w, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) w[i] = eps_int[i] * pow4(T_ext[(int64_t)perm[i] * ld + col]);
-}
 __global__ void fill_value_kernel(double* p, int64_t n, double v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -106,22 +87,6 @@ void sum_segments(const double* buf, int world, int64_t count, int64_t n, int ld
     debug_sync(s, "sum_segments");
 }
 
-void permute_in(const double* x_ext, int ld, int col, const int32_t* perm, double* x_int, int64_t n, cudaStream_t s) {
-    permute_in_kernel<<<nblk(n, 256), 256, 0, s>>>(x_ext, ld, col, perm, x_int, n);
-    HM_CUDA(cudaGetLastError());
-    debug_sync(s, "permute_in");
-}
-void permute_out(const double* y_int, const int32_t* perm, double* y_ext, int ld, int col, int64_t n, cudaStream_t s) {
-    permute_out_kernel<<<nblk(n, 256), 256, 0, s>>>(y_int, perm, y_ext, ld, col, n);
-    HM_CUDA(cudaGetLastError());
-    debug_sync(s, "permute_out");
-}
-void flux_prologue(const double* T_ext, int ld, int col, const int32_t* perm, const double* eps_int, double* w_int,
-                   int64_t n, cudaStream_t s) {
-    flux_prologue_kernel<<<nblk(n, 256), 256, 0, s>>>(T_ext, ld, col, perm, eps_int, w_int, n);
-    HM_CUDA(cudaGetLastError());
-    debug_sync(s, "flux_prologue");
-}
 void proj_facets(const int64_t* rp, const int32_t* col_idx, const double* val, const double* T, const double* x,
                  int mode, int ld, int col, double* eta, int64_t n, cudaStream_t s) {
     if (n == 0) return;

@@ -98,6 +98,10 @@ struct EngineSmem {
     unsigned long long rfull[kRetireSlots], rempty[kRetireSlots];
     unsigned long long epoch;   // this launch's epoch (read_epoch)
 };
+// the whole engine state must fit the 227 KB opt-in limit (HM_BUILD_DEFINES overrides of the stage
+// geometry fail here, at compile time, instead of at the first launch)
+static_assert(sizeof(EngineSmem) + 128 <= 232448, "engine shared memory exceeds 227 KB");
+static_assert(kLookahead > 0 && (kStageDoubles * 8) % 16 == 0, "stage geometry");
 
 __device__ __forceinline__ void emit(const ProgArgs& A, const Pass& P, int64_t row, double s) {
     switch (P.mode) {
@@ -332,7 +336,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                                 v[q] = __ldcg(in + j);
                             } else {
                                 const int64_t e = -(int64_t)j - 1;
-                                const double t = __ldg(A.user_in + e * A.ld + A.col);
+                                // coherent load: after a copy-in pass the input is written earlier in
+                                // this launch (the dependency wait is the acquire)
+                                const double t = __ldcg(A.user_in + e * A.ld + A.col);
                                 v[q] = im == IN_PERM ? t : __ldg(A.eps_ext + e) * (A.eta_in ? t : pow4(t));
                             }
                         }

@@ -696,6 +696,8 @@ void engine_mrhs_launch(const ProgArgs& A, int grid, cudaStream_t s) {
     debug_sync(s, "engine_mrhs_kernel");
 }
 
+int engine_mrhs_max_passes() { return kMaxPassesM; }
+
 int engine_mrhs_grid() {
     int dev = 0, sms = 0, per = 0;
     HM_CUDA(cudaGetDevice(&dev));

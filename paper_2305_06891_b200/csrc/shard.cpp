@@ -74,6 +74,7 @@ struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -92,10 +93,11 @@ NcclApi& nccl() {
         api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
         api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
         api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+        api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
         api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
         api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
     });
-    if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.CommDestroy)
+    if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.CommDestroy || !api.Broadcast)
         throw Error(HM_ERR_NCCL, "libnccl.so.2 not found or incomplete (needed for world > 1)");
     return api;
 }
@@ -121,6 +123,9 @@ struct NcclExchanger : Exchanger {
         nccl_check(nccl().AllGather(buf + (int64_t)rank * count, buf, (size_t)count, ncclFloat64, comm, s),
                    "ncclAllGather");
     }
+    void broadcast(void* buf, size_t bytes, int root, cudaStream_t s) override {
+        nccl_check(nccl().Broadcast(buf, buf, bytes, ncclChar, root, comm, s), "ncclBroadcast");
+    }
     const char* kind() const override { return "nccl"; }
 };
 
@@ -132,9 +137,10 @@ struct LocalGroup {
     int arrived = 0;
     int64_t generation = 0;
     std::vector<double*> bufs;
+    std::vector<void*> vbufs;
     std::vector<cudaEvent_t> ready[2], done[2];
     std::vector<int> devices;
-    explicit LocalGroup(int w) : world(w), bufs(w, nullptr), devices(w, 0) {
+    explicit LocalGroup(int w) : world(w), bufs(w, nullptr), vbufs(w, nullptr), devices(w, 0) {
         for (int p = 0; p < 2; ++p) {
             ready[p].assign(w, nullptr);
             done[p].assign(w, nullptr);
@@ -208,6 +214,21 @@ struct LocalGroupExchanger : Exchanger {
         G->barrier();
         for (int q = 0; q < world; ++q)
             if (q != rank) HM_CUDA(cudaStreamWaitEvent(s, G->done[par][q], 0));
+    }
+    void broadcast(void* buf, size_t bytes, int root, cudaStream_t s) override {
+        const int par = (int)(n_ex++ & 1);
+        G->vbufs[rank] = buf;
+        HM_CUDA(cudaEventRecord(G->ready[par][rank], s));
+        G->barrier();
+        if (rank != root && bytes > 0) {
+            HM_CUDA(cudaStreamWaitEvent(s, G->ready[par][root], 0));
+            HM_CUDA(cudaMemcpyPeerAsync(buf, device, G->vbufs[root], G->devices[root], bytes, s));
+        }
+        HM_CUDA(cudaEventRecord(G->done[par][rank], s));
+        G->barrier();
+        if (rank == root)
+            for (int q = 0; q < world; ++q)
+                if (q != rank) HM_CUDA(cudaStreamWaitEvent(s, G->done[par][q], 0));
     }
     const char* kind() const override { return "local-group"; }
 };

@@ -48,6 +48,15 @@ def run(cfgid, exact=False):
         qo = vf.flux_from_dense(Fd, Cd, f.area, cfg.emissivity, T)[:, 0]
         out["flux_vs_dense"] = rel(q, qo)
         del Fd, Cd
+    if exact:   # sphere-exact: C^-1 x by Sherman-Morrison (SURVEY.md §8(c) pins), O(n) at any size
+        a = f.area
+        k = 1.0 / (4.0 * np.pi)
+        cex = (a.sum() - a) * k
+        bb = (1.0 - cfg.emissivity) / cex
+        Md = 1.0 + k * bb * a
+        Mx, Mb = x / Md, bb / Md
+        zcl = Mx + (k * (a @ Mx) / (1.0 - k * (a @ Mb))) * Mb
+        out["solve_vs_sherman_morrison"] = rel(z, zcl)
     rows = synth.sample_rows(synth.stream_seed(cfg.seed, 999), f.n, 2000 if f.n < 400000 else 300)
     r = vf.sampled_residual(f.centroid, f.normal, f.area, cfg.emissivity, rows, z[:, None], x[:, None])[:, 0]
     out["residual_sampled"] = float(np.linalg.norm(r) / np.linalg.norm(x[rows]))

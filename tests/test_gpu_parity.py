@@ -407,13 +407,47 @@ def test_config3_capped_cylinder_sampled(hm, ctx):
     assert rel(yw[rows], ys) <= 10 * cfg.eps_aca
 
 
-# ---------------------------------------------------------------- BASELINE configs[3], configs[4] (F apply)
-# Their solve needs the H-arithmetic H-LU; the F apply runs at full size.
+# ---------------------------------------------------------------- BASELINE configs[3], configs[4]
+# The hierarchical (stage-B) H-LU runs at any n (reading R33); C4 and C5 are checked on the
+# north star's sampled rows and against the sphere-exact closed forms.
+def sherman_morrison(f, eps, x):
+    """Sphere-exact C^-1 x (SURVEY.md §8(c) pins): C = M - k b a^T, M = diag(1 + k b_i a_i), b_i =
+    (1 - eps_i) / c_i, c_i = (sum a - a_i) / (4 pi), k = 1 / (4 pi); O(n) at any size."""
+    a = f.area
+    k = 1.0 / (4.0 * math.pi)
+    cex = (a.sum() - a) * k
+    bb = (1.0 - eps) / cex
+    Md = 1.0 + k * bb * a
+    Mx, Mb = x / Md, bb / Md
+    return Mx + (k * (a @ Mx) / (1.0 - k * (a @ Mb))) * Mb
+
+
+def solve_and_flux_checks(hm, ctx, cfg, F, LU, rows, tol):
+    """Sampled solve residual (kappa(C) ~ 1.7, so the relative residual ~ the forward error) and the
+    flux properties that hold at any size (energy conservation, uniform T -> q = 0)."""
+    import torch
+    f = cfg.facets
+    x = cfg.rhs()[:, 0].copy()
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, x, z)
+    r = vf.sampled_residual(f.centroid, f.normal, f.area, cfg.emissivity, rows, z[:, None], x[:, None])[:, 0]
+    assert np.linalg.norm(r) / np.linalg.norm(x[rows]) <= tol
+    T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+    q = torch.empty_like(T)
+    hm.hm_radiative_flux(ctx, F, LU, T, q)
+    torch.cuda.synchronize()
+    Aq = f.area * q.cpu().numpy()
+    assert abs(Aq.sum()) <= tol * np.abs(Aq).sum()
+    hm.hm_radiative_flux(ctx, F, LU, torch.full_like(T, 700.0), q)
+    torch.cuda.synchronize()
+    assert np.abs(q.cpu().numpy()).max() <= tol * vf.SIGMA_SB * 700.0 ** 4
+
+
 @pytest.mark.slow
-def test_config4_apply_sampled(hm, ctx):
+def test_config4_apply_and_solve_sampled(hm, ctx):
     """C4 (icosphere sub 7, 327,680 facets, leaf 128): F x, single vector and 64 right-hand sides (DMMA
-    engine), vs 300 sampled dense rows within 10 eps_ACA; the stage-A factorisation reports
-    HM_ERR_UNSUPPORTED (needs ~2.4 TB dense) instead of failing."""
+    engine), vs 300 sampled dense rows; the hierarchical H-LU's solve residual on 2,000 sampled rows
+    and the flux at any-size properties, all within 10 eps_ACA = 1e-5."""
     import torch
     cfg = synth.make_config(4, nrhs=64)
     f = cfg.facets
@@ -429,17 +463,35 @@ def test_config4_apply_sampled(hm, ctx):
     Yh = Y.cpu().numpy()
     assert max(rel(Yh[rows, c], Ys[:, c]) for c in range(64)) <= 10 * cfg.eps_aca
     assert rel(y1.cpu().numpy()[rows], Ys[:, 0]) <= 10 * cfg.eps_aca
-    with pytest.raises(hm.HMError) as ei:
-        hm.hm_factor_hlu(ctx, F, cfg.emissivity)
-    assert ei.value.status == "HM_ERR_UNSUPPORTED"
+    del Y, y1
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    rows2k = synth.sample_rows(synth.stream_seed(cfg.seed, 999), f.n, 2000)
+    solve_and_flux_checks(hm, ctx, cfg, F, LU, rows2k, 10 * cfg.eps_aca)
 
 
 @pytest.mark.slow
-def test_config5_flat_apply_sampled(hm, ctx):
+@pytest.mark.parametrize("sub", [7, 8])
+def test_sphere_exact_solve_sherman_morrison(hm, ctx, sub):
+    """C4 / C5 geometry (icosphere sub 7 / 8: 327,680 / 1,310,720 facets, leaf 128) in sphere-exact mode
+    with eps ~ U[0.3, 0.95]: the hierarchical H-LU's C^-1 x equals the Sherman-Morrison closed form
+    within 10 eps_ACA (1e-5 / 1e-4) -- the north star's solve parity where no dense oracle exists."""
+    cfg = synth.make_config(4 if sub == 7 else 5, exact=True, nrhs=1)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    x = synth.uniform(5, f.n)
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, x, z)
+    assert rel(z, sherman_morrison(f, cfg.emissivity, x)) <= 10 * cfg.eps_aca
+
+
+@pytest.mark.slow
+def test_config5_flat_apply_solve_sampled(hm, ctx):
     """C5 at its BASELINE parameters (icosphere sub 8, 1,310,720 flat facets, eps_ACA = 1e-5, leaf 128,
     64 right-hand sides T ~ U[300,1000] K as sigma T^4): F X through the DMMA engine and the single-vector
-    engine vs 200 sampled dense rows of the oracle within 10 eps_ACA (A25: 1e-4).
-    The 64-column result's first column equals the single-vector apply to rounding."""
+    engine vs 200 sampled dense rows of the oracle (SURVEY.md §8(c) item 7) within 10 eps_ACA (A25: 1e-4);
+    then the hierarchical H-LU: the solve residual on 2,000 sampled rows, the flux properties, and the
+    64-column flux (DMMA engine) equal to the single-column flux column by column."""
     import torch
     cfg = synth.make_config(5)
     f = cfg.facets
@@ -459,6 +511,17 @@ def test_config5_flat_apply_sampled(hm, ctx):
     assert max(rel(Yh[rows, c], Ys[:, c]) for c in range(64)) <= 10 * cfg.eps_aca
     assert rel(y1h[rows], Ys[:, 0]) <= 10 * cfg.eps_aca
     assert rel(Yh[:, 0], y1h) <= 1e-12
+    del Yh
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    rows2k = synth.sample_rows(synth.stream_seed(cfg.seed, 999), f.n, 2000)
+    solve_and_flux_checks(hm, ctx, cfg, F, LU, rows2k, 10 * cfg.eps_aca)
+    Tm = torch.from_numpy(np.ascontiguousarray(cfg.T)).cuda()
+    qm = torch.empty_like(Tm)
+    hm.hm_radiative_flux(ctx, F, LU, Tm, qm)
+    q1 = torch.empty(f.n, dtype=torch.float64, device="cuda")
+    hm.hm_radiative_flux(ctx, F, LU, Tm[:, 5].contiguous(), q1)
+    torch.cuda.synchronize()
+    assert rel(qm[:, 5].cpu().numpy(), q1.cpu().numpy()) <= 1e-10
 
 
 @pytest.mark.slow
@@ -814,3 +877,59 @@ def test_multi_rhs_level_form(hm, ctx, cut):
         assert rel(Q[:, col].cpu().numpy(), q1.cpu().numpy()) <= 1e-12
         assert rel(Z[:, col].cpu().numpy(), Zd[:, col]) <= 10 * cfg.eps_aca
         assert rel(Q[:, col].cpu().numpy(), Qd[:, col]) <= 10 * cfg.eps_aca
+
+
+# ---------------------------------------------------------------- stage B vs stage A, exported factors
+@pytest.mark.parametrize("cut", [0, 3])
+def test_hierarchical_and_dense_factorisations_agree(hm, ctx, cut):
+    """The hierarchical H-LU (stage B, default; reading R33) and the dense-tile factorisation (stage A,
+    method="dense", reading R28) on the same F: both solves within 10 eps_ACA of the dense oracle, and of
+    each other; the hierarchical factors store no more bytes (SVD truncation vs cross approximation)."""
+    cfg = synth.make_config(2, geometry=synth.icosphere(4))
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    LUb = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=cut)
+    LUa = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=cut, method="dense")
+    x = cfg.rhs()[:, 0].copy()
+    zb, za = np.empty(f.n), np.empty(f.n)
+    hm.hm_solve_C(ctx, LUb, x, zb)
+    hm.hm_solve_C(ctx, LUa, x, za)
+    Fd, Cd, _ = vf.dense_operators(f, cfg.emissivity)
+    zd = np.linalg.solve(Cd, x)
+    assert rel(zb, zd) <= 10 * cfg.eps_aca and rel(za, zd) <= 10 * cfg.eps_aca
+    assert rel(zb, za) <= 10 * cfg.eps_aca
+    assert hm.hm_storage_report(F, LUb)["bytes_C"] <= 1.02 * hm.hm_storage_report(F, LUa)["bytes_C"]
+
+
+def test_apply_is_exact_on_the_exported_factors(hm, ctx):
+    """the matrix-vector products 'do not involve any further approximation'.  The GPU's
+    F x and C^-1 b equal the long-double products of the factors the library exports (hm_export_factors:
+    F's items; L^-1 and U^-1 of the inverse-factor solve form) to rounding."""
+    cfg = synth.make_config(1)
+    f = cfg.facets
+    n = f.n
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    perm = hm.hm_export_perm(g)
+    x = cfg.rhs()[:, 0].copy()
+    xi = x[perm].astype(np.longdouble)
+
+    def apply_items(items, v):
+        out = np.zeros(n, dtype=np.longdouble)
+        for r0, m, c0, nn, D in items:
+            if isinstance(D, tuple):
+                U, V = (a.astype(np.longdouble) for a in D)
+                out[r0:r0 + m] += U @ (V.T @ v[c0:c0 + nn])
+            else:
+                out[r0:r0 + m] += D.astype(np.longdouble) @ v[c0:c0 + nn]
+        return out
+
+    y = np.empty(n)
+    hm.hm_apply_F(ctx, F, x, y)
+    yl = apply_items(hm.hm_export_factors(hm.HM_OP_F, F, LU), xi)
+    assert np.abs(y[perm] - yl).max() <= 1e-14 * np.abs(yl).max()
+    z = np.empty(n)
+    hm.hm_solve_C(ctx, LU, x, z)
+    zl = apply_items(hm.hm_export_factors(hm.HM_OP_UINV, F, LU),
+                     apply_items(hm.hm_export_factors(hm.HM_OP_LINV, F, LU), xi))
+    assert np.abs(z[perm] - zl).max() <= 1e-13 * np.abs(zl).max()

@@ -1,0 +1,176 @@
+"""The hierarchical (stage-B) H-LU of the library, driven on the HOST without a GPU.
+
+The library's H-arithmetic factorisation (csrc/hla.cpp, reading R33: the 4-step recursion
+of PAPER.md:770-775 with truncation after every low-rank sum at eps_LU) is fed the
+ORACLE's own H-matrix F (oracle/hmatrix.py, an independent assembly) through hm_hmat_from_host on a
+host-only context; the factors it produces come back through hm_export_factors and are composed here
+into C^-1 in the solve form of reading R27.  Bars:
+  * against the exact inverse of the same H-matrix's C_H = I - Lambda F_H: the H-LU's own truncation
+    error, <= 1e-7 relative (eps_LU = 1e-6, kappa(C) ~ 1.7);
+  * against the dense oracle C^-1 b: <= 10 eps_ACA (north star);
+  * sphere-exact icosphere: C^-1 x equals the Sherman-Morrison closed form (SURVEY.md §8(c) pins);
+  * structure: L^-1 unit lower, U^-1 upper, every block inside F's partition;
+  * bitwise reproducible whatever the OpenMP schedule (1 thread vs all threads).
+No compute runs on a device here: these tests cover the host factorisation only (the GPU parity
+tests run it through hm_factor_hlu on a B200 and apply the factors with the CUDA engine).
+"""
+import json
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import hmatrix as ohm
+from oracle import viewfactor as vf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def hm():
+    import paper_2305_06891_b200 as hm
+    return hm
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def host_factor(hm, cfg, n_min=None, cut=0, eps=None):
+    f = cfg.facets
+    n_min = n_min or cfg.n_min
+    eps = eps or cfg.eps_aca
+    H = ohm.assemble(f, n_min, cfg.eta, eps, closed=cfg.extra.get("closed", True))
+    ctx = hm.hm_init(-1)
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=n_min, eta=cfg.eta)
+    assert (hm.hm_export_perm(g) == H.perm).all()
+    blocks = sorted(H.blocks, key=lambda b: (b.r0, b.c0))
+    part = hm.hm_export_partition(g)
+    assert [(b.r0, b.c0) for b in blocks] == [(int(p[1]), int(p[3])) for p in part]
+    F = hm.hm_hmat_from_host(ctx, g, [(b.U, b.V) if b.kind == ohm.KIND_LR else b.D for b in blocks])
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, eps_lu=eps, cut_level=cut)
+    return dict(ctx=ctx, g=g, F=F, LU=LU, H=H, perm=H.perm, part=part)
+
+
+def dense_op(hm, n, items):
+    M = np.zeros((n, n))
+    for r0, m, c0, nn, D in items:
+        M[r0:r0 + m, c0:c0 + nn] += D if not isinstance(D, tuple) else D[0] @ D[1].T
+    return M
+
+
+def cinv_internal(hm, r, n, cut):
+    """C^-1 in internal order from the exported solve form: U_cut^-1 (I - W^U_{c-1}) ... (I - W^U_0)
+    L_cut^-1 (I - W^L_{c-1}) ... (I - W^L_0) (top-down sweeps, reading R27)."""
+    Li = dense_op(hm, n, hm.hm_export_factors(hm.HM_OP_LINV, r["F"], r["LU"]))
+    Ui = dense_op(hm, n, hm.hm_export_factors(hm.HM_OP_UINV, r["F"], r["LU"]))
+    Lm, Um = np.eye(n), np.eye(n)
+    for lv in range(cut):
+        Lm = (np.eye(n) - dense_op(hm, n, hm.hm_export_factors(hm.HM_OP_WL(lv), r["F"], r["LU"]))) @ Lm
+        Um = (np.eye(n) - dense_op(hm, n, hm.hm_export_factors(hm.HM_OP_WU(lv), r["F"], r["LU"]))) @ Um
+    return Ui @ Um @ Li @ Lm, Li, Ui
+
+
+@pytest.mark.parametrize("cut", [0, 2, 5])
+def test_host_hlu_c1_matches_exact_and_dense(hm, cut):
+    """C1 (icosphere sub 3, 1,280 facets, eps 1e-6): all three solve forms (cut 0 = inverse factors,
+    cut 2 = mixed, cut 5 = depth = pure level form)."""
+    cfg = synth.make_config(1)
+    f = cfg.facets
+    n = f.n
+    r = host_factor(hm, cfg, cut=cut)
+    Cinv, Li, Ui = cinv_internal(hm, r, n, cut)
+    perm = r["perm"]
+    lam = (1.0 - cfg.emissivity[perm]) / f.area[perm]
+    CH = np.eye(n) - lam[:, None] * r["H"].to_dense_internal()
+    b = cfg.rhs()[perm, 0]
+    z = Cinv @ b
+    assert rel(z, np.linalg.solve(CH, b)) <= 1e-7            # truncation error of the H-LU alone
+    Fd, Cd, _ = vf.dense_operators(f, cfg.emissivity)
+    zd = np.linalg.solve(Cd, cfg.rhs()[:, 0])[perm]
+    assert rel(z, zd) <= 10 * cfg.eps_aca                     # north-star bar vs the dense oracle
+    if cut == 0:   # structure of the inverse factors: L^-1 unit lower, U^-1 upper
+        assert np.allclose(np.diag(Li), 1.0) and np.abs(np.triu(Li, 1)).max() == 0.0
+        assert np.abs(np.tril(Ui, -1)).max() == 0.0
+    # every exported block lies inside one block of F's partition
+    spans = {(int(p[1]), int(p[3])): (int(p[2]), int(p[4])) for p in r["part"]}
+    for r0, m, c0, nn, _ in hm.hm_export_factors(hm.HM_OP_LINV, r["F"], r["LU"]):
+        assert spans[(r0, c0)] == (r0 + m, c0 + nn)
+
+
+def test_host_hlu_sphere_exact_sherman_morrison(hm):
+    """Sphere-exact icosphere sub 3 with eps ~ U[0.3, 0.95]: C = M - k b a^T (rank-one update of a
+    diagonal), so C^-1 x has the Sherman-Morrison closed form at any size."""
+    cfg = synth.make_config(2, geometry=synth.icosphere(3, exact=True))
+    f = cfg.facets
+    n = f.n
+    r = host_factor(hm, cfg, cut=0)
+    Cinv, _, _ = cinv_internal(hm, r, n, 0)
+    perm = r["perm"]
+    x = synth.uniform(5, n)
+    z = np.empty(n)
+    z[perm] = Cinv @ x[perm]
+    a = f.area
+    k = 1.0 / (4.0 * math.pi)
+    cex = (a.sum() - a) * k
+    bb = (1.0 - cfg.emissivity) / cex
+    Md = 1.0 + k * bb * a
+    Mx, Mb = x / Md, bb / Md
+    zcl = Mx + (k * (a @ Mx) / (1.0 - k * (a @ Mb))) * Mb
+    assert rel(z, zcl) <= 10 * cfg.eps_aca
+
+
+@pytest.mark.parametrize("n_fac,n_min", [(1, 64), (2, 64), (5, 2), (20, 64), (20, 2), (80, 3)])
+def test_host_hlu_edge_cases(hm, n_fac, n_min):
+    """Tiny cavities: one facet (F = 0, C = I), two facets, a deep tree on 5 facets, a single dense
+    leaf (n_min >= n: the H-LU is one dense LU), icospheres with leaves of 2-3 facets (deep recursion with
+    low-rank blocks at every level)."""
+    geo = synth.line_facets(n_fac) if n_fac < 20 else synth.icosphere(0 if n_fac == 20 else 1)
+    cfg = synth.make_config(2, geometry=geo)
+    f = cfg.facets
+    n = f.n
+    r = host_factor(hm, cfg, n_min=n_min, cut=0)
+    Cinv, _, _ = cinv_internal(hm, r, n, 0)
+    Fd, Cd, _ = vf.dense_operators(f, cfg.emissivity, closed=cfg.extra.get("closed", True))
+    perm = r["perm"]
+    Ci = Cd[np.ix_(perm, perm)]
+    assert np.abs(Cinv @ Ci - np.eye(n)).max() <= 1e-6
+
+
+def test_host_hlu_bitwise_reproducible_across_thread_counts(hm):
+    """The OpenMP tasks only split independent target blocks: 1 thread and the default thread count
+    give bitwise-identical factors."""
+    code = (
+        "import sys, json, hashlib, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_2305_06891_b200 as hm, synth\n"
+        "from test_hlu_host import host_factor\n"
+        "r = host_factor(hm, synth.make_config(1), cut=0)\n"
+        "h = hashlib.sha256()\n"
+        "for op in (hm.HM_OP_LINV, hm.HM_OP_UINV):\n"
+        "    for it in hm.hm_export_factors(op, r['F'], r['LU']):\n"
+        "        D = it[4]\n"
+        "        for a in (D if isinstance(D, tuple) else (D,)): h.update(np.ascontiguousarray(a).tobytes())\n"
+        "print(json.dumps(h.hexdigest()))\n" % (ROOT, os.path.join(ROOT, "tests")))
+    out = []
+    for thr in ("1", str(os.cpu_count() or 4)):
+        env = dict(os.environ, OMP_NUM_THREADS=thr)
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+        assert p.returncode == 0, p.stderr
+        out.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    assert out[0] == out[1]
+
+
+def test_host_only_context_refuses_the_hot_path(hm):
+    """A host-only context holds factors for export only: the hot path needs the CUDA engine (no CPU
+    fallback)."""
+    r = host_factor(hm, synth.make_config(1), cut=0)
+    x = np.ones(r["g"].n)
+    y = np.empty_like(x)
+    with pytest.raises(hm.HMError):
+        hm.hm_solve_C(r["ctx"], r["LU"], x, y)
+    with pytest.raises(hm.HMError):
+        hm.hm_apply_F(r["ctx"], r["F"], x, y)

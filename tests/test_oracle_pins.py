@@ -158,6 +158,18 @@ def test_own_lu_matches_lapack(cfg1):
     zl = np.linalg.solve(C, b)
     assert np.linalg.norm(z - zl) <= 1e-14 * np.linalg.norm(zl)
     assert np.linalg.norm(C @ z - b) <= 1e-14 * np.linalg.norm(b)
+    # the factor-once / solve-many pair of the CPU baseline (getrf + getrs): the same solution, and the
+    # factors reproduce C (P L U = C)
+    fac = vf.lu_factor(C)
+    z2 = vf.lu_factor_solve(fac, b)
+    assert np.linalg.norm(z2 - zl) <= 1e-14 * np.linalg.norm(zl)
+    lu, piv = fac
+    L = np.tril(lu, -1) + np.eye(f.n)
+    U = np.triu(lu)
+    PA = C.copy()
+    for i, p in enumerate(piv):      # LAPACK row interchanges, applied in order
+        PA[[i, p]] = PA[[p, i]]
+    assert np.abs(L @ U - PA).max() <= 1e-14 * np.abs(C).max()
 
 
 def test_blackbody_identity():
@@ -485,3 +497,26 @@ def test_parallel_plates_view_factor_converges_to_closed_form():
     assert abs(errs[-1]) <= 2.5e-4 * ex
     for a, b in zip(errs, errs[1:]):
         assert 3.8 <= a / b <= 4.2
+
+
+def test_aca_probe_rows_find_a_missed_block_part():
+    """Reading R30 (the probe rows of aca_partial), pinned on a constructed block: X = diag(A, B) with
+    A = u1 v1^T + 1e-9 R (rank one up to noise far below eps) and B = 1e-3 u2 v2^T in the other
+    quadrant.  Plain partial pivoting starts in A's rows, every pivot row after the first lies in A
+    (u vanishes on B's rows), the noise cross trips the stop test and B is never seen: rank 1, error
+    ||B||_F / ||X||_F ~ 1e-3.  With three probes the stop is retried at rows m/4, m/2, 3m/4; the one in
+    B's half passes the test, so the result has B's cross too: rank 2, error at the noise level."""
+    rng = np.random.default_rng(7)
+    m = n = 40
+    h = m // 2
+    X = np.zeros((m, n))
+    u1, v1, u2, v2 = (rng.uniform(0.5, 1.5, h) for _ in range(4))
+    X[:h, :h] = np.outer(u1, v1) + 1e-9 * rng.standard_normal((h, h))
+    X[h:, h:] = 1e-3 * np.outer(u2, v2)
+    eps = 1e-6
+    plain = aca.aca_partial(lambda i: X[i, :], lambda j: X[:, j], m, n, eps, probes=0)
+    probed = aca.aca_partial(lambda i: X[i, :], lambda j: X[:, j], m, n, eps, probes=3)
+    err = lambda r: np.linalg.norm(X - r.U @ r.V.T) / np.linalg.norm(X)
+    assert plain.rank == 1 and err(plain) > 1e-4                 # B missed
+    assert probed.rank == 2 and err(probed) <= eps               # B found by the probe at row m/2
+    assert all(i < h for i in plain.rows) and any(i >= h for i in probed.rows)
