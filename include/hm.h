@@ -217,6 +217,15 @@ hm_status hm_solve_C(hm_ctx* ctx, const hm_hlu* LU, int32_t nrhs, const double* 
 hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* F, const hm_hlu* LU, int32_t nrhs,
                             const double* T, double* q, void* stream);
 
+/* Open cavities (F assembled with closed_cavity = 0): add the radiation to ambient of
+   eqn:flux_to_ambient, B_N = sum_i int_{Gamma_i} (1 - c_i)(T^4 - T_inf^4) phi_N dS,
+   with sigma and eps_i restored (reading R34): every later hm_radiative_flux on LU returns
+   q_i + sigma eps_i (1 - c_i)(T_i^4 - T_inf^4), and hm_cavity_flux / hm_cavity_jacobian include the
+   projected term (its T-derivative in the Jacobian).  c_i = clamped row sums of F (eq:clamped_rowsum,
+   hm_export_row_sums).  enable = 0 removes the term.  HM_ERR_INVALID_ARG for a closed-cavity F or a
+   negative / non-finite T_inf. */
+hm_status hm_set_ambient(hm_ctx* ctx, hm_hlu* LU, int32_t enable, double T_inf);
+
 /* ---- cavity operator around the hot path ------------------------ */
 /* Facet <- node projection P (n_facets x n_nodes, PAPER.md:175-183 eqn:projection_operator,
    P_iM = (1/A_i) int_{Gamma_i} phi_M dS) as host CSR arrays in EXTERNAL facet order: row_ptr[n+1]

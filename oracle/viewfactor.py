@@ -147,6 +147,16 @@ def flux_from_dense(F: np.ndarray, C: np.ndarray, A: np.ndarray, eps: np.ndarray
     return q
 
 
+def ambient_flux(A: np.ndarray, eps: np.ndarray, cvec: np.ndarray, T: np.ndarray, T_inf: float) -> np.ndarray:
+    """Open-cavity radiation to ambient, eqn:flux_to_ambient, per facet in W/m^2 with
+    sigma and eps_i restored (reading R34): q^amb_i = sigma eps_i (1 - c_i) (T_i^4 - T_inf^4) --
+    the part 1 - c_i of facet i's view that misses the cavity sees a black body at T_inf.  Its nodal
+    form B_N = sum_i A_i q^amb_i P_iN is the paper's integral with the one-point facet rule."""
+    T = np.asarray(T, dtype=np.float64)
+    scale = (SIGMA_SB * eps * (1.0 - cvec))
+    return scale[:, None] * (T ** 4 - T_inf ** 4) if T.ndim == 2 else scale * (T ** 4 - T_inf ** 4)
+
+
 def flux_literal(F: np.ndarray, C: np.ndarray, A: np.ndarray, eps: np.ndarray, T: np.ndarray) -> np.ndarray:
     """eq:qi_new_location written out term by term, tiny n only:
     q_i = sigma eps_i / A_i sum_j eps_j sum_k F_ik Cinv_kj (eta_j - eta_i)."""

@@ -104,6 +104,7 @@ def load_library(path: str = LIB_PATH):
         "hm_cavity_jacobian": (C.c_int, [P, P, P, P, I32, P, P, P, P]),
         "hm_shard_plan": (C.c_int, [P, C.c_int, P, P, C.POINTER(I64), P]),
         "hm_export_factors": (C.c_int, [P, P, I32, C.POINTER(I64), C.POINTER(I64), P, P]),
+        "hm_set_ambient": (C.c_int, [P, P, I32, D]),
         "hm_hmat_from_host": (C.c_int, [P, P, P, P, P, P, C.POINTER(P)]),
         "hm_destroy_geom": (None, [P]),
         "hm_destroy_hmat": (None, [P]),
@@ -322,6 +323,12 @@ def hm_factor_hlu(ctx: Context, F: HMatrix, emissivity, eps_lu=0.0, cut_level=-1
     h = C.c_void_p()
     ctx.check(ctx.lib.hm_factor_hlu(ctx.h, F.h, e.ctypes.data, C.byref(p), C.byref(h)), "hm_factor_hlu")
     return HLU(ctx, h, F)
+
+
+def hm_set_ambient(ctx: Context, LU: HLU, T_inf=None) -> None:
+    """Open cavities: add the radiation to ambient at T_inf K (eqn:flux_to_ambient, reading R34) to the
+    fluxes computed with LU; T_inf=None removes it."""
+    ctx.check(ctx.lib.hm_set_ambient(ctx.h, LU.h, 0 if T_inf is None else 1, float(T_inf or 0.0)), "hm_set_ambient")
 
 
 def _rows(F_or_geom_ctx, geom):

@@ -817,6 +817,40 @@ hm_status hm_export_factors(const hm_hmat* Fh, const hm_hlu* LUh, int32_t op, in
     });
 }
 
+hm_status hm_set_ambient(hm_ctx* ctx, hm_hlu* LUh, int32_t enable, double T_inf) {
+    if (!ctx || !LUh) return HM_ERR_INVALID_ARG;
+    Ctx* c = &ctx->c;
+    return guarded(c, [&] {
+        HLU& L = LUh->h;
+        if (!enable) {
+            L.ambient = false;
+            return;
+        }
+        if (c->host_only) throw Error(HM_ERR_NOT_READY, "host-only context: no hot path");
+        if (!(T_inf >= 0.0) || !std::isfinite(T_inf)) throw Error(HM_ERR_INVALID_ARG, "T_inf must be finite and >= 0");
+        const HMat& F = *L.F;
+        if (F.params.closed_cavity)
+            throw Error(HM_ERR_INVALID_ARG, "the ambient term belongs to open cavities (PAPER.md:886-891); F was "
+                                            "assembled with closed-cavity row scaling");
+        const Geom& g = *F.geom;
+        const int64_t n = g.n;
+        std::vector<double> a(n);
+        for (int64_t i = 0; i < n; ++i) a[i] = g.area[i] * (1.0 - F.c_ext[g.perm[i]]);   // A_i (1 - c_i)
+        const cudaStream_t s = c->stream;
+        L.amb_int.upload(c, a, "ambient A(1-c)", s);
+        if (g.shard.sharded()) {
+            const Shard& S = g.shard;
+            std::vector<double> ap(S.n_pad(), 0.0);
+            for (int64_t i = 0; i < n; ++i) ap[S.pad(i)] = a[i];
+            L.amb_pad.upload(c, ap, "ambient A(1-c) (padded)", s);
+        }
+        HM_CUDA(cudaStreamSynchronize(s));
+        const double t2 = T_inf * T_inf;
+        L.t_inf4 = t2 * t2;
+        L.ambient = true;
+    });
+}
+
 hm_status hm_export_row_sums(const hm_hmat* F, double* s, double* c) {
     if (!F) return HM_ERR_INVALID_ARG;
     if (s) std::copy(F->h.s_ext.begin(), F->h.s_ext.end(), s);
@@ -955,6 +989,8 @@ void launch_flux(Ctx* c, HLU& L, const double* Td, double* qd, int ld, int col, 
         a.eps_int = L.eps_pad.p;
         a.area_int = L.area_pad.p;
         a.g_int = L.g_pad.p;
+        a.amb = L.ambient ? L.amb_pad.p : nullptr;
+        a.t_inf4 = L.t_inf4;
         a.T_pad = L.T_pad;
         L.sp_flux.launch(c, g, a, s);
     } else {
@@ -962,6 +998,8 @@ void launch_flux(Ctx* c, HLU& L, const double* Td, double* qd, int ld, int col, 
         a.eps_ext = L.eps_ext.p;
         a.area_int = g.d_geo.p + 6 * g.n;
         a.g_int = L.g_int.p;
+        a.amb = L.ambient ? L.amb_int.p : nullptr;
+        a.t_inf4 = L.t_inf4;
         L.prog_flux.launch(a, s);
     }
 }
@@ -976,6 +1014,8 @@ void launch_flux_m(HLU& L, const double* Td, double* qd, int ld, int r, cudaStre
     a.eps_ext = L.eps_ext.p;
     a.area_int = g.d_geo.p + 6 * g.n;
     a.g_int = L.g_int.p;
+    a.amb = L.ambient ? L.amb_int.p : nullptr;
+    a.t_inf4 = L.t_inf4;
     L.prog_flux_m.launch(a, s);
 }
 
@@ -1017,6 +1057,8 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
                 a.eps_ext = L.eps_ext.p;
                 a.area_int = g.d_geo.p + 6 * g.n;
                 a.g_int = L.g_int.p;
+                a.amb = L.ambient ? L.amb_int.p : nullptr;
+                a.t_inf4 = L.t_inf4;
                 L.prog_flux_h.launch(a, s);
                 if (hout) HM_CUDA(cudaMemcpyAsync(q, qd, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
                 if (!async_ok) HM_CUDA(cudaStreamSynchronize(s));
@@ -1036,6 +1078,8 @@ hm_status hm_radiative_flux(hm_ctx* ctx, const hm_hmat* Fh, const hm_hlu* LUh, i
                 a.eps_int = L.eps_pad.p;
                 a.area_int = L.area_pad.p;
                 a.g_int = L.g_pad.p;
+                a.amb = L.ambient ? L.amb_pad.p : nullptr;
+                a.t_inf4 = L.t_inf4;
                 a.T_pad = L.T_loc_m.p;
                 L.sp_flux_m.launch(c, g, a, s);
             }
@@ -1194,6 +1238,8 @@ void cavity_column(Ctx* c, HLU& L, Proj& P, const double* Tn, const double* xn, 
     a.eps_ext = L.eps_ext.p;
     a.area_int = g.d_geo.p + 6 * g.n;
     a.g_int = L.g_int.p;
+    a.amb = L.ambient ? L.amb_int.p : nullptr;
+    a.t_inf4 = (mode == 0 ? L.t_inf4 : 0.0);   // Jacobian mode: d/dT of the constant T_inf^4 is 0
     a.eta_in = 1;
     a.rbar_out = 1;
     L.prog_flux.launch(a, s);
@@ -1213,6 +1259,8 @@ void cavity_column_sharded(Ctx* c, HLU& L, Proj& P, const double* Tn, const doub
     a.eps_int = L.eps_pad.p;
     a.area_int = L.area_pad.p;
     a.g_int = L.g_pad.p;
+    a.amb = L.ambient ? L.amb_pad.p : nullptr;
+    a.t_inf4 = (mode == 0 ? L.t_inf4 : 0.0);   // Jacobian mode: d/dT of the constant T_inf^4 is 0
     a.T_pad = L.T_pad;
     a.eta_in = 1;
     a.rbar_out = 1;

@@ -342,6 +342,8 @@ struct ProgArgs {
     const double* eps_ext;      // emissivity in external order (IN_FLUX gathers)
     const double* area_int;
     const double* g_int;
+    const double* amb;          // open-cavity ambient term (eqn:flux_to_ambient): A_i (1 - c_i) per row, or nullptr
+    double t_inf4;              // T_inf^4 (0 in the Jacobian mode: the derivative drops the constant)
     double sigma;
     int32_t eta_in;             // 1: the flux input is the facet power eta itself (not T: no T^4)
     int32_t rbar_out;           // 1: emit A o q = (Rbar eta) (eq:Rbardef) instead of q
@@ -490,6 +492,9 @@ struct HLU {
     DBuf<double> xtB;            // [y | t] backward pass
     DBuf<double> z;              // internal-order result
     DBuf<double> eps_int, eps_ext, g_int;
+    DBuf<double> amb_int, amb_pad;   // hm_set_ambient: A_i (1 - c_i), internal / padded order
+    bool ambient = false;
+    double t_inf4 = 0.0;
     DBuf<double> host_stage_in, host_stage_out;
     double setup_seconds[4] = {0, 0, 0, 0};
     int64_t bytes = 0, bytes_leaf = 0, n_blocks = 0, n_lr = 0, rank_sum = 0;

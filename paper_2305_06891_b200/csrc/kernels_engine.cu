@@ -113,7 +113,8 @@ __device__ __forceinline__ void emit(const ProgArgs& A, const Pass& P, int64_t r
             const double t = __ldcg(A.T_pad + row);
             const double eta = A.eta_in ? t : pow4(t);
             const double sc = A.rbar_out ? A.eps_int[row] : A.eps_int[row] / A.area_int[row];
-            A.user_out[(row - A.local0) * A.ld + A.col] = A.sigma * sc * (s - eta * A.g_int[row]);
+            const double amb = A.amb ? A.amb[row] * (eta - A.t_inf4) : 0.0;   // eqn:flux_to_ambient (R34)
+            A.user_out[(row - A.local0) * A.ld + A.col] = A.sigma * sc * (s - eta * A.g_int[row] + amb);
             break;
         }
         default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form);
@@ -122,7 +123,8 @@ __device__ __forceinline__ void emit(const ProgArgs& A, const Pass& P, int64_t r
             const double in = A.user_in[e * A.ld + A.col];
             const double eta = A.eta_in ? in : pow4(in);
             const double sc = A.rbar_out ? A.eps_int[row] : A.eps_int[row] / A.area_int[row];
-            A.user_out[e * A.ld + A.col] = A.sigma * sc * (s - eta * A.g_int[row]);
+            const double amb = A.amb ? A.amb[row] * (eta - A.t_inf4) : 0.0;   // eqn:flux_to_ambient (R34)
+            A.user_out[e * A.ld + A.col] = A.sigma * sc * (s - eta * A.g_int[row] + amb);
         }
     }
 }

@@ -200,14 +200,16 @@ __device__ __forceinline__ void emit_m(const ProgArgs& A, const Pass& P, int64_t
         case OUT_LOCAL: A.user_out[(row - A.local0) * A.ld + col] = s; break;   // sharded: this rank's rows
         case OUT_FLUX_LOCAL: {   // sharded flux epilogue: T (padded rows x 64) and eps / A / g padded
             const double eta = pow4(__ldcg(A.T_pad + row * kMrhsMax + col));
+            const double amb = A.amb ? A.amb[row] * (eta - A.t_inf4) : 0.0;   // eqn:flux_to_ambient (R34)
             A.user_out[(row - A.local0) * A.ld + col] =
-                A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row]);
+                A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row] + amb);
             break;
         }
         default: {  // OUT_FLUX: q = sigma (eps/A) (F z - eta g)  (eq:qi_new_location, operator form)
             const int64_t e = A.perm[row];
             const double eta = pow4(A.user_in[e * A.ld + col]);
-            A.user_out[e * A.ld + col] = A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row]);
+            const double amb = A.amb ? A.amb[row] * (eta - A.t_inf4) : 0.0;   // eqn:flux_to_ambient (R34)
+            A.user_out[e * A.ld + col] = A.sigma * (A.eps_int[row] / A.area_int[row]) * (s - eta * A.g_int[row] + amb);
         }
     }
 }
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 const bool flux = P.mode == OUT_FLUX;
                 for (int r0 = cw; r0 < nrows; r0 += 4 * kMConsumerWarps) {
                     int64_t e[4];
-                    double sc[4], gg[4];
+                    double sc[4], gg[4], am[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int r = r0 + u * kMConsumerWarps;
@@ -523,6 +525,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                         e[u] = __ldg(A.perm + row);
                         sc[u] = flux ? A.sigma * (__ldg(A.eps_int + row) / __ldg(A.area_int + row)) : 0.0;
                         gg[u] = flux ? __ldg(A.g_int + row) : 0.0;
+                        am[u] = flux && A.amb ? __ldg(A.amb + row) : 0.0;
                     }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -539,7 +542,8 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                         for (int u = 0; u < 4; ++u) {
                             const int r = r0 + u * kMConsumerWarps;
                             if (r < nrows && col < R)
-                                A.user_out[e[u] * A.ld + col] = flux ? sc[u] * (v[u] - pow4(t[u]) * gg[u]) : v[u];
+                                A.user_out[e[u] * A.ld + col] =
+                                    flux ? sc[u] * (v[u] - pow4(t[u]) * gg[u] + am[u] * (pow4(t[u]) - A.t_inf4)) : v[u];
                         }
                     }
                 }

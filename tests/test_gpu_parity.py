@@ -704,6 +704,33 @@ def test_parallel_plates_open_cavity(hm, ctx, m):
     torch.cuda.synchronize()
     qo = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]
     assert rel(q.cpu().numpy(), qo) <= 10 * cfg.eps_aca
+    # the open cavity's radiation to ambient (eqn:flux_to_ambient, reading R34), single vector and 8
+    # columns (DMMA engine): q + sigma eps (1 - c)(T^4 - T_inf^4) vs the oracle; then switched off again
+    cvec = vf.clamp_row_sums(vf.row_sums(vf.dense_F(f.centroid, f.normal, f.area), f.area))
+    hm.hm_set_ambient(ctx, LU, 300.0)
+    hm.hm_radiative_flux(ctx, F, LU, T, q)
+    T8 = synth.temperatures(cfg.seed, f.n, 8)
+    q8 = np.empty_like(T8)
+    hm.hm_radiative_flux(ctx, F, LU, T8, q8)
+    torch.cuda.synchronize()
+    qa = qo + vf.ambient_flux(f.area, cfg.emissivity, cvec, cfg.T[:, 0], 300.0)
+    assert rel(q.cpu().numpy(), qa) <= 10 * cfg.eps_aca
+    qa8 = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, T8) + vf.ambient_flux(f.area, cfg.emissivity, cvec, T8, 300.0)
+    assert max(rel(q8[:, c], qa8[:, c]) for c in range(8)) <= 10 * cfg.eps_aca
+    hm.hm_set_ambient(ctx, LU, None)
+    hm.hm_radiative_flux(ctx, F, LU, T, q)
+    torch.cuda.synchronize()
+    assert rel(q.cpu().numpy(), qo) <= 10 * cfg.eps_aca
+
+
+def test_ambient_rejected_for_closed_cavity(hm, ctx):
+    """eqn:flux_to_ambient belongs to open cavities: a closed-cavity F refuses it."""
+    cfg = synth.make_config(1)
+    f = cfg.facets
+    g, F = build(hm, ctx, f, cfg.n_min, cfg.eps_aca)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    with pytest.raises(hm.HMError):
+        hm.hm_set_ambient(ctx, LU, 300.0)
 
 
 def test_flux_cuda_graph_replay(hm, ctx):

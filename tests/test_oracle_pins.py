@@ -499,6 +499,34 @@ def test_parallel_plates_view_factor_converges_to_closed_form():
         assert 3.8 <= a / b <= 4.2
 
 
+def test_ambient_flux_open_plates_closed_forms():
+    """Reading R34 (eqn:flux_to_ambient) on the open parallel plates: (a) T = T_inf
+    everywhere: no net flux at all (the cavity exchange of an isothermal enclosure vanishes, Rbar 1 = 0,
+    and so does the ambient term); (b) isothermal plates at T != T_inf: the cavity exchange still vanishes
+    and the total loss sum_i A_i q_i equals sigma eps (T^4 - T_inf^4) sum_i A_i (1 - c_i), where
+    sum_i A_i c_i = sum_ij F_ij = 2 A F_12 -- so the total converges to 2 (1 - 0.199825) sigma eps
+    (T^4 - T_inf^4) (Howell's closed form of F_12) at O(h^2)."""
+    ex = _howell_parallel_squares(1.0, 1.0)
+    errs = []
+    for m in (10, 20, 40):
+        f = synth.parallel_plates(m)
+        eps = np.full(f.n, 0.8)
+        F, C, cvec = vf.dense_operators(f, eps, closed=False)
+        for T, Tinf in ((np.full(f.n, 450.0), 450.0), (np.full(f.n, 900.0), 300.0)):
+            q = vf.flux_from_dense(F, C, f.area, eps, T)[:, 0] + vf.ambient_flux(f.area, eps, cvec, T, Tinf)
+            base = vf.SIGMA_SB * 0.8 * (900.0 ** 4)
+            if T[0] == Tinf:
+                assert np.abs(q).max() <= 1e-12 * base
+            else:
+                qa = vf.SIGMA_SB * 0.8 * (1.0 - cvec) * (900.0 ** 4 - 300.0 ** 4)
+                assert np.abs(q - qa).max() <= 1e-12 * base
+                tot = float(f.area @ q) / (vf.SIGMA_SB * 0.8 * (900.0 ** 4 - 300.0 ** 4))
+                errs.append(tot - 2.0 * (1.0 - ex))
+    assert abs(errs[-1]) <= 1e-3
+    for a, b in zip(errs, errs[1:]):
+        assert 3.8 <= a / b <= 4.2
+
+
 def test_aca_probe_rows_find_a_missed_block_part():
     """Reading R30 (the probe rows of aca_partial), pinned on a constructed block: X = diag(A, B) with
     A = u1 v1^T + 1e-9 R (rank one up to noise far below eps) and B = 1e-3 u2 v2^T in the other
