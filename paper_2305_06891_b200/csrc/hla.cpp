@@ -1104,6 +1104,11 @@ HFactor::~HFactor() = default;
 
 int HFactor::threads() const { return omp_get_max_threads(); }
 
+void parallel_for(int64_t n, const std::function<void(int64_t)>& f) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < n; ++i) f(i);
+}
+
 void HFactor::for_each_leaf(const std::function<void(int, Mat&)>& f) {
     const int64_t nb = (int64_t)by_block_.size();
 #pragma omp parallel for schedule(dynamic, 256)

@@ -97,6 +97,8 @@ private:
 // Truncate U V^T (U m x K, V n x K) in place to the smallest rank whose Frobenius tail is
 // <= eps ||U V^T||_F; returns the new rank (U, V resized to m x k', n x k').
 void prof_dump();
+// f(i) for i in [0, n), OpenMP-parallel (host helper for callers compiled without OpenMP)
+void parallel_for(int64_t n, const std::function<void(int64_t)>& f);
 int truncate(int64_t m, int64_t n, int K, std::vector<double>& U, std::vector<double>& V, double eps);
 
 }  // namespace hla

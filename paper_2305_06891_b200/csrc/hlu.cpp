@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <malloc.h>
 #include <memory>
 
 #include <unordered_map>
@@ -411,8 +412,11 @@ void read_items(Ctx* c, const HOp& op, const std::function<bool(size_t)>& want_v
         double* hp = host.get((size_t)std::max<int64_t>(tot, 1));
         if (tot > 0) HM_CUDA(cudaMemcpyAsync(hp, stage.p, (size_t)tot * sizeof(double), cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaStreamSynchronize(s));
-        for (size_t q = i0; q < i1; ++q)
-            fn(q, hp + po[q - i0], vo[q - i0] >= 0 ? hp + vo[q - i0] : nullptr);
+        // items of a batch write disjoint destinations: scatter them on all host threads
+        hla::parallel_for((int64_t)(i1 - i0), [&](int64_t d) {
+            const size_t q = i0 + (size_t)d;
+            fn(q, hp + po[d], vo[d] >= 0 ? hp + vo[d] : nullptr);
+        });
         i0 = i1;
     }
 }
@@ -655,7 +659,17 @@ void stage_b_root(HLU& L, const HMat& F, const Geom& g, const std::vector<double
 // the library's communicator (one header, the block records, the payload); every rank rebuilds the
 // same block lists on its own copy, keeps its rows when it packs (build_hop with the shard).  A
 // failure on rank 0 travels in the header, so no rank waits on a broadcast that never comes.
+void stage_b_inner(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& lam, int Lc, FactorSet& out);
+
+// The factorisation's millions of small host blocks are freed when it ends; hand the arena memory back
+// to the system (glibc keeps freed small chunks in its per-thread arenas otherwise, and a process that
+// factors twice at C5 size would hold both peaks)
 void stage_b(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& lam, int Lc, FactorSet& out) {
+    struct Trim { ~Trim() { malloc_trim(0); } } trim;
+    stage_b_inner(L, F, g, lam, Lc, out);
+}
+
+void stage_b_inner(HLU& L, const HMat& F, const Geom& g, const std::vector<double>& lam, int Lc, FactorSet& out) {
     Ctx* c = L.ctx;
     if (c->host_only || !g.shard.sharded() || !c->ex) {
         stage_b_root(L, F, g, lam, Lc, out);

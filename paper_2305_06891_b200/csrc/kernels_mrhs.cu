@@ -611,7 +611,19 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
         if (chunk != nchunks - 1) continue;
         // ---- last chunk of the task: emit (split panels combine deterministically), publish
         if (type == UNIT_STREAM) {
-            if (grp < 0) {
+            if (grp < 0 && P.mode == OUT_ASSIGN) {
+                // internal n x 64 result (t or y): one 16-byte store per fragment pair (columns past R
+                // hold values of the zero-free padding columns and are never read)
+#pragma unroll
+                for (int i = 0; i < kMaxTiles; ++i) {
+                    int mt, nt;
+                    if (!warp_tile(i, cw, M8, N8, mt, nt)) break;
+                    const int row = mt * 8 + ar;
+                    const int col = nt * 8 + 2 * ak;
+                    if (row < nrows)
+                        *reinterpret_cast<double2*>(P.out + (out0 + row) * kMrhsMax + col) = make_double2(acc[i][0], acc[i][1]);
+                }
+            } else if (grp < 0) {
 #pragma unroll
                 for (int i = 0; i < kMaxTiles; ++i) {
                     int mt, nt;
