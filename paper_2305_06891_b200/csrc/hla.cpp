@@ -555,6 +555,14 @@ struct Impl {
     std::mutex mu;
     std::string where;
     int64_t task_min;   // spawn tasks only for blocks with at least this many entries
+    // which admissible blocks are accumulated dense: -1 (default) those between two leaf clusters,
+    // > 0 those of at most this many entries, 0 none (HM_HLU_ACC_MAX; measured on C2, 8 threads:
+    // leaf pairs 8.3 s, <= 80 x 80 entries 10.9 s, none 12.0 s)
+    int64_t acc_max = getenv("HM_HLU_ACC_MAX") ? atol(getenv("HM_HLU_ACC_MAX")) : -1;
+    bool acc_block(const Mat& A) const {
+        if (acc_max < 0) return nodes[A.rn].is_leaf() && nodes[A.cn].is_leaf();
+        return A.m * A.n <= acc_max;
+    }
 
     bool big(const Mat& M) const { return M.m * M.n >= task_min; }
 
@@ -812,7 +820,7 @@ struct Impl {
             c->c0 = cj.begin;
             c->m = ri.size();
             c->n = cj.size();
-            if (ri.is_leaf() && cj.is_leaf()) {   // leaf pair: accumulate dense (see densify_leaf_pairs)
+            if (acc_block(*c)) {   // accumulate dense (see densify_leaf_pairs)
                 c->type = T_DENSE;
                 c->D.assign((size_t)(c->m * c->n), 0.0);
             } else {
@@ -823,8 +831,78 @@ struct Impl {
         return T;
     }
 
+    // ---- dense view C (m x n, ldc) += alpha A B, any operand types (a dense target with a block
+    // structure below it -- an admissible block accumulated dense -- is split along the operands)
+    void mm_dview(double* Cp, int64_t ldc, int64_t m, int64_t n, const Mat& A, const Mat& B, double alpha) {
+        if (A.type == T_LR || B.type == T_LR) {
+            if (A.type == T_LR && B.type == T_LR) {
+                if (A.k == 0 || B.k == 0) return;
+                Vec core((size_t)A.k * B.k, 0.0);
+                gemm_tn(A.k, B.k, A.n, 1.0, A.V.data(), A.n, B.U.data(), B.m, core.data(), A.k);
+                Vec Up((size_t)(A.m * B.k), 0.0);
+                gemm_nn(A.m, B.k, A.k, 1.0, A.U.data(), A.m, core.data(), A.k, Up.data(), A.m);
+                gemm_nt(m, n, B.k, alpha, Up.data(), A.m, B.V.data(), B.n, Cp, ldc);
+            } else if (A.type == T_LR) {
+                if (A.k == 0) return;
+                Vec T((size_t)(B.n * A.k), 0.0);
+                hmul(B, true, A.V.data(), A.n, A.k, T.data(), B.n, 1.0);
+                gemm_nt(m, n, A.k, alpha, A.U.data(), A.m, T.data(), B.n, Cp, ldc);
+            } else {
+                if (B.k == 0) return;
+                Vec Z((size_t)(A.m * B.k), 0.0);
+                hmul(A, false, B.U.data(), B.m, B.k, Z.data(), A.m, 1.0);
+                gemm_nt(m, n, B.k, alpha, Z.data(), A.m, B.V.data(), B.n, Cp, ldc);
+            }
+            return;
+        }
+        if (A.type == T_DENSE && B.type == T_DENSE) {
+            gemm_nn(m, n, A.n, alpha, A.D.data(), A.m, B.D.data(), B.m, Cp, ldc);
+        } else if (A.type == T_SUB && B.type == T_DENSE) {
+            hmul(A, false, B.D.data(), B.m, B.n, Cp, ldc, alpha);
+        } else if (A.type == T_DENSE && B.type == T_SUB) {
+            Vec At = transpose(A.D.data(), A.m, A.n, A.m);   // sigma x rho
+            Vec Z((size_t)(B.n * A.m), 0.0);                 // B^T A^T = (A B)^T
+            hmul(B, true, At.data(), A.n, A.m, Z.data(), B.n, 1.0);
+            for (int64_t j = 0; j < n; ++j)
+                for (int64_t i = 0; i < m; ++i) Cp[i + j * ldc] += alpha * Z[j + i * B.n];
+        } else {   // both subdivided: quadrants of the view
+            const int64_t m0 = A.ch(0, 0)->m, n0 = B.ch(0, 0)->n;
+            for (int q = 0; q < 4; ++q) {
+                const int i = q >> 1, j = q & 1;
+                double* Cq = Cp + (i ? m0 : 0) + (j ? n0 : 0) * ldc;
+                const int64_t mq = i ? m - m0 : m0, nq = j ? n - n0 : n0;
+                for (int l = 0; l < 2; ++l) mm_dview(Cq, ldc, mq, nq, *A.ch(i, l), *B.ch(l, j), alpha);
+            }
+        }
+    }
+
+    // an admissible block accumulated dense, as a temporary low-rank operand (for products whose
+    // target is not dense: their update then has the block's rank, not its dimension)
+    std::unique_ptr<Mat> acc_as_lr(const Mat& A) {
+        auto T = std::make_unique<Mat>();
+        T->m = A.m;
+        T->n = A.n;
+        T->r0 = A.r0;
+        T->c0 = A.c0;
+        T->rn = A.rn;
+        T->cn = A.cn;
+        T->type = T_LR;
+        T->k = dense_to_lr(A.D.data(), A.m, A.n, T->U, T->V);
+        return T;
+    }
+
     // ---- C += alpha A B
     void mm(Mat& C, const Mat& A, const Mat& B, double alpha) {
+        // (only when the other operand is not low rank: then the update has that operand's rank anyway)
+        const bool ca = A.acc && A.type == T_DENSE && B.type != T_LR;
+        const bool cb = B.acc && B.type == T_DENSE && A.type != T_LR;
+        if (C.type != T_DENSE && (ca || cb)) {
+            std::unique_ptr<Mat> a2, b2;
+            if (ca) a2 = acc_as_lr(A);
+            if (cb) b2 = acc_as_lr(B);
+            mm(C, a2 ? *a2 : A, b2 ? *b2 : B, alpha);
+            return;
+        }
         if (A.type == T_LR || B.type == T_LR) {
             if (A.type == T_LR && B.type == T_LR) {
                 if (A.k == 0 || B.k == 0) return;
@@ -854,20 +932,8 @@ struct Impl {
         }
         // A, B dense or subdivided
         if (C.type == T_DENSE) {
-            if (A.type == T_DENSE && B.type == T_DENSE) {
-                ProfT _p(13);
-                gemm_nn(C.m, C.n, A.n, alpha, A.D.data(), A.m, B.D.data(), B.m, C.D.data(), C.m);
-            } else if (A.type == T_SUB && B.type == T_DENSE) {
-                hmul(A, false, B.D.data(), B.m, B.n, C.D.data(), C.m, alpha);
-            } else if (A.type == T_DENSE && B.type == T_SUB) {
-                Vec At = transpose(A.D.data(), A.m, A.n, A.m);   // sigma x rho
-                Vec Z((size_t)(B.n * A.m), 0.0);                 // B^T A^T = (A B)^T
-                hmul(B, true, At.data(), A.n, A.m, Z.data(), B.n, 1.0);
-                for (int64_t j = 0; j < C.n; ++j)
-                    for (int64_t i = 0; i < C.m; ++i) C.D[i + j * C.m] += alpha * Z[j + i * B.n];
-            } else {
-                throw std::logic_error("hla: dense target of two subdivided factors");
-            }
+            ProfT _p(13);
+            mm_dview(C.D.data(), C.m, C.m, C.n, A, B, alpha);
             return;
         }
         if (C.type == T_LR) {
@@ -1005,7 +1071,7 @@ struct Impl {
             for (auto& c : A.c) densify_leaf_pairs(*c);
             return;
         }
-        if (A.type != T_LR || !nodes[A.rn].is_leaf() || !nodes[A.cn].is_leaf()) return;
+        if (A.type != T_LR || !acc_block(A)) return;
         A.D.assign((size_t)(A.m * A.n), 0.0);
         gemm_nt(A.m, A.n, A.k, 1.0, A.U.data(), A.m, A.V.data(), A.n, A.D.data(), A.m);
         A.U.clear();
@@ -1135,7 +1201,7 @@ void HFactor::factor(double eps) {
     const auto t0 = std::chrono::steady_clock::now();
     Impl I{nodes_, eps};
     I.task_min = env_task_min();
-    if (!getenv("HM_HLU_NO_DENSE_LEAF_PAIRS")) run_tasks(I, [&](Impl& im) { im.densify_leaf_pairs(*root_); });
+    if (I.acc_max != 0) run_tasks(I, [&](Impl& im) { im.densify_leaf_pairs(*root_); });
     run_tasks(I, [&](Impl& im) { im.lu(*root_); });
     singular_ = I.singular;
     singular_where_ = I.where;
