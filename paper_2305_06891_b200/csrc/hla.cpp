@@ -451,10 +451,13 @@ int truncate(int64_t m, int64_t n, int K, Vec& U, Vec& V, double eps) {
         }
     }
     ProfT _g(3);
-    U.resize((size_t)(m * kn));
-    V.resize((size_t)(n * kn));
-    apply_q(fu, A.data(), kn, U.data());
-    apply_q(fv, B.data(), kn, V.data());
+    // fresh exact-size factors (a resize would keep the m x K capacity of the untruncated sum alive in
+    // every block: measured 2x host memory at C5)
+    Vec Un((size_t)(m * kn)), Vn((size_t)(n * kn));
+    apply_q(fu, A.data(), kn, Un.data());
+    apply_q(fv, B.data(), kn, Vn.data());
+    U.swap(Un);
+    V.swap(Vn);
     return kn;
 }
 
@@ -540,8 +543,11 @@ int compress_dense(const double* D, int64_t m, int64_t n, double eps, Vec& U, Ve
         V.clear();
         return 0;
     }
-    U.resize((size_t)(m * k));
-    apply_q(f, Ui.data(), k, U.data());
+    Vec Un((size_t)(m * k));
+    apply_q(f, Ui.data(), k, Un.data());
+    U.swap(Un);
+    Vt.resize((size_t)(n * k));
+    Vt.shrink_to_fit();
     V.swap(Vt);
     return k;
 }

@@ -956,7 +956,7 @@ void factor_hlu(HLU& L, const double* emissivity) {
             P.n_x = n;
             // prologue: b (or w = eps T^4) into the internal n x 64 layout, then every gather is a
             // 512-byte TMA row copy
-            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, 32);
+            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, elementwise_rows(n));
             P.add_stream(L.leafL.p1m, L.leafL, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN);
             P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
                          (int)P.h_passes.size() - 2);
@@ -967,13 +967,13 @@ void factor_hlu(HLU& L, const double* emissivity) {
         // final results go to an internal n x 64 buffer, then an element-wise epilogue pass emits them
         // (permute-out / flux epilogue) coalesced and fully parallel
         mprog(L.prog_solve_m, IN_PERM, Fm.y_m.p, OUT_ASSIGN);
-        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_PERM);
+        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_PERM);
         L.prog_solve_m.finalize(c, s, &g);
         mprog(L.prog_flux_m, IN_FLUX, Fm.xt_m.p, OUT_ASSIGN);
         L.prog_flux_m.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
         L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
                                  (int)L.prog_flux_m.h_passes.size() - 2);
-        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_FLUX);
+        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_FLUX);
         L.prog_flux_m.finalize(c, s, &g);
     } else if (!g.shard.sharded()) {
         // level form (cut level > 0) with 64 columns: the same tree-scheduled sweeps as the single-vector
@@ -984,7 +984,7 @@ void factor_hlu(HLU& L, const double* emissivity) {
         auto mprog_lf = [&](Program& P, int in_mode, double* out_u) {
             P.mrhs = true;
             P.n_x = n;
-            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, 32);
+            P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, elementwise_rows(n));
             P.sweep_dep[0] = (int32_t)P.h_passes.size() - 1;
             for (int lv = 0; lv < Lc; ++lv) {
                 HOp& op = L.fwd[lv];
@@ -1007,13 +1007,13 @@ void factor_hlu(HLU& L, const double* emissivity) {
             P.add_stream(L.leafU.p2m, L.leafU, L.xtB_m.p, out_u, OUT_ASSIGN, DEP_BWD_P2, &u2);
         };
         mprog_lf(L.prog_solve_m, IN_PERM, Fm.y_m.p);
-        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_PERM);
+        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_PERM);
         L.prog_solve_m.finalize(c, s, &g);
         mprog_lf(L.prog_flux_m, IN_FLUX, Fm.xt_m.p);
         L.prog_flux_m.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
         L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
                                  (int)L.prog_flux_m.h_passes.size() - 2);
-        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, 32, Fm.y_m.p, OUT_FLUX);
+        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_FLUX);
         L.prog_flux_m.finalize(c, s, &g);
     }
 

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -417,6 +418,14 @@ struct SegProgram {
     }
     void launch(Ctx* ctx, const Geom& g, ProgArgs a, cudaStream_t s);
 };
+
+// rows per element-wise unit of the multi-RHS programs (prologue / permute / epilogue): one unit per
+// SM (measured C2 64-RHS flux: 32-row units took 15 + 30 us for the prologue and epilogue, every
+// unit paying the pipeline's per-chunk latency), at least 32 rows
+inline int elementwise_rows(int64_t n) {
+    const int64_t r = (n + 147) / 148;
+    return (int)std::max<int64_t>(32, (r + 7) & ~int64_t(7));
+}
 
 size_t engine_smem_bytes();
 int engine_mrhs_grid();

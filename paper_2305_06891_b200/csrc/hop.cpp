@@ -26,6 +26,11 @@ static int env_int(const char* name, int dflt) {
     return v >= 1 && v <= 1 << 20 ? v : dflt;
 }
 
+static bool force_colsrc() {
+    const char* e = getenv("HM_FORCE_COLSRC");
+    return e && e[0] == '1';
+}
+
 // Cut panels into pieces (only panels above 512 KB are split, for load balance) and pieces into
 // chunks of <= one engine stage of contiguous payload (<= 256 columns), each chunk with its own 16-byte
 // aligned column-source segment (so the engine can TMA both).
@@ -120,7 +125,8 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
                                 ok = false;
                             }
                         }
-                        u.nruns = ok ? nr : 0;
+                        // HM_FORCE_COLSRC=1 (tests): every chunk takes the per-column colsrc path
+                        u.nruns = ok && !force_colsrc() ? nr : 0;
                     }
                     while (PC.cs.size() % 4) PC.cs.push_back(0);
                     u.ld = pn.ld;

@@ -136,7 +136,25 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const dou
 // fragment feeds two DMMAs and shared-memory fragment traffic per DMMA drops from (TM + 1) / TM to
 // (TM / 2 + 2) / TM (shared memory is the co-bottleneck with the TMA writes).  Otherwise tiles
 // t = cw + 8 i, (mt, nt) = (t / N8, t mod N8).  Tile i of the warp -> (mt, nt); false past the last.
+// 64 columns and an odd number of row tiles <= 7 (40-row leaf panels: 5): one column tile per warp and
+// every row tile ("1-D"), so all 8 warps issue the same M8 DMMAs per k-step (the 2-D tiling gives
+// ceil(M8/2) and floor(M8/2) row tiles to the two warp halves).  Off by default: measured on C2 64-RHS
+// flux 0.915 ms (1-D) vs 0.901 ms (2-D) -- the 2-D tiling's fewer shared-memory fragment loads per DMMA
+// outweigh its imbalance; HM_MRHS_TILE1D=1 at build time selects 1-D
+#ifndef HM_MRHS_GATHER_LDG
+#define HM_MRHS_GATHER_LDG 1
+#endif
+#ifndef HM_MRHS_TILE1D
+#define HM_MRHS_TILE1D 0
+#endif
+__device__ __forceinline__ bool use_1d(int M8, int N8) { return HM_MRHS_TILE1D && N8 == 8 && (M8 & 1) && M8 <= 7; }
+
 __device__ __forceinline__ bool warp_tile(int i, int cw, int M8, int N8, int& mt, int& nt) {
+    if (use_1d(M8, N8)) {
+        mt = i;
+        nt = cw;
+        return i < M8;
+    }
     if (N8 == 8) {
         mt = (cw >> 2) + 2 * (i >> 1);
         nt = 2 * (cw & 3) + (i & 1);
@@ -185,6 +203,38 @@ __device__ __forceinline__ void mma_chunk2d(double (&acc)[kMaxTiles][2], const d
             dmma(acc[2 * j], a[j], b0);
             dmma(acc[2 * j + 1], a[j], b1);
         }
+    }
+}
+
+// 1-D tiling: RM row tiles x this warp's column tile cw, acc[j]
+template <int RM>
+__device__ __forceinline__ void mma_chunk1d(double (&acc)[kMaxTiles][2], const double* __restrict__ Ap,
+                                            const double* __restrict__ Xp, int ld, int ncols, int cw, int ar,
+                                            int ak) {
+    int arow[RM];
+#pragma unroll
+    for (int j = 0; j < RM; ++j) arow[j] = j * 8 + ar;
+    const int bc = cw * 8 + ar;
+    const int nfull = ncols & ~3;
+    for (int k4 = 0; k4 < nfull; k4 += 4) {
+        const double* Ak = Ap + (k4 + ak) * ld;
+        double a[RM];
+#pragma unroll
+        for (int j = 0; j < RM; ++j) a[j] = Ak[arow[j]];
+        const double b = Xp[(k4 + ak) * kXStride + bc];
+#pragma unroll
+        for (int j = 0; j < RM; ++j) dmma(acc[j], a[j], b);
+    }
+    if (nfull < ncols) {   // k tail: zero A past ncols (stale A could be NaN; X rows there are zero)
+        const int kk = nfull + ak;
+        const bool kv = kk < ncols;
+        const double* Ak = Ap + kk * ld;
+        double a[RM];
+#pragma unroll
+        for (int j = 0; j < RM; ++j) a[j] = kv ? Ak[arow[j]] : 0.0;
+        const double b = Xp[kk * kXStride + bc];
+#pragma unroll
+        for (int j = 0; j < RM; ++j) dmma(acc[j], a[j], b);
     }
 }
 
@@ -342,7 +392,27 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 const int im = P.in_mode;
                 const int32_t* cs = P.colsrc + H.cs_off;   // colsrc_ext for fused-prologue passes
                 const int ncol4 = (ncols + 3) & ~3;
-                if (im == IN_PLAIN) {
+                if (im == IN_PLAIN && HM_MRHS_GATHER_LDG) {
+                    // X rows (512 B each, written by an earlier pass: L2) by coalesced 16-byte loads, 16
+                    // rows in flight per warp -- one load + one shared store per row and warp (the per-row
+                    // TMA issue serialises over the lanes through the uniform datapath: measured 8 % of
+                    // the kernel's stall samples)
+                    for (int c0 = gw; c0 < ncol4; c0 += 16 * kMGatherers) {
+                        double2 v[16];
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const int c = c0 + u * kMGatherers;
+                            v[u] = make_double2(0.0, 0.0);
+                            if (c < ncols)
+                                v[u] = __ldcg(reinterpret_cast<const double2*>(in + (int64_t)__ldg(cs + c) * kMrhsMax) + lane);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const int c = c0 + u * kMGatherers;
+                            if (c < ncol4) reinterpret_cast<double2*>(St.X + c * kXStride)[lane] = v[u];
+                        }
+                    }
+                } else if (im == IN_PLAIN) {
                     // each X row (512 B, written by an earlier pass) arrives by a 1-D TMA bulk copy:
                     // warp gw, lane l -> column c = gw + kMGatherers * l
                     const int c = gw + kMGatherers * lane;
@@ -484,7 +554,15 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             // this warp's tiles t = cw + 8 i (row tiles mt, column tile nt); the k loop is
             // specialised on the tile count so the fragments of a k-step are loaded as a batch into
             // distinct registers and then feed back-to-back DMMAs
-            if (N8 == 8) {
+            if (use_1d(M8, N8)) {
+                switch (M8) {
+                    case 1: mma_chunk1d<1>(acc, Ap, Xp, ldp, ncols, cw, ar, ak); break;
+                    case 3: mma_chunk1d<3>(acc, Ap, Xp, ldp, ncols, cw, ar, ak); break;
+                    case 5: mma_chunk1d<5>(acc, Ap, Xp, ldp, ncols, cw, ar, ak); break;
+                    case 7: mma_chunk1d<7>(acc, Ap, Xp, ldp, ncols, cw, ar, ak); break;
+                    default: break;
+                }
+            } else if (N8 == 8) {
                 switch ((M8 - (cw >> 2) + 1) >> 1) {   // this warp's row tiles
 #define HM_MMA2_CASE(RM) \
     case RM: mma_chunk2d<RM>(acc, Ap, Xp, ldp, ncols, cw, ar, ak); break;

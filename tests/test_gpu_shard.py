@@ -279,3 +279,35 @@ def test_nccl_exchanger_selftest():
     hm.hm_nccl_selftest(0, 1 << 16)
     with pytest.raises(hm.HMError):
         hm.hm_nccl_selftest(0, 0)
+
+
+def test_virtual_shards_forced_colsrc_path():
+    """ADVICE (round 1): the sharded flux's IN_FLUXI gathers read per-column sources (colsrc) only for
+    chunks whose sources exceed the run-length descriptor; HM_FORCE_COLSRC=1 sends EVERY chunk of every
+    operator down that path, so a null or wrong column-source array faults or mismatches here.  G = 2
+    virtual ranks against the dense oracle."""
+    import os
+    import paper_2305_06891_b200 as hm
+    cfg = synth.make_config(2, geometry=synth.icosphere(3))
+    f = cfg.facets
+    out, errs = {}, []
+    os.environ["HM_FORCE_COLSRC"] = "1"
+    try:
+        th = [threading.Thread(target=_run_rank, args=(hm, r, 2, 1300, cfg, out, errs)) for r in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+    finally:
+        del os.environ["HM_FORCE_COLSRC"]
+    assert not errs, errs
+    n = f.n
+    Y, Z, Q = np.empty(n), np.empty(n), np.empty(n)
+    for r in range(2):
+        o = out[r]
+        Y[o["rows"]], Z[o["rows"]], Q[o["rows"]] = o["y"], o["z"], o["q"]
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity)
+    x = cfg.rhs()[:, 0]
+    assert rel(Y, Fd @ x) <= 10 * cfg.eps_aca
+    assert rel(Z, vf.solve(C, x)) <= 10 * cfg.eps_aca
+    assert rel(Q, vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]) <= 10 * cfg.eps_aca
