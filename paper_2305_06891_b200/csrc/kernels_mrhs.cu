@@ -142,7 +142,7 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const dou
 // flux 0.915 ms (1-D) vs 0.901 ms (2-D) -- the 2-D tiling's fewer shared-memory fragment loads per DMMA
 // outweigh its imbalance; HM_MRHS_TILE1D=1 at build time selects 1-D
 #ifndef HM_MRHS_GATHER_LDG
-#define HM_MRHS_GATHER_LDG 1
+#define HM_MRHS_GATHER_LDG 0
 #endif
 #ifndef HM_MRHS_TILE1D
 #define HM_MRHS_TILE1D 0
@@ -394,9 +394,10 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 const int ncol4 = (ncols + 3) & ~3;
                 if (im == IN_PLAIN && HM_MRHS_GATHER_LDG) {
                     // X rows (512 B each, written by an earlier pass: L2) by coalesced 16-byte loads, 16
-                    // rows in flight per warp -- one load + one shared store per row and warp (the per-row
-                    // TMA issue serialises over the lanes through the uniform datapath: measured 8 % of
-                    // the kernel's stall samples)
+                    // rows in flight per warp (HM_MRHS_GATHER_LDG=1 at build time).  Off: although the
+                    // per-row TMA issue serialises over the lanes (8 % of the kernel's stall samples),
+                    // the register path measured slower (C2 64-RHS flux 1.180 vs 0.913 ms): the gather
+                    // warps then wait out the L2 latency themselves instead of moving on
                     for (int c0 = gw; c0 < ncol4; c0 += 16 * kMGatherers) {
                         double2 v[16];
 #pragma unroll

@@ -265,7 +265,8 @@ hm_status hm_nccl_unique_id(void* id_out) {
 }
 
 // One-rank communicator on `device`, then the exact in-place allgather call the sharded hot path
-// issues (NcclExchanger::allgather) on a device buffer of `count` doubles, checked element by
+// issues (NcclExchanger::allgather) and the factor broadcast's ncclBroadcast on a device buffer of
+// `count` doubles, checked element by
 // element.  A one-GPU box cannot run world > 1 over NCCL (duplicate device), so this is how the
 // dlopen'd symbols, the unique-id handoff and the call form are exercised on real hardware.
 hm_status hm_nccl_selftest(int device, int64_t count) {
@@ -284,6 +285,7 @@ hm_status hm_nccl_selftest(int device, int64_t count) {
         if (cudaStreamCreate(&s) != cudaSuccess) { cudaFree(d); return HM_ERR_CUDA; }
         cudaMemcpyAsync(d, h.data(), sizeof(double) * (size_t)count, cudaMemcpyHostToDevice, s);
         ex.allgather(d, count, s);
+        ex.broadcast(d, sizeof(double) * (size_t)count, 0, s);   // the factor broadcast's call form
         cudaMemcpyAsync(back.data(), d, sizeof(double) * (size_t)count, cudaMemcpyDeviceToHost, s);
         const cudaError_t ce = cudaStreamSynchronize(s);
         cudaStreamDestroy(s);
