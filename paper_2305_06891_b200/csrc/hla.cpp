@@ -33,8 +33,8 @@ namespace hla {
 
 using Vec = std::vector<double>;
 
-static std::atomic<int64_t> g_prof[16];
-static std::atomic<int64_t> g_ns[16];
+static std::atomic<int64_t> g_prof[24];
+static std::atomic<int64_t> g_ns[24];
 struct ProfT {
     int id;
     std::chrono::steady_clock::time_point t0;
@@ -50,9 +50,10 @@ void prof_dump() {
     for (int b = 0; b < 5; ++b)
         if (g_hist[b]) fprintf(stderr, "  addlr-lr max(m,n) bucket %d: %lld calls, mean update rank %.1f\n", b,
                                (long long)g_hist[b].load(), (double)g_histk[b].load() / g_hist[b].load());
-    static const char* names[16] = {"trunc", "qr", "jacobi", "trunc-gemm", "addlr-lr", "agglom", "mm-lrlr", "mm-lrA",
-                                    "mm-lrB", "hmul-dense", "hmul-lr", "solve-dense", "lu-dense", "mm-dd", "addlr-subtop", "compress-dense"};
-    for (int i = 0; i < 16; ++i)
+    static const char* names[24] = {"trunc", "qr", "jacobi", "trunc-gemm", "addlr-lr", "agglom", "mm-lrlr", "mm-lrA",
+                                    "mm-lrB", "hmul-dense", "hmul-lr", "solve-dense", "lu-dense", "mm-dd", "addlr-subtop", "compress-dense",
+                                    "trsmR-dense", "mmLR-dd", "mmLR-dsub", "mmLR-subd", "mmLR-subsub", "addlr-dense", "form-leaf", "x"};
+    for (int i = 0; i < 24; ++i)
         if (g_prof[i]) fprintf(stderr, "  %-12s %10lld calls %9.3f s\n", names[i], (long long)g_prof[i].load(), g_ns[i].load() * 1e-9);
 }
 
@@ -688,6 +689,7 @@ struct Impl {
     void trsm_right(const Mat& T, bool lower, Mat& X) {
         const int kind = lower ? S_LLT : S_LUT;   // (X T^-1)^T = T^-T X^T
         if (X.type == T_DENSE) {
+            ProfT _p(16);
             Vec Xt = transpose(X.D.data(), X.m, X.n, X.m);
             solve(T, kind, Xt.data(), X.n, X.m);
             for (int64_t j = 0; j < X.n; ++j)
@@ -721,6 +723,7 @@ struct Impl {
         if (C.type == T_SUB && fan_depth == 0) g_prof[14].fetch_add(1);
         struct FD { bool on; FD(bool b) : on(b) { if (on) ++fan_depth; } ~FD() { if (on) --fan_depth; } } fd(C.type == T_SUB);
         if (C.type == T_DENSE) {
+            ProfT _p(21);
             gemm_nt(C.m, C.n, k, alpha, U, ldu, V, ldv, C.D.data(), C.m);
         } else if (C.type == T_LR) {
             ProfT _p(4);
@@ -944,6 +947,7 @@ struct Impl {
         }
         if (C.type == T_LR) {
             if (A.type == T_DENSE && B.type == T_DENSE) {
+                ProfT _p(17);
                 const int64_t rho = A.m, sig = A.n, tau = B.n;
                 if (sig <= rho && sig <= tau) {
                     Vec Bt = transpose(B.D.data(), B.m, B.n, B.m);   // tau x sigma
@@ -961,18 +965,21 @@ struct Impl {
                     }
                 }
             } else if (A.type == T_DENSE && B.type == T_SUB) {
+                ProfT _p(18);
                 Vec At = transpose(A.D.data(), A.m, A.n, A.m);
                 Vec Z((size_t)(B.n * A.m), 0.0);
                 hmul(B, true, At.data(), A.n, A.m, Z.data(), B.n, 1.0);
                 Vec I = identity(A.m);
                 addlr(C, I.data(), A.m, Z.data(), B.n, (int)A.m, alpha);
             } else if (A.type == T_SUB && B.type == T_DENSE) {
+                ProfT _p(19);
                 Vec Z((size_t)(A.m * B.n), 0.0);
                 hmul(A, false, B.D.data(), B.m, B.n, Z.data(), A.m, 1.0);
                 Vec I = identity(B.n);
                 addlr(C, Z.data(), A.m, I.data(), B.n, (int)B.n, alpha);
             } else {
                 // both subdivided: form the product in C's subdivision, collapse it, add it
+                ProfT _p(20);
                 auto T = lr_shape(C);
                 const bool par = big(C);
                 for (int q = 0; q < 4; ++q) {
@@ -1012,6 +1019,7 @@ struct Impl {
     void lu(Mat& A) {
         if (singular.load(std::memory_order_relaxed)) return;
         if (A.type == T_DENSE) {
+            ProfT _p(12);
             if (!lu_dense(A.D.data(), A.m)) {
                 std::lock_guard<std::mutex> g(mu);
                 if (!singular) where = "rows [" + std::to_string(A.r0) + ", " + std::to_string(A.r0 + A.m) + ")";
@@ -1037,7 +1045,11 @@ struct Impl {
     }
 
     void form(Mat& A, int cut) {
-        if (A.type == T_DENSE) { invert_packed(A.D.data(), A.m); return; }
+        if (A.type == T_DENSE) {
+            ProfT _p(22);
+            invert_packed(A.D.data(), A.m);
+            return;
+        }
         const int level = nodes[A.rn].level;
         Mat &A00 = *A.ch(0, 0), &A01 = *A.ch(0, 1), &A10 = *A.ch(1, 0), &A11 = *A.ch(1, 1);
         if (level < cut) {   // W^L_t = L21 L11^-1, W^U_t = U12 U22^-1
