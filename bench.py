@@ -516,6 +516,8 @@ def main():
                        "ranks_F": {"mean": rep["rank_mean"], "max": rep["rank_max"]},
                        "ranks_C": {"mean": rep["rank_mean_C"], "max": rep["rank_max_C"]},
                        "setup_s": dict(rep["setup_seconds"], wall=setup_wall),
+                       "hlu": {"method": "hierarchical (stage B, DESIGN.md R33)" if rep["lu_method"] == 0 else "dense tiles (stage A)",
+                               "truncations": rep["lu_truncations"], "host_threads": rep["lu_threads"]},
                        "solve_form": "inverse factors (cut level 0, DESIGN.md R27)",
                        "level_form": level_form, "recompressed": recompressed, "multi_rhs": multi_rhs,
                        "cavity_jacobian_action": jcav, "shard": shard, "graph_replay": graph_replay,

@@ -136,6 +136,9 @@ typedef struct {
     int64_t bytes_F_local;            /* world > 1: this rank's stored bytes of F (= bytes_F)   */
     int64_t bytes_C_local;            /* world > 1: this rank's bytes of the solve operators    */
     int64_t rank, world;
+    int64_t lu_method;                /* 0 hierarchical (stage B), 1 dense tiles (stage A)           */
+    int64_t lu_truncations;           /* stage B: low-rank truncations (QR + SVD) of the factorisation */
+    int64_t lu_threads;               /* stage B: host threads of the factorisation (0: on rank 0 only) */
 } hm_storage;
 
 /* ---- lifetime ------------------------------------------------------------------------- */

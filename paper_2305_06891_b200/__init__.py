@@ -55,7 +55,8 @@ class hm_storage(C.Structure):
                 ("n_lowrank_C", C.c_int64), ("rank_max_C", C.c_int64), ("rank_mean_C", C.c_double),
                 ("launches_apply_F", C.c_int64), ("launches_solve_C", C.c_int64),
                 ("setup_seconds", C.c_double * 8), ("bytes_F_local", C.c_int64), ("bytes_C_local", C.c_int64),
-                ("rank", C.c_int64), ("world", C.c_int64)]
+                ("rank", C.c_int64), ("world", C.c_int64), ("lu_method", C.c_int64),
+                ("lu_truncations", C.c_int64), ("lu_threads", C.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "setup_seconds"}

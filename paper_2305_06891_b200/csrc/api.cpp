@@ -1213,6 +1213,9 @@ hm_status hm_storage_report(const hm_hmat* Fh, const hm_hlu* LUh, hm_storage* ou
         out->n_lowrank_C = L.n_lr;
         out->rank_max_C = L.rank_max;
         out->rank_mean_C = L.n_lr ? double(L.rank_sum) / L.n_lr : 0.0;
+        out->lu_method = L.params.method;
+        out->lu_truncations = L.hlu_truncations;
+        out->lu_threads = (int64_t)L.hlu_threads;
         out->launches_solve_C = g.shard.sharded() ? (int64_t)L.sp_solve.segs.size() : 1;
         out->bytes_C_local = g.shard.sharded() ? 8 * (L.leafL_loc.p1_doubles() + L.leafL_loc.p2_doubles() +
                                                       L.leafU_loc.p1_doubles() + L.leafU_loc.p2_doubles())

@@ -8,6 +8,7 @@ Bars:
   * y = F x, z = C^-1 b, q vs the dense oracle: <= 10 eps_ACA relative l2 (north_star).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -422,11 +423,31 @@ def sherman_morrison(f, eps, x):
     return Mx + (k * (a @ Mx) / (1.0 - k * (a @ Mb))) * Mb
 
 
-def sampled_residual_batched(f, eps, rows, z, x, batch=200):
+_RES_ARGS = None
+
+
+def _residual_rows(r):
+    from threadpoolctl import threadpool_limits
+    f, eps, z, x = _RES_ARGS
+    with threadpool_limits(1):   # one BLAS thread per worker
+        return vf.sampled_residual(f.centroid, f.normal, f.area, eps, r, z[:, None], x[:, None])[:, 0]
+
+
+def sampled_residual_batched(f, eps, rows, z, x, batch=32):
     """The oracle's sampled residual on `rows`, evaluated `batch` rows at a time
-    (a dense row of C5 is 10 MB: 2,000 at once would be 21 GB)."""
-    return np.concatenate([vf.sampled_residual(f.centroid, f.normal, f.area, eps, rows[i:i + batch], z[:, None],
-                                               x[:, None])[:, 0] for i in range(0, len(rows), batch)])
+    (a dense row of C5 is 10 MB: 2,000 at once would be 21 GB) by forked workers, one BLAS thread each
+    (numpy only in the children; the oracle itself is unchanged)."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    global _RES_ARGS
+    _RES_ARGS = (f, eps, z, x)
+    parts = [rows[i:i + batch] for i in range(0, len(rows), batch)]
+    try:
+        with ProcessPoolExecutor(max(1, min(12, (os.cpu_count() or 2) - 2)), mp_context=mp.get_context("fork")) as ex:
+            res = list(ex.map(_residual_rows, parts))
+    finally:
+        _RES_ARGS = None
+    return np.concatenate(res)
 
 
 def solve_and_flux_checks(hm, ctx, cfg, F, LU, rows, tol):
