@@ -638,12 +638,28 @@ void stage_b_root(HLU& L, const HMat& F, const Geom& g, const std::vector<double
                 S.dense = put(M.D.data(), M.m * M.n);
             }
         } else {
-            S.kind = KIND_LR;
-            S.k = M.k;
-            S.u_ld = M.m;
-            S.v_ld = M.n;
-            S.U = put(M.U.data(), M.m * M.k);
-            S.V = put(M.V.data(), M.n * M.k);
+            // a low-rank block above the operator panels' rank limit (a phase-1 panel holds <= 128 stacked
+            // ranks) is stored as several blocks of <= 64 columns of U and V on the same footprint
+            // (U V^T = sum of the parts; multi-body geometries reach ranks in the hundreds at the top
+            // levels of the inverse factors)
+            const int lvl = g.nodes[v.node].level;
+            auto& dst = lvl < Lc ? (v.side == 1 ? out.fwd[lvl] : out.bwd[lvl]) : (v.side == 1 ? out.srcL : out.srcU);
+            for (int p0 = 0; p0 < M.k; p0 += 64) {
+                const int kp = std::min(64, M.k - p0);
+                S.kind = KIND_LR;
+                S.k = kp;
+                S.u_ld = M.m;
+                S.v_ld = M.n;
+                S.U = put(M.U.data() + (int64_t)p0 * M.m, M.m * kp);
+                S.V = put(M.V.data() + (int64_t)p0 * M.n, M.n * kp);
+                dst.push_back(S);
+            }
+            if (M.k == 0) {
+                S.kind = KIND_LR;
+                S.k = 0;
+                dst.push_back(S);
+            }
+            return;
         }
         const int lvl = g.nodes[v.node].level;
         if (lvl < Lc) (v.side == 1 ? out.fwd[lvl] : out.bwd[lvl]).push_back(S);

@@ -205,6 +205,8 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
         const SrcBlock& B = blocks[b];
         if (!mine(B)) continue;
         if (B.kind != KIND_LR) { ++op.n_dense; continue; }
+        if (B.k > 128)   // a phase-1 panel stacks whole blocks of <= 128 rows (callers split larger ranks)
+            throw Error(HM_ERR_UNSUPPORTED, "low-rank block of rank " + std::to_string(B.k) + " > 128 in the operator builder");
         ++op.n_lr;
         op.rank_sum += B.k;
         op.rank_max = std::max(op.rank_max, B.k);
