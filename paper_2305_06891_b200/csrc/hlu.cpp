@@ -976,7 +976,11 @@ void factor_hlu(HLU& L, const double* emissivity) {
             P.add_stream(L.leafL.p1m, L.leafL, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN);
             P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
                          (int)P.h_passes.size() - 2);
+            const int32_t l2 = (int32_t)P.h_passes.size() - 1;
             P.add_stream(L.leafU.p1m, L.leafU, L.xtB_m.p, L.xtB_m.p, OUT_ASSIGN);
+            // U^-1 phase 1 of a cluster waits for L^-1 phase 2 on its row group only (as in the
+            // single-vector programs): the next operator starts group by group, no full pass drain
+            if (!getenv("HM_MRHS_NO_LINKS")) P.link_rows(l2, (int32_t)P.h_passes.size() - 1);
             P.add_stream(L.leafU.p2m, L.leafU, L.xtB_m.p, out_u, mode_u, DEP_BARRIER, nullptr, IN_PLAIN,
                          (int)P.h_passes.size() - 2);
         };
@@ -987,6 +991,8 @@ void factor_hlu(HLU& L, const double* emissivity) {
         L.prog_solve_m.finalize(c, s, &g);
         mprog(L.prog_flux_m, IN_FLUX, Fm.xt_m.p, OUT_ASSIGN);
         L.prog_flux_m.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
+        if (!getenv("HM_MRHS_NO_LINKS"))
+            L.prog_flux_m.link_rows((int32_t)L.prog_flux_m.h_passes.size() - 2, (int32_t)L.prog_flux_m.h_passes.size() - 1);
         L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
                                  (int)L.prog_flux_m.h_passes.size() - 2);
         L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_FLUX);
