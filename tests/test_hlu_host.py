@@ -174,3 +174,38 @@ def test_host_only_context_refuses_the_hot_path(hm):
         hm.hm_solve_C(r["ctx"], r["LU"], x, y)
     with pytest.raises(hm.HMError):
         hm.hm_apply_F(r["ctx"], r["F"], x, y)
+
+
+def test_host_factor_api_errors(hm):
+    """hm_hmat_from_host / hm_export_factors / hm_factor_hlu reject what they cannot hold: a low-rank
+    payload on an inadmissible block, a rank beyond min(m, n), an export of W levels the solve form does
+    not have, the dense stage-A method without a device, and a missing eps_lu for a caller-given F."""
+    import ctypes as C
+    cfg = synth.make_config(1)
+    f = cfg.facets
+    r = host_factor(hm, cfg, cut=0)
+    ctx, g = r["ctx"], r["g"]
+    part = r["part"]
+    blocks = sorted(r["H"].blocks, key=lambda b: (b.r0, b.c0))
+    hb = [(b.U, b.V) if b.kind == ohm.KIND_LR else b.D for b in blocks]
+    dense_i = int(np.nonzero(part[:, 5] == 0)[0][0])          # an inadmissible (near-field) block
+    m = int(part[dense_i, 2] - part[dense_i, 1])
+    n = int(part[dense_i, 4] - part[dense_i, 3])
+    bad = list(hb)
+    bad[dense_i] = (np.ones((m, 1)), np.ones((n, 1)))
+    with pytest.raises(hm.HMError):
+        hm.hm_hmat_from_host(ctx, g, bad)
+    lr_i = int(np.nonzero(part[:, 6] == 1)[0][0])
+    m = int(part[lr_i, 2] - part[lr_i, 1])
+    n = int(part[lr_i, 4] - part[lr_i, 3])
+    bad = list(hb)
+    k = min(m, n) + 1
+    bad[lr_i] = (np.ones((m, k)), np.ones((n, k)))
+    with pytest.raises(hm.HMError):
+        hm.hm_hmat_from_host(ctx, g, bad)
+    with pytest.raises(hm.HMError):                          # cut 0: no W levels
+        hm.hm_export_factors(hm.HM_OP_WL(0), r["F"], r["LU"])
+    with pytest.raises(hm.HMError):
+        hm.hm_factor_hlu(ctx, r["F"], cfg.emissivity, eps_lu=1e-6, method="dense")
+    with pytest.raises(hm.HMError):                          # caller-given F carries no eps_aca default
+        hm.hm_factor_hlu(ctx, r["F"], cfg.emissivity)
