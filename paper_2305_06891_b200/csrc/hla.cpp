@@ -155,7 +155,55 @@ static Vec transpose(const double* A, int64_t m, int64_t n, int64_t lda) {   // 
 
 enum SolveKind : int { S_LL = 0, S_LU = 1, S_LLT = 2, S_LUT = 3 };
 // B (m x r) <- op(T)^-1 B with T the packed LU of an m x m dense diagonal leaf (ld m)
+static void trsm_dense1(int kind, const double* T, int64_t m, double* B, int64_t ldb, int64_t r);
 static void trsm_dense(int kind, const double* T, int64_t m, double* B, int64_t ldb, int64_t r) {
+    // the column forms (unit lower / upper, the common ones) four right-hand sides at a time: every
+    // column of T is loaded once per four updates
+    int64_t j = 0;
+    if (kind == S_LL || kind == S_LU) {
+        for (; j + 4 <= r; j += 4) {
+            double* __restrict b0 = B + j * ldb;
+            double* __restrict b1 = b0 + ldb;
+            double* __restrict b2 = b1 + ldb;
+            double* __restrict b3 = b2 + ldb;
+            if (kind == S_LL) {
+                for (int64_t l = 0; l < m; ++l) {
+                    const double* __restrict t = T + l * m;
+                    const double x0 = b0[l], x1 = b1[l], x2 = b2[l], x3 = b3[l];
+#pragma omp simd
+                    for (int64_t i = l + 1; i < m; ++i) {
+                        const double ti = t[i];
+                        b0[i] -= ti * x0;
+                        b1[i] -= ti * x1;
+                        b2[i] -= ti * x2;
+                        b3[i] -= ti * x3;
+                    }
+                }
+            } else {
+                for (int64_t l = m - 1; l >= 0; --l) {
+                    const double* __restrict t = T + l * m;
+                    const double inv = 1.0 / t[l];
+                    b0[l] *= inv;
+                    b1[l] *= inv;
+                    b2[l] *= inv;
+                    b3[l] *= inv;
+                    const double x0 = b0[l], x1 = b1[l], x2 = b2[l], x3 = b3[l];
+#pragma omp simd
+                    for (int64_t i = 0; i < l; ++i) {
+                        const double ti = t[i];
+                        b0[i] -= ti * x0;
+                        b1[i] -= ti * x1;
+                        b2[i] -= ti * x2;
+                        b3[i] -= ti * x3;
+                    }
+                }
+            }
+        }
+    }
+    if (j < r) trsm_dense1(kind, T, m, B + j * ldb, ldb, r - j);
+}
+
+static void trsm_dense1(int kind, const double* T, int64_t m, double* B, int64_t ldb, int64_t r) {
     for (int64_t j = 0; j < r; ++j) {
         double* b = B + j * ldb;
         switch (kind) {
