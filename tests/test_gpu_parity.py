@@ -426,6 +426,11 @@ def sherman_morrison(f, eps, x):
 _RES_ARGS = None
 
 
+def _residual_init(*args):
+    global _RES_ARGS
+    _RES_ARGS = args
+
+
 def _residual_rows(r):
     from threadpoolctl import threadpool_limits
     f, eps, z, x = _RES_ARGS
@@ -435,18 +440,16 @@ def _residual_rows(r):
 
 def sampled_residual_batched(f, eps, rows, z, x, batch=32):
     """The oracle's sampled residual on `rows`, evaluated `batch` rows at a time
-    (a dense row of C5 is 10 MB: 2,000 at once would be 21 GB) by forked workers, one BLAS thread each
-    (numpy only in the children; the oracle itself is unchanged)."""
+    (a dense row of C5 is 10 MB: 2,000 at once would be 21 GB) by worker processes from a clean fork
+    server (no fork of this multi-threaded CUDA process), one BLAS thread each; the oracle itself is
+    unchanged."""
     import multiprocessing as mp
     from concurrent.futures import ProcessPoolExecutor
-    global _RES_ARGS
-    _RES_ARGS = (f, eps, z, x)
     parts = [rows[i:i + batch] for i in range(0, len(rows), batch)]
-    try:
-        with ProcessPoolExecutor(max(1, min(12, (os.cpu_count() or 2) - 2)), mp_context=mp.get_context("fork")) as ex:
-            res = list(ex.map(_residual_rows, parts))
-    finally:
-        _RES_ARGS = None
+    nw = max(1, min(12, (os.cpu_count() or 2) - 2))
+    with ProcessPoolExecutor(nw, mp_context=mp.get_context("forkserver"), initializer=_residual_init,
+                             initargs=(f, eps, z, x)) as ex:
+        res = list(ex.map(_residual_rows, parts))
     return np.concatenate(res)
 
 
