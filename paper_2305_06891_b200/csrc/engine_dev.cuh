@@ -6,6 +6,10 @@
 
 #include "hm_internal.h"
 
+#ifndef HM_PAYLOAD_EVICT_FIRST
+#define HM_PAYLOAD_EVICT_FIRST 1
+#endif
+
 namespace hm {
 namespace dev {
 
@@ -49,6 +53,21 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+// The factor payload is read once per apply and is larger than L2: stream it with an L2 evict-first
+// policy so that the lines worth keeping (inputs, the phase-1 -> phase-2 scratch) stay resident
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes, unsigned long long* b,
+                                                 uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
         : "memory");
 }
 // split-K arrival: release this thread's (and, cumulatively, its warp's) partial-sum writes,

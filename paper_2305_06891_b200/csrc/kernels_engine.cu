@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
         if (lane != 0) return;
         unsigned long long st_empty = 0, st_meta = 0, st_chunks = 0, st_pempty = 0;
         const long long t_start = clock64();
+        const uint64_t pol = l2_evict_first_policy();
         int64_t k = 0;     // headers posted
         int64_t kp = 0;    // payloads issued
         auto issue_payload = [&]() {
@@ -177,7 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             if (u.type == UNIT_STREAM) {
                 const uint32_t pb = (uint32_t)u.ncols * (uint32_t)u.ld * 8u;
                 mbar_expect_tx(&S.full[p], pb);
-                tma_load_1d(S.st[p].payload, S.passes[u.pass].arena + u.a_off, pb, &S.full[p]);
+                if (HM_PAYLOAD_EVICT_FIRST)
+                    tma_load_1d_hint(S.st[p].payload, S.passes[u.pass].arena + u.a_off, pb, &S.full[p], pol);
+                else
+                    tma_load_1d(S.st[p].payload, S.passes[u.pass].arena + u.a_off, pb, &S.full[p]);
             } else {
                 mbar_arrive(&S.full[p]);
             }

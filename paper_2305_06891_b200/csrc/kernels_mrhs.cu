@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
         // ------------------------------------------------ producer
         unsigned long long nxt = 0, st_e = 0, st_m = 0;
         const long long t0 = clock64();
+        const uint64_t pol = l2_evict_first_policy();
         if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - queue_base;
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
         int64_t k = 0;
@@ -343,8 +344,13 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                     if (!end && utype == UNIT_STREAM) {   // column j -> payload + j * padded_ld(ld)
                         const double* src = S.passes[upass].arena + uoff;
                         const int ldp = padded_ld(uld);
-                        for (int j = lane; j < uncols; j += 32)
-                            tma_load_1d(St.payload + j * ldp, src + (int64_t)j * uld, (uint32_t)uld * 8u, &S.full[s]);
+                        for (int j = lane; j < uncols; j += 32) {
+                            if (HM_PAYLOAD_EVICT_FIRST)
+                                tma_load_1d_hint(St.payload + j * ldp, src + (int64_t)j * uld, (uint32_t)uld * 8u,
+                                                 &S.full[s], pol);
+                            else
+                                tma_load_1d(St.payload + j * ldp, src + (int64_t)j * uld, (uint32_t)uld * 8u, &S.full[s]);
+                        }
                     }
                 }
                 nxt = __shfl_sync(0xffffffffu, nxt, 0);
