@@ -18,7 +18,8 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhm.so")
+# HM_LIB: another build of the same library (tests of the HM_DEVICE_CHECKS build; never a CPU fallback)
+LIB_PATH = os.environ.get("HM_LIB") or os.path.join(_HERE, "libhm.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "hm.h")
 
 STATUS = {0: "HM_OK", 1: "HM_ERR_INVALID_ARG", 2: "HM_ERR_CUDA", 3: "HM_ERR_OOM", 4: "HM_ERR_NCCL",

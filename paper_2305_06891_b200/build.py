@@ -28,27 +28,31 @@ SOURCES = ["tree.cpp", "hop.cpp", "api.cpp", "hlu.cpp", "hla.cpp", "engine.cpp",
            "kernels_mrhs.cu", "kernels_recompress.cu"]
 
 
-def _digest() -> str:
+def _digest(extra=()) -> str:
     h = hashlib.sha256()
     for f in sorted(os.listdir(CSRC)) + ["../../include/hm.h"]:
         p = os.path.join(CSRC, f)
         if os.path.isfile(p):
             h.update(f.encode())
             h.update(open(p, "rb").read())
-    h.update(" ".join(ARCH + COMMON + [str(EXTRA)]).encode())
+    h.update(" ".join(ARCH + COMMON + [str(EXTRA)] + list(extra)).encode())
     return h.hexdigest()
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    stamp = os.path.join(BUILD, "stamp")
-    dg = _digest()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == dg:
-        return LIB
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB) -> str:
+    """Compile every source for sm_100a and link `lib`.  `defines`: extra -D flags (e.g. the device-check
+    build, ("HM_DEVICE_CHECKS=1",), linked to another path so the product library is untouched)."""
+    extra = ["-D" + d for d in defines]
+    bdir = BUILD if lib == LIB else os.path.join(BUILD, os.path.splitext(os.path.basename(lib))[0])
+    os.makedirs(bdir, exist_ok=True)
+    stamp = os.path.join(bdir, "stamp")
+    dg = _digest(extra)
+    if not force and os.path.exists(lib) and os.path.exists(stamp) and open(stamp).read() == dg:
+        return lib
 
     def compile_one(src):
-        obj = os.path.join(BUILD, src + ".o")
-        cmd = [NVCC] + ARCH + COMMON + EXTRA.get(src, []) + (["-Xptxas", "-v"] if verbose and src.endswith(".cu") else [])
+        obj = os.path.join(bdir, src + ".o")
+        cmd = [NVCC] + ARCH + COMMON + extra + EXTRA.get(src, []) + (["-Xptxas", "-v"] if verbose and src.endswith(".cu") else [])
         if src.endswith(".cpp"):
             cmd += ["-x", "cu"] if False else []
         cmd += ["-c", os.path.join(CSRC, src), "-o", obj]
@@ -61,15 +65,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-Xlinker", "--no-undefined", "-o", tmp] + objs + ["-ldl", "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     with open(stamp, "w") as f:
         f.write(dg)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -60,6 +60,8 @@ int add_stream_impl(Program& P, const StreamPass& sp, const HOp& op, const doubl
     }
     P.h_passes.push_back(p);
     P.pass_xdep.push_back(xdep);
+    const DBuf<int32_t>& cs = (in_mode == IN_PLAIN || in_mode == IN_FLUXI) ? op.colsrc : op.colsrc_ext;
+    P.h_chk.insert(P.h_chk.end(), {(int64_t)op.arena.n, (int64_t)cs.n, op.xt_len});
     return idx;
 }
 
@@ -106,12 +108,13 @@ void Program::add_elementwise(int type, int64_t n, double* out, int rows_per_uni
     p.n_tasks = p.n_units;
     h_passes.push_back(p);
     pass_xdep.push_back(-2);
+    h_chk.insert(h_chk.end(), {0, 0, 0});
 }
 
 void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
     for (const Unit& u : h_units)
         if (u.type == UNIT_STREAM && (u.ncols > (mrhs ? kMrhsMaxCols : kUnitMaxCols) || u.ld > 128 ||
-                                      (int64_t)u.ncols * u.ld > (mrhs ? kUnitPayloadDoubles : kStageDoubles)))
+                                      (int64_t)u.ncols * u.ld > (mrhs ? kMrhsPayloadDoubles : kStageDoubles)))
             throw Error(HM_ERR_UNSUPPORTED, "work unit exceeds the engine stage size");
     const int64_t P = (int64_t)h_passes.size();
     if (P > (mrhs ? engine_mrhs_max_passes() : engine_max_passes()))
@@ -260,7 +263,20 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
             }
         }
     }
+#if HM_DEVICE_CHECKS
+    // HM_CHECK_SELFTEST=1 (tests of the checked build): move one chunk past the end of its arena -- the
+    // engine must trap on it
+    if (const char* e = getenv("HM_CHECK_SELFTEST"); e && e[0] == '1')
+        for (Unit& u : h_units)
+            if (u.type == UNIT_STREAM) {
+                u.a_off = h_chk[3 * (size_t)u.pass];
+                break;
+            }
+#endif
     passes.upload(ctx, h_passes, "engine passes", s);
+#if HM_DEVICE_CHECKS
+    chk.upload(ctx, h_chk, "engine check bounds", s);
+#endif
     units.upload(ctx, h_units, "engine units", s);
     tasks.upload(ctx, h_tasks, "engine tasks", s);
     done.alloc(ctx, (size_t)std::max<int64_t>(n_counters, 1), "engine dependency counters");
@@ -291,6 +307,7 @@ void Program::launch(ProgArgs a, cudaStream_t s) {
     a.n_units = (int64_t)h_units.size();
     a.done = done.p;
     a.epoch_dev = epoch_dev.p;
+    a.chk = chk.p;   // null unless HM_DEVICE_CHECKS
     if (a.ld == 0) a.ld = 1;
     static const bool want_stats = [] { const char* e = getenv("HM_ENGINE_STATS"); return e && e[0] == '1'; }();
     if (want_stats) {

@@ -9,6 +9,12 @@
 #ifndef HM_PAYLOAD_EVICT_FIRST
 #define HM_PAYLOAD_EVICT_FIRST 1
 #endif
+// debug builds (HM_BUILD_DEFINES="HM_DEVICE_CHECKS=1"): every chunk descriptor and every gathered index
+// is checked on the device against the program's bounds (compute-sanitizer is not available on the
+// GPU pool); a violation prints the chunk and traps, and the call fails with HM_ERR_CUDA
+#ifndef HM_DEVICE_CHECKS
+#define HM_DEVICE_CHECKS 0
+#endif
 
 namespace hm {
 namespace dev {
@@ -70,6 +76,20 @@ __device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uin
         "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
         : "memory");
 }
+// 16-byte asynchronous global -> shared copy (L2 only: the source may have been written by another SM
+// earlier in this launch); per-lane addresses, no serialisation over the lanes
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_hint(void* dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
+                 : "memory");
+}
+// arrive on the mbarrier once this thread's earlier cp.async copies have landed (the pending count is
+// raised first, so the barrier's expected count is unchanged)
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* b) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 // split-K arrival: release this thread's (and, cumulatively, its warp's) partial-sum writes,
 // acquire the other pieces' when last
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
@@ -116,6 +136,57 @@ __device__ __forceinline__ void wait_counter(const ProgArgs& A, unsigned long lo
     }
 }
 
+
+#if HM_DEVICE_CHECKS
+// producer side, before a payload copy: the chunk [a_off, a_off + ncols ld) inside pass `pass`'s arena
+static __device__ __forceinline__ void check_payload(const ProgArgs& A, int pass, int64_t a_off, int ncols, int ld) {
+    if (pass < 0 || pass >= A.n_passes || a_off < 0 || ncols < 0 || ld < 0 ||
+        a_off + (int64_t)ncols * ld > A.chk[3 * pass]) {
+        printf("hm device check failed: payload of pass %d at %lld + %d x %d outside its arena\n", pass, (long long)a_off,
+               ncols, ld);
+        __trap();
+    }
+}
+// One warp: the chunk H of pass P against A.chk (arena doubles, column-source entries, input index
+// bound of the pass), its stage limits, and every column source (lane-parallel); trap on a violation
+static __device__ __noinline__ void check_chunk(const ProgArgs& A, const Unit& H, const Pass& P, int max_cols,
+                                         int64_t max_payload, int lane) {
+    int why = 0;
+    if (H.pass < 0 || H.pass >= A.n_passes) why = 1;
+    const int64_t* b = why ? nullptr : A.chk + 3 * H.pass;
+    if (!why && (H.ncols <= 0 || H.ncols > max_cols || H.ld <= 0 || H.ld > 128 || (H.ld & 1) || H.nrows <= 0 ||
+                 H.nrows > H.ld || (int64_t)H.ncols * H.ld > max_payload))
+        why = 2;
+    if (!why && (H.a_off < 0 || H.a_off + (int64_t)H.ncols * H.ld > b[0])) why = 3;
+    const bool ext = P.in_mode == IN_PERM || P.in_mode == IN_FLUX;
+    if (!why && H.nruns > 0 && !ext) {
+        int64_t tot = 0;
+        for (int r = 0; r < H.nruns && r < kMaxRuns; ++r) {
+            if (H.run_src[r] < 0 || (int64_t)H.run_src[r] + H.run_len[r] > b[2]) why = 4;
+            tot += H.run_len[r];
+        }
+        if (H.nruns > kMaxRuns || tot != H.ncols) why = 4;
+    }
+    if (!why && (!P.colsrc || H.cs_off < 0 || H.cs_off + H.ncols > b[1])) why = 5;
+    int bad = why;
+    if (!why) {
+        for (int c = lane; c < H.ncols; c += 32) {
+            const int32_t j = P.colsrc[H.cs_off + c];
+            const bool ok = ext ? (j >= 0 ? (int64_t)j < b[2] : -(int64_t)j - 1 < A.n_x) : (j >= 0 && (int64_t)j < b[2]);
+            if (!ok) bad = 6;
+        }
+    }
+    bad = __reduce_max_sync(0xffffffffu, (unsigned)bad);
+    if (bad) {
+        if (lane == 0)
+            printf("hm device check %d failed: pass %d (of %d) task %lld chunk %d: a_off %lld ncols %d ld %d nrows %d "
+                   "cs_off %lld nruns %d\n",
+                   bad, H.pass, A.n_passes, (long long)H.task, H.chunk, (long long)H.a_off, H.ncols, H.ld, H.nrows,
+                   (long long)H.cs_off, H.nruns);
+        __trap();
+    }
+}
+#endif
 
 }  // namespace dev
 }  // namespace hm

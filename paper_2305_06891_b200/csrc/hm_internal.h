@@ -212,7 +212,16 @@ constexpr int kUnitPayloadDoubles = 4096;   // 32 KB TMA stage (multi-RHS engine
 #endif
 constexpr int kStageDoubles = HM_STAGE_DOUBLES;   // single-vector engine payload stage (doubles): 56.6 KB
 constexpr int kMrhsMax = 64;                // multi-RHS block width (columns of X per program launch)
-constexpr int kMrhsMaxCols = 64;            // multi-RHS chunk: <= 64 panel columns (X tile 64 x 64)
+// multi-RHS chunk geometry (experiment overrides through HM_BUILD_DEFINES): <= HM_MRHS_MAXCOLS panel
+// columns (X tile HM_MRHS_MAXCOLS x 64) and <= HM_MRHS_PAYLOAD doubles of payload per chunk
+#ifndef HM_MRHS_MAXCOLS
+#define HM_MRHS_MAXCOLS 64
+#endif
+#ifndef HM_MRHS_PAYLOAD
+#define HM_MRHS_PAYLOAD 4096
+#endif
+constexpr int kMrhsMaxCols = HM_MRHS_MAXCOLS;
+constexpr int kMrhsPayloadDoubles = HM_MRHS_PAYLOAD;
 constexpr int kUnitMaxCols = 256;
 constexpr int64_t kPieceDoubles = 65536;    // panels above 512 KB are split into pieces
 
@@ -272,6 +281,7 @@ struct HOp {
     DBuf<int32_t> colsrc;          // per-unit, 16-byte aligned column-source segments
     DBuf<int32_t> colsrc_ext;      // same, x-region entries as -(external index + 1) (fused prologue)
     int64_t n_t = 0;              // total rank (size of t)
+    int64_t xt_len = 0;           // column sources index [0, xt_len) of the XT buffer (x region + t_off + n_t)
     struct ItemRec {              // one phase-2 item (a leaf-row slice of one block)
         int64_t a_off;            // U slice / dense slice, column-major with stride a_ld
         int64_t a_ld;
@@ -351,6 +361,9 @@ struct ProgArgs {
     int64_t local0;             // sharded: padded index of this rank's first row
     int32_t nrhs;               // multi-RHS: columns of this launch (<= kMrhsMax; user arrays have ld >= nrhs)
     const double* T_pad;        // sharded flux: gathered temperatures (padded internal order)
+    // HM_DEVICE_CHECKS builds only: per pass {arena doubles, column-source entries, input index bound}
+    // (the engines check every chunk descriptor and gathered index against them, then trap)
+    const int64_t* chk;
 };
 
 // input modes of a stream pass: the prologue / permute-in fused into the gather
@@ -382,6 +395,8 @@ struct Program {
     int64_t n_counters = 0;
     DBuf<unsigned long long> trace;
     DBuf<unsigned long long> stats;
+    std::vector<int64_t> h_chk;   // per pass: arena doubles, column-source entries, input index bound
+    DBuf<int64_t> chk;            // (uploaded in HM_DEVICE_CHECKS builds)
     // builder: panel_node (optional) maps each panel of `sp` to its tree node (tree kinds)
     // xdep (DEP_BARRIER passes): the pass whose completion x-only tasks wait for instead of the
     // previous pass (-2: no distinction, -1: no wait)

@@ -300,6 +300,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
     if (nx + t_off + tcount >= INT32_MAX || (int64_t)colsrc.size() >= INT32_MAX)
         throw Error(HM_ERR_UNSUPPORTED, "index space exceeds int32");
 
+    op.xt_len = nx + t_off + tcount;
     op.arena.alloc(ctx, (size_t)std::max<int64_t>(off, 2), "operator arena");
     HM_CUDA(cudaMemsetAsync(op.arena.p, 0, sizeof(double) * (size_t)std::max<int64_t>(off, 2), s));
     std::vector<int32_t> ucs;
@@ -315,8 +316,10 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
         // row-group links 0.927 ms, without links 1.005 ms, largest first 0.913 ms); HM_MRHS_KEY_ORDER=1
         // selects the keyed order
         static const bool keyed = getenv("HM_MRHS_KEY_ORDER") != nullptr;
-        make_units(ctx, op.p1m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax, false, keyed && op.p1_by_key ? 1 : 0);
-        make_units(ctx, op.p2m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax, false, keyed && op.p2_by_row ? 2 : 0);
+        make_units(ctx, op.p1m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax, false, keyed && op.p1_by_key ? 1 : 0,
+                   kMrhsPayloadDoubles);
+        make_units(ctx, op.p2m, colsrc, ucs, s, kMrhsMaxCols, kMrhsMax, false, keyed && op.p2_by_row ? 2 : 0,
+                   kMrhsPayloadDoubles);
     }
     op.colsrc.upload(ctx, ucs, "colsrc", s);
     // the same column sources for passes that gather straight from the caller's external-order

@@ -176,6 +176,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             st_pempty += clock64() - c0;
             const Unit& u = S.gs[g].hdr;
             if (u.type == UNIT_STREAM) {
+#if HM_DEVICE_CHECKS
+                check_payload(A, u.pass, u.a_off, u.ncols, u.ld);
+#endif
                 const uint32_t pb = (uint32_t)u.ncols * (uint32_t)u.ld * 8u;
                 mbar_expect_tx(&S.full[p], pb);
                 if (HM_PAYLOAD_EVICT_FIRST)
@@ -213,6 +216,13 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             }
             st_meta += clock64() - c0;
             const int nch = task.n_units;
+#if HM_DEVICE_CHECKS
+            if (task.first_unit < 0 || nch < 1 || task.first_unit + nch > A.n_units) {
+                printf("hm device check failed: task %llu units [%lld, +%d) of %lld\n", t, (long long)task.first_unit, nch,
+                       (long long)A.n_units);
+                __trap();
+            }
+#endif
             for (int c = 0; c < nch; ++c) {
                 const int g = wait_slot(k);
                 ++st_chunks;
@@ -281,6 +291,9 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
                 }
                 c0 = clock64();
                 st_dep += c0 - c1;
+#if HM_DEVICE_CHECKS
+                if (type == UNIT_STREAM) check_chunk(A, H, S.passes[H.pass < A.n_passes ? H.pass : 0], kMaxCols, kStageDoubles, lane);
+#endif
                 if (type == UNIT_STREAM) {
                     const Pass& P = S.passes[H.pass];
                     const double* in = P.in ? P.in : A.user_in;

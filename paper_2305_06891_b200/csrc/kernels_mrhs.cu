@@ -30,17 +30,41 @@ constexpr int kMConsumer0 = 32 * (1 + kMGatherers);
 constexpr int kMPubWarp = 1 + kMGatherers + kMConsumerWarps;          // warp 11: publisher
 constexpr int kMThreads = 32 * (kMPubWarp + 1);                        // 384
 constexpr int kPubSlots = 8;          // task-end descriptors in flight (consumers -> publisher)
-constexpr int kMStages = 3;
+#ifndef HM_MRHS_STAGES
+#define HM_MRHS_STAGES 3
+#endif
+constexpr int kMStages = HM_MRHS_STAGES;
 // Shared-memory strides for conflict-free fragment loads: an 8-byte fragment load by a half-warp
 // (lanes g = 0..3 row, t = 0..3 k) reads words t * stride + g; the 16 words fall into distinct bank
 // pairs iff stride = 4 or 12 (mod 16).
-constexpr int kXStride = 68;          // X tile row stride (doubles)
+// X tile row stride (doubles).  HM_MRHS_X_RUNS = 0 (default): 68, conflict-free B-fragment loads, one
+// bulk copy per X row.  = 1: 64, unpadded, so that a run of consecutive input rows lands as ONE bulk
+// copy -- measured slower (C2 64-RHS flux 0.888 vs 0.779 ms): the 4-way conflicts of the B-fragment
+// loads cost the consumers more than the per-row copy issue costs the gatherers
+#ifndef HM_MRHS_X_RUNS
+#define HM_MRHS_X_RUNS 0
+#endif
+constexpr int kXStride = HM_MRHS_X_RUNS ? 64 : 68;
 __host__ __device__ constexpr int padded_ld(int ld) {   // smem column stride of a chunk with ld rows
     return ld + ((ld & 15) <= 4 ? 4 - (ld & 15) : (ld & 15) <= 12 ? 12 - (ld & 15) : 20 - (ld & 15));
 }
+// shared-memory column stride of a chunk.  HM_MRHS_WHOLE_CHUNK = 2 (default): every chunk lands as ONE
+// bulk copy of its contiguous payload (stride ld).  The producer is one warp, and per-column copies are
+// issued lane by lane (a uniform-operand loop): at 64 copies per chunk that issue loop, not HBM, bounded
+// the engine (C2 64-RHS flux 0.884 ms -> 0.779 ms).  The price is bank conflicts on the A-fragment
+// loads of chunks whose ld is not 4, 8 or 12 (mod 16) (ncu: 1.63x the ideal shared wavefronts).  = 1: only
+// those conflict-free chunks whole, the others per column at padded_ld(ld) (0.803 ms); = 0: all per
+// column (0.884 ms)
+#ifndef HM_MRHS_WHOLE_CHUNK
+#define HM_MRHS_WHOLE_CHUNK 2
+#endif
+__host__ __device__ constexpr bool whole_chunk(int ld) {
+    return HM_MRHS_WHOLE_CHUNK == 2 || (HM_MRHS_WHOLE_CHUNK && ((ld & 15) == 4 || (ld & 15) == 8 || (ld & 15) == 12));
+}
+__host__ __device__ constexpr int smem_ld(int ld) { return whole_chunk(ld) ? ld : padded_ld(ld); }
 // payload columns land at stride padded_ld(ld) (one bulk copy per column): at most
-// kUnitPayloadDoubles + 6 * kMrhsMaxCols doubles
-constexpr int kMPayload = kUnitPayloadDoubles + 6 * kMrhsMaxCols;
+// kMrhsPayloadDoubles + 6 * kMrhsMaxCols doubles
+constexpr int kMPayload = kMrhsPayloadDoubles + (HM_MRHS_WHOLE_CHUNK == 2 ? 0 : 6 * kMrhsMaxCols);
 constexpr int kMaxPassesM = 96;
 constexpr int kMaxTiles = 16;         // 8x8 accumulator tiles per consumer warp (128 rows x 64 cols / 8 warps)
 
@@ -65,6 +89,7 @@ struct MSmem {
 };
 
 static_assert(sizeof(MSmem) + 128 <= 232448, "multi-RHS engine shared memory exceeds 227 KB");
+static_assert(kMrhsMaxCols <= 64 && kMrhsMaxCols % 4 == 0, "X tile: the two gatherer warps cover <= 64 columns");
 static_assert(padded_ld(40) == 44 && padded_ld(80) == 84 && padded_ld(126) == 132 && padded_ld(2) == 4, "padded_ld");
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -146,6 +171,16 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const dou
 #endif
 #ifndef HM_MRHS_TILE1D
 #define HM_MRHS_TILE1D 0
+#endif
+#ifndef HM_MRHS_GATHER_CPASYNC
+#define HM_MRHS_GATHER_CPASYNC 0
+#endif
+#ifndef HM_MRHS_PAYLOAD_CPASYNC
+#define HM_MRHS_PAYLOAD_CPASYNC 0
+#endif
+// rows in flight per consumer warp in the element-wise units (4: fewest register spills of the kernel)
+#ifndef HM_MRHS_EROWS
+#define HM_MRHS_EROWS 4
 #endif
 __device__ __forceinline__ bool use_1d(int M8, int N8) { return HM_MRHS_TILE1D && N8 == 8 && (M8 & 1) && M8 <= 7; }
 
@@ -302,11 +337,25 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             const unsigned long long t = nxt;
             const bool end = t >= (unsigned long long)A.n_tasks;
             Task task{};
+            // element-wise units (prologue / permute / epilogue) are taken one at a time: the next task
+            // index is grabbed only after the unit has been consumed.  Grabbing ahead let the first CTAs
+            // to arrive hold up to four barrier-gated units each and run them back to back (C2 64-RHS
+            // flux epilogue 42-50 us for 148 one-per-SM units)
+            bool ew = false;
             if (!end) {
                 task = A.tasks[t];
-                if (lane == 0) nxt = atomicAdd(A.queue, 1ull) - queue_base;
+                ew = S.passes[task.pass].type != UNIT_STREAM;
+                if (lane == 0 && !ew) nxt = atomicAdd(A.queue, 1ull) - queue_base;
             }
             const int nch = end ? 1 : task.n_units;
+#if HM_DEVICE_CHECKS
+            if (!end && (task.first_unit < 0 || nch < 1 || task.first_unit + nch > A.n_units)) {
+                if (lane == 0)
+                    printf("hm device check failed: task %llu units [%lld, +%d) of %lld\n", t, (long long)task.first_unit,
+                           nch, (long long)A.n_units);
+                __trap();
+            }
+#endif
             for (int base = 0; base < nch; base += 32) {
                 long long c0 = clock64();
                 Unit mine{};
@@ -326,6 +375,15 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                     const int uld = __shfl_sync(0xffffffffu, mine.ld, c);
                     const int upass = __shfl_sync(0xffffffffu, mine.pass, c);
                     const long long uoff = __shfl_sync(0xffffffffu, (long long)mine.a_off, c);
+                    // payload route (whole_chunk): one bulk copy of the chunk (default); else column by
+                    // column at padded_ld(ld), by per-column bulk copies (issued lane by lane) or by 16-byte
+                    // cp.async from every lane (HM_MRHS_PAYLOAD_CPASYNC=1: measured slower, 0.846 vs 0.796 ms)
+                    const bool stream = !end && utype == UNIT_STREAM;
+#if HM_DEVICE_CHECKS
+                    if (stream) check_payload(A, upass, uoff, uncols, uld);
+#endif
+                    const bool whole = stream && whole_chunk(uld);
+                    const bool cpa = stream && !whole && HM_MRHS_PAYLOAD_CPASYNC;
                     if (lane == c) {
                         if (end) {
                             St.hdr.type = -1;
@@ -334,14 +392,35 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                         } else {
                             St.hdr = mine;
                             mbar_arrive(&S.posted[s]);
-                            if (mine.type == UNIT_STREAM)
+                            if (stream && !cpa)
                                 mbar_expect_tx(&S.full[s], (uint32_t)mine.ncols * (uint32_t)mine.ld * 8u);
-                            else
+                            else if (!stream)
                                 mbar_arrive(&S.full[s]);
                         }
                     }
                     __syncwarp();
-                    if (!end && utype == UNIT_STREAM) {   // column j -> payload + j * padded_ld(ld)
+                    if (whole) {   // one copy of the whole chunk
+                        if (lane == 0) {
+                            const double* src = S.passes[upass].arena + uoff;
+                            const uint32_t pb = (uint32_t)uncols * (uint32_t)uld * 8u;
+                            if (HM_PAYLOAD_EVICT_FIRST)
+                                tma_load_1d_hint(St.payload, src, pb, &S.full[s], pol);
+                            else
+                                tma_load_1d(St.payload, src, pb, &S.full[s]);
+                        }
+                    } else if (cpa) {   // 16-byte pieces (column j, piece q) -> payload + j * padded_ld(ld) + 2 q
+                        const double* src = S.passes[upass].arena + uoff;
+                        const int ldp = padded_ld(uld);
+                        const int h = uld >> 1;
+                        const int tot = uncols * h;
+                        for (int i = lane; i < tot; i += 32) {
+                            const int j = i / h, q = i - j * h;
+                            cp_async16_hint(St.payload + j * ldp + 2 * q, src + (int64_t)j * uld + 2 * q, pol);
+                        }
+                        cp_async_mbar_arrive(&S.full[s]);
+                        __syncwarp();
+                        if (lane == c) mbar_arrive(&S.full[s]);   // after every lane's pending increment
+                    } else if (stream) {   // column j -> payload + j * padded_ld(ld)
                         const double* src = S.passes[upass].arena + uoff;
                         const int ldp = padded_ld(uld);
                         for (int j = lane; j < uncols; j += 32) {
@@ -356,6 +435,14 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                 nxt = __shfl_sync(0xffffffffu, nxt, 0);
             }
             if (end) break;
+            if (ew) {   // wait until the unit's (last) stage is released, then take the next task
+                const int64_t kl = k - 1;
+                if (lane == 0) {
+                    mbar_wait(&S.empty[(int)(kl % kMStages)], (uint32_t)((kl / kMStages) & 1));
+                    nxt = atomicAdd(A.queue, 1ull) - queue_base;
+                }
+                nxt = __shfl_sync(0xffffffffu, nxt, 0);
+            }
         }
         if (A.stats && lane == 0) {
             atomicAdd(A.stats + 0, st_e);
@@ -391,6 +478,10 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             }
             c0 = clock64();
             st_d += c0 - c1;
+#if HM_DEVICE_CHECKS
+            if (type == UNIT_STREAM && gw == 0)
+                check_chunk(A, H, S.passes[H.pass < A.n_passes ? H.pass : 0], kMrhsMaxCols, kMrhsPayloadDoubles, lane);
+#endif
             if (type == UNIT_STREAM) {
                 const Pass& P = S.passes[H.pass];
                 const double* in = P.in;
@@ -419,6 +510,41 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                             if (c < ncol4) reinterpret_cast<double2*>(St.X + c * kXStride)[lane] = v[u];
                         }
                     }
+                } else if (im == IN_PLAIN && HM_MRHS_GATHER_CPASYNC) {
+                    // X rows (512 B each, written by an earlier pass: L2) by 16-byte cp.async, one row per
+                    // warp instruction (lane l: doubles 2l, 2l + 1), no per-lane serialisation; each lane
+                    // arrives on the stage's barrier when its copies have landed.  Off by default: measured
+                    // slower than the per-row bulk copies (C2 64-RHS flux 0.818 vs 0.795 ms)
+                    const int c = gw + kMGatherers * lane;
+                    const int32_t jl = c < ncols ? __ldg(cs + c) : -1;
+                    const int nmine = (ncol4 - gw + kMGatherers - 1) / kMGatherers;   // rows of this warp (with k padding)
+                    for (int u = 0; u < nmine; ++u) {
+                        const int cc = gw + kMGatherers * u;
+                        const int32_t j = __shfl_sync(0xffffffffu, jl, u);
+                        double* dst = St.X + cc * kXStride + 2 * lane;
+                        if (j >= 0)
+                            cp_async16(dst, in + (int64_t)j * kMrhsMax + 2 * lane);
+                        else   // k-step padding column: zero (consumers multiply it)
+                            *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+                    }
+                    cp_async_mbar_arrive(&S.gathered[s]);
+                } else if (im == IN_PLAIN && HM_MRHS_X_RUNS && H.nruns > 0) {
+                    // runs of consecutive input rows (the chunk's run-length column sources): rows are
+                    // contiguous in the internal 64-wide vector and, at stride 64, in the tile, so each
+                    // run arrives by ONE bulk copy; warp gw, lane l -> run r = gw + kMGatherers * l
+                    const int nr = H.nruns;
+                    const int r = gw + kMGatherers * lane;
+                    int start = 0;
+                    for (int q = 0; q < r && q < nr; ++q) start += H.run_len[q];
+                    const int len = r < nr ? (int)H.run_len[r] : 0;
+                    const uint32_t bytes = (uint32_t)len * kMrhsMax * 8u;
+                    const uint32_t tot = __reduce_add_sync(0xffffffffu, bytes);
+                    if (lane == 0 && tot) mbar_add_tx(&S.gathered[s], tot);
+                    __syncwarp();
+                    if (len > 0)
+                        tma_load_1d(St.X + start * kXStride, in + (int64_t)H.run_src[r] * kMrhsMax, bytes, &S.gathered[s]);
+                    if (gw == 0)   // k-step padding rows [ncols, ncol4): zero (consumers multiply them)
+                        for (int i = lane; i < (ncol4 - ncols) * kXStride; i += 32) St.X[ncols * kXStride + i] = 0.0;
                 } else if (im == IN_PLAIN) {
                     // each X row (512 B, written by an earlier pass) arrives by a 1-D TMA bulk copy:
                     // warp gw, lane l -> column c = gw + kMGatherers * l
@@ -557,7 +683,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             }
             const double* Ap = St.payload;
             const double* Xp = St.X;
-            const int ldp = padded_ld(ld);
+            const int ldp = smem_ld(ld);
             // this warp's tiles t = cw + 8 i (row tiles mt, column tile nt); the k loop is
             // specialised on the tile count so the fragments of a k-step are loaded as a batch into
             // distinct registers and then feed back-to-back DMMAs
@@ -595,16 +721,20 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             }
             }
         } else if (type == UNIT_EPILOGUE) {
-            // rows x R of the internal result through the pass's output mode: row-wise, warp cw takes
-            // rows cw, cw + 8, ..., four rows in flight, lanes take the columns (coalesced); the per-row
-            // scalars (perm, eps, A, g) are loaded once per row
+            // rows x R of the internal result through the pass's output mode: warp cw takes rows
+            // cw, cw + 8, ..., kERows of them in flight; lane l covers columns 2l, 2l + 1 (the internal
+            // 64-wide row as one 16-byte load per lane).  The per-row scalars (perm, eps, A, g) are loaded
+            // for all kERows rows first, so the dependent loads of T's row e = perm[row] are in flight
+            // together (the unit is latency-bound: one round trip per batch, not per row)
             if (P.mode == OUT_PERM || P.mode == OUT_FLUX) {
                 const bool flux = P.mode == OUT_FLUX;
-                for (int r0 = cw; r0 < nrows; r0 += 4 * kMConsumerWarps) {
-                    int64_t e[4];
-                    double sc[4], gg[4], am[4];
+                constexpr int kERows = HM_MRHS_EROWS;
+                const int c2 = 2 * lane;
+                for (int r0 = cw; r0 < nrows; r0 += kERows * kMConsumerWarps) {
+                    int64_t e[kERows];
+                    double sc[kERows], gg[kERows], am[kERows];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kERows; ++u) {
                         const int r = r0 + u * kMConsumerWarps;
                         const int64_t row = out0 + (r < nrows ? r : 0);
                         e[u] = __ldg(A.perm + row);
@@ -612,23 +742,29 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                         gg[u] = flux ? __ldg(A.g_int + row) : 0.0;
                         am[u] = flux && A.amb ? __ldg(A.amb + row) : 0.0;
                     }
+                    double2 v[kERows];
+                    double t0[kERows], t1[kERows];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int col = lane + 32 * h;
-                        double v[4], t[4];
+                    for (int u = 0; u < kERows; ++u) {
+                        const int r = r0 + u * kMConsumerWarps;
+                        const bool ok = r < nrows && c2 < R;
+                        v[u] = ok ? __ldcg(reinterpret_cast<const double2*>(P.in + (out0 + r) * kMrhsMax + c2))
+                                  : make_double2(0.0, 0.0);
+                        t0[u] = ok && flux ? __ldg(A.user_in + e[u] * A.ld + c2) : 0.0;
+                        t1[u] = ok && flux && c2 + 1 < R ? __ldg(A.user_in + e[u] * A.ld + c2 + 1) : 0.0;
+                    }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int r = r0 + u * kMConsumerWarps;
-                            const bool ok = r < nrows && col < R;
-                            v[u] = ok ? __ldcg(P.in + (out0 + r) * kMrhsMax + col) : 0.0;
-                            t[u] = ok && flux ? __ldg(A.user_in + e[u] * A.ld + col) : 0.0;
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int r = r0 + u * kMConsumerWarps;
-                            if (r < nrows && col < R)
-                                A.user_out[e[u] * A.ld + col] =
-                                    flux ? sc[u] * (v[u] - pow4(t[u]) * gg[u] + am[u] * (pow4(t[u]) - A.t_inf4)) : v[u];
+                    for (int u = 0; u < kERows; ++u) {
+                        const int r = r0 + u * kMConsumerWarps;
+                        if (r >= nrows || c2 >= R) continue;
+                        double* dst = A.user_out + e[u] * A.ld + c2;
+                        if (flux) {
+                            const double h0 = pow4(t0[u]), h1 = pow4(t1[u]);
+                            dst[0] = sc[u] * (v[u].x - h0 * gg[u] + am[u] * (h0 - A.t_inf4));
+                            if (c2 + 1 < R) dst[1] = sc[u] * (v[u].y - h1 * gg[u] + am[u] * (h1 - A.t_inf4));
+                        } else {
+                            dst[0] = v[u].x;
+                            if (c2 + 1 < R) dst[1] = v[u].y;
                         }
                     }
                 }
@@ -658,33 +794,36 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
             }
         } else {
             // element-wise prologue: rows x R of the caller's external-order array permuted into the
-            // internal n x 64 layout (UNIT_PROLOGUE: w = eps T^4); row-wise as the epilogue (perm and eps
-            // once per row, lanes over the columns, four rows in flight per warp)
-            for (int r0 = cw; r0 < nrows; r0 += 4 * kMConsumerWarps) {
-                int64_t e[4];
-                double ep[4];
+            // internal n x 64 layout (UNIT_PROLOGUE: w = eps T^4); as the epilogue: perm and eps for
+            // kPRows rows first, then their T rows in flight together, lane l -> columns 2l, 2l + 1
+            // (one 16-byte store per lane into the internal row)
+            constexpr int kPRows = HM_MRHS_EROWS;
+            const int c2 = 2 * lane;
+            for (int r0 = cw; r0 < nrows; r0 += kPRows * kMConsumerWarps) {
+                int64_t e[kPRows];
+                double ep[kPRows];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kPRows; ++u) {
                     const int r = r0 + u * kMConsumerWarps;
                     const int64_t row = out0 + (r < nrows ? r : 0);
                     e[u] = __ldg(A.perm + row);
                     ep[u] = type == UNIT_PROLOGUE ? __ldg(A.eps_int + row) : 1.0;
                 }
+                double t0[kPRows], t1[kPRows];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int col = lane + 32 * h;
-                    double v[4];
+                for (int u = 0; u < kPRows; ++u) {
+                    const int r = r0 + u * kMConsumerWarps;
+                    const bool ok = r < nrows && c2 < R;
+                    t0[u] = ok ? __ldg(A.user_in + e[u] * A.ld + c2) : 0.0;
+                    t1[u] = ok && c2 + 1 < R ? __ldg(A.user_in + e[u] * A.ld + c2 + 1) : 0.0;
+                }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int r = r0 + u * kMConsumerWarps;
-                        v[u] = (r < nrows && col < R) ? __ldg(A.user_in + e[u] * A.ld + col) : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int r = r0 + u * kMConsumerWarps;
-                        if (r < nrows && col < R)
-                            P.out[(out0 + r) * kMrhsMax + col] = type == UNIT_PROLOGUE ? ep[u] * pow4(v[u]) : v[u];
-                    }
+                for (int u = 0; u < kPRows; ++u) {
+                    const int r = r0 + u * kMConsumerWarps;
+                    if (r >= nrows || c2 >= R) continue;
+                    const double2 w = type == UNIT_PROLOGUE ? make_double2(ep[u] * pow4(t0[u]), ep[u] * pow4(t1[u]))
+                                                            : make_double2(t0[u], t1[u]);
+                    *reinterpret_cast<double2*>(P.out + (out0 + r) * kMrhsMax + c2) = w;
                 }
             }
             // the rest of the 64-wide rows stays zero-free of stale values: columns R..63 are never read
