@@ -80,6 +80,25 @@ def run(cfgid, exact=False):
     ms, info = hm.hm_profile_flux(ctx, F, LU, Td, qd, 20)
     out["flux_ms"] = ms
     out["flux_GBs"] = (st["bytes_F"] + st["bytes_C"]) / (ms["flux"] * 1e-3) / 1e9
+    if "--mrhs" in sys.argv:   # 64-RHS flux (DMMA engine; C5's BASELINE workload): time, FP64 TFLOP/s, column 0
+        T64 = torch.from_numpy(np.ascontiguousarray(synth.make_config(cfgid, exact=exact, nrhs=64).T)).cuda()
+        q64 = torch.empty_like(T64)
+        for _ in range(2):
+            hm.hm_radiative_flux(ctx, F, LU, T64, q64)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        it = 5
+        e0.record()
+        for _ in range(it):
+            hm.hm_radiative_flux(ctx, F, LU, T64, q64)
+        e1.record()
+        torch.cuda.synchronize()
+        t64 = e0.elapsed_time(e1) / it
+        out["flux64_ms"] = t64
+        out["flux64_TFLOPs"] = 2 * 64 * (st["bytes_F"] + st["bytes_C"]) / 8 / (t64 * 1e-3) / 1e12
+        q1 = torch.empty_like(Td)
+        hm.hm_radiative_flux(ctx, F, LU, T64[:, 0].contiguous(), q1)
+        out["flux64_col0_vs_single"] = rel(q64[:, 0].cpu().numpy(), q1.cpu().numpy())
     print(json.dumps(out), flush=True)
 
 
