@@ -91,7 +91,7 @@ class HMatrix:
 
 def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True,
              adm_mode: int = 0, k_max: int = 48, probes: int = 0, pivoting: str = "partial",
-             recompress: bool = False) -> HMatrix:
+             recompress: bool = False, quadrature: bool = False) -> HMatrix:
     """Trees (Alg. 1, 2), dense near field, partial-pivot ACA far field (optionally recompressed,
     aca.recompress at eps_aca), then row sums and closed-cavity scaling of the row factors (U and
     dense rows)."""
@@ -100,6 +100,7 @@ def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True
     c = facets.centroid[perm]
     nrm = facets.normal[perm]
     A = facets.area[perm]
+    Q = _vf.quadrature_table(facets.tris[perm]) if quadrature else None   # reading R35
     blocks = []
     for blk in _tree.build_block_tree(tr, eta):
         r0, r1, c0, c1 = blk.row.begin, blk.row.end, blk.col.begin, blk.col.end
@@ -111,12 +112,12 @@ def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True
             kcap = _aca.storage_cap(m, n, k_max)
             if pivoting == "full":   # the paper's variant on the explicit block
                 I, J = np.meshgrid(rows, cols, indexing="ij")
-                Xb = _vf.entry_pairs(c, nrm, A, I.ravel(), J.ravel()).reshape(m, n)
+                Xb = _vf.entry_pairs(c, nrm, A, I.ravel(), J.ravel(), Q).reshape(m, n)
                 res = _aca.aca_full(Xb, eps_aca, kcap)
             else:
                 res = _aca.aca_partial(
-                    lambda i: _vf.entry_pairs(c, nrm, A, np.full(n, r0 + i), cols),
-                    lambda j: _vf.entry_pairs(c, nrm, A, rows, np.full(m, c0 + j)),
+                    lambda i: _vf.entry_pairs(c, nrm, A, np.full(n, r0 + i), cols, Q),
+                    lambda j: _vf.entry_pairs(c, nrm, A, rows, np.full(m, c0 + j), Q),
                     m, n, eps_aca, kcap, probes)
             hb.margin = res.margin
             k = res.rank
@@ -127,7 +128,7 @@ def assemble(facets, n_min: int, eta: float, eps_aca: float, closed: bool = True
                 hb.kind, hb.rank, hb.U, hb.V = KIND_LR, U.shape[1], U, V
         if hb.kind != KIND_LR:
             I, J = np.meshgrid(rows, cols, indexing="ij")
-            hb.D = _vf.entry_pairs(c, nrm, A, I.ravel(), J.ravel()).reshape(m, n)
+            hb.D = _vf.entry_pairs(c, nrm, A, I.ravel(), J.ravel(), Q).reshape(m, n)
         blocks.append(hb)
     H = HMatrix(facets.n, perm, tr, blocks, np.ones(facets.n), closed)
     # row sums from the H-matrix itself: s = (F_H 1) / A  (eq:rowsum)

@@ -257,6 +257,26 @@ def parallel_plates(m: int, L: float = 1.0, gap: float = 1.0) -> Facets:
                   np.ascontiguousarray(box), None, f"plates{m}x{m}")
 
 
+def parallel_plates_tri(m: int, L: float = 1.0, gap: float = 1.0) -> Facets:
+    """The parallel plates of parallel_plates(m) with every square cell split into two triangles along its
+    (0,0)-(1,1) diagonal (2 m^2 facets per plate, vertices kept): the plate geometry for the adaptive
+    quadrature of reading R35, which integrates over triangles.  Normals face the other plate."""
+    g = np.linspace(0.0, L, m + 1)
+    V, T = [], []
+    for z in (0.0, gap):
+        base = len(V)
+        for x in g:
+            for y in g:
+                V.append((x, y, z))
+        idx = lambda i, j: base + i * (m + 1) + j   # noqa: E731
+        for i in range(m):
+            for j in range(m):
+                T.append((idx(i, j), idx(i + 1, j), idx(i + 1, j + 1)))
+                T.append((idx(i, j), idx(i + 1, j + 1), idx(i, j + 1)))
+    return _facets_from_tris(np.asarray(V, dtype=np.float64), np.asarray(T, dtype=np.int64),
+                             interior=(0.5 * L, 0.5 * L, 0.5 * gap), name=f"plates-tri{m}x{m}")
+
+
 def line_facets(n: int) -> Facets:
     """PAPER.md:368-370 Example 1: n equidistant facets on a straight line; facet i is the
     interval [i-1/2, i+1/2] on the x axis (the facet-extent boxes that reproduce Fig. 1)."""
