@@ -94,6 +94,15 @@ typedef struct {
                               rank-k' approximation at eps_aca (QR + SVD truncation, Frobenius tail;
                               PAPER.md:642, reading R32): fewer stored bytes, ranks no longer
                               the raw ACA ranks; 0: off (default)                                    */
+    int32_t quadrature;    /* 0: one-point centroid rule for every entry (default); 1: the
+                              adaptive Gauss quadrature of PAPER.md:156 (reading R35): with d
+                              the centroid distance and h the longer of the two facets' longest edges,
+                              d >= 10h one point, 4h <= d < 10h the 3-point rule on each triangle,
+                              1.5h <= d < 4h the 6-point (Dunavant degree-4) rule, d < 1.5h the 6-point
+                              rule on each of the 4 midpoint sub-triangles; each point pair with its own
+                              back-facing test.  Needs `vertices`.                                    */
+    const double* vertices;/* quadrature = 1: host array n x 9, external order, facet i's triangle
+                              (x0 y0 z0 x1 y1 z1 x2 y2 z2); read during the call only; else ignored */
 } hm_aca_params;
 
 /* H-LU parameters. */
@@ -182,7 +191,8 @@ hm_status hm_build_geometry(hm_ctx* ctx, int64_t n, const double* xyz, const dou
                             const double* area, const double* facet_aabb,
                             const hm_tree_params* params, hm_geom** out);
 /* Dense near field + batched partial-pivot ACA far field of F (eq:Fdef_new_location by the
-   one-point centroid rule), then (closed_cavity) row sums F_H 1 / A,
+   one-point centroid rule, or params->quadrature's adaptive Gauss rule), then
+   (closed_cavity) row sums F_H 1 / A,
    clamp and row scaling. */
 hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params* params,
                           hm_hmat** F_out);

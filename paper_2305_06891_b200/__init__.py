@@ -40,7 +40,8 @@ class hm_tree_params(C.Structure):
 
 class hm_aca_params(C.Structure):
     _fields_ = [("eps_aca", C.c_double), ("k_max", C.c_int32), ("closed_cavity", C.c_int32),
-                ("probes", C.c_int32), ("pivoting", C.c_int32), ("recompress", C.c_int32)]
+                ("probes", C.c_int32), ("pivoting", C.c_int32), ("recompress", C.c_int32),
+                ("quadrature", C.c_int32), ("vertices", C.c_void_p)]
 
 
 class hm_lu_params(C.Structure):
@@ -330,9 +331,20 @@ def hm_build_geometry(ctx: Context, centroid, normal, area, facet_aabb=None, n_m
 
 
 def hm_assemble_aca(ctx: Context, geom: Geometry, eps_aca=1e-6, k_max=0, closed_cavity=True, probes=0,
-                    pivoting="partial", recompress=False) -> HMatrix:
+                    pivoting="partial", recompress=False, quadrature="one-point", vertices=None) -> HMatrix:
+    """quadrature="adaptive" (reading R35) needs `vertices`: (n, 3, 3) or (n, 9) triangle vertices,
+    external order."""
+    q = {"one-point": 0, "adaptive": 1}[quadrature]
+    vtx = None
+    if q:
+        if vertices is None:
+            raise ValueError("quadrature='adaptive' needs the facets' triangle vertices")
+        vtx = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64).reshape(-1, 9))
+        if vtx.shape[0] != geom.n:
+            raise ValueError(f"vertices: {vtx.shape[0]} facets, geometry has {geom.n}")
     p = hm_aca_params(float(eps_aca), int(k_max), int(bool(closed_cavity)), int(probes),
-                      {"partial": 0, "full": 1}[pivoting], int(bool(recompress)))
+                      {"partial": 0, "full": 1}[pivoting], int(bool(recompress)), q,
+                      vtx.ctypes.data if vtx is not None else None)
     h = C.c_void_p()
     ctx.check(ctx.lib.hm_assemble_aca(ctx.h, geom.h, C.byref(p), C.byref(h)), "hm_assemble_aca")
     return HMatrix(ctx, h, geom)

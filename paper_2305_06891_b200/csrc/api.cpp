@@ -59,6 +59,51 @@ void dfree(Ctx* ctx, void* p) {
 // implemented in hlu.cpp
 void factor_hlu(HLU& L, const double* emissivity);
 
+// Reading R35: the adaptive-quadrature table, internal order -- per facet the points of
+// the 3-point degree-2 rule, of Dunavant's 6-point degree-4 rule and of that rule on the 4 midpoint
+// sub-triangles (v0, m01, m20), (m01, v1, m12), (m20, m12, v2), (m12, m20, m01), each point
+// x = (b0 v0 + b1 v1) + b2 v2 (no contraction: the oracle forms the same doubles), then the squared
+// longest edge.  vertices_ext: n x 9, external order.
+std::vector<double> quad_table(const Geom& g, const double* V) {
+    const int64_t n = g.n;
+    std::vector<double> Q((size_t)n * kQStride, 0.0);
+    const double t = 2.0 / 3.0, u = 1.0 / 6.0;
+    const double b3[3][3] = {{t, u, u}, {u, t, u}, {u, u, t}};
+    const double A = 0.445948490915965, B = 0.108103018168070, Cc = 0.091576213509771, D = 0.816847572980459;
+    const double b6[6][3] = {{B, A, A}, {A, B, A}, {A, A, B}, {D, Cc, Cc}, {Cc, D, Cc}, {Cc, Cc, D}};
+    for (int64_t i = 0; i < n; ++i) {
+        const double* v0 = V + 9 * (int64_t)g.perm[i];
+        const double* v1 = v0 + 3;
+        const double* v2 = v0 + 6;
+        double* row = Q.data() + i * kQStride;
+        int k = 0;
+        auto put = [&](const double* b, const double* p0, const double* p1, const double* p2) {
+            for (int c = 0; c < 3; ++c) row[3 * k + c] = (b[0] * p0[c] + b[1] * p1[c]) + b[2] * p2[c];
+            ++k;
+        };
+        for (int p = 0; p < 3; ++p) put(b3[p], v0, v1, v2);
+        for (int p = 0; p < 6; ++p) put(b6[p], v0, v1, v2);
+        double m01[3], m12[3], m20[3];
+        for (int c = 0; c < 3; ++c) {
+            m01[c] = (v0[c] + v1[c]) * 0.5;
+            m12[c] = (v1[c] + v2[c]) * 0.5;
+            m20[c] = (v2[c] + v0[c]) * 0.5;
+        }
+        const double* sub[4][3] = {{v0, m01, m20}, {m01, v1, m12}, {m20, m12, v2}, {m12, m20, m01}};
+        for (int q = 0; q < 4; ++q)
+            for (int p = 0; p < 6; ++p) put(b6[p], sub[q][0], sub[q][1], sub[q][2]);
+        double h2 = 0.0;
+        const double* ed[3][2] = {{v0, v1}, {v1, v2}, {v2, v0}};
+        for (int e = 0; e < 3; ++e) {
+            const double ex = ed[e][1][0] - ed[e][0][0], ey = ed[e][1][1] - ed[e][0][1], ez = ed[e][1][2] - ed[e][0][2];
+            const double l2 = (ex * ex + ey * ey) + ez * ez;
+            h2 = e == 0 ? l2 : std::max(h2, l2);
+        }
+        row[kQH2] = h2;
+    }
+    return Q;
+}
+
 }  // namespace hm
 
 using namespace hm;
@@ -316,6 +361,9 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         if (params->probes < 0 || params->probes > 16) throw Error(HM_ERR_INVALID_ARG, "probes must be in [0, 16]");
         if (params->pivoting != 0 && params->pivoting != 1) throw Error(HM_ERR_INVALID_ARG, "pivoting must be 0 or 1");
         if (params->recompress != 0 && params->recompress != 1) throw Error(HM_ERR_INVALID_ARG, "recompress must be 0 or 1");
+        if (params->quadrature != 0 && params->quadrature != 1) throw Error(HM_ERR_INVALID_ARG, "quadrature must be 0 or 1");
+        if (params->quadrature == 1 && !params->vertices)
+            throw Error(HM_ERR_INVALID_ARG, "quadrature = 1 (adaptive) needs the facets' triangle vertices");
         const Geom& g = geom->g;
         const cudaStream_t s = c->stream;
         const int64_t n = g.n;
@@ -325,6 +373,10 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
         F.ctx = c;
         F.geom = &g;
         F.params = *params;
+        F.params.vertices = nullptr;   // the caller's array is read during this call only
+        DBuf<double> dquad;            // reading R35 table (assembly only)
+        if (params->quadrature == 1) dquad.upload(c, quad_table(g, params->vertices), "quadrature table", s);
+        const double* quad = dquad.p;
         const int KMAX = params->k_max > 0 ? params->k_max : 48;
         const size_t nb = g.blocks.size();
         F.blk_kind.assign(nb, KIND_DENSE);
@@ -382,7 +434,7 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             dblk.upload(c, hblk, "fp-aca blocks", s);
             dkcap.upload(c, hkcap, "fp-aca kcap", s);
             drank.alloc(c, ids.size(), "fp-aca ranks");
-            k::fill_entries(g.d_geo.p, n, dfill.p, (int)ids.size(), scratch.p, err.p, s);
+            k::fill_entries(g.d_geo.p, n, dfill.p, (int)ids.size(), scratch.p, err.p, s, quad);
             k::cpaca_batch(scratch.p, 1, dblk.p, dkcap.p, (int)ids.size(), params->eps_aca, scratch.p, drank.p, s);
             std::vector<int32_t> hrank(ids.size());
             HM_CUDA(cudaMemcpyAsync(hrank.data(), drank.p, ids.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -451,7 +503,7 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             dmargin.alloc(c, ids.size(), "aca margins");
             scratch.alloc(c, (size_t)std::max<int64_t>(cur, 2), "aca scratch");
             k::aca_batch(g.d_geo.p, n, dblk.p, duoff.p, dvoff.p, params->probes, dkcap.p, (int)ids.size(), params->eps_aca, scratch.p,
-                         drank.p, dmargin.p, err.p, s, max_m, max_n);
+                         drank.p, dmargin.p, err.p, s, max_m, max_n, quad);
             std::vector<int32_t> hrank(ids.size());
             HM_CUDA(cudaMemcpyAsync(hrank.data(), drank.p, ids.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
             HM_CUDA(cudaStreamSynchronize(s));
@@ -538,8 +590,8 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             }
         }
         F.op.p1_by_key = true;   // phase 1 in cluster order (row-group links of the flux program)
-        build_hop(c, g, src, F.op, s);
-        if (g.shard.sharded()) build_hop(c, g, src, F.op_loc, s, &g.shard);   // this rank's block rows
+        build_hop(c, g, src, F.op, s, nullptr, 0, quad);
+        if (g.shard.sharded()) build_hop(c, g, src, F.op_loc, s, &g.shard, 0, quad);   // this rank's block rows
         batches.clear();
         F.setup_seconds[1] = now_seconds() - t0;
 

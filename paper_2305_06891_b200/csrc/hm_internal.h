@@ -309,7 +309,12 @@ struct HOp {
 // buffer get disjoint t regions, so a level's phase 1 never overwrites t still to be read by another
 // subtree's phase 2 of an earlier level)
 void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s,
-               const Shard* sh = nullptr, int64_t t_off = 0);
+               const Shard* sh = nullptr, int64_t t_off = 0, const double* quad = nullptr);
+// adaptive Gauss quadrature of the view-factor entries (reading R35): per facet
+// (internal order) kQStride doubles: 3 + 6 + 24 quadrature points (x, y, z) of the three tiers, then
+// the squared longest edge
+constexpr int kQStride = 100, kQOff1 = 0, kQOff2 = 9, kQOff3 = 27, kQH2 = 99;
+std::vector<double> quad_table(const Geom& g, const double* vertices_ext);
 
 // ------------------------------------------------------------------ persistent stream engine
 struct Pass {
@@ -551,9 +556,10 @@ namespace k {
 void aca_batch(const double* geo, int64_t n, const int64_t* blk /*[nb][4] r0,m,c0,n*/,
                const int64_t* uoff, const int64_t* voff, int probes, const int32_t* kcap, int nb, double eps,
                double* scratch, int32_t* rank_out, double* margin_out, int32_t* err, cudaStream_t s,
-               int64_t max_m, int64_t max_n);
+               int64_t max_m, int64_t max_n, const double* quad = nullptr);
+// quad: the adaptive-quadrature table of reading R35 (internal order, kQStride doubles per facet) or null
 void fill_entries(const double* geo, int64_t n, const int64_t* tasks /*[nt][6] dst,r0,rows,c0,cols,dld*/,
-                  int nt, double* arena, int32_t* err, cudaStream_t s);
+                  int nt, double* arena, int32_t* err, cudaStream_t s, const double* quad = nullptr);
 // dst element (i,j) at arena[dst + j*dld + i] = src[i*rs + j*cs] (src absolute address)
 void pack(const int64_t* tasks /*[nt][7] dst,src,rows,cols,rs,cs,dld*/, int nt, double* arena, cudaStream_t s);
 void scale_rows(const int64_t* tasks /*[nt][5] a_off,ld,m,ncols,r0*/, int nt, double* arena, const double* cdiv,

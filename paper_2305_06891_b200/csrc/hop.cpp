@@ -175,7 +175,7 @@ static void make_units(Ctx* ctx, StreamPass& P, const std::vector<int32_t>& pcs,
 }
 
 void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, cudaStream_t s, const Shard* sh,
-               int64_t t_off) {
+               int64_t t_off, const double* quad) {
     const int64_t n = g.n;
     // sharded: only blocks with rows on this rank; x indices and outputs in the
     // padded layout (x region of XT = n_pad), t after it
@@ -338,7 +338,7 @@ void build_hop(Ctx* ctx, const Geom& g, std::vector<SrcBlock>& blocks, HOp& op, 
         DBuf<int32_t> err;
         err.alloc(ctx, 4, "err");
         HM_CUDA(cudaMemsetAsync(err.p, 0, 4 * sizeof(int32_t), s));
-        k::fill_entries(g.d_geo.p, n, d_fill.p, (int)(fill.size() / 6), op.arena.p, err.p, s);
+        k::fill_entries(g.d_geo.p, n, d_fill.p, (int)(fill.size() / 6), op.arena.p, err.p, s, quad);
         int32_t h[4];
         HM_CUDA(cudaMemcpyAsync(h, err.p, sizeof(h), cudaMemcpyDeviceToHost, s));
         HM_CUDA(cudaStreamSynchronize(s));

@@ -1,5 +1,6 @@
 // Setup kernels that produce the hot path's data:
-//   K1 vf_entry     -- one-point view-factor entry, eq:Fdef_new_location
+//   K1 vf_entry     -- view-factor entry, eq:Fdef_new_location: one-point centroid
+//                      rule, or the adaptive Gauss quadrature of PAPER.md:156 (reading R35) for near pairs
 //   K2 fill_entries -- dense near-field blocks
 //   K3 aca_batch    -- adaptive cross approximation with partial pivoting,
 //                      one CTA per admissible block, reading R10 step by step
@@ -17,9 +18,53 @@ constexpr double kPi = 3.141592653589793;  // the double nearest to pi
 
 struct GeoView {
     const double *cx, *cy, *cz, *nx, *ny, *nz, *A;
-    __device__ GeoView(const double* g, int64_t n)
-        : cx(g), cy(g + n), cz(g + 2 * n), nx(g + 3 * n), ny(g + 4 * n), nz(g + 5 * n), A(g + 6 * n) {}
+    const double* Q;   // adaptive quadrature table (reading R35), internal order, kQStride per facet; or null
+    __device__ GeoView(const double* g, int64_t n, const double* q)
+        : cx(g), cy(g + n), cz(g + 2 * n), nx(g + 3 * n), ny(g + 4 * n), nz(g + 5 * n), A(g + 6 * n), Q(q) {}
 };
+
+// ---------------------------------------------------------------- adaptive Gauss quadrature (R35)
+// the rule's order grows as facets get closer.  Table row of a facet (built on the host,
+// api.cpp quad_table): the 3 points of the degree-2 rule, the 6 of Dunavant's degree-4 rule, the 24 of
+// that rule on the 4 midpoint sub-triangles (x, y, z each), then the squared longest edge.
+__device__ __forceinline__ double tier_weight(int tier, int p) {
+    constexpr double w3 = 1.0 / 3.0;
+    constexpr double wa = 0.223381589678011, wb = 0.109951743655322;   // Dunavant degree 4
+    if (tier == 1) return w3;
+    const double w = (p % 6) < 3 ? wa : wb;
+    return tier == 2 ? w : __dmul_rn(0.25, w);
+}
+// F_ab = A_a A_b sum_p sum_q w_p w_q cos_p cos_q / (pi r_pq^2), points p on facet a, q on facet b (a < b),
+// p-major; a point pair facing away (R3) adds nothing
+__device__ double quad_entry(const GeoView& g, int64_t a, int64_t b, int tier, int32_t* err) {
+    const int off = tier == 1 ? kQOff1 : tier == 2 ? kQOff2 : kQOff3;
+    const int np = tier == 1 ? 3 : tier == 2 ? 6 : 24;
+    const double* Pa = g.Q + a * kQStride + off;
+    const double* Pb = g.Q + b * kQStride + off;
+    const double nax = g.nx[a], nay = g.ny[a], naz = g.nz[a], nbx = g.nx[b], nby = g.ny[b], nbz = g.nz[b];
+    double s = 0.0;
+    for (int p = 0; p < np; ++p) {
+        const double xa = Pa[3 * p], ya = Pa[3 * p + 1], za = Pa[3 * p + 2];
+        const double wp = tier_weight(tier, p);
+        for (int q = 0; q < np; ++q) {
+            const double dx = __dsub_rn(Pb[3 * q], xa);
+            const double dy = __dsub_rn(Pb[3 * q + 1], ya);
+            const double dz = __dsub_rn(Pb[3 * q + 2], za);
+            const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            if (r2 == 0.0) {
+                if (atomicCAS(err, 0, 1) == 0) { err[1] = (int32_t)a; err[2] = (int32_t)b; }
+                return 0.0;
+            }
+            const double ca = __dadd_rn(__dadd_rn(__dmul_rn(nax, dx), __dmul_rn(nay, dy)), __dmul_rn(naz, dz));
+            const double cb = -__dadd_rn(__dadd_rn(__dmul_rn(nbx, dx), __dmul_rn(nby, dy)), __dmul_rn(nbz, dz));
+            if (!(ca > 0.0 && cb > 0.0)) continue;
+            const double t = __ddiv_rn(__dmul_rn(__dmul_rn(wp, tier_weight(tier, q)), __dmul_rn(ca, cb)),
+                                       __dmul_rn(__dmul_rn(kPi, r2), r2));
+            s = __dadd_rn(s, t);
+        }
+    }
+    return __dmul_rn(__dmul_rn(g.A[a], g.A[b]), s);
+}
 
 // K1: F_ij = (A_i A_j cos(phi_i) cos(phi_j)) / (pi R^2) by the centroid rule, canonical
 // pair (a,b) = (min,max); back-facing pairs -> 0 (R3); F_ii = 0.
@@ -36,6 +81,11 @@ __device__ __forceinline__ double vf_entry(const GeoView& g, int64_t i, int64_t 
     if (r2 == 0.0) {
         if (atomicCAS(err, 0, 1) == 0) { err[1] = (int32_t)a; err[2] = (int32_t)b; }
         return 0.0;
+    }
+    if (g.Q) {   // reading R35: pairs closer than 10 h take a quadrature tier (tau^2 = 100, 16, 2.25)
+        const double h2 = fmax(g.Q[a * kQStride + kQH2], g.Q[b * kQStride + kQH2]);
+        if (!(r2 >= __dmul_rn(100.0, h2)))
+            return quad_entry(g, a, b, r2 >= __dmul_rn(16.0, h2) ? 1 : r2 >= __dmul_rn(2.25, h2) ? 2 : 3, err);
     }
     if (!(ca > 0.0 && cb > 0.0)) return 0.0;
     const double num = __dmul_rn(__dmul_rn(g.A[a], g.A[b]), __dmul_rn(ca, cb));
@@ -96,7 +146,8 @@ __global__ void __launch_bounds__(kAcaThreads)
 aca_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restrict__ blk,
            const int64_t* __restrict__ uoff, const int64_t* __restrict__ voff,
            const int32_t* __restrict__ kcap_arr, double eps, double* __restrict__ scratch,
-           int32_t* __restrict__ rank_out, double* __restrict__ margin_out, int32_t* err, int probes) {
+           int32_t* __restrict__ rank_out, double* __restrict__ margin_out, int32_t* err, int probes,
+           const double* __restrict__ quad) {
     __shared__ int64_t s_probe;
     extern __shared__ uint32_t smem_bits[];
     __shared__ ArgMax s_am[kAcaWarps];
@@ -109,7 +160,7 @@ aca_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restri
     double* U = scratch + uoff[b];
     double* V = scratch + voff[b];
     const int kcap = kcap_arr[b];
-    const GeoView g(geo, ntot);
+    const GeoView g(geo, ntot, quad);
     uint32_t* used_r = smem_bits;
     uint32_t* used_c = smem_bits + ((m + 31) >> 5);
     const int tid = threadIdx.x;
@@ -239,10 +290,10 @@ aca_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restri
 }
 
 __global__ void fill_kernel(const double* __restrict__ geo, int64_t ntot, const int64_t* __restrict__ tasks,
-                            double* __restrict__ arena, int32_t* err) {
+                            double* __restrict__ arena, int32_t* err, const double* __restrict__ quad) {
     const int64_t* t = tasks + 6 * blockIdx.x;
     const int64_t dst = t[0], r0 = t[1], rows = t[2], c0 = t[3], cols = t[4], dld = t[5];
-    const GeoView g(geo, ntot);
+    const GeoView g(geo, ntot, quad);
     for (int64_t e = threadIdx.x; e < rows * cols; e += blockDim.x) {
         const int64_t i = e % rows, j = e / rows;  // column-major slice
         arena[dst + j * dld + i] = vf_entry(g, r0 + i, c0 + j, err);
@@ -276,21 +327,21 @@ namespace k {
 
 void aca_batch(const double* geo, int64_t n, const int64_t* blk, const int64_t* uoff, const int64_t* voff, int probes,
                const int32_t* kcap, int nb, double eps, double* scratch, int32_t* rank_out, double* margin_out,
-               int32_t* err, cudaStream_t s, int64_t max_m, int64_t max_n) {
+               int32_t* err, cudaStream_t s, int64_t max_m, int64_t max_n, const double* quad) {
     if (nb == 0) return;
     const size_t smem = sizeof(uint32_t) * (size_t)(((max_m + 31) >> 5) + ((max_n + 31) >> 5));
     if (smem > 48 * 1024)
         HM_CUDA(cudaFuncSetAttribute(aca_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     aca_kernel<<<nb, kAcaThreads, smem, s>>>(geo, n, blk, uoff, voff, kcap, eps, scratch, rank_out, margin_out,
-                                             err, probes);
+                                             err, probes, quad);
     HM_CUDA(cudaGetLastError());
     debug_sync(s, "aca_kernel");
 }
 
 void fill_entries(const double* geo, int64_t n, const int64_t* tasks, int nt, double* arena, int32_t* err,
-                  cudaStream_t s) {
+                  cudaStream_t s, const double* quad) {
     if (nt == 0) return;
-    fill_kernel<<<nt, 256, 0, s>>>(geo, n, tasks, arena, err);
+    fill_kernel<<<nt, 256, 0, s>>>(geo, n, tasks, arena, err, quad);
     HM_CUDA(cudaGetLastError());
     debug_sync(s, "fill_kernel");
 }

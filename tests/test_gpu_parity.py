@@ -991,3 +991,67 @@ def test_apply_is_exact_on_the_exported_factors(hm, ctx):
     zl = apply_items(hm.hm_export_factors(hm.HM_OP_UINV, F, LU),
                      apply_items(hm.hm_export_factors(hm.HM_OP_LINV, F, LU), xi))
     assert np.abs(z[perm] - zl).max() <= 1e-13 * np.abs(zl).max()
+
+
+@pytest.mark.parametrize("case_name", ["C1", "plates-tri"])
+def test_adaptive_quadrature_matches_oracle(hm, ctx, case_name):
+    """NEXT-4 adaptive Gauss quadrature of the entries (reading R35) through the C ABI, on
+    the closed C1 sphere and on triangulated plates 0.2 apart (an open cavity whose inter-plate pairs
+    fall in the quadrature tiers): the GPU evaluates the same entry doubles as the oracle, so partition,
+    kinds and ACA ranks are exactly the oracle's and F x equals the oracle's H-matrix within 1e-13; F x,
+    C^-1 b and the flux (single vector and 8 columns) are within 10 eps of the dense adaptive oracle --
+    and F differs from the one-point F (the option is not ignored)."""
+    import torch
+    if case_name == "C1":
+        cfg, closed, n_min = synth.make_config(1), True, 64
+    else:
+        cfg = synth.make_config(7, geometry=synth.parallel_plates_tri(16, gap=0.2))
+        closed, n_min = False, cfg.n_min
+    f = cfg.facets
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=n_min, eta=1.0)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca, closed_cavity=closed, quadrature="adaptive", vertices=f.tris)
+    H = ohm.assemble(f, n_min, 1.0, cfg.eps_aca, closed=closed, quadrature=True)
+    assert (hm.hm_export_perm(g) == H.perm).all()
+    assert (hm.hm_export_partition(g, F) == H.partition()).all()
+    x = cfg.rhs()[:, 0]
+    y = np.empty(f.n)
+    hm.hm_apply_F(ctx, F, x, y)
+    assert rel(y, H.apply(x)) <= TOL_EXACT
+    Fd, C, _ = vf.dense_operators(f, cfg.emissivity, closed=closed, quadrature=True)
+    assert rel(y, Fd @ x) <= 10 * cfg.eps_aca
+    F1 = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca, closed_cavity=closed)
+    y1 = np.empty(f.n)
+    hm.hm_apply_F(ctx, F1, x, y1)
+    assert rel(y1, y) > 1e-4
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    z = np.empty(f.n)
+    hm.hm_solve_C(ctx, LU, x, z)
+    assert rel(z, vf.solve(C, x)) <= 10 * cfg.eps_aca
+    T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
+    q = torch.empty_like(T)
+    hm.hm_radiative_flux(ctx, F, LU, T, q)
+    torch.cuda.synchronize()
+    qo = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]
+    assert rel(q.cpu().numpy(), qo) <= 10 * cfg.eps_aca
+    T8 = synth.temperatures(cfg.seed, f.n, 8)
+    q8 = np.empty_like(T8)
+    hm.hm_radiative_flux(ctx, F, LU, T8, q8)
+    qo8 = vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, T8)
+    assert max(rel(q8[:, c], qo8[:, c]) for c in range(8)) <= 10 * cfg.eps_aca
+
+
+def test_adaptive_quadrature_argument_checks(hm, ctx):
+    """quadrature = 1 without vertices is an argument error of the C ABI (HM_ERR_INVALID_ARG), and the
+    binding checks the vertex array's length."""
+    cfg = synth.make_config(1)
+    f = cfg.facets
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=64, eta=1.0)
+    with pytest.raises(ValueError):
+        hm.hm_assemble_aca(ctx, g, eps_aca=1e-6, quadrature="adaptive")
+    with pytest.raises(ValueError):
+        hm.hm_assemble_aca(ctx, g, eps_aca=1e-6, quadrature="adaptive", vertices=f.tris[:-1])
+    import ctypes as C
+    lib = hm.load_library()
+    p = hm.hm_aca_params(1e-6, 0, 1, 0, 0, 0, 1, None)
+    h = C.c_void_p()
+    assert lib.hm_assemble_aca(ctx.h, g.h, C.byref(p), C.byref(h)) != 0
