@@ -924,23 +924,26 @@ void factor_hlu(HLU& L, const double* emissivity) {
     L.prog_solve_h.add_stream(L.leafU.p2, L.leafU, L.xtB.p, nullptr, OUT_PERM, DEP_BWD_P2, &mU2);
     L.prog_solve_h.finalize(c, s, &g);
     solve_passes(L.prog_flux, IN_FLUX);
-    auto add_U2_F1 = [&](Program& P) {   // U^-1 phase 2 -> F phase 1, linked group by group (cut level 0)
+    // U^-1 phase 2 -> F phase 1, linked group by group (cut level 0); returns the pass that writes z
+    // (the F input), which F's x-only (near-field) phase-2 tasks wait for -- F may have no phase 1 at all
+    // (no low-rank block: small n, or every admissible block capped), so it is not "two passes back"
+    auto add_U2_F1 = [&](Program& P) {
         const size_t a = P.h_passes.size();
         P.add_stream(L.leafU.p2, L.leafU, L.xtB.p, Fm.xt.p, OUT_ASSIGN, DEP_BWD_P2, &mU2);
+        const int zpass = (int)P.h_passes.size() - 1;
         const size_t b = P.h_passes.size();
         P.add_stream(F.op.p1, F.op, Fm.xt.p, Fm.xt.p, OUT_ASSIGN);
         if (Lc == 0 && b == a + 1 && P.h_passes.size() == b + 1) P.link_rows((int32_t)a, (int32_t)b);
+        return zpass;
     };
-    add_U2_F1(L.prog_flux);
+    const int zf = add_U2_F1(L.prog_flux);
     // x-only (near-field) tasks of phase 2 wait for z, not for phase 1
-    L.prog_flux.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN,
-                           (int)L.prog_flux.h_passes.size() - 2);
+    L.prog_flux.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN, zf);
     L.prog_flux.finalize(c, s, &g);
     // the same flux program behind a copy-in pass, for a pinned host T (single vector, world == 1)
     solve_passes(L.prog_flux_h, IN_FLUX, L.T_dev.p);
-    add_U2_F1(L.prog_flux_h);
-    L.prog_flux_h.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN,
-                             (int)L.prog_flux_h.h_passes.size() - 2);
+    const int zh = add_U2_F1(L.prog_flux_h);
+    L.prog_flux_h.add_stream(F.op.p2, F.op, Fm.xt.p, nullptr, OUT_FLUX, DEP_BARRIER, nullptr, IN_PLAIN, zh);
     L.prog_flux_h.finalize(c, s, &g);
 
     // ---- flux constant g = F C^-1 eps, with a setup program
@@ -949,9 +952,8 @@ void factor_hlu(HLU& L, const double* emissivity) {
     {
         Program pg;
         solve_passes(pg, IN_PERM);
-        add_U2_F1(pg);
-        pg.add_stream(F.op.p2, F.op, Fm.xt.p, L.g_int.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
-                      (int)pg.h_passes.size() - 2);
+        const int zg = add_U2_F1(pg);
+        pg.add_stream(F.op.p2, F.op, Fm.xt.p, L.g_int.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, zg);
         pg.finalize(c, s, &g);
         DBuf<double> eps_ext;
         eps_ext.upload(c, std::vector<double>(emissivity, emissivity + n), "eps (external)", s);
@@ -973,16 +975,18 @@ void factor_hlu(HLU& L, const double* emissivity) {
             // prologue: b (or w = eps T^4) into the internal n x 64 layout, then every gather is a
             // 512-byte TMA row copy
             P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA_m.p, elementwise_rows(n));
+            // x-only phase-2 tasks wait for the pass that wrote their x input (an operator may have no
+            // phase 1: no low-rank block)
+            const int x0 = (int)P.h_passes.size() - 1;
             P.add_stream(L.leafL.p1m, L.leafL, L.xtA_m.p, L.xtA_m.p, OUT_ASSIGN);
-            P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
-                         (int)P.h_passes.size() - 2);
+            P.add_stream(L.leafL.p2m, L.leafL, L.xtA_m.p, L.xtB_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, x0);
             const int32_t l2 = (int32_t)P.h_passes.size() - 1;
+            const size_t nb = P.h_passes.size();
             P.add_stream(L.leafU.p1m, L.leafU, L.xtB_m.p, L.xtB_m.p, OUT_ASSIGN);
             // U^-1 phase 1 of a cluster waits for L^-1 phase 2 on its row group only (as in the
             // single-vector programs): the next operator starts group by group, no full pass drain
-            if (!getenv("HM_MRHS_NO_LINKS")) P.link_rows(l2, (int32_t)P.h_passes.size() - 1);
-            P.add_stream(L.leafU.p2m, L.leafU, L.xtB_m.p, out_u, mode_u, DEP_BARRIER, nullptr, IN_PLAIN,
-                         (int)P.h_passes.size() - 2);
+            if (!getenv("HM_MRHS_NO_LINKS") && P.h_passes.size() == nb + 1) P.link_rows(l2, (int32_t)nb);
+            P.add_stream(L.leafU.p2m, L.leafU, L.xtB_m.p, out_u, mode_u, DEP_BARRIER, nullptr, IN_PLAIN, l2);
         };
         // final results go to an internal n x 64 buffer, then an element-wise epilogue pass emits them
         // (permute-out / flux epilogue) coalesced and fully parallel
@@ -990,11 +994,13 @@ void factor_hlu(HLU& L, const double* emissivity) {
         L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_PERM);
         L.prog_solve_m.finalize(c, s, &g);
         mprog(L.prog_flux_m, IN_FLUX, Fm.xt_m.p, OUT_ASSIGN);
-        L.prog_flux_m.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
-        if (!getenv("HM_MRHS_NO_LINKS"))
-            L.prog_flux_m.link_rows((int32_t)L.prog_flux_m.h_passes.size() - 2, (int32_t)L.prog_flux_m.h_passes.size() - 1);
-        L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
-                                 (int)L.prog_flux_m.h_passes.size() - 2);
+        {
+            Program& P = L.prog_flux_m;
+            const int z = (int)P.h_passes.size() - 1;   // U^-1 phase 2 writes z, the F input
+            P.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
+            if (!getenv("HM_MRHS_NO_LINKS") && (int)P.h_passes.size() == z + 2) P.link_rows(z, z + 1);
+            P.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, z);
+        }
         L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_FLUX);
         L.prog_flux_m.finalize(c, s, &g);
     } else if (!g.shard.sharded()) {
@@ -1032,9 +1038,9 @@ void factor_hlu(HLU& L, const double* emissivity) {
         L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_PERM);
         L.prog_solve_m.finalize(c, s, &g);
         mprog_lf(L.prog_flux_m, IN_FLUX, Fm.xt_m.p);
+        const int z = (int)L.prog_flux_m.h_passes.size() - 1;   // the pass that writes z (F's input)
         L.prog_flux_m.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
-        L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN,
-                                 (int)L.prog_flux_m.h_passes.size() - 2);
+        L.prog_flux_m.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, z);
         L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_FLUX);
         L.prog_flux_m.finalize(c, s, &g);
     }

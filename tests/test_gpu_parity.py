@@ -192,6 +192,34 @@ def test_single_dense_leaf_equals_dense(hm, ctx):
     assert rel(z, vf.solve(C, x)) <= 1e-13
 
 
+def test_flux_of_an_operator_without_low_rank_blocks(hm, ctx):
+    """Regression: with k_max = 1 every admissible block of the icosphere sub 4 (5,120 facets) reaches the
+    rank cap and is stored dense, so F has no phase 1.  The flux program's near-field tasks must still
+    wait for the solve's output z (they used to wait for "the pass two back", the solve's own phase 1,
+    and read z early).  Single vector and 64 columns, 20 repeated calls each, against the dense oracle."""
+    import torch
+    f = synth.icosphere(4)
+    eps = synth.emissivities(5, f.n)
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=64, eta=1.0)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=1e-6, k_max=1)
+    P = hm.hm_export_partition(g, F)
+    assert (P[:, 6] != 1).all() and (P[:, 5] == 1).any()       # admissible blocks, none low-rank
+    LU = hm.hm_factor_hlu(ctx, F, eps)
+    Fd, C, _ = vf.dense_operators(f, eps)
+    T = synth.temperatures(11, f.n, 64)
+    qo = vf.flux_from_dense(Fd, C, f.area, eps, T)
+    T1 = torch.from_numpy(T[:, 0].copy()).cuda()
+    q1 = torch.empty_like(T1)
+    T64 = torch.from_numpy(T.copy()).cuda()
+    q64 = torch.empty_like(T64)
+    for _ in range(20):
+        hm.hm_radiative_flux(ctx, F, LU, T1, q1)
+        hm.hm_radiative_flux(ctx, F, LU, T64, q64)
+        torch.cuda.synchronize()
+        assert rel(q1.cpu().numpy(), qo[:, 0]) <= 1e-5
+        assert max(rel(q64[:, c].cpu().numpy(), qo[:, c]) for c in range(64)) <= 1e-5
+
+
 @pytest.mark.parametrize("k", [1, 2, 3, 5])
 def test_tiny_inputs(hm, ctx, k):
     """Degenerate sizes: k facets of the icosahedron (one dense leaf). k = 1: F = 0, so F x = 0,
