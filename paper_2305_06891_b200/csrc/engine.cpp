@@ -154,26 +154,11 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
     auto c_all = [&](int sw, int node) { return (int32_t)(P + sw * 2 * nn + nn + node); };
     std::vector<int64_t> cnt(n_counters, 0);  // tasks that increment each counter
     auto sweep_of = [](int kind) { return kind >= DEP_BWD_P1 ? 1 : 0; };
-    // Reader / writer tree dependencies (programs without row-group links, i.e. the level forms; on by
-    // default, HM_DEP_REFINED=0 restores the conservative rule).  The update of node t reads the rows of
-    // one child (fwd: t1, bwd: t2) and writes the other's.  Counter c_p1 then counts the READERS of node
-    // t (its phase-1 tasks and its x-only phase-2 tasks, the dense W slices) and c_all its WRITERS (every
-    // phase-2 task).  A task below t on the written side waits for the writers (RAW); on the read side
-    // only for the readers (WAR) -- it no longer waits for t's t-reading phase 2, so the read side of
-    // every level proceeds while the written side is updated.  Transitive: t's own tasks waited for
-    // t's ancestors by the same rule.
-    static const bool refined_env = [] { const char* e = getenv("HM_DEP_REFINED"); return !(e && e[0] == '0'); }();
-    const bool refined = refined_env && row_links.empty();
     for (size_t i = 0; i < h_tasks.size(); ++i) {
         Task& t = h_tasks[i];
         const int kind = task_kind[i], node = task_node[i];
         cnt[t.pass]++;
-        if (refined && (kind == DEP_FWD_P1 || kind == DEP_BWD_P1)) {
-            t.inc_id[0] = c_p1(sweep_of(kind), node);
-        } else if (refined && (kind == DEP_FWD_P2 || kind == DEP_BWD_P2)) {
-            t.inc_id[0] = c_all(sweep_of(kind), node);
-            if (task_xonly[i]) t.inc_id[1] = c_p1(sweep_of(kind), node);
-        } else if (kind == DEP_FWD_P1 || kind == DEP_BWD_P1) {
+        if (kind == DEP_FWD_P1 || kind == DEP_BWD_P1) {
             t.inc_id[0] = c_p1(sweep_of(kind), node);
             t.inc_id[1] = c_all(sweep_of(kind), node);
         } else if (kind == DEP_FWD_P2 || kind == DEP_BWD_P2) {
@@ -223,26 +208,11 @@ void Program::finalize(Ctx* ctx, cudaStream_t s, const Geom* g) {
         const int sw = sweep_of(kind);
         static const char* diag = getenv("HM_DIAG_DEPS");
         if (diag && diag[0] == 'n') continue;
-        int par = g->nodes[node].parent, below = node;   // below: the child of par on the path to node
-        while (par >= 0 && cnt[c_all(sw, par)] == 0 && cnt[c_p1(sw, par)] == 0) {
-            below = par;
-            par = g->nodes[par].parent;
-        }
+        int par = g->nodes[node].parent;
+        while (par >= 0 && cnt[c_all(sw, par)] == 0) par = g->nodes[par].parent;
         if (!(diag && diag[0] == 'c')) {
-            if (par < 0) {
-                wait(sweep_dep[sw]);
-            } else if (refined) {
-                // fwd: b_t2 -= W b_t1 writes child[1]; bwd: b_t1 -= W b_t2 writes child[0]
-                const bool written = g->nodes[par].child[sw == 0 ? 1 : 0] == below;
-                if (written) {
-                    wait(c_all(sw, par));
-                } else {
-                    wait(c_p1(sw, par));
-                    if (cnt[c_p1(sw, par)] == 0) wait(c_all(sw, par));   // no reader counted: conservative
-                }
-            } else {
-                wait(c_all(sw, par));
-            }
+            if (par >= 0) wait(c_all(sw, par));
+            else wait(sweep_dep[sw]);
         }
         if ((kind == DEP_FWD_P2 || kind == DEP_BWD_P2) && !xonly && !(diag && diag[0] == 'i')) wait(c_p1(sw, node));
     }
