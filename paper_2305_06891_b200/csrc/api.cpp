@@ -673,7 +673,7 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             F.x_dev.alloc(c, (size_t)n, "apply x (pinned host copy-in)");
             Program& P = F.prog_apply_h;
             P.n_x = n;
-            P.add_elementwise(UNIT_COPYIN, n, F.x_dev.p, 1024);
+            P.add_elementwise(UNIT_COPYIN, n, F.x_dev.p, copyin_rows(n));
             P.add_stream(F.op.p1, F.op, F.xt.p, F.xt.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PERM);
             P.add_stream(F.op.p2, F.op, F.xt.p, nullptr, OUT_PERM, DEP_BARRIER, nullptr, IN_PERM, 0);
             P.finalize(c, s);

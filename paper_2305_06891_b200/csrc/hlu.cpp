@@ -890,7 +890,7 @@ void factor_hlu(HLU& L, const double* emissivity) {
         P.n_x = n;
         // pinned host input: an element-wise pass copies it into copy_in first (the payload stream
         // starts meanwhile; every reader of the input waits for the pass)
-        if (copy_in) P.add_elementwise(UNIT_COPYIN, n, copy_in, 1024);
+        if (copy_in) P.add_elementwise(UNIT_COPYIN, n, copy_in, copyin_rows(n));
         if (Lc > 0) {
             P.add_elementwise(in_mode == IN_FLUX ? UNIT_PROLOGUE : UNIT_PERMUTE, n, L.xtA.p);
             in_mode = IN_PLAIN;

@@ -447,6 +447,14 @@ inline int elementwise_rows(int64_t n) {
     return (int)std::max<int64_t>(32, (r + 7) & ~int64_t(7));
 }
 
+// rows per copy-in unit (pinned host input read through its device alias over PCIe): about one unit per
+// SM, so the pass is one or two latency-bound round trips per CTA instead of a few long units (1,024-row
+// units left 20 units on C2, each a chain of four round trips); multiple of 4 (unrolled loads)
+inline int copyin_rows(int64_t n) {
+    const int64_t r = (n + 147) / 148;
+    return (int)std::max<int64_t>(64, (r + 3) & ~int64_t(3));
+}
+
 size_t engine_smem_bytes();
 int engine_mrhs_grid();
 int engine_mrhs_max_passes();

@@ -544,9 +544,19 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const ProgArgs A) {
             }
         } else {
             if (u.type == UNIT_COPYIN) {   // pinned host input -> device copy (overlaps the payload stream)
-                for (int i = ct; i < u.nrows; i += kConsumers) {
-                    const int64_t row = u.out0 + i;
-                    P.out[row * A.ld + A.col] = A.host_in[row * A.ld + A.col];
+                // four PCIe reads in flight per thread (the unit is latency-bound)
+                for (int i0 = ct; i0 < u.nrows; i0 += 4 * kConsumers) {
+                    double v[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int i = i0 + q * kConsumers;
+                        v[q] = i < u.nrows ? A.host_in[(u.out0 + i) * A.ld + A.col] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int i = i0 + q * kConsumers;
+                        if (i < u.nrows) P.out[(u.out0 + i) * A.ld + A.col] = v[q];
+                    }
                 }
             } else if (u.type == UNIT_PROLOGUE_INT) {   // sharded: w = eps T^4 in place on padded internal rows
                 for (int i = ct; i < u.nrows; i += kConsumers) {
