@@ -76,20 +76,6 @@ __device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uin
         "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
         : "memory");
 }
-// 16-byte asynchronous global -> shared copy (L2 only: the source may have been written by another SM
-// earlier in this launch); per-lane addresses, no serialisation over the lanes
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16_hint(void* dst, const void* src, uint64_t pol) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
-                 : "memory");
-}
-// arrive on the mbarrier once this thread's earlier cp.async copies have landed (the pending count is
-// raised first, so the barrier's expected count is unchanged)
-__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* b) {
-    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
-}
 // split-K arrival: release this thread's (and, cumulatively, its warp's) partial-sum writes,
 // acquire the other pieces' when last
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {

@@ -37,14 +37,11 @@ constexpr int kMStages = HM_MRHS_STAGES;
 // Shared-memory strides for conflict-free fragment loads: an 8-byte fragment load by a half-warp
 // (lanes g = 0..3 row, t = 0..3 k) reads words t * stride + g; the 16 words fall into distinct bank
 // pairs iff stride = 4 or 12 (mod 16).
-// X tile row stride (doubles).  HM_MRHS_X_RUNS = 0 (default): 68, conflict-free B-fragment loads, one
-// bulk copy per X row.  = 1: 64, unpadded, so that a run of consecutive input rows lands as ONE bulk
-// copy -- measured slower (C2 64-RHS flux 0.888 vs 0.779 ms): the 4-way conflicts of the B-fragment
-// loads cost the consumers more than the per-row copy issue costs the gatherers
-#ifndef HM_MRHS_X_RUNS
-#define HM_MRHS_X_RUNS 0
-#endif
-constexpr int kXStride = HM_MRHS_X_RUNS ? 64 : 68;
+// X tile row stride (doubles): 68, conflict-free B-fragment loads.  (Measured and removed: an unpadded
+// stride 64, so that a run of consecutive input rows lands as ONE bulk copy -- C2 64-RHS flux 0.888 vs
+// 0.779 ms: the 4-way B-fragment conflicts cost the consumers more than the per-row copy issue costs the
+// gatherers.)
+constexpr int kXStride = 68;
 __host__ __device__ constexpr int padded_ld(int ld) {   // smem column stride of a chunk with ld rows
     return ld + ((ld & 15) <= 4 ? 4 - (ld & 15) : (ld & 15) <= 12 ? 12 - (ld & 15) : 20 - (ld & 15));
 }
@@ -171,12 +168,6 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const dou
 #endif
 #ifndef HM_MRHS_TILE1D
 #define HM_MRHS_TILE1D 0
-#endif
-#ifndef HM_MRHS_GATHER_CPASYNC
-#define HM_MRHS_GATHER_CPASYNC 0
-#endif
-#ifndef HM_MRHS_PAYLOAD_CPASYNC
-#define HM_MRHS_PAYLOAD_CPASYNC 0
 #endif
 // rows in flight per consumer warp in the element-wise units (4: fewest register spills of the kernel)
 #ifndef HM_MRHS_EROWS
@@ -376,14 +367,13 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                     const int upass = __shfl_sync(0xffffffffu, mine.pass, c);
                     const long long uoff = __shfl_sync(0xffffffffu, (long long)mine.a_off, c);
                     // payload route (whole_chunk): one bulk copy of the chunk (default); else column by
-                    // column at padded_ld(ld), by per-column bulk copies (issued lane by lane) or by 16-byte
-                    // cp.async from every lane (HM_MRHS_PAYLOAD_CPASYNC=1: measured slower, 0.846 vs 0.796 ms)
+                    // column at padded_ld(ld), one bulk copy per column issued lane by lane.  (Measured and
+                    // removed: 16-byte cp.async from every lane for the padded chunks, 0.846 vs 0.796 ms.)
                     const bool stream = !end && utype == UNIT_STREAM;
 #if HM_DEVICE_CHECKS
                     if (stream) check_payload(A, upass, uoff, uncols, uld);
 #endif
                     const bool whole = stream && whole_chunk(uld);
-                    const bool cpa = stream && !whole && HM_MRHS_PAYLOAD_CPASYNC;
                     if (lane == c) {
                         if (end) {
                             St.hdr.type = -1;
@@ -392,7 +382,7 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                         } else {
                             St.hdr = mine;
                             mbar_arrive(&S.posted[s]);
-                            if (stream && !cpa)
+                            if (stream)
                                 mbar_expect_tx(&S.full[s], (uint32_t)mine.ncols * (uint32_t)mine.ld * 8u);
                             else if (!stream)
                                 mbar_arrive(&S.full[s]);
@@ -408,18 +398,6 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                             else
                                 tma_load_1d(St.payload, src, pb, &S.full[s]);
                         }
-                    } else if (cpa) {   // 16-byte pieces (column j, piece q) -> payload + j * padded_ld(ld) + 2 q
-                        const double* src = S.passes[upass].arena + uoff;
-                        const int ldp = padded_ld(uld);
-                        const int h = uld >> 1;
-                        const int tot = uncols * h;
-                        for (int i = lane; i < tot; i += 32) {
-                            const int j = i / h, q = i - j * h;
-                            cp_async16_hint(St.payload + j * ldp + 2 * q, src + (int64_t)j * uld + 2 * q, pol);
-                        }
-                        cp_async_mbar_arrive(&S.full[s]);
-                        __syncwarp();
-                        if (lane == c) mbar_arrive(&S.full[s]);   // after every lane's pending increment
                     } else if (stream) {   // column j -> payload + j * padded_ld(ld)
                         const double* src = S.passes[upass].arena + uoff;
                         const int ldp = padded_ld(uld);
@@ -510,41 +488,6 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                             if (c < ncol4) reinterpret_cast<double2*>(St.X + c * kXStride)[lane] = v[u];
                         }
                     }
-                } else if (im == IN_PLAIN && HM_MRHS_GATHER_CPASYNC) {
-                    // X rows (512 B each, written by an earlier pass: L2) by 16-byte cp.async, one row per
-                    // warp instruction (lane l: doubles 2l, 2l + 1), no per-lane serialisation; each lane
-                    // arrives on the stage's barrier when its copies have landed.  Off by default: measured
-                    // slower than the per-row bulk copies (C2 64-RHS flux 0.818 vs 0.795 ms)
-                    const int c = gw + kMGatherers * lane;
-                    const int32_t jl = c < ncols ? __ldg(cs + c) : -1;
-                    const int nmine = (ncol4 - gw + kMGatherers - 1) / kMGatherers;   // rows of this warp (with k padding)
-                    for (int u = 0; u < nmine; ++u) {
-                        const int cc = gw + kMGatherers * u;
-                        const int32_t j = __shfl_sync(0xffffffffu, jl, u);
-                        double* dst = St.X + cc * kXStride + 2 * lane;
-                        if (j >= 0)
-                            cp_async16(dst, in + (int64_t)j * kMrhsMax + 2 * lane);
-                        else   // k-step padding column: zero (consumers multiply it)
-                            *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
-                    }
-                    cp_async_mbar_arrive(&S.gathered[s]);
-                } else if (im == IN_PLAIN && HM_MRHS_X_RUNS && H.nruns > 0) {
-                    // runs of consecutive input rows (the chunk's run-length column sources): rows are
-                    // contiguous in the internal 64-wide vector and, at stride 64, in the tile, so each
-                    // run arrives by ONE bulk copy; warp gw, lane l -> run r = gw + kMGatherers * l
-                    const int nr = H.nruns;
-                    const int r = gw + kMGatherers * lane;
-                    int start = 0;
-                    for (int q = 0; q < r && q < nr; ++q) start += H.run_len[q];
-                    const int len = r < nr ? (int)H.run_len[r] : 0;
-                    const uint32_t bytes = (uint32_t)len * kMrhsMax * 8u;
-                    const uint32_t tot = __reduce_add_sync(0xffffffffu, bytes);
-                    if (lane == 0 && tot) mbar_add_tx(&S.gathered[s], tot);
-                    __syncwarp();
-                    if (len > 0)
-                        tma_load_1d(St.X + start * kXStride, in + (int64_t)H.run_src[r] * kMrhsMax, bytes, &S.gathered[s]);
-                    if (gw == 0)   // k-step padding rows [ncols, ncol4): zero (consumers multiply them)
-                        for (int i = lane; i < (ncol4 - ncols) * kXStride; i += 32) St.X[ncols * kXStride + i] = 0.0;
                 } else if (im == IN_PLAIN) {
                     // each X row (512 B, written by an earlier pass) arrives by a 1-D TMA bulk copy:
                     // warp gw, lane l -> column c = gw + kMGatherers * l

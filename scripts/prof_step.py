@@ -1,7 +1,7 @@
 """Profiling driver: set up config C (default 2), warm up, then run STEPS flux evaluations inside
 cudaProfilerStart/Stop so that `ncu --profile-from-start off` sees only hot-path kernels.
 
-    python scripts/prof_step.py [--config 2] [--steps 2]
+    python scripts/prof_step.py [--config 2] [--steps 2] [--cut 99]
 """
 import argparse
 import os
@@ -14,6 +14,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--cut", type=int, default=-1, help="solve form (cut level; 99: pure level form)")
     a = ap.parse_args()
     import torch
     import paper_2305_06891_b200 as hm
@@ -23,7 +24,7 @@ def main():
     ctx = hm.hm_init(0)
     g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
     F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
-    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity, cut_level=a.cut)
     T = torch.from_numpy(cfg.T[:, 0].copy()).cuda()
     q = torch.empty_like(T)
     for _ in range(3):
