@@ -18,12 +18,12 @@ def rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
 
 
-def _run_rank(hm, rank, world, key, cfg, out, errs):
+def _run_rank(hm, rank, world, key, cfg, out, errs, aca_kw=None):
     try:
         f = cfg.facets
         ctx = hm.hm_init(0, rank, world, key, hm.HM_FLAG_LOCAL_GROUP)
         g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
-        F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)
+        F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca, **(aca_kw or {}))
         LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
         perm = hm.hm_export_perm(g)
         b, e = hm.hm_local_range(g, rank, world)
@@ -86,6 +86,45 @@ def test_virtual_shards_match_single_rank_and_oracle(world):
     assert rel(Y, Fd @ x) <= 10 * cfg.eps_aca
     assert rel(Z, vf.solve(C, x)) <= 10 * cfg.eps_aca
     assert rel(Q, vf.flux_from_dense(Fd, C, f.area, cfg.emissivity, cfg.T[:, 0])[:, 0]) <= 10 * cfg.eps_aca
+
+
+def test_virtual_shards_adaptive_quadrature():
+    """Reading R35 on the sharded path: each rank assembles its block rows with the adaptive quadrature
+    (the table is built from the caller's vertices on every rank, the dense near field of the local
+    operator is filled with it); apply, solve and flux equal the world = 1 adaptive operators."""
+    import paper_2305_06891_b200 as hm
+    world = 2
+    cfg = synth.make_config(2, geometry=synth.icosphere(3))
+    f = cfg.facets
+    kw = dict(quadrature="adaptive", vertices=f.tris)
+    out, errs = {}, []
+    th = [threading.Thread(target=_run_rank, args=(hm, r, world, 3000 + world, cfg, out, errs, kw)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    n = f.n
+    Y, Z, Q = np.empty(n), np.empty(n), np.empty(n)
+    for r in range(world):
+        o = out[r]
+        Y[o["rows"]], Z[o["rows"]], Q[o["rows"]] = o["y"], o["z"], o["q"]
+    ctx = hm.hm_init(0)
+    g = hm.hm_build_geometry(ctx, f.centroid, f.normal, f.area, f.aabb, n_min=cfg.n_min, eta=cfg.eta)
+    F = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca, **kw)
+    LU = hm.hm_factor_hlu(ctx, F, cfg.emissivity)
+    x = cfg.rhs()[:, 0].copy()
+    y1, z1, q1 = np.empty(n), np.empty(n), np.empty(n)
+    hm.hm_apply_F(ctx, F, x, y1)
+    hm.hm_solve_C(ctx, LU, x, z1)
+    hm.hm_radiative_flux(ctx, F, LU, cfg.T[:, 0].copy(), q1)
+    assert rel(Y, y1) <= 1e-13
+    assert rel(Z, z1) <= 1e-13
+    assert rel(Q, q1) <= 1e-12
+    F0 = hm.hm_assemble_aca(ctx, g, eps_aca=cfg.eps_aca)   # and the option is in effect
+    y0 = np.empty(n)
+    hm.hm_apply_F(ctx, F0, x, y0)
+    assert rel(y0, y1) > 1e-4
 
 
 @pytest.mark.parametrize("world,cut", [(2, 99), (4, 99), (4, 1), (8, 2)])
