@@ -544,11 +544,27 @@ void stage_b_root(HLU& L, const HMat& F, const Geom& g, const std::vector<double
     out.fwd.assign(std::max(Lc, 0), {});
     out.bwd.assign(std::max(Lc, 0), {});
     int64_t total = 0;
-    auto dense_out = [](const hla::Mat& M) { return M.type != hla::T_LR || (int64_t)M.k * (M.m + M.n) >= M.m * M.n; };
+    // A block is stored dense when that is no larger than its factors -- or, in the level form, when it
+    // belongs to the W of a node of at most HM_DENSE_W_ROWS rows (default 640): those levels are
+    // latency-bound (~16 us per level whatever their bytes, profiles/round2_trace_levelform_c2.txt), and
+    // a dense W is one pass per level instead of a phase-1 / phase-2 pair
+    static const int64_t dense_w_rows = [] {
+        const char* e = getenv("HM_DENSE_W_ROWS");
+        return e ? (int64_t)atoll(e) : (int64_t)640;
+    }();
+    auto dense_out = [&](const hla::LeafView& v) {
+        const hla::Mat& M = *v.M;
+        if (M.type != hla::T_LR || (int64_t)M.k * (M.m + M.n) >= M.m * M.n) return true;
+        if (v.node >= 0 && g.nodes[v.node].level < Lc) {
+            const Node& N = g.nodes[v.node];
+            return N.end - N.begin <= dense_w_rows;
+        }
+        return false;
+    };
     hf->visit([&](const hla::LeafView& v) {
         const hla::Mat& M = *v.M;
         if (v.side == 0) total += 2 * M.m * M.m;
-        else if (dense_out(M)) total += M.m * M.n;
+        else if (dense_out(v)) total += M.m * M.n;
         else total += M.k * (M.m + M.n);
     });
     DBuf<double> dev;
@@ -622,7 +638,7 @@ void stage_b_root(HLU& L, const HMat& F, const Geom& g, const std::vector<double
             out.srcU.push_back(S);
             return;
         }
-        if (dense_out(M)) {
+        if (dense_out(v)) {
             S.kind = KIND_DENSE;
             S.d_rs = 1;
             S.d_cs = M.m;
