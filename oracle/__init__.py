@@ -18,10 +18,13 @@ Plain, slow, obviously-correct numpy (fp64) written from PAPER.md:
                     pivoting (R31) and QR + SVD recompression (R32).
   cavity.py      -- the cavity operator around the hot path: R, Rbar, S = P^T Rbar P, the flux
                     residual and J^cav (PAPER.md:163-260, NEXT-1).
+  hlu.py         -- the H-LU of C in F's partition: the 4-step recursion on
+                    dense blocks with an SVD truncation after every step, its
+                    solve and the inverse-factor solve form (reading R27).
   hmatrix.py     -- the oracle's own H-matrix (dense near field + ACA far field) and its
                     block-recursive matrix-vector product.
 
 Parity status per function is listed in DESIGN.md §"Oracle pins".  Unpinned:
-none of the functions here; the GPU H-LU *ranks* (which the oracle does not
-reproduce) are "parity unpinned" and only their effect (C^-1 b) is checked.
+none.  The library's H-LU factors are compared with hlu.py block by block at
+4 eps (ranks within 2): the two truncate at different points (reading R33).
 """

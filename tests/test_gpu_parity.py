@@ -1021,6 +1021,45 @@ def test_apply_is_exact_on_the_exported_factors(hm, ctx):
     assert np.abs(z[perm] - zl).max() <= 1e-13 * np.abs(zl).max()
 
 
+def test_hlu_factors_match_oracle_hlu(hm, case):
+    """The factors hm_factor_hlu builds from the GPU's own F (device context, stage B, cut 0) against
+    the oracle's H-LU (oracle/hlu.py) of the oracle's own H-matrix (equal to the GPU's
+    F to 1e-13, test_apply_equals_oracle_hmatrix_and_dense): every admissible block of L^-1 and U^-1
+    within 4 eps of its Frobenius norm, ranks within 2, rank exactly 1 in sphere-exact mode (bars
+    derived in tests/test_hlu_host.py::test_host_hlu_factors_match_oracle_hlu); then the GPU solve
+    against the oracle H-LU's solve within 10 eps."""
+    from oracle import hlu as ohlu
+    cfg, f, H = case["cfg"], case["f"], case["H"]
+    n = f.n
+    LU = hm.hm_factor_hlu(case["F"].ctx, case["F"], cfg.emissivity, cut_level=0)
+    perm = H.perm
+    lam = (1.0 - cfg.emissivity[perm]) / f.area[perm]
+    CH = np.eye(n) - lam[:, None] * H.to_dense_internal()
+    part = H.partition()
+    eps = cfg.eps_aca
+    O = ohlu.hlu(CH, H.tree, part, eps)
+    Li, Ui, rk = ohlu.inverse_factors(O, part, eps)
+    got = {(r0, c0): D for r0, m, c0, nn, D in
+           hm.hm_export_factors(hm.HM_OP_LINV, case["F"], LU) + hm.hm_export_factors(hm.HM_OP_UINV, case["F"], LU)}
+    for p in part:
+        if p[5] != 1:
+            continue
+        a0, a1, b0, b1 = (int(v) for v in p[1:5])
+        X = (Li if a0 > b0 else Ui)[a0:a1, b0:b1]
+        D = got[(a0, b0)]
+        Y = D[0] @ D[1].T if isinstance(D, tuple) else D
+        assert np.linalg.norm(Y - X) <= 4 * eps * np.linalg.norm(X)
+        kp = D[0].shape[1] if isinstance(D, tuple) else np.linalg.matrix_rank(D, tol=eps * np.linalg.norm(D, 2))
+        assert abs(kp - rk[(a0, b0)]) <= 2
+        if case["name"] == "ico3-exact":
+            assert kp == 1 and rk[(a0, b0)] == 1
+    x = cfg.rhs()[:, 0].copy()
+    z = np.empty(n)
+    hm.hm_solve_C(case["F"].ctx, LU, x, z)
+    zo = O.solve(x[perm])
+    assert rel(z[perm], zo) <= 10 * eps
+
+
 @pytest.mark.parametrize("case_name", ["C1", "plates-tri"])
 def test_adaptive_quadrature_matches_oracle(hm, ctx, case_name):
     """NEXT-4 adaptive Gauss quadrature of the entries (reading R35) through the C ABI, on

@@ -662,3 +662,81 @@ def test_adaptive_quadrature_parallel_plates_match_closed_form():
         assert abs(F0[:h, h:].sum() - ex) == pytest.approx(one_err, rel=0.05)
         assert abs(F1[:h, h:].sum() - ex) <= 2e-6
         assert np.abs(F1[:h, :h]).max() == 0.0 and np.abs(F1[h:, h:]).max() == 0.0
+
+
+# ------------------------------------------------------------------ H-LU
+def _hlu_case(cfg, n_min=None):
+    from oracle import hlu as ohlu
+    f = cfg.facets
+    H = hmatrix.assemble(f, n_min or cfg.n_min, cfg.eta, cfg.eps_aca)
+    perm = H.perm
+    lam = (1.0 - cfg.emissivity[perm]) / f.area[perm]
+    CH = np.eye(f.n) - lam[:, None] * H.to_dense_internal()
+    return ohlu, H, CH, perm
+
+
+def test_hlu_untruncated_is_the_unpivoted_lu():
+    """PAPER.md:770-777 without truncation (eps = 0) on a deep tree (icosphere sub 2, leaves of <= 16):
+    the four-step recursion must return a unit lower L and an upper U with L U = C to rounding.  The
+    LU without pivoting of a matrix with nonsingular leading minors is unique, so this is the textbook
+    factorisation; a wrong operand in any step (L11 for U11, a transposed substitution, a missing
+    Schur update) breaks L U = C.  The triangular solves then equal LAPACK's solve."""
+    cfg = synth.make_config(2, geometry=synth.icosphere(2))
+    ohlu, H, CH, perm = _hlu_case(cfg, n_min=16)
+    assert H.tree.depth >= 4
+    O = ohlu.hlu(CH, H.tree, H.partition(), 0.0)
+    assert np.array_equal(np.diag(O.L), np.ones(CH.shape[0])) and not np.triu(O.L, 1).any()
+    assert not np.tril(O.U, -1).any()
+    assert np.linalg.norm(O.L @ O.U - CH) <= 1e-14 * np.linalg.norm(CH)
+    b = synth.uniform(7, CH.shape[0])
+    assert np.linalg.norm(O.solve(b) - np.linalg.solve(CH, b)) <= 1e-13 * np.linalg.norm(np.linalg.solve(CH, b))
+
+
+def test_hlu_sphere_exact_rank_one_and_sherman_morrison():
+    """Sphere-exact icosphere sub 3, eps ~ U[0.3, 0.95]: C = M - k b a^T (diagonal plus rank one).
+    By the recursion, U12 = L11^-1 C12 and L21 = C21 U11^-1 are rank one and the Schur complement is
+    again diagonal plus rank one, so every admissible block of the exact L and U has rank 1: the
+    truncation at eps = 1e-6 must keep exactly one singular value per block, and the H-LU solve must
+    equal the Sherman-Morrison closed form within the truncation accuracy."""
+    cfg = synth.make_config(2, geometry=synth.icosphere(3, exact=True))
+    ohlu, H, CH, perm = _hlu_case(cfg)
+    O = ohlu.hlu(CH, H.tree, H.partition(), cfg.eps_aca)
+    nadm = int(H.partition()[:, 5].sum())
+    assert len(O.ranks_L) + len(O.ranks_U) == nadm and nadm > 0
+    assert set(O.ranks_L.values()) == {1} and set(O.ranks_U.values()) == {1}
+    f = cfg.facets
+    a = f.area
+    k = 1.0 / (4.0 * math.pi)
+    cex = (a.sum() - a) * k
+    bb = (1.0 - cfg.emissivity) / cex
+    Md = 1.0 + k * bb * a
+    x = synth.uniform(5, f.n)
+    Mx, Mb = x / Md, bb / Md
+    zcl = Mx + (k * (a @ Mx) / (1.0 - k * (a @ Mb))) * Mb
+    z = np.empty(f.n)
+    z[perm] = O.solve(x[perm])
+    assert np.linalg.norm(z - zcl) <= 10 * cfg.eps_aca * np.linalg.norm(zcl)
+    Li, Ui, rk = ohlu.inverse_factors(O, H.partition(), cfg.eps_aca)   # C^-1 = D^-1 + rank one
+    assert set(rk.values()) == {1}
+
+
+def test_hlu_truncated_config1_within_eps():
+    """C1 at eps_LU = eps_ACA = 1e-6 ("within a prescribed, controllable accuracy"):
+    L U reproduces C to a few eps, the solve is within 10 eps of the dense oracle's C^-1 b (north star),
+    the truncation really compresses (admissible blocks far below full rank), and the inverse factors
+    (reading R27) compose to C^-1 within the same bar."""
+    cfg = synth.make_config(1)
+    ohlu, H, CH, perm = _hlu_case(cfg)
+    eps = cfg.eps_aca
+    part = H.partition()
+    O = ohlu.hlu(CH, H.tree, part, eps)
+    assert np.linalg.norm(O.L @ O.U - CH) <= 10 * eps * np.linalg.norm(CH)
+    f = cfg.facets
+    Fd, Cd, _ = vf.dense_operators(f, cfg.emissivity)
+    xb = cfg.rhs()[:, 0]
+    zd = np.linalg.solve(Cd, xb)[perm]
+    assert np.linalg.norm(O.solve(xb[perm]) - zd) <= 10 * eps * np.linalg.norm(zd)
+    full = sum(min(int(p[2] - p[1]), int(p[4] - p[3])) for p in part if p[5] == 1)
+    assert sum(O.ranks_L.values()) + sum(O.ranks_U.values()) < 0.25 * full
+    Li, Ui, _ = ohlu.inverse_factors(O, part, eps)
+    assert np.linalg.norm(Ui @ (Li @ xb[perm]) - zd) <= 10 * eps * np.linalg.norm(zd)
