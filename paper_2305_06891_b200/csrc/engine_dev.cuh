@@ -68,6 +68,16 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// The multi-RHS phase-1 -> phase-2 scratch t (n_t x 64) is re-read by every leaf-row slice of its block:
+// an L2 evict-last policy for its stores (and gathers) keeps it resident against the streamed payload
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_v2_hint(double* p, double a, double b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes, unsigned long long* b,
                                                  uint64_t pol) {
     asm volatile(

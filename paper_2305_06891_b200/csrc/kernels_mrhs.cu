@@ -170,6 +170,11 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[kMaxTiles][2], const dou
 #define HM_MRHS_TILE1D 0
 #endif
 // rows in flight per consumer warp in the element-wise units (4: fewest register spills of the kernel)
+// L2 policy of the phase-1 -> phase-2 scratch (t): 0 none; 1 evict-last stores of internal results;
+// 2 also evict-last X-row gathers
+#ifndef HM_MRHS_T_HINT
+#define HM_MRHS_T_HINT 0
+#endif
 #ifndef HM_MRHS_EROWS
 #define HM_MRHS_EROWS 4
 #endif
@@ -498,7 +503,11 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                     __syncwarp();
                     if (mine) {
                         const int32_t j = __ldg(cs + c);
-                        tma_load_1d(St.X + c * kXStride, in + (int64_t)j * kMrhsMax, kMrhsMax * 8u, &S.gathered[s]);
+                        if (HM_MRHS_T_HINT >= 2)
+                            tma_load_1d_hint(St.X + c * kXStride, in + (int64_t)j * kMrhsMax, kMrhsMax * 8u, &S.gathered[s],
+                                             l2_evict_last_policy());
+                        else
+                            tma_load_1d(St.X + c * kXStride, in + (int64_t)j * kMrhsMax, kMrhsMax * 8u, &S.gathered[s]);
                     } else if (c < ncol4) {   // k-step padding columns: zero (consumers multiply them)
 #pragma unroll
                         for (int q = 0; q < kMrhsMax; ++q) St.X[c * kXStride + q] = 0.0;
@@ -787,8 +796,12 @@ __global__ void __launch_bounds__(kMThreads, 1) engine_mrhs_kernel(const ProgArg
                     if (!warp_tile(i, cw, M8, N8, mt, nt)) break;
                     const int row = mt * 8 + ar;
                     const int col = nt * 8 + 2 * ak;
-                    if (row < nrows)
-                        *reinterpret_cast<double2*>(P.out + (out0 + row) * kMrhsMax + col) = make_double2(acc[i][0], acc[i][1]);
+                    if (row < nrows) {
+                        if (HM_MRHS_T_HINT >= 1)
+                            st_v2_hint(P.out + (out0 + row) * kMrhsMax + col, acc[i][0], acc[i][1], l2_evict_last_policy());
+                        else
+                            *reinterpret_cast<double2*>(P.out + (out0 + row) * kMrhsMax + col) = make_double2(acc[i][0], acc[i][1]);
+                    }
                 }
             } else if (grp < 0) {
 #pragma unroll

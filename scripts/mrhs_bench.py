@@ -46,4 +46,5 @@ def main(cfg_id=2, r=64, iters=10):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 2, int(sys.argv[2]) if len(sys.argv) > 2 else 64,
+         int(sys.argv[3]) if len(sys.argv) > 3 else 10)
