@@ -476,6 +476,21 @@ def main():
                 "bytes_local": rep3["bytes_F_local"] + rep3["bytes_C_local"], "setup_s": setup3,
                 "comm_share": (1.0 - ms3["flux_no_exchange"] / ms3["flux"]) if "flux_no_exchange" in ms3 else None}
         del LU3, F3, g3
+    read_only = None
+    if world == 1:   # a read-only streaming ceiling beside the copy peak (reads can exceed copy)
+        buf = torch.ones(1 << 28, dtype=torch.float64, device="cuda")     # 2 GiB
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = float("inf")
+        for _ in range(6):
+            torch.cuda.synchronize()
+            r0.record()
+            buf.sum()
+            r1.record()
+            torch.cuda.synchronize()
+            best = min(best, r0.elapsed_time(r1))
+        read_only = {"gbs": buf.numel() * 8 / (best * 1e-3) / 1e9, "how": "torch.sum over 2 GiB fp64, best of 6 (CUDA events)",
+                     "ubench_ldg_gbs_round1": 7290.0}
+        del buf
     peak, peak_src = peaks()
     bytes_step = rep["bytes_F"] + rep["bytes_C"]
     bytes_local = rep["bytes_F_local"] + rep["bytes_C_local"]    # this rank's stored bytes (= bytes_step at N=1)
@@ -527,7 +542,9 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "engine_kernel (flux program)" + (" + NCCL allgathers, rank 0" if world > 1 else ""),
                          "achieved": achieved,
                          "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "read_only_probe": read_only,
+                         "frac_of_read_only": achieved / read_only["gbs"] if read_only else None},
             "e2e": {"value": args.steps / (ms_e2e / 1e3), "unit": "applies/s",
                     "h2d_bytes_per_step": 8 * n_loc, "d2h_bytes_per_step": 8 * n_loc},
             "gpu_launches": launches * args.steps,   # engine launches by this rank in the timed region
