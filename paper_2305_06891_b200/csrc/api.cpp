@@ -687,8 +687,10 @@ hm_status hm_assemble_aca(hm_ctx* ctx, const hm_geom* geom, const hm_aca_params*
             P.add_elementwise(UNIT_PERMUTE, n, F.xt_m.p, elementwise_rows(n));   // x -> internal n x 64 (coalesced)
             const int xin = (int)P.h_passes.size() - 1;   // x-only phase-2 tasks wait for it (no phase 1: no LR block)
             P.add_stream(F.op.p1m, F.op, F.xt_m.p, F.xt_m.p, OUT_ASSIGN);
-            P.add_stream(F.op.p2m, F.op, F.xt_m.p, F.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, xin);
-            P.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), F.y_m.p, OUT_PERM);
+            // HM_MRHS_FUSED_EPI=1: phase 2 emits the permuted result itself (no epilogue pass)
+            const bool fused = mrhs_fused_epilogue();
+            P.add_stream(F.op.p2m, F.op, F.xt_m.p, F.y_m.p, fused ? OUT_PERM : OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, xin);
+            if (!fused) P.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), F.y_m.p, OUT_PERM);
             P.finalize(c, s);
         }
         HM_CUDA(cudaStreamSynchronize(s));

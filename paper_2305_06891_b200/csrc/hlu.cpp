@@ -1006,8 +1006,10 @@ void factor_hlu(HLU& L, const double* emissivity) {
         };
         // final results go to an internal n x 64 buffer, then an element-wise epilogue pass emits them
         // (permute-out / flux epilogue) coalesced and fully parallel
-        mprog(L.prog_solve_m, IN_PERM, Fm.y_m.p, OUT_ASSIGN);
-        L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_PERM);
+        // (HM_MRHS_FUSED_EPI=1: the last stream pass emits through the output mode itself, no epilogue pass)
+        const bool fused = mrhs_fused_epilogue();
+        mprog(L.prog_solve_m, IN_PERM, Fm.y_m.p, fused ? OUT_PERM : OUT_ASSIGN);
+        if (!fused) L.prog_solve_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_PERM);
         L.prog_solve_m.finalize(c, s, &g);
         mprog(L.prog_flux_m, IN_FLUX, Fm.xt_m.p, OUT_ASSIGN);
         {
@@ -1015,9 +1017,9 @@ void factor_hlu(HLU& L, const double* emissivity) {
             const int z = (int)P.h_passes.size() - 1;   // U^-1 phase 2 writes z, the F input
             P.add_stream(F.op.p1m, F.op, Fm.xt_m.p, Fm.xt_m.p, OUT_ASSIGN);
             if (!getenv("HM_MRHS_NO_LINKS") && (int)P.h_passes.size() == z + 2) P.link_rows(z, z + 1);
-            P.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, z);
+            P.add_stream(F.op.p2m, F.op, Fm.xt_m.p, Fm.y_m.p, fused ? OUT_FLUX : OUT_ASSIGN, DEP_BARRIER, nullptr, IN_PLAIN, z);
         }
-        L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_FLUX);
+        if (!fused) L.prog_flux_m.add_elementwise(UNIT_EPILOGUE, n, nullptr, elementwise_rows(n), Fm.y_m.p, OUT_FLUX);
         L.prog_flux_m.finalize(c, s, &g);
     } else if (!g.shard.sharded()) {
         // level form (cut level > 0) with 64 columns: the same tree-scheduled sweeps as the single-vector

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -445,6 +446,14 @@ struct SegProgram {
 inline int elementwise_rows(int64_t n) {
     const int64_t r = (n + 147) / 148;
     return (int)std::max<int64_t>(32, (r + 7) & ~int64_t(7));
+}
+
+// multi-RHS programs: the last stream pass emits the caller's result itself (OUT_PERM / OUT_FLUX from the
+// task's accumulators) instead of writing the internal n x 64 buffer for an element-wise epilogue pass
+// (HM_MRHS_FUSED_EPI=1; read when a program is built)
+inline bool mrhs_fused_epilogue() {
+    const char* e = getenv("HM_MRHS_FUSED_EPI");
+    return e && e[0] == '1';
 }
 
 // rows per copy-in unit (pinned host input read through its device alias over PCIe): about one unit per
